@@ -1,0 +1,930 @@
+/*
+ * mhw_oracle.c -- CPU restatement of the mhwalk M-H walk path.
+ *
+ * TEST INFRASTRUCTURE ONLY (the checker, never the product). See mhw_oracle.h.
+ * Citations are file:line relative to the reference's proj/ directory.
+ * Compiled with -ffp-contract=off so every double expression rounds exactly as
+ * written (the decision path must not be FMA-contracted).
+ */
+#define _GNU_SOURCE
+#include "mhw_oracle.h"
+
+#include <pthread.h>
+#include <stdio.h>
+#include <stdlib.h>
+#include <string.h>
+#include <time.h>
+
+/* ================================================================== RNG */
+
+/* splitmix64, rng.hpp:8-13 */
+uint64_t og_splitmix64(uint64_t* state) {
+    uint64_t z = (*state += 0x9e3779b97f4a7c15ULL);
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+    return z ^ (z >> 31);
+}
+
+/* xoshiro256** seeded by splitmix64, rng.hpp:17-40 */
+typedef struct { uint64_t s[4]; } xo_t;
+
+static void xo_seed(xo_t* r, uint64_t seed) {
+    uint64_t sm = seed;
+    for (int i = 0; i < 4; ++i) r->s[i] = og_splitmix64(&sm);
+}
+static inline uint64_t rotl64(uint64_t x, int k) { return (x << k) | (x >> (64 - k)); }
+static inline uint64_t xo_next(xo_t* r) {
+    const uint64_t result = rotl64(r->s[1] * 5, 7) * 9;
+    const uint64_t t = r->s[1] << 17;
+    r->s[2] ^= r->s[0];
+    r->s[3] ^= r->s[1];
+    r->s[1] ^= r->s[2];
+    r->s[0] ^= r->s[3];
+    r->s[2] ^= t;
+    r->s[3] = rotl64(r->s[3], 45);
+    return result;
+}
+/* uniform_index: Lemire with rejection on the high 32 bits, rng.hpp:42-55 */
+static uint32_t xo_index(xo_t* r, uint32_t n) {
+    uint64_t x = xo_next(r) >> 32;
+    uint64_t m = x * (uint64_t)n;
+    uint64_t lo = m & 0xffffffffULL;
+    if (lo < n) {
+        uint64_t threshold = (0x100000000ULL - n) % n;
+        while (lo < threshold) {
+            x = xo_next(r) >> 32;
+            m = x * (uint64_t)n;
+            lo = m & 0xffffffffULL;
+        }
+    }
+    return (uint32_t)(m >> 32);
+}
+/* uniform_real: 53 bits, rng.hpp:58-60 */
+static double xo_real(xo_t* r) { return (double)(xo_next(r) >> 11) * 0x1.0p-53; }
+
+/* walker_stream, rng.hpp:68-76 */
+static void xo_walker(xo_t* r, uint64_t seed, uint64_t node, uint64_t k) {
+    uint64_t sm = seed;
+    uint64_t a = og_splitmix64(&sm);
+    sm ^= node * 0x9e3779b97f4a7c15ULL + 0x7f4a7c15ULL;
+    uint64_t b = og_splitmix64(&sm);
+    sm ^= k * 0xbf58476d1ce4e5b9ULL + 0x1ce4e5b9ULL;
+    uint64_t c = og_splitmix64(&sm);
+    xo_seed(r, a ^ (b + c));
+}
+
+void og_xoshiro_walker_draws(uint64_t seed, uint64_t node, uint64_t k, uint32_t bound,
+                             uint32_t count, uint32_t* out) {
+    xo_t r;
+    xo_walker(&r, seed, node, k);
+    for (uint32_t i = 0; i < count; ++i) out[i] = xo_index(&r, bound);
+}
+
+/* Philox4x32-10 (Salmon et al., SC'11 "Parallel random numbers: as easy as
+ * 1, 2, 3"): 10 rounds of the 4x32 S-box with Weyl key schedule. */
+void og_philox4x32_10(const uint32_t ctr[4], const uint32_t key[2], uint32_t out[4]) {
+    uint32_t c0 = ctr[0], c1 = ctr[1], c2 = ctr[2], c3 = ctr[3];
+    uint32_t k0 = key[0], k1 = key[1];
+    for (int r = 0; r < 10; ++r) {
+        if (r) { k0 += 0x9E3779B9u; k1 += 0xBB67AE85u; }
+        const uint64_t p0 = (uint64_t)0xD2511F53u * c0;
+        const uint64_t p1 = (uint64_t)0xCD9E8D57u * c2;
+        const uint32_t n0 = (uint32_t)(p1 >> 32) ^ c1 ^ k0;
+        const uint32_t n2 = (uint32_t)(p0 >> 32) ^ c3 ^ k1;
+        c1 = (uint32_t)p1;
+        c3 = (uint32_t)p0;
+        c0 = n0;
+        c2 = n2;
+    }
+    out[0] = c0; out[1] = c1; out[2] = c2; out[3] = c3;
+}
+
+/* Domain-separated key: (lo32(seed), hi32(seed) ^ domain). */
+void og_philox_key(uint64_t seed, uint32_t domain, uint32_t key[2]) {
+    key[0] = (uint32_t)seed;
+    key[1] = (uint32_t)(seed >> 32) ^ domain;
+}
+
+#define DOM_WALK   0x00000000u
+#define DOM_INIT   0x5EED1417u
+#define DOM_RMAT   0x2A7E0001u
+#define DOM_WEIGHT 0x3E1647u
+#define DOM_ETYPE  0x7E7E0003u
+#define DOM_HETERO 0x4E7E0004u
+
+/* One "transition block": the draws of one M-H transition / one init pick.
+ * xoshiro: sequential stream (reference). philox: block (id, blk) gives
+ * w0 -> candidate (Lemire), (w1,w2) -> 53-bit unit, w3 then sub-blocks
+ * (ctr[3] = 1, 2, ...) -> Lemire retry words. */
+typedef struct {
+    int philox;
+    xo_t* xo;
+    uint32_t key[2];
+    uint32_t ctr[4];
+    uint32_t w[4];
+    uint32_t rpos;
+} draw_t;
+
+static void draw_open(draw_t* d, int philox, xo_t* xo, const uint32_t key[2], uint64_t id,
+                      uint32_t blk) {
+    d->philox = philox;
+    d->xo = xo;
+    if (!philox) return;
+    d->key[0] = key[0];
+    d->key[1] = key[1];
+    d->ctr[0] = (uint32_t)id;
+    d->ctr[1] = (uint32_t)(id >> 32);
+    d->ctr[2] = blk;
+    d->ctr[3] = 0;
+    og_philox4x32_10(d->ctr, d->key, d->w);
+    d->rpos = 3;
+}
+static uint32_t draw_retry_word(draw_t* d) {
+    if (d->rpos == 4) {
+        d->ctr[3] += 1;
+        og_philox4x32_10(d->ctr, d->key, d->w);
+        d->rpos = 0;
+    }
+    return d->w[d->rpos++];
+}
+static uint32_t draw_index(draw_t* d, uint32_t n) {
+    if (!d->philox) return xo_index(d->xo, n);
+    uint64_t m = (uint64_t)d->w[0] * n;
+    uint32_t lo = (uint32_t)m;
+    if (lo < n) {
+        const uint32_t threshold = (uint32_t)((0x100000000ULL - n) % n);
+        while (lo < threshold) {
+            m = (uint64_t)draw_retry_word(d) * n;
+            lo = (uint32_t)m;
+        }
+    }
+    return (uint32_t)(m >> 32);
+}
+static double draw_real(draw_t* d) {
+    if (!d->philox) return xo_real(d->xo);
+    const uint64_t x = ((uint64_t)d->w[1] << 32) | d->w[2];
+    return (double)(x >> 11) * 0x1.0p-53;
+}
+
+uint32_t og_lemire_philox(const uint32_t key[2], uint64_t id, uint32_t blk, uint32_t n) {
+    draw_t d;
+    draw_open(&d, 1, NULL, key, id, blk);
+    return draw_index(&d, n);
+}
+double og_unit_philox(const uint32_t key[2], uint64_t id, uint32_t blk) {
+    draw_t d;
+    draw_open(&d, 1, NULL, key, id, blk);
+    return draw_real(&d);
+}
+
+/* ============================================================ graph build */
+
+typedef struct { uint32_t src, dst; uint64_t pos; } raw_edge_t;
+
+static int cmp_raw(const void* a, const void* b) {
+    const raw_edge_t* x = (const raw_edge_t*)a;
+    const raw_edge_t* y = (const raw_edge_t*)b;
+    if (x->src != y->src) return x->src < y->src ? -1 : 1;
+    if (x->dst != y->dst) return x->dst < y->dst ? -1 : 1;
+    return x->pos < y->pos ? -1 : (x->pos > y->pos);
+}
+
+/* build_csr + load_edge_list symmetrization (graph.cpp:35-66, :94-97).
+ * Duplicates are summed in input order (the reference's std::sort leaves the
+ * order of >2 equal keys unspecified; for <=2 duplicates the sum is exact). */
+int og_build_csr(uint64_t n_edges, const uint32_t* src, const uint32_t* dst, const double* w,
+                 int symmetrize, uint32_t n_nodes, uint32_t* n_out, uint64_t* m_out,
+                 uint64_t** offsets, uint32_t** nbr, double** weights) {
+    uint64_t cap = symmetrize ? 2 * n_edges : n_edges;
+    raw_edge_t* e = (raw_edge_t*)malloc((cap ? cap : 1) * sizeof(raw_edge_t));
+    double* ew = (double*)malloc((cap ? cap : 1) * sizeof(double));
+    if (!e || !ew) { free(e); free(ew); return OG_ERR_NOMEM; }
+    uint64_t k = 0;
+    uint32_t max_id = 0;
+    for (uint64_t i = 0; i < n_edges; ++i) {
+        e[k].src = src[i]; e[k].dst = dst[i]; e[k].pos = k; ew[k] = w ? w[i] : 1.0; ++k;
+        if (symmetrize && src[i] != dst[i]) {
+            e[k].src = dst[i]; e[k].dst = src[i]; e[k].pos = k; ew[k] = w ? w[i] : 1.0; ++k;
+        }
+        if (src[i] > max_id) max_id = src[i];
+        if (dst[i] > max_id) max_id = dst[i];
+    }
+    uint32_t n = n_edges == 0 ? 0 : max_id + 1;
+    if (n_nodes > n) n = n_nodes;
+    qsort(e, k, sizeof(raw_edge_t), cmp_raw);
+    uint64_t out = 0;
+    double* sw = (double*)malloc((k ? k : 1) * sizeof(double));
+    raw_edge_t* se = e;
+    for (uint64_t i = 0; i < k; ++i) {
+        const double wi = ew[e[i].pos];
+        if (out > 0 && se[out - 1].src == e[i].src && se[out - 1].dst == e[i].dst) {
+            sw[out - 1] += wi;
+        } else {
+            se[out] = e[i];
+            sw[out] = wi;
+            ++out;
+        }
+    }
+    uint64_t* off = (uint64_t*)calloc((size_t)n + 1, sizeof(uint64_t));
+    uint32_t* nb = (uint32_t*)malloc((out ? out : 1) * sizeof(uint32_t));
+    for (uint64_t i = 0; i < out; ++i) { off[se[i].src + 1]++; nb[i] = se[i].dst; }
+    for (uint32_t v = 0; v < n; ++v) off[v + 1] += off[v];
+    free(e);
+    free(ew);
+    *n_out = n;
+    *m_out = out;
+    *offsets = off;
+    *nbr = nb;
+    *weights = sw;
+    return OG_OK;
+}
+
+static int cmp_u64(const void* a, const void* b) {
+    const uint64_t x = *(const uint64_t*)a, y = *(const uint64_t*)b;
+    return x < y ? -1 : (x > y);
+}
+
+/* R-MAT pairs: edge e draws `scale` 32-bit words
+ * from Philox block (e, level/4); quadrant by integer thresholds; MSB first.
+ * Self-loops dropped, pairs canonicalized (lo<hi) and deduplicated. */
+int og_rmat_pairs(uint32_t scale, uint32_t edge_factor, double a, double b, double c,
+                  uint64_t seed, uint64_t* n_pairs, uint32_t** lo, uint32_t** hi) {
+    const uint64_t t1 = (uint64_t)(a * 4294967296.0);
+    const uint64_t t2 = (uint64_t)((a + b) * 4294967296.0);
+    const uint64_t t3 = (uint64_t)((a + b + c) * 4294967296.0);
+    const uint64_t ne = (uint64_t)edge_factor << scale;
+    uint32_t key[2];
+    og_philox_key(seed, DOM_RMAT, key);
+    uint64_t* keys = (uint64_t*)malloc((ne ? ne : 1) * sizeof(uint64_t));
+    if (!keys) return OG_ERR_NOMEM;
+    uint64_t k = 0;
+    for (uint64_t e = 0; e < ne; ++e) {
+        uint32_t s = 0, d = 0, words[4] = {0, 0, 0, 0};
+        for (uint32_t l = 0; l < scale; ++l) {
+            if ((l & 3) == 0) {
+                const uint32_t ctr[4] = {(uint32_t)e, (uint32_t)(e >> 32), l >> 2, 0};
+                og_philox4x32_10(ctr, key, words);
+            }
+            const uint64_t r = words[l & 3];
+            uint32_t bs, bd;
+            if (r < t1) { bs = 0; bd = 0; }
+            else if (r < t2) { bs = 0; bd = 1; }
+            else if (r < t3) { bs = 1; bd = 0; }
+            else { bs = 1; bd = 1; }
+            s = (s << 1) | bs;
+            d = (d << 1) | bd;
+        }
+        if (s == d) continue;
+        const uint32_t x = s < d ? s : d, y = s < d ? d : s;
+        keys[k++] = ((uint64_t)x << 32) | y;
+    }
+    qsort(keys, k, sizeof(uint64_t), cmp_u64);
+    uint64_t u = 0;
+    for (uint64_t i = 0; i < k; ++i) {
+        if (u == 0 || keys[u - 1] != keys[i]) keys[u++] = keys[i];
+    }
+    *lo = (uint32_t*)malloc((u ? u : 1) * sizeof(uint32_t));
+    *hi = (uint32_t*)malloc((u ? u : 1) * sizeof(uint32_t));
+    for (uint64_t i = 0; i < u; ++i) {
+        (*lo)[i] = (uint32_t)(keys[i] >> 32);
+        (*hi)[i] = (uint32_t)keys[i];
+    }
+    free(keys);
+    *n_pairs = u;
+    return OG_OK;
+}
+
+/* fp32 weight of an undirected pair, U[wlo, whi): keyed by the pair so it is
+ * independent of generation order; computed in double, rounded once to float. */
+float og_pair_weight(uint64_t seed, uint32_t lo, uint32_t hi, float wlo, float whi) {
+    uint32_t key[2], w[4];
+    og_philox_key(seed, DOM_WEIGHT, key);
+    const uint32_t ctr[4] = {lo, hi, 0, 0};
+    og_philox4x32_10(ctr, key, w);
+    const uint64_t x = ((uint64_t)w[0] << 32) | w[1];
+    const double u = (double)(x >> 11) * 0x1.0p-53;
+    return (float)((double)wlo + ((double)whi - (double)wlo) * u);
+}
+
+uint32_t og_pair_etype(uint64_t seed, uint32_t lo, uint32_t hi, uint32_t n_types) {
+    uint32_t key[2];
+    og_philox_key(seed, DOM_ETYPE, key);
+    draw_t d;
+    draw_open(&d, 1, NULL, key, ((uint64_t)hi << 32) | lo, 0);
+    return draw_index(&d, n_types);
+}
+
+/* Heterogeneous A/P/V graph (BASELINE cfg3): types contiguous by id
+ * (A = [0,nA), P = [nA,nA+nP), V = rest). A node a draws Poisson(8) (Knuth
+ * product method on Philox units of block (a, j)) P targets uniformly; each P
+ * links to one uniform V. Pairs deduplicated. */
+int og_hetero_pairs(uint32_t n_nodes, uint64_t seed, uint32_t* nA_out, uint32_t* nP_out,
+                    uint64_t* n_pairs, uint32_t** lo, uint32_t** hi) {
+    const uint32_t nA = (uint32_t)((uint64_t)n_nodes * 60 / 100);
+    const uint32_t nP = (uint32_t)((uint64_t)n_nodes * 35 / 100);
+    const uint32_t nV = n_nodes - nA - nP;
+    const double L = 0x1.5fc21041027adp-12; /* exp(-8) */
+    uint32_t key[2];
+    og_philox_key(seed, DOM_HETERO, key);
+    uint64_t cap = (uint64_t)nA * 24 + nP + 16, k = 0;
+    uint64_t* keys = (uint64_t*)malloc(cap * sizeof(uint64_t));
+    if (!keys) return OG_ERR_NOMEM;
+    for (uint32_t a = 0; a < nA; ++a) {
+        /* Poisson count: blocks (a, 0..): words w1,w2 -> unit; stop when product <= L */
+        uint32_t cnt = 0;
+        double prod = 1.0;
+        for (uint32_t j = 0;; ++j) {
+            prod = prod * og_unit_philox(key, a, j);
+            if (prod <= L) break;
+            ++cnt;
+        }
+        for (uint32_t j = 0; j < cnt; ++j) {
+            const uint32_t p = nA + og_lemire_philox(key, ((uint64_t)1 << 40) | a, j, nP);
+            if (k == cap) {
+                cap *= 2;
+                keys = (uint64_t*)realloc(keys, cap * sizeof(uint64_t));
+            }
+            keys[k++] = ((uint64_t)a << 32) | p;
+        }
+    }
+    for (uint32_t p = 0; p < nP; ++p) {
+        const uint32_t v = nA + nP + og_lemire_philox(key, ((uint64_t)2 << 40) | p, 0, nV);
+        if (k == cap) {
+            cap *= 2;
+            keys = (uint64_t*)realloc(keys, cap * sizeof(uint64_t));
+        }
+        keys[k++] = ((uint64_t)(nA + p) << 32) | v;
+    }
+    qsort(keys, k, sizeof(uint64_t), cmp_u64);
+    uint64_t u = 0;
+    for (uint64_t i = 0; i < k; ++i) {
+        if (u == 0 || keys[u - 1] != keys[i]) keys[u++] = keys[i];
+    }
+    *lo = (uint32_t*)malloc((u ? u : 1) * sizeof(uint32_t));
+    *hi = (uint32_t*)malloc((u ? u : 1) * sizeof(uint32_t));
+    for (uint64_t i = 0; i < u; ++i) {
+        (*lo)[i] = (uint32_t)(keys[i] >> 32);
+        (*hi)[i] = (uint32_t)keys[i];
+    }
+    free(keys);
+    *n_pairs = u;
+    *nA_out = nA;
+    *nP_out = nP;
+    return OG_OK;
+}
+
+void og_free(void* p) { free(p); }
+
+/* ================================================================ models */
+
+static inline uint32_t deg_of(const og_graph* g, uint32_t v) {
+    return (uint32_t)(g->offsets[v + 1] - g->offsets[v]);
+}
+
+/* Graph::neighbor_index_of: lower_bound in N(v), graph.cpp:13-18 */
+static int nbr_index(const og_graph* g, uint32_t v, uint32_t u, uint32_t* idx) {
+    uint64_t lo = g->offsets[v], hi = g->offsets[v + 1];
+    while (lo < hi) {
+        const uint64_t mid = lo + (hi - lo) / 2;
+        if (g->nbr[mid] < u) lo = mid + 1; else hi = mid;
+    }
+    if (lo == g->offsets[v + 1] || g->nbr[lo] != u) return 0;
+    *idx = (uint32_t)(lo - g->offsets[v]);
+    return 1;
+}
+
+/* Graph::edge_type, graph.hpp:47-50 */
+static inline uint16_t edge_type(const og_graph* g, uint32_t v, uint32_t idx) {
+    if (g->etype) return g->etype[g->offsets[v] + idx];
+    return (uint16_t)(g->ntype[v] * g->n_ntypes + g->ntype[g->nbr[g->offsets[v] + idx]]);
+}
+static inline uint16_t edge_type_count(const og_graph* g) {
+    if (g->etype) return g->n_etypes;
+    return (uint16_t)(g->n_ntypes * g->n_ntypes);
+}
+
+static inline int second_order(const og_model* m) {
+    return m->kind == OG_NODE2VEC || m->kind == OG_EDGE2VEC || m->kind == OG_FAIRWALK;
+}
+
+/* metapath_next, models.hpp:82-85 */
+static inline uint32_t metapath_next(const og_model* m, uint32_t affix) {
+    if (affix + 1 < m->mp_len) return affix + 1;
+    return (m->metapath[0] == m->metapath[m->mp_len - 1] && m->mp_len > 1) ? 1 : 0;
+}
+static inline uint16_t required_type(const og_model* m, uint32_t affix) {
+    return m->metapath[metapath_next(m, affix)];
+}
+
+size_t og_type_counts_size(const og_graph* g) { return (size_t)g->n * g->n_ntypes; }
+
+/* WalkModel::bind, models.cpp:29-74 */
+int og_model_bind(const og_graph* g, og_model* m, char* err, size_t errlen) {
+    m->num_types = g->n_ntypes;
+    if (second_order(m)) {
+        if (m->p <= 0 || m->q <= 0) { snprintf(err, errlen, "p and q must be positive"); return OG_ERR_INVALID; }
+        if (!g->symmetric) { snprintf(err, errlen, "model requires a symmetric graph (load with symmetrize)"); return OG_ERR_INVALID; }
+    }
+    if (m->kind == OG_METAPATH2VEC || m->kind == OG_FAIRWALK || m->kind == OG_EDGE2VEC) {
+        if (!g->ntype) { snprintf(err, errlen, "model requires node types"); return OG_ERR_INVALID; }
+    }
+    if (m->kind == OG_METAPATH2VEC) {
+        if (m->mp_len < 2) { snprintf(err, errlen, "metapath needs at least 2 types"); return OG_ERR_INVALID; }
+        for (uint32_t i = 0; i < m->mp_len; ++i) {
+            if (m->metapath[i] >= m->num_types) { snprintf(err, errlen, "metapath type %u not in graph", m->metapath[i]); return OG_ERR_INVALID; }
+        }
+    }
+    if (m->kind == OG_EDGE2VEC) {
+        const uint32_t dim = edge_type_count(g);
+        if (m->M_dim != dim) { snprintf(err, errlen, "edge type matrix must be %ux%u", dim, dim); return OG_ERR_INVALID; }
+        for (uint32_t i = 0; i < dim * dim; ++i) {
+            if (m->M[i] < 0) { snprintf(err, errlen, "edge type matrix entries must be non-negative"); return OG_ERR_INVALID; }
+        }
+    }
+    if (m->kind == OG_FAIRWALK) {
+        if (!m->type_counts) { snprintf(err, errlen, "type_counts buffer missing"); return OG_ERR_INVALID; }
+        memset(m->type_counts, 0, og_type_counts_size(g) * sizeof(uint32_t));
+        for (uint32_t v = 0; v < g->n; ++v) {
+            for (uint64_t e = g->offsets[v]; e < g->offsets[v + 1]; ++e) {
+                ++m->type_counts[(size_t)v * m->num_types + g->ntype[g->nbr[e]]];
+            }
+        }
+    }
+    return OG_OK;
+}
+
+/* WalkModel::alpha, models.cpp:76-80 */
+static double alpha(const og_graph* g, const og_model* m, uint32_t prev, uint32_t cand) {
+    uint32_t idx;
+    if (cand == prev) return 1.0 / m->p;
+    if (nbr_index(g, prev, cand, &idx)) return 1.0;
+    return 1.0 / m->q;
+}
+
+/* WalkModel::calculate_weight, models.cpp:82-123 */
+double og_weight(const og_graph* g, const og_model* m, uint32_t v, uint32_t affix, uint32_t i) {
+    const uint64_t base = g->offsets[v];
+    const double w = g->w[base + i];
+    if (m->kind == OG_DEEPWALK) return w;
+    if (m->kind == OG_METAPATH2VEC) {
+        const uint32_t u = g->nbr[base + i];
+        return g->ntype[u] == required_type(m, affix) ? w : 0.0;
+    }
+    if (affix == OG_NO_AFFIX) return w;
+    const uint32_t s = g->nbr[base + affix];
+    const uint32_t u = g->nbr[base + i];
+    const double a = alpha(g, m, s, u);
+    switch (m->kind) {
+    case OG_NODE2VEC:
+        return a * w;
+    case OG_EDGE2VEC: {
+        uint32_t sv = 0;
+        nbr_index(g, s, v, &sv);
+        const uint16_t in_t = edge_type(g, s, sv);
+        const uint16_t out_t = edge_type(g, v, i);
+        return a * m->M[(size_t)in_t * m->M_dim + out_t] * w;
+    }
+    case OG_FAIRWALK: {
+        const uint32_t group = m->type_counts[(size_t)v * m->num_types + g->ntype[u]];
+        return a * w / (double)group;
+    }
+    default:
+        return w;
+    }
+}
+
+/* accept rule, samplers.hpp:24 verbatim */
+int og_accept(double wc, double wl, double u) { return wl <= 0.0 || wc >= wl || u * wl < wc; }
+
+void og_decide(const og_graph* g, const og_model* m, uint64_t count, const uint32_t* pos,
+               const uint32_t* affix, const uint32_t* cand, const uint32_t* last,
+               const double* u, double* wc, double* wl, uint8_t* accept) {
+    for (uint64_t i = 0; i < count; ++i) {
+        wc[i] = og_weight(g, m, pos[i], affix[i], cand[i]);
+        wl[i] = og_weight(g, m, pos[i], affix[i], last[i]);
+        accept[i] = (uint8_t)og_accept(wc[i], wl[i], u[i]);
+    }
+}
+
+/* ============================================================== samplers */
+
+/* alias_build, samplers.cpp:95-131: sequential total, scaled = w*n/total,
+ * LIFO small/large stacks, leftovers 1.0. */
+int og_alias_build(uint32_t n, const double* w, double* prob, uint32_t* alias) {
+    double total = 0.0;
+    for (uint32_t i = 0; i < n; ++i) total += w[i];
+    if (n == 0 || total <= 0) return OG_ERR_INVALID;
+    for (uint32_t i = 0; i < n; ++i) if (w[i] < 0) return OG_ERR_INVALID;
+    double* scaled = (double*)malloc(n * sizeof(double));
+    uint32_t* small = (uint32_t*)malloc(n * sizeof(uint32_t));
+    uint32_t* large = (uint32_t*)malloc(n * sizeof(uint32_t));
+    uint32_t ns = 0, nl = 0;
+    for (uint32_t i = 0; i < n; ++i) {
+        prob[i] = 1.0;
+        alias[i] = i;
+        scaled[i] = w[i] * (double)n / total;
+    }
+    for (uint32_t i = 0; i < n; ++i) {
+        if (scaled[i] < 1.0) small[ns++] = i; else large[nl++] = i;
+    }
+    while (ns > 0 && nl > 0) {
+        const uint32_t s = small[--ns];
+        const uint32_t l = large[nl - 1];
+        prob[s] = scaled[s];
+        alias[s] = l;
+        scaled[l] -= 1.0 - scaled[s];
+        if (scaled[l] < 1.0) {
+            --nl;
+            small[ns++] = l;
+        }
+    }
+    for (uint32_t i = 0; i < ns; ++i) prob[small[i]] = 1.0;
+    for (uint32_t i = 0; i < nl; ++i) prob[large[i]] = 1.0;
+    free(scaled);
+    free(small);
+    free(large);
+    return OG_OK;
+}
+
+/* direct_sample with the unit supplied, samplers.cpp:133-146 */
+uint32_t og_direct_sample_u(uint32_t n, const double* w, double u) {
+    double total = 0.0;
+    for (uint32_t i = 0; i < n; ++i) total += w[i];
+    double r = u * total;
+    for (uint32_t i = 0; i < n; ++i) {
+        r -= w[i];
+        if (r < 0) return i;
+    }
+    for (uint32_t i = n; i-- > 0;) {
+        if (w[i] > 0) return i;
+    }
+    return 0;
+}
+
+/* ---- per-state sampling context */
+typedef struct {
+    const og_graph* g;
+    const og_model* m;
+    uint32_t v, affix, n;
+} st_t;
+
+static inline double st_w(const st_t* s, uint32_t i) { return og_weight(s->g, s->m, s->v, s->affix, i); }
+
+/* mh_transition, samplers.hpp:18-27 */
+static uint32_t mh_transition(const st_t* s, uint32_t last, draw_t* d) {
+    const uint32_t cand = draw_index(d, s->n);
+    const double wc = st_w(s, cand);
+    const double wl = st_w(s, last);
+    const int accept = wl <= 0.0 || wc >= wl || draw_real(d) * wl < wc;
+    return accept ? cand : last;
+}
+
+/* random_positive, samplers.cpp:22-33 */
+static int random_positive(const st_t* s, draw_t* d, uint32_t* out) {
+    uint32_t positive = 0;
+    for (uint32_t i = 0; i < s->n; ++i) if (st_w(s, i) > 0) ++positive;
+    if (positive == 0) return 0;
+    uint32_t pick = draw_index(d, positive);
+    for (uint32_t i = 0; i < s->n; ++i) {
+        if (st_w(s, i) > 0 && pick-- == 0) { *out = i; return 1; }
+    }
+    return 0;
+}
+
+/* Source of init draws: xoshiro = the querying walker's stream (manager.cpp:40);
+ * philox = slot-keyed blocks (slot, j). */
+typedef struct {
+    int philox;
+    xo_t* xo;
+    uint32_t key[2];
+    uint64_t slot;
+} init_src_t;
+
+static void init_block(const init_src_t* src, uint32_t j, draw_t* d) {
+    draw_open(d, src->philox, src->xo, src->key, src->slot, j);
+}
+
+/* mh_init, samplers.cpp:37-83. Philox block plan: random -> block 0;
+ * high_weight probes -> blocks 0..hw-1, fallback -> block hw; burn_in ->
+ * block 0 pick, blocks 1..k transitions. */
+static int mh_init(const st_t* s, const og_config* c, const init_src_t* src, uint32_t* out) {
+    draw_t d;
+    if (s->n == 0) return 0;
+    switch (c->init_kind) {
+    case OG_INIT_RANDOM:
+        init_block(src, 0, &d);
+        return random_positive(s, &d, out);
+    case OG_INIT_HIGH_WEIGHT: {
+        double best_w = 0.0;
+        uint32_t best = 0;
+        int found = 0;
+        if (s->n <= c->hw_sample_size) {
+            for (uint32_t i = 0; i < s->n; ++i) {
+                const double w = st_w(s, i);
+                if (w > best_w) { best_w = w; best = i; found = 1; }
+            }
+        } else {
+            for (uint32_t probe = 0; probe < c->hw_sample_size; ++probe) {
+                init_block(src, probe, &d);
+                const uint32_t i = draw_index(&d, s->n);
+                const double w = st_w(s, i);
+                if (w > best_w || (w == best_w && found && i < best)) {
+                    if (w > 0) { best_w = w; best = i; found = 1; }
+                }
+            }
+            if (!found) {
+                init_block(src, c->hw_sample_size, &d);
+                return random_positive(s, &d, out);
+            }
+        }
+        if (found) *out = best;
+        return found;
+    }
+    case OG_INIT_BURN_IN: {
+        uint32_t last;
+        init_block(src, 0, &d);
+        if (!random_positive(s, &d, &last)) return 0;
+        for (uint32_t i = 0; i < c->burn_in_steps; ++i) {
+            init_block(src, 1 + i, &d);
+            last = mh_transition(s, last, &d);
+        }
+        *out = last;
+        return 1;
+    }
+    }
+    return 0;
+}
+
+/* slot layout, manager.cpp:14-17 + models.cpp:146-172 */
+uint64_t og_slot_count(const og_graph* g, const og_model* m) {
+    switch (m->kind) {
+    case OG_DEEPWALK: return g->n;
+    case OG_METAPATH2VEC: return (uint64_t)g->n * m->num_types;
+    default: return g->m;
+    }
+}
+static inline uint64_t slot_index(const og_graph* g, const og_model* m, uint32_t v, uint32_t affix) {
+    switch (m->kind) {
+    case OG_DEEPWALK: return v;
+    case OG_METAPATH2VEC: return (uint64_t)v * m->num_types + required_type(m, affix);
+    default: return g->offsets[v] + affix;
+    }
+}
+
+int og_init_philox(const og_graph* g, const og_model* m, const og_config* c, uint32_t v,
+                   uint32_t affix, uint64_t slot, uint32_t* last) {
+    st_t s = {g, m, v, affix, deg_of(g, v)};
+    init_src_t src;
+    src.philox = 1;
+    src.xo = NULL;
+    og_philox_key(c->seed, DOM_INIT, src.key);
+    src.slot = slot;
+    return mh_init(&s, c, &src, last);
+}
+
+/* ================================================================ engine */
+
+enum { ST_EMPTY = 0, ST_READY = 2, ST_DEAD = 3 };
+
+typedef struct {
+    uint8_t* status;
+    uint32_t* last;
+} chain_t;
+
+typedef struct {
+    uint32_t v, affix;
+    xo_t xo;
+    uint64_t walker, row;
+    uint32_t len;
+    int alive;
+} walker_t;
+
+/* One walker step = WalkerContext::next_edge (engine.cpp:75-87) + the push and
+ * update_state of engine.cpp:201-204. Returns 1 stepped, 0 dead end, -1 error. */
+static int walker_step(const og_graph* g, const og_model* m, const og_config* c, chain_t* ch,
+                       walker_t* w, uint32_t step, uint32_t stride, uint32_t* rows,
+                       og_stats* st, char* err, size_t errlen) {
+    const uint32_t v = w->v;
+    const uint32_t deg = deg_of(g, v);
+    if (deg == 0) return 0;
+    const int philox = c->rng == OG_RNG_PHILOX;
+    uint32_t wkey[2];
+    og_philox_key(c->seed, DOM_WALK, wkey);
+    draw_t d;
+    draw_open(&d, philox, &w->xo, wkey, w->walker, step);
+    uint32_t edge;
+    if (second_order(m) && w->affix == OG_NO_AFFIX) {
+        /* bootstrap: draw_static (engine.cpp:81-83, :130-134) */
+        const double* ws = g->w + g->offsets[v];
+        double total = 0.0;
+        for (uint32_t i = 0; i < deg; ++i) total += ws[i];
+        if (total <= 0) return 0;
+        edge = og_direct_sample_u(deg, ws, draw_real(&d));
+    } else {
+        /* SamplerManager::sample, manager.cpp:30-72 */
+        const uint64_t slot = slot_index(g, m, v, w->affix);
+        st_t s = {g, m, v, w->affix, deg};
+        if (ch->status[slot] == ST_EMPTY) {
+            init_src_t src;
+            src.philox = philox;
+            src.xo = &w->xo;
+            og_philox_key(c->seed, DOM_INIT, src.key);
+            src.slot = slot;
+            uint32_t init;
+            st->init_calls++;
+            if (mh_init(&s, c, &src, &init)) {
+                ch->last[slot] = init;
+                ch->status[slot] = ST_READY;
+            } else {
+                ch->status[slot] = ST_DEAD;
+            }
+        }
+        if (ch->status[slot] == ST_DEAD) return 0;
+        const uint32_t last = ch->last[slot];
+        /* the philox block is (walker, step); xoshiro continues the stream */
+        if (philox) draw_open(&d, 1, NULL, wkey, w->walker, step);
+        const uint32_t next = mh_transition(&s, last, &d);
+        if (next != last) ch->last[slot] = next;
+        edge = next;
+    }
+    const uint32_t nxt = g->nbr[g->offsets[v] + edge];
+    rows[w->row * stride + w->len] = nxt;
+    w->len++;
+    /* update_state, models.cpp:125-136 */
+    if (m->kind == OG_DEEPWALK) {
+        w->affix = OG_NO_AFFIX;
+    } else if (m->kind == OG_METAPATH2VEC) {
+        w->affix = metapath_next(m, w->affix);
+    } else {
+        uint32_t back;
+        if (!nbr_index(g, nxt, v, &back)) {
+            snprintf(err, errlen, "second-order walk on asymmetric adjacency: no back edge %u->%u", nxt, v);
+            return -1;
+        }
+        w->affix = back;
+    }
+    w->v = nxt;
+    st->steps++;
+    return 1;
+}
+
+int og_generate_walks(const og_graph* g, const og_model* m, const og_config* c, uint32_t stride,
+                      uint32_t* rows, uint32_t* lens, uint64_t* n_rows, og_stats* stats,
+                      char* err, size_t errlen) {
+    memset(stats, 0, sizeof(*stats));
+    if (c->K == 0 || c->L == 0) {
+        snprintf(err, errlen, "walks_per_node, walk_length and threads must be positive");
+        return OG_ERR_INVALID;
+    }
+    if (stride < c->L + 1) { snprintf(err, errlen, "row stride too small"); return OG_ERR_INVALID; }
+    const uint64_t slots = og_slot_count(g, m);
+    if (slots > ((uint64_t)1 << 40)) { snprintf(err, errlen, "sampler layout too large"); return OG_ERR_INVALID; }
+    chain_t ch;
+    ch.status = (uint8_t*)calloc(slots ? slots : 1, 1);
+    ch.last = (uint32_t*)calloc(slots ? slots : 1, sizeof(uint32_t));
+    const uint64_t total = (uint64_t)g->n * c->K;
+    int rc = OG_OK;
+    uint64_t row = 0;
+    if (c->order == OG_ORDER_WALKER) {
+        for (uint64_t idx = 0; idx < total && rc == OG_OK; ++idx) {
+            walker_t w;
+            w.v = (uint32_t)(idx / c->K);
+            const uint32_t k = (uint32_t)(idx % c->K);
+            xo_walker(&w.xo, c->seed, w.v, k);
+            w.walker = idx;
+            if (m->kind == OG_METAPATH2VEC) {
+                if (g->ntype[w.v] != m->metapath[0]) { stats->skipped++; continue; }
+                w.affix = 0;
+            } else {
+                w.affix = OG_NO_AFFIX;
+            }
+            w.row = row++;
+            rows[w.row * stride] = w.v;
+            w.len = 1;
+            for (uint32_t step = 0; step < c->L; ++step) {
+                const int r = walker_step(g, m, c, &ch, &w, step, stride, rows, stats, err, errlen);
+                if (r < 0) { rc = OG_ERR_INVALID; break; }
+                if (r == 0) { stats->early++; break; }
+            }
+            lens[w.row] = w.len;
+        }
+    } else {
+        walker_t* ws = (walker_t*)malloc((total ? total : 1) * sizeof(walker_t));
+        uint64_t nw = 0;
+        for (uint64_t idx = 0; idx < total; ++idx) {
+            walker_t* w = &ws[nw];
+            w->v = (uint32_t)(idx / c->K);
+            const uint32_t k = (uint32_t)(idx % c->K);
+            if (m->kind == OG_METAPATH2VEC) {
+                if (g->ntype[w->v] != m->metapath[0]) { stats->skipped++; continue; }
+                w->affix = 0;
+            } else {
+                w->affix = OG_NO_AFFIX;
+            }
+            xo_walker(&w->xo, c->seed, w->v, k);
+            w->walker = idx;
+            w->row = row++;
+            rows[w->row * stride] = w->v;
+            w->len = 1;
+            w->alive = 1;
+            ++nw;
+        }
+        for (uint32_t step = 0; step < c->L && rc == OG_OK; ++step) {
+            for (uint64_t i = 0; i < nw; ++i) {
+                walker_t* w = &ws[i];
+                if (!w->alive) continue;
+                const int r = walker_step(g, m, c, &ch, w, step, stride, rows, stats, err, errlen);
+                if (r < 0) { rc = OG_ERR_INVALID; break; }
+                if (r == 0) { stats->early++; w->alive = 0; }
+            }
+        }
+        for (uint64_t i = 0; i < nw; ++i) lens[ws[i].row] = ws[i].len;
+        free(ws);
+    }
+    stats->walks = row;
+    *n_rows = row;
+    free(ch.status);
+    free(ch.last);
+    return rc;
+}
+
+/* ===================================================== threaded baseline */
+
+typedef struct {
+    const og_graph* g;
+    const og_model* m;
+    const og_config* c;
+    chain_t* ch;
+    uint64_t begin, stride, count;
+    og_stats st;
+    uint32_t* row;
+} mt_arg_t;
+
+static void* mt_worker(void* p) {
+    mt_arg_t* a = (mt_arg_t*)p;
+    char err[256];
+    memset(&a->st, 0, sizeof(a->st));
+    for (uint64_t j = 0; j < a->count; ++j) {
+        const uint64_t idx = a->begin + j * a->stride;
+        walker_t w;
+        w.v = (uint32_t)(idx / a->c->K);
+        w.walker = idx;
+        xo_walker(&w.xo, a->c->seed, w.v, idx % a->c->K);
+        if (a->m->kind == OG_METAPATH2VEC) {
+            if (a->g->ntype[w.v] != a->m->metapath[0]) { a->st.skipped++; continue; }
+            w.affix = 0;
+        } else {
+            w.affix = OG_NO_AFFIX;
+        }
+        w.row = 0;
+        w.len = 1;
+        for (uint32_t step = 0; step < a->c->L; ++step) {
+            w.len = 1;
+            const int r = walker_step(a->g, a->m, a->c, a->ch, &w, step, 0, a->row, &a->st, err, sizeof err);
+            if (r <= 0) { a->st.early++; break; }
+        }
+        a->st.walks++;
+    }
+    return NULL;
+}
+
+int og_walks_sample_mt(const og_graph* g, const og_model* m, const og_config* c,
+                       uint64_t walker_begin, uint64_t walker_stride, uint64_t walker_count,
+                       uint32_t threads, og_stats* stats, double* seconds) {
+    const uint64_t slots = og_slot_count(g, m);
+    chain_t ch;
+    ch.status = (uint8_t*)calloc(slots ? slots : 1, 1);
+    ch.last = (uint32_t*)calloc(slots ? slots : 1, sizeof(uint32_t));
+    if (threads == 0) threads = 1;
+    mt_arg_t* args = (mt_arg_t*)calloc(threads, sizeof(mt_arg_t));
+    pthread_t* th = (pthread_t*)calloc(threads, sizeof(pthread_t));
+    uint32_t* scratch = (uint32_t*)calloc(threads, sizeof(uint32_t) * 4);
+    struct timespec t0, t1;
+    clock_gettime(CLOCK_MONOTONIC, &t0);
+    for (uint32_t t = 0; t < threads; ++t) {
+        const uint64_t b = walker_count * t / threads, e = walker_count * (t + 1) / threads;
+        args[t].g = g; args[t].m = m; args[t].c = c; args[t].ch = &ch;
+        args[t].begin = walker_begin + b * walker_stride;
+        args[t].stride = walker_stride;
+        args[t].count = e - b;
+        args[t].row = scratch + 4 * t;
+        pthread_create(&th[t], NULL, mt_worker, &args[t]);
+    }
+    memset(stats, 0, sizeof(*stats));
+    for (uint32_t t = 0; t < threads; ++t) {
+        pthread_join(th[t], NULL);
+        stats->walks += args[t].st.walks;
+        stats->early += args[t].st.early;
+        stats->skipped += args[t].st.skipped;
+        stats->steps += args[t].st.steps;
+        stats->init_calls += args[t].st.init_calls;
+    }
+    clock_gettime(CLOCK_MONOTONIC, &t1);
+    *seconds = (double)(t1.tv_sec - t0.tv_sec) + 1e-9 * (double)(t1.tv_nsec - t0.tv_nsec);
+    free(args);
+    free(th);
+    free(scratch);
+    free(ch.status);
+    free(ch.last);
+    return OG_OK;
+}
