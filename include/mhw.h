@@ -1,0 +1,277 @@
+/*
+ * mhw.h -- C ABI of the B200-native M-H random-walk engine (libmhw.so).
+ *
+ * Drop-in boundary for the reference's walk path (the C++ API of
+ * /root/reference/proj, "mhwalk"). Plain C: POD structs, pointers and sizes,
+ * no C++ or torch types. Each entry point names the reference interface it
+ * replaces (file:line relative to the reference's proj/ directory).
+ *
+ * Status codes mirror the reference's error classes (errors.hpp:8-21, mapped
+ * to exit codes at tools/mhwalk.cpp:529-541):
+ *   MHW_OK 0, MHW_ERR_IO 1 (IoError), MHW_ERR_INVALID 2 (ParseError /
+ *   ValidationError), MHW_ERR_CUDA 4 (device failure or out of memory).
+ * The message of the last failure on the calling thread is mhw_last_error().
+ *
+ * Threading: every call is blocking and reentrant per handle (a graph or
+ * session handle must not be used by two host threads at once). Walker
+ * parallelism is internal: GPU threads, plus one host thread per device for
+ * mhw_generate_walks_multi.
+ */
+#ifndef MHW_H
+#define MHW_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define MHW_API __attribute__((visibility("default")))
+#else
+#define MHW_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef int32_t mhw_status;
+#define MHW_OK 0
+#define MHW_ERR_IO 1
+#define MHW_ERR_INVALID 2
+#define MHW_ERR_CUDA 4
+
+/* ModelKind order, models.hpp:13 */
+typedef enum {
+    MHW_DEEPWALK = 0,
+    MHW_NODE2VEC = 1,
+    MHW_METAPATH2VEC = 2,
+    MHW_EDGE2VEC = 3,
+    MHW_FAIRWALK = 4
+} mhw_model_kind;
+
+/* InitStrategy::Kind order, samplers.hpp:30 */
+typedef enum { MHW_INIT_RANDOM = 0, MHW_INIT_HIGH_WEIGHT = 1, MHW_INIT_BURN_IN = 2 } mhw_init_kind;
+
+/* SamplerKind order, engine.hpp:12. Only MHW_SAMPLER_MH is the product path;
+ * the baseline samplers are rejected with MHW_ERR_INVALID. */
+typedef enum {
+    MHW_SAMPLER_MH = 0,
+    MHW_SAMPLER_ALIAS = 1,
+    MHW_SAMPLER_DIRECT = 2,
+    MHW_SAMPLER_REJECTION = 3
+} mhw_sampler_kind;
+
+/* throughput: persistent kernel, chain updates linearised by CAS (exact M-H
+ * per slot, interleaving order not reproducible).
+ * deterministic: step-synchronous, same-slot contenders folded in walker-id
+ * order; byte-reproducible (the GPU counterpart of threads=1,
+ * engine.hpp:43-46). */
+typedef enum { MHW_SCHEDULE_THROUGHPUT = 0, MHW_SCHEDULE_DETERMINISTIC = 1 } mhw_schedule;
+
+#define MHW_NO_AFFIX 0xFFFFFFFFu /* kNoAffix, models.hpp:17 */
+
+/* Host view of a CSR graph. Replaces mhwalk::Graph (graph.hpp:15-55) with the
+ * device layout's types: int64 offsets, int32 sorted ids, fp32 weights
+ * (NULL = unweighted, every weight 1.0), uint16 node/edge types. */
+typedef struct mhw_graph_view {
+    uint32_t node_count;
+    uint64_t arc_count;
+    const int64_t* offsets;      /* node_count + 1 */
+    const int32_t* neighbors;    /* arc_count, strictly ascending per slice */
+    const float* weights;        /* arc_count or NULL */
+    const uint16_t* node_types;  /* node_count or NULL */
+    const uint16_t* edge_types;  /* arc_count or NULL */
+    uint16_t num_node_types;
+    uint16_t num_edge_types;
+    int32_t symmetric;           /* Graph::symmetric */
+} mhw_graph_view;
+
+/* Replaces mhwalk::WalkModel's public fields (models.hpp:40-47). */
+typedef struct mhw_model_desc {
+    int32_t kind;                 /* mhw_model_kind */
+    double p, q;
+    const uint16_t* metapath;     /* metapath2vec */
+    uint32_t metapath_len;
+    const double* type_matrix;    /* edge2vec, dim x dim row-major */
+    uint32_t type_matrix_dim;
+} mhw_model_desc;
+
+/* Replaces mhwalk::WalkConfig + InitStrategy (engine.hpp:19-26,
+ * samplers.hpp:29-34). node_begin/node_end select the walker partition
+ * (start nodes [begin, end), end == 0 means all nodes). */
+typedef struct mhw_walk_config {
+    uint32_t walks_per_node;   /* K, default 10 */
+    uint32_t walk_length;      /* L steps, default 80 */
+    uint64_t seed;
+    int32_t sampler;           /* mhw_sampler_kind */
+    int32_t init_kind;         /* mhw_init_kind */
+    uint32_t burn_in_steps;    /* default 100 */
+    uint32_t hw_sample_size;   /* default 32 */
+    int32_t schedule;          /* mhw_schedule */
+    uint32_t node_begin;
+    uint32_t node_end;
+} mhw_walk_config;
+
+/* Replaces mhwalk::RunStats (engine.hpp:28-36). init_seconds is not
+ * separable inside the fused kernel and is reported as 0; walk_seconds is the
+ * device time of the walk kernels (CUDA events). */
+typedef struct mhw_walk_stats {
+    uint64_t walks;
+    uint64_t early_terminations;
+    uint64_t skipped_starts;
+    uint64_t steps;
+    uint64_t slot_inits;
+    double steps_per_sec;
+    double init_seconds;
+    double walk_seconds;
+} mhw_walk_stats;
+
+typedef struct mhw_graph_info {
+    uint32_t node_count;
+    uint64_t arc_count;
+    int32_t weighted;
+    int32_t symmetric;          /* the flag */
+    int32_t verified_symmetric; /* every arc has its back arc (checked on device) */
+    uint16_t num_node_types;
+    uint16_t num_edge_types;
+    uint32_t max_degree;
+    uint32_t isolated_nodes;
+    uint64_t device_bytes;
+    int32_t device;
+} mhw_graph_info;
+
+typedef struct mhw_graph mhw_graph;
+typedef struct mhw_walks mhw_walks;
+typedef struct mhw_session mhw_session;
+
+MHW_API const char* mhw_last_error(void);
+MHW_API const char* mhw_version(void);
+MHW_API int32_t mhw_device_count(void);
+
+/* ---- graphs (device-resident CSR) ------------------------------------ */
+
+/* Copies a host CSR to `device`. Replaces constructing mhwalk::Graph in
+ * memory (graph.hpp:15-55); validates slices like build_csr's output. */
+MHW_API mhw_status mhw_graph_upload(const mhw_graph_view* view, int32_t device, mhw_graph** out);
+
+/* Device CSR build from an edge list with build_csr semantics: sort by
+ * (src, dst), duplicates summed, optional symmetrisation without self-loop
+ * doubling, n = max id + 1 unless node_count is larger. Replaces
+ * load_edge_list's build step (graph.cpp:35-100). */
+MHW_API mhw_status mhw_graph_from_edges(uint64_t edge_count, const uint32_t* src, const uint32_t* dst,
+                                const float* weights, int32_t symmetrize, uint32_t node_count,
+                                int32_t device, mhw_graph** out);
+
+/* Synthetic generators, built on device.
+ * weighted = 0 -> unweighted; edge_type_count > 0 -> one uniform type per
+ * undirected edge (both directions). */
+MHW_API mhw_status mhw_graph_generate_rmat(uint32_t scale, uint32_t edge_factor, double a, double b,
+                                   double c, uint64_t seed, int32_t weighted, float weight_lo,
+                                   float weight_hi, uint32_t edge_type_count, int32_t device,
+                                   mhw_graph** out);
+MHW_API mhw_status mhw_graph_generate_hetero(uint32_t node_count, uint64_t seed, float weight_lo,
+                                     float weight_hi, int32_t device, mhw_graph** out);
+
+/* load_node_types / load_edge_types (graph.cpp:102-177) from arrays. */
+MHW_API mhw_status mhw_graph_set_node_types(mhw_graph* g, const uint16_t* types, uint16_t num_types);
+MHW_API mhw_status mhw_graph_set_edge_types(mhw_graph* g, const uint16_t* types, uint16_t num_types);
+
+/* Copy of the graph to another device (peer copy); walkers can then be
+ * partitioned across replicas with mhw_generate_walks_multi. */
+MHW_API mhw_status mhw_graph_replicate(const mhw_graph* g, int32_t device, mhw_graph** out);
+
+MHW_API mhw_status mhw_graph_info_get(const mhw_graph* g, mhw_graph_info* info);
+
+/* Parity dump of the device CSR into host arrays (any may be NULL). */
+MHW_API mhw_status mhw_graph_download(const mhw_graph* g, int64_t* offsets, int32_t* neighbors,
+                              float* weights, uint16_t* node_types, uint16_t* edge_types);
+MHW_API void mhw_graph_free(mhw_graph* g);
+
+/* ---- walks ------------------------------------------------------------ */
+
+/* Replaces generate_walks (engine.hpp:47, engine.cpp:157-234): blocking,
+ * returns a host corpus in the reference's order (walker idx = v*K + k,
+ * skipped starts omitted). */
+MHW_API mhw_status mhw_generate_walks(const mhw_graph* g, const mhw_model_desc* model,
+                              const mhw_walk_config* config, mhw_walks** out);
+
+/* Same, with walkers partitioned across replicas (one host thread per
+ * device, contiguous start-node ranges balanced by active walkers). The
+ * corpus is the concatenation in replica order. */
+MHW_API mhw_status mhw_generate_walks_multi(const mhw_graph* const* replicas, int32_t n_replicas,
+                                    const mhw_model_desc* model, const mhw_walk_config* config,
+                                    mhw_walks** out);
+
+/* Corpus size of a call (rows = walks incl. isolated starts, stride = padded
+ * row length) so callers can provide their own (pinned) buffers. */
+MHW_API mhw_status mhw_walk_rows(const mhw_graph* g, const mhw_model_desc* model, const mhw_walk_config* config,
+                         uint64_t* rows, uint32_t* stride);
+
+/* generate_walks into caller-owned host buffers (rows x stride nodes,
+ * rows lengths); capacity_rows guards the buffer size. */
+MHW_API mhw_status mhw_generate_walks_into(const mhw_graph* g, const mhw_model_desc* model,
+                                   const mhw_walk_config* config, uint32_t* h_nodes,
+                                   uint32_t* h_lengths, uint64_t capacity_rows,
+                                   mhw_walk_stats* stats);
+
+MHW_API uint64_t mhw_walks_count(const mhw_walks* w);
+MHW_API uint32_t mhw_walks_stride(const mhw_walks* w);
+MHW_API const uint32_t* mhw_walks_nodes(const mhw_walks* w);   /* count x stride, row r = walk r */
+MHW_API const uint32_t* mhw_walks_lengths(const mhw_walks* w); /* count */
+MHW_API mhw_status mhw_walks_stats(const mhw_walks* w, mhw_walk_stats* stats);
+MHW_API void mhw_walks_free(mhw_walks* w);
+
+/* Writes the corpus like write_corpus (engine.cpp:236-259): one walk per
+ * line, space separated, plus <path>.stats.jsonl. */
+MHW_API mhw_status mhw_walks_write(const mhw_walks* w, const char* path);
+
+/* Balanced walker partition: cut points of [0, n) into `parts` contiguous
+ * start-node ranges with equal active-walker counts.
+ * cuts has parts + 1 entries. */
+MHW_API mhw_status mhw_partition_nodes(const mhw_graph* g, const mhw_model_desc* model, int32_t parts,
+                               uint32_t* cuts);
+
+/* ---- device-resident sessions (benchmarks, repeated runs) ------------- */
+
+MHW_API mhw_status mhw_session_create(const mhw_graph* g, const mhw_model_desc* model,
+                              const mhw_walk_config* config, mhw_session** out);
+/* Enqueues one full generate_walks on `stream` (cudaStream_t, NULL = the
+ * session's own): chain table reset to EMPTY, then the walk kernels. The
+ * corpus stays in HBM. */
+MHW_API mhw_status mhw_session_run(mhw_session* s, void* stream);
+/* Synchronizes and fetches the counters of the last run. */
+MHW_API mhw_status mhw_session_stats(mhw_session* s, mhw_walk_stats* stats);
+/* Device pointers of the padded walk buffer (rows x stride) and lengths. */
+MHW_API mhw_status mhw_session_buffers(mhw_session* s, uint32_t** d_nodes, uint32_t** d_lengths,
+                               uint64_t* rows, uint32_t* stride);
+/* D2H of the corpus into caller buffers (pinned for full speed). */
+MHW_API mhw_status mhw_session_download(mhw_session* s, uint32_t* h_nodes, uint32_t* h_lengths,
+                                void* stream);
+/* Number of kernels the last mhw_session_run enqueued. */
+MHW_API uint32_t mhw_session_launches(const mhw_session* s);
+MHW_API void mhw_session_free(mhw_session* s);
+
+/* ---- parity entry points ---------------------------------------------- */
+
+/* (state, candidate, last, u) -> (w'(cand), w'(last), accept) on device, for
+ * host arrays of `count` triples. calculate_weight (models.cpp:82-123) and
+ * the accept rule of mh_transition (samplers.hpp:21-26). */
+MHW_API mhw_status mhw_decide(const mhw_graph* g, const mhw_model_desc* model, uint64_t count,
+                      const uint32_t* position, const uint32_t* affixture,
+                      const uint32_t* candidate, const uint32_t* last, const double* u,
+                      double* w_cand, double* w_last, uint8_t* accept);
+
+/* Per-node static-weight alias tables, alias_build (samplers.cpp:95-131),
+ * into host arrays of arc_count entries (node v's table at offsets[v]). */
+MHW_API mhw_status mhw_alias_tables(const mhw_graph* g, double* prob, uint32_t* alias);
+
+/* Slot initialisation of (position, affixture) states under the engine's
+ * slot-keyed Philox layout (mh_init, samplers.cpp:37-83); returns the initial
+ * Last index or MHW_NO_AFFIX for a dead end. */
+MHW_API mhw_status mhw_init_states(const mhw_graph* g, const mhw_model_desc* model,
+                           const mhw_walk_config* config, uint64_t count,
+                           const uint32_t* position, const uint32_t* affixture, uint32_t* last);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MHW_H */

@@ -1,0 +1,502 @@
+// api.cu -- the extern "C" boundary (include/mhw.h). Every entry point
+// converts exceptions to status codes (errors.hpp classes -> 1/2/4) and keeps
+// the message in a thread-local buffer (mhw_last_error).
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <new>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "internal.h"
+#include "walk.h"
+
+struct mhw_walks {
+    std::vector<uint32_t> nodes;
+    std::vector<uint32_t> lens;
+    uint64_t rows = 0;
+    uint32_t stride = 0;
+    mhw_walk_stats stats{};
+};
+
+namespace {
+
+thread_local std::string g_error;
+
+void set_error(const std::string& s) { g_error = s; }
+
+template <class F>
+mhw_status guard(F&& f) {
+    try {
+        f();
+        return MHW_OK;
+    } catch (const mhw::Error& e) {
+        set_error(e.what());
+        return e.code;
+    } catch (const std::bad_alloc&) {
+        set_error("host out of memory");
+        return MHW_ERR_CUDA;
+    } catch (const std::exception& e) {
+        set_error(e.what());
+        return MHW_ERR_CUDA;
+    }
+}
+
+void need(const void* p, const char* what) {
+    if (!p) mhw::invalid(std::string(what) + " must not be NULL");
+}
+
+mhw::Graph* new_graph(int device) {
+    int count = 0;
+    if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0)
+        throw mhw::Error(MHW_ERR_CUDA, "no CUDA device available (the engine has no CPU fallback)");
+    if (device < 0 || device >= count) mhw::invalid("device index out of range");
+    auto* g = new mhw_graph();
+    g->device = device;
+    return g;
+}
+
+template <class F>
+mhw_status build_graph(int32_t device, mhw_graph** out, F&& f) {
+    return guard([&] {
+        need(out, "out");
+        std::unique_ptr<mhw_graph> g(static_cast<mhw_graph*>(new_graph(device)));
+        mhw::DeviceGuard dg(device);
+        f(*g);
+        *out = g.release();
+    });
+}
+
+void run_into(const mhw_graph* gc, const mhw_model_desc* model, const mhw_walk_config* cfg, uint32_t* nodes,
+              uint32_t* lens, uint64_t capacity, mhw_walk_stats* stats, uint64_t* rows_out) {
+    need(gc, "graph");
+    need(model, "model");
+    need(cfg, "config");
+    auto* g = const_cast<mhw_graph*>(gc);
+    mhw::DeviceGuard dg(g->device);
+    mhw_session s;
+    mhw::session_create(s, *g, *model, *cfg);
+    if (nodes && s.rows > capacity) mhw::invalid("output buffer too small for the corpus");
+    mhw::session_run(s, nullptr);
+    mhw_walk_stats st{};
+    mhw::session_stats(s, st);
+    if (nodes || lens) mhw::session_download(s, nodes, lens, nullptr);
+    if (stats) *stats = st;
+    if (rows_out) *rows_out = s.rows;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* mhw_last_error(void) { return g_error.c_str(); }
+const char* mhw_version(void) { return "mhw 0.1.0 (sm_100a)"; }
+
+int32_t mhw_device_count(void) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return n;
+}
+
+mhw_status mhw_graph_upload(const mhw_graph_view* view, int32_t device, mhw_graph** out) {
+    return build_graph(device, out, [&](mhw::Graph& g) {
+        need(view, "view");
+        mhw::graph_upload(g, *view);
+    });
+}
+
+mhw_status mhw_graph_from_edges(uint64_t edge_count, const uint32_t* src, const uint32_t* dst,
+                                const float* weights, int32_t symmetrize, uint32_t node_count,
+                                int32_t device, mhw_graph** out) {
+    return build_graph(device, out, [&](mhw::Graph& g) {
+        if (edge_count) {
+            need(src, "src");
+            need(dst, "dst");
+            if (weights)
+                for (uint64_t i = 0; i < edge_count; ++i)
+                    if (!(weights[i] >= 0)) mhw::invalid("negative edge weight");
+        }
+        mhw::graph_from_edges(g, edge_count, src, dst, weights, symmetrize != 0, node_count);
+    });
+}
+
+mhw_status mhw_graph_generate_rmat(uint32_t scale, uint32_t edge_factor, double a, double b, double c,
+                                   uint64_t seed, int32_t weighted, float weight_lo, float weight_hi,
+                                   uint32_t edge_type_count, int32_t device, mhw_graph** out) {
+    return build_graph(device, out, [&](mhw::Graph& g) {
+        if (weighted && !(weight_lo >= 0 && weight_hi >= weight_lo)) mhw::invalid("bad weight range");
+        if (edge_type_count > 65535) mhw::invalid("too many edge types");
+        mhw::graph_generate_rmat(g, scale, edge_factor, a, b, c, seed, weighted != 0, weight_lo, weight_hi,
+                                 edge_type_count);
+    });
+}
+
+mhw_status mhw_graph_generate_hetero(uint32_t node_count, uint64_t seed, float weight_lo, float weight_hi,
+                                     int32_t device, mhw_graph** out) {
+    return build_graph(device, out, [&](mhw::Graph& g) {
+        if (!(weight_lo >= 0 && weight_hi >= weight_lo)) mhw::invalid("bad weight range");
+        mhw::graph_generate_hetero(g, node_count, seed, weight_lo, weight_hi);
+    });
+}
+
+mhw_status mhw_graph_set_node_types(mhw_graph* g, const uint16_t* types, uint16_t num_types) {
+    return guard([&] {
+        need(g, "graph");
+        need(types, "types");
+        mhw::graph_set_node_types(*g, types, num_types);
+    });
+}
+
+mhw_status mhw_graph_set_edge_types(mhw_graph* g, const uint16_t* types, uint16_t num_types) {
+    return guard([&] {
+        need(g, "graph");
+        need(types, "types");
+        mhw::graph_set_edge_types(*g, types, num_types);
+    });
+}
+
+mhw_status mhw_graph_replicate(const mhw_graph* g, int32_t device, mhw_graph** out) {
+    return build_graph(device, out, [&](mhw::Graph& d) {
+        need(g, "graph");
+        mhw::graph_replicate(*g, d, device);
+    });
+}
+
+mhw_status mhw_graph_info_get(const mhw_graph* g, mhw_graph_info* info) {
+    return guard([&] {
+        need(g, "graph");
+        need(info, "info");
+        info->node_count = g->n;
+        info->arc_count = g->m;
+        info->weighted = g->weighted();
+        info->symmetric = g->symmetric;
+        info->verified_symmetric = g->verified_sym;
+        info->num_node_types = g->n_ntypes;
+        info->num_edge_types = g->n_etypes;
+        info->max_degree = g->max_deg;
+        info->isolated_nodes = g->isolated;
+        info->device_bytes = g->device_bytes();
+        info->device = g->device;
+    });
+}
+
+mhw_status mhw_graph_download(const mhw_graph* g, int64_t* offsets, int32_t* neighbors, float* weights,
+                              uint16_t* node_types, uint16_t* edge_types) {
+    return guard([&] {
+        need(g, "graph");
+        mhw::graph_download(*g, offsets, neighbors, weights, node_types, edge_types);
+    });
+}
+
+void mhw_graph_free(mhw_graph* g) {
+    if (!g) return;
+    mhw::DeviceGuard dg(g->device);
+    if (g->stream) cudaStreamDestroy(g->stream);
+    delete g;
+}
+
+mhw_status mhw_generate_walks(const mhw_graph* g, const mhw_model_desc* model, const mhw_walk_config* config,
+                              mhw_walks** out) {
+    return guard([&] {
+        need(out, "out");
+        need(g, "graph");
+        need(model, "model");
+        need(config, "config");
+        auto* gg = const_cast<mhw_graph*>(g);
+        mhw::DeviceGuard dg(gg->device);
+        mhw_session s;
+        mhw::session_create(s, *gg, *model, *config);
+        std::unique_ptr<mhw_walks> w(new mhw_walks());
+        w->rows = s.rows;
+        w->stride = s.stride;
+        w->nodes.resize(s.rows * s.stride);
+        w->lens.resize(s.rows);
+        mhw::session_run(s, nullptr);
+        mhw::session_stats(s, w->stats);
+        mhw::session_download(s, w->nodes.data(), w->lens.data(), nullptr);
+        *out = w.release();
+    });
+}
+
+mhw_status mhw_generate_walks_multi(const mhw_graph* const* replicas, int32_t n_replicas,
+                                    const mhw_model_desc* model, const mhw_walk_config* config, mhw_walks** out) {
+    return guard([&] {
+        need(out, "out");
+        need(replicas, "replicas");
+        need(model, "model");
+        need(config, "config");
+        if (n_replicas <= 0) mhw::invalid("need at least one replica");
+        for (int i = 0; i < n_replicas; ++i) need(replicas[i], "replica");
+        const uint32_t n = replicas[0]->n;
+        const uint32_t b = config->node_begin, e = config->node_end ? config->node_end : n;
+        std::vector<uint32_t> cuts(n_replicas + 1);
+        {
+            auto* g0 = const_cast<mhw_graph*>(replicas[0]);
+            mhw::partition_nodes(*g0, *model, n_replicas, cuts.data());
+        }
+        // clamp the balanced cuts to the requested range
+        for (auto& c : cuts) c = std::min(std::max(c, b), e);
+        cuts.front() = b;
+        cuts.back() = e;
+        std::vector<std::unique_ptr<mhw_session>> ss(n_replicas);
+        std::vector<std::string> errs(n_replicas);
+        std::vector<mhw_status> codes(n_replicas, MHW_OK);
+        auto par = [&](auto&& body) {
+            std::vector<std::thread> th;
+            for (int i = 0; i < n_replicas; ++i)
+                th.emplace_back([&, i] {
+                    try {
+                        body(i);
+                    } catch (const mhw::Error& x) {
+                        codes[i] = x.code;
+                        errs[i] = x.what();
+                    } catch (const std::exception& x) {
+                        codes[i] = MHW_ERR_CUDA;
+                        errs[i] = x.what();
+                    }
+                });
+            for (auto& t : th) t.join();
+            for (int i = 0; i < n_replicas; ++i)
+                if (codes[i]) throw mhw::Error(codes[i], errs[i]);
+        };
+        par([&](int i) {
+            auto* g = const_cast<mhw_graph*>(replicas[i]);
+            mhw::DeviceGuard dg(g->device);
+            mhw_walk_config c = *config;
+            c.node_begin = cuts[i];
+            c.node_end = cuts[i + 1];
+            ss[i].reset(new mhw_session());
+            if (cuts[i] < cuts[i + 1]) mhw::session_create(*ss[i], *g, *model, c);
+        });
+        std::unique_ptr<mhw_walks> w(new mhw_walks());
+        std::vector<uint64_t> row0(n_replicas + 1, 0);
+        for (int i = 0; i < n_replicas; ++i) row0[i + 1] = row0[i] + ss[i]->rows;
+        w->rows = row0.back();
+        w->stride = (config->walk_length + 1 + 3) & ~3u;
+        w->nodes.resize(w->rows * w->stride);
+        w->lens.resize(w->rows);
+        std::vector<mhw_walk_stats> st(n_replicas);
+        par([&](int i) {
+            if (!ss[i]->g) return;
+            mhw::DeviceGuard dg(ss[i]->g->device);
+            mhw::session_run(*ss[i], nullptr);
+            mhw::session_stats(*ss[i], st[i]);
+            mhw::session_download(*ss[i], w->nodes.data() + row0[i] * w->stride, w->lens.data() + row0[i], nullptr);
+        });
+        mhw_walk_stats t{};
+        double wall = 0;
+        for (int i = 0; i < n_replicas; ++i) {
+            t.walks += st[i].walks;
+            t.early_terminations += st[i].early_terminations;
+            t.skipped_starts += st[i].skipped_starts;
+            t.steps += st[i].steps;
+            t.slot_inits += st[i].slot_inits;
+            wall = std::max(wall, st[i].walk_seconds);
+        }
+        // skipped starts outside [b, e) are not walkers of this call
+        t.walk_seconds = wall;
+        t.steps_per_sec = wall > 0 ? (double)t.steps / wall : 0.0;
+        w->stats = t;
+        *out = w.release();
+    });
+}
+
+uint64_t mhw_walks_count(const mhw_walks* w) { return w ? w->rows : 0; }
+uint32_t mhw_walks_stride(const mhw_walks* w) { return w ? w->stride : 0; }
+const uint32_t* mhw_walks_nodes(const mhw_walks* w) { return w ? w->nodes.data() : nullptr; }
+const uint32_t* mhw_walks_lengths(const mhw_walks* w) { return w ? w->lens.data() : nullptr; }
+
+mhw_status mhw_walks_stats(const mhw_walks* w, mhw_walk_stats* stats) {
+    return guard([&] {
+        need(w, "walks");
+        need(stats, "stats");
+        *stats = w->stats;
+    });
+}
+
+void mhw_walks_free(mhw_walks* w) { delete w; }
+
+mhw_status mhw_walks_write(const mhw_walks* w, const char* path) {
+    return guard([&] {
+        need(w, "walks");
+        need(path, "path");
+        FILE* f = std::fopen(path, "wb");
+        if (!f) throw mhw::Error(MHW_ERR_IO, std::string("cannot open for writing: ") + path);
+        std::vector<char> buf;
+        buf.reserve(1 << 20);
+        char tmp[16];
+        for (uint64_t r = 0; r < w->rows; ++r) {
+            const uint32_t* row = w->nodes.data() + r * w->stride;
+            for (uint32_t i = 0; i < w->lens[r]; ++i) {
+                if (i) buf.push_back(' ');
+                uint32_t x = row[i];
+                int k = 0;
+                do {
+                    tmp[k++] = (char)('0' + x % 10);
+                    x /= 10;
+                } while (x);
+                while (k) buf.push_back(tmp[--k]);
+            }
+            buf.push_back('\n');
+            if (buf.size() > (1u << 20) - 1024) {
+                if (std::fwrite(buf.data(), 1, buf.size(), f) != buf.size()) {
+                    std::fclose(f);
+                    throw mhw::Error(MHW_ERR_IO, std::string("write failed: ") + path);
+                }
+                buf.clear();
+            }
+        }
+        const bool ok = std::fwrite(buf.data(), 1, buf.size(), f) == buf.size();
+        if (std::fclose(f) != 0 || !ok) throw mhw::Error(MHW_ERR_IO, std::string("write failed: ") + path);
+        // stats sidecar (engine.cpp:248-259)
+        const std::string side = std::string(path) + ".stats.jsonl";
+        FILE* s = std::fopen(side.c_str(), "wb");
+        if (!s) throw mhw::Error(MHW_ERR_IO, "cannot open for writing: " + side);
+        const auto& st = w->stats;
+        std::fprintf(s,
+                     "{\"early_terminations\":%llu,\"init_seconds\":%.17g,\"skipped_starts\":%llu,"
+                     "\"steps\":%llu,\"steps_per_sec\":%.17g,\"walk_seconds\":%.17g,\"walks\":%llu}\n",
+                     (unsigned long long)st.early_terminations, st.init_seconds,
+                     (unsigned long long)st.skipped_starts, (unsigned long long)st.steps, st.steps_per_sec,
+                     st.walk_seconds, (unsigned long long)st.walks);
+        std::fclose(s);
+    });
+}
+
+mhw_status mhw_partition_nodes(const mhw_graph* g, const mhw_model_desc* model, int32_t parts, uint32_t* cuts) {
+    return guard([&] {
+        need(g, "graph");
+        need(model, "model");
+        need(cuts, "cuts");
+        mhw::partition_nodes(*const_cast<mhw_graph*>(g), *model, parts, cuts);
+    });
+}
+
+mhw_status mhw_walk_rows(const mhw_graph* g, const mhw_model_desc* model, const mhw_walk_config* config,
+                         uint64_t* rows, uint32_t* stride) {
+    return guard([&] {
+        need(g, "graph");
+        need(model, "model");
+        need(config, "config");
+        auto* gg = const_cast<mhw_graph*>(g);
+        mhw::DeviceGuard dg(gg->device);
+        mhw_session s;
+        mhw::session_create(s, *gg, *model, *config);
+        if (rows) *rows = s.rows;
+        if (stride) *stride = s.stride;
+    });
+}
+
+mhw_status mhw_generate_walks_into(const mhw_graph* g, const mhw_model_desc* model,
+                                   const mhw_walk_config* config, uint32_t* h_nodes, uint32_t* h_lengths,
+                                   uint64_t capacity_rows, mhw_walk_stats* stats) {
+    return guard([&] { run_into(g, model, config, h_nodes, h_lengths, capacity_rows, stats, nullptr); });
+}
+
+mhw_status mhw_session_create(const mhw_graph* g, const mhw_model_desc* model, const mhw_walk_config* config,
+                              mhw_session** out) {
+    return guard([&] {
+        need(out, "out");
+        need(g, "graph");
+        need(model, "model");
+        need(config, "config");
+        auto* gg = const_cast<mhw_graph*>(g);
+        mhw::DeviceGuard dg(gg->device);
+        std::unique_ptr<mhw_session> s(new mhw_session());
+        mhw::session_create(*s, *gg, *model, *config);
+        *out = s.release();
+    });
+}
+
+mhw_status mhw_session_run(mhw_session* s, void* stream) {
+    return guard([&] {
+        need(s, "session");
+        mhw::session_run(*s, static_cast<cudaStream_t>(stream));
+    });
+}
+
+mhw_status mhw_session_stats(mhw_session* s, mhw_walk_stats* stats) {
+    return guard([&] {
+        need(s, "session");
+        need(stats, "stats");
+        mhw::session_stats(*s, *stats);
+    });
+}
+
+mhw_status mhw_session_buffers(mhw_session* s, uint32_t** d_nodes, uint32_t** d_lengths, uint64_t* rows,
+                               uint32_t* stride) {
+    return guard([&] {
+        need(s, "session");
+        if (d_nodes) *d_nodes = s->out.p;
+        if (d_lengths) *d_lengths = s->lens.p;
+        if (rows) *rows = s->rows;
+        if (stride) *stride = s->stride;
+    });
+}
+
+mhw_status mhw_session_download(mhw_session* s, uint32_t* h_nodes, uint32_t* h_lengths, void* stream) {
+    return guard([&] {
+        need(s, "session");
+        mhw::session_download(*s, h_nodes, h_lengths, static_cast<cudaStream_t>(stream));
+    });
+}
+
+uint32_t mhw_session_launches(const mhw_session* s) { return s ? s->launches : 0; }
+
+void mhw_session_free(mhw_session* s) {
+    if (!s) return;
+    int dev = s->g ? s->g->device : 0;
+    mhw::DeviceGuard dg(dev);
+    delete s;
+}
+
+mhw_status mhw_decide(const mhw_graph* g, const mhw_model_desc* model, uint64_t count, const uint32_t* position,
+                      const uint32_t* affixture, const uint32_t* candidate, const uint32_t* last, const double* u,
+                      double* w_cand, double* w_last, uint8_t* accept) {
+    return guard([&] {
+        need(g, "graph");
+        need(model, "model");
+        if (count) {
+            need(position, "position");
+            need(affixture, "affixture");
+            need(candidate, "candidate");
+            need(last, "last");
+            need(u, "u");
+            need(w_cand, "w_cand");
+            need(w_last, "w_last");
+            need(accept, "accept");
+        }
+        mhw::run_decide(*const_cast<mhw_graph*>(g), *model, count, position, affixture, candidate, last, u, w_cand,
+                        w_last, accept);
+    });
+}
+
+mhw_status mhw_alias_tables(const mhw_graph* g, double* prob, uint32_t* alias) {
+    return guard([&] {
+        need(g, "graph");
+        need(prob, "prob");
+        need(alias, "alias");
+        mhw::graph_alias_tables(*const_cast<mhw_graph*>(g), prob, alias);
+    });
+}
+
+mhw_status mhw_init_states(const mhw_graph* g, const mhw_model_desc* model, const mhw_walk_config* config,
+                           uint64_t count, const uint32_t* position, const uint32_t* affixture, uint32_t* last) {
+    return guard([&] {
+        need(g, "graph");
+        need(model, "model");
+        need(config, "config");
+        if (count) {
+            need(position, "position");
+            need(affixture, "affixture");
+            need(last, "last");
+        }
+        mhw::run_init_states(*const_cast<mhw_graph*>(g), *model, *config, count, position, affixture, last);
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,137 @@
+// internal.h -- host-side objects shared by graph.cu, walk.cu and api.cu.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/mhw.h"
+#include "mhw_device.cuh"
+
+namespace mhw {
+
+// Error carrying an mhw_status (errors.hpp classes -> status codes).
+struct Error : std::runtime_error {
+    mhw_status code;
+    Error(mhw_status c, const std::string& msg) : std::runtime_error(msg), code(c) {}
+};
+
+[[noreturn]] void throw_cuda(cudaError_t e, const char* what, const char* file, int line);
+
+#define MHW_CK(call)                                                    \
+    do {                                                                \
+        cudaError_t _e = (call);                                        \
+        if (_e != cudaSuccess) ::mhw::throw_cuda(_e, #call, __FILE__, __LINE__); \
+    } while (0)
+
+inline void invalid(const std::string& msg) { throw Error(MHW_ERR_INVALID, msg); }
+
+// RAII device buffer on the current device.
+template <class T>
+struct DBuf {
+    T* p = nullptr;
+    size_t n = 0;
+    DBuf() = default;
+    explicit DBuf(size_t count) { alloc(count); }
+    DBuf(const DBuf&) = delete;
+    DBuf& operator=(const DBuf&) = delete;
+    DBuf(DBuf&& o) noexcept : p(o.p), n(o.n) { o.p = nullptr; o.n = 0; }
+    DBuf& operator=(DBuf&& o) noexcept {
+        if (this != &o) {
+            reset();
+            p = o.p;
+            n = o.n;
+            o.p = nullptr;
+            o.n = 0;
+        }
+        return *this;
+    }
+    ~DBuf() { reset(); }
+    void alloc(size_t count) {
+        reset();
+        if (count) MHW_CK(cudaMalloc(&p, count * sizeof(T)));
+        n = count;
+    }
+    void reset() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        n = 0;
+    }
+    size_t bytes() const { return n * sizeof(T); }
+};
+
+// Switches the current device for the lifetime of the guard.
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        cudaGetDevice(&prev);
+        if (prev != dev) MHW_CK(cudaSetDevice(dev));
+    }
+    ~DeviceGuard() {
+        int cur = -1;
+        cudaGetDevice(&cur);
+        if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+    }
+};
+
+// Device-resident CSR replica (mhw_graph).
+struct Graph {
+    int device = 0;
+    uint32_t n = 0;
+    uint64_t m = 0;
+    DBuf<NodeRec> nodes;
+    DBuf<uint32_t> ids;
+    DBuf<float> w;           // empty: unweighted
+    DBuf<uint16_t> ntype;    // empty: untyped (types are also in NodeRec)
+    DBuf<uint16_t> etype;    // empty: derived
+    DBuf<uint32_t> rev;      // lazily built
+    DBuf<double> wtotal;     // lazily built
+    DBuf<uint32_t> tcount;   // lazily built
+    uint16_t n_ntypes = 0, n_etypes = 0;
+    bool symmetric = false;
+    bool verified_sym = false;
+    uint32_t max_deg = 0;
+    uint32_t isolated = 0;
+    cudaStream_t stream = nullptr;
+
+    bool weighted() const { return w.n != 0; }
+    bool has_ntypes() const { return ntype.n != 0; }
+    DevGraph view() const;
+    uint64_t device_bytes() const;
+};
+
+// Graph construction (graph.cu).
+void graph_init_stream(Graph& g);
+void graph_finalize(Graph& g, const int64_t* d_offsets, const uint16_t* d_ntypes);
+void graph_upload(Graph& g, const mhw_graph_view& v);
+void graph_from_edges(Graph& g, uint64_t ne, const uint32_t* src, const uint32_t* dst, const float* w,
+                      bool symmetrize, uint32_t n_nodes);
+void graph_generate_rmat(Graph& g, uint32_t scale, uint32_t ef, double a, double b, double c,
+                         uint64_t seed, bool weighted, float wlo, float whi, uint32_t n_etypes);
+void graph_generate_hetero(Graph& g, uint32_t n_nodes, uint64_t seed, float wlo, float whi);
+void graph_set_node_types(Graph& g, const uint16_t* types, uint16_t num_types);
+void graph_set_edge_types(Graph& g, const uint16_t* types, uint16_t num_types);
+void graph_replicate(const Graph& src, Graph& dst, int device);
+void graph_download(const Graph& g, int64_t* offsets, int32_t* nbr, float* w, uint16_t* ntypes,
+                    uint16_t* etypes);
+void graph_ensure_rev(Graph& g);
+void graph_ensure_wtotal(Graph& g);
+void graph_ensure_tcount(Graph& g);
+void graph_alias_tables(Graph& g, double* prob, uint32_t* alias);
+
+// Bound model (host validation of WalkModel::bind, models.cpp:29-74).
+struct Model {
+    mhw_model_desc desc{};
+    DBuf<uint16_t> metapath;
+    DBuf<double> M;
+    std::vector<uint16_t> h_metapath;
+    DevModel dev{};
+};
+void model_bind(Model& m, Graph& g, const mhw_model_desc& d);
+
+}  // namespace mhw
+
+struct mhw_graph : mhw::Graph {};

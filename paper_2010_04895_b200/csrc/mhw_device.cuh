@@ -1,0 +1,493 @@
+// mhw_device.cuh -- device-side building blocks of the B200 walk engine.
+//
+// Graph layout in HBM, the counter-based random streams, the five walk models'
+// dynamic edge weights as inlined functors (models.cpp:76-136 of the
+// reference), the M-H accept rule (samplers.hpp:21-26) and slot
+// initialisation (samplers.cpp:22-83). Everything here is __device__ code
+// inlined into the kernels of graph.cu / walk.cu.
+//
+// Exactness: every fp64 operation that feeds
+// a decision is an explicit round-to-nearest intrinsic, in the reference's
+// association order, and the library is compiled with -fmad=false.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace mhw {
+
+constexpr uint32_t kNoAffix = 0xFFFFFFFFu;   // models.hpp:17
+constexpr uint32_t kEmpty = 0xFFFFFFFFu;     // chain slot never initialised
+constexpr uint32_t kDead = 0xFFFFFFFEu;      // chain slot is a dead end
+constexpr uint32_t kIdxMask = 0x3FFFFFFFu;   // low 30 bits: Last index
+constexpr uint32_t kMaxDegree = 0x3FFFFFF0u; // degrees must fit the index field
+constexpr uint32_t kNoBack = 0xFFFFFFFFu;    // rev[] entry of an arc without back arc
+
+enum Kind : int { DEEPWALK = 0, NODE2VEC = 1, METAPATH2VEC = 2, EDGE2VEC = 3, FAIRWALK = 4 };
+enum InitKind : int { INIT_RANDOM = 0, INIT_HIGH_WEIGHT = 1, INIT_BURN_IN = 2 };
+
+// Philox key domains; identical in oracle/mhw_oracle.c.
+constexpr uint32_t DOM_WALK = 0x00000000u;
+constexpr uint32_t DOM_INIT = 0x5EED1417u;
+constexpr uint32_t DOM_RMAT = 0x2A7E0001u;
+constexpr uint32_t DOM_WEIGHT = 0x3E1647u;
+constexpr uint32_t DOM_ETYPE = 0x7E7E0003u;
+constexpr uint32_t DOM_HETERO = 0x4E7E0004u;
+
+// One 16-byte record per node: a single 32-byte sector load yields the slice
+// base, degree, node type and flags.
+struct __align__(16) NodeRec {
+    long long off;
+    uint32_t deg;
+    uint16_t type;
+    uint16_t flags;
+};
+constexpr uint16_t NF_ALLPOS = 1;  // every static weight of the slice is > 0
+
+__host__ __device__ constexpr bool second_order(int k) {
+    return k == NODE2VEC || k == EDGE2VEC || k == FAIRWALK;
+}
+
+struct DevGraph {
+    uint32_t n;
+    uint64_t m;
+    const NodeRec* __restrict__ nodes;
+    const uint32_t* __restrict__ ids;
+    const float* __restrict__ w;          // nullptr: unweighted (1.0)
+    const uint16_t* __restrict__ etype;   // nullptr: derived from node types
+    const uint32_t* __restrict__ rev;     // index of v in N(u) for arc v->u
+    const double* __restrict__ wtotal;    // sequential fp64 slice sums
+    const uint32_t* __restrict__ tcount;  // fairwalk type counts, n * n_ntypes
+    uint16_t n_ntypes;
+    uint16_t n_etypes;
+    int verified_sym;                     // every arc has its back arc
+};
+
+struct DevModel {
+    int kind;
+    double inv_p, inv_q;     // 1.0/p, 1.0/q computed on the host (models.cpp:77-79)
+    int alpha_trivial;       // 1/p == 1 == 1/q: alpha is 1.0 whatever the class
+    const uint16_t* metapath;
+    uint32_t mp_len;
+    const double* M;         // edge2vec type matrix, M_dim x M_dim
+    uint32_t M_dim;
+    int M_allpos;
+    uint16_t num_types;      // graph.num_node_types at bind (models.cpp:30)
+};
+
+struct DevCfg {
+    uint64_t seed;
+    uint32_t K, L;
+    int init_kind;
+    uint32_t burn_in;
+    uint32_t hw;
+};
+
+// ------------------------------------------------------------------ Philox
+// Philox4x32-10 (Salmon et al., SC'11): 10 rounds, Weyl key schedule.
+__host__ __device__ __forceinline__ uint4 philox10(uint4 c, uint2 k) {
+#pragma unroll
+    for (int r = 0; r < 10; ++r) {
+        if (r) {
+            k.x += 0x9E3779B9u;
+            k.y += 0xBB67AE85u;
+        }
+#ifdef __CUDA_ARCH__
+        const uint32_t hi0 = __umulhi(0xD2511F53u, c.x), lo0 = 0xD2511F53u * c.x;
+        const uint32_t hi1 = __umulhi(0xCD9E8D57u, c.z), lo1 = 0xCD9E8D57u * c.z;
+#else
+        const uint64_t p0 = (uint64_t)0xD2511F53u * c.x, p1 = (uint64_t)0xCD9E8D57u * c.z;
+        const uint32_t hi0 = (uint32_t)(p0 >> 32), lo0 = (uint32_t)p0;
+        const uint32_t hi1 = (uint32_t)(p1 >> 32), lo1 = (uint32_t)p1;
+#endif
+        c = make_uint4(hi1 ^ c.y ^ k.x, lo1, hi0 ^ c.w ^ k.y, lo0);
+    }
+    return c;
+}
+
+__host__ __device__ __forceinline__ uint2 philox_key(uint64_t seed, uint32_t domain) {
+    return make_uint2((uint32_t)seed, (uint32_t)(seed >> 32) ^ domain);
+}
+
+__host__ __device__ __forceinline__ double unit53(uint32_t hi, uint32_t lo) {
+    const uint64_t x = ((uint64_t)hi << 32) | lo;
+    return (double)(x >> 11) * 0x1.0p-53;  // rng.hpp:59 construction
+}
+
+// Lemire rejection tail: retry words are w3, then sub-blocks ctr.w = 1, 2, ...
+static __device__ __noinline__ uint32_t lemire_slow(uint4 w, uint2 key, uint4 ctr, uint32_t n) {
+    const uint32_t threshold = (uint32_t)((0x100000000ULL - n) % n);
+    uint64_t m = (uint64_t)w.x * n;
+    uint32_t rpos = 3;
+    while ((uint32_t)m < threshold) {
+        if (rpos == 4) {
+            ctr.w += 1;
+            w = philox10(ctr, key);
+            rpos = 0;
+        }
+        const uint32_t x = rpos == 0 ? w.x : rpos == 1 ? w.y : rpos == 2 ? w.z : w.w;
+        ++rpos;
+        m = (uint64_t)x * n;
+    }
+    return (uint32_t)(m >> 32);
+}
+
+// The draws of one transition: block (id, blk) of a domain.
+struct Draw {
+    uint4 w;
+    uint4 ctr;
+    uint2 key;
+    __device__ __forceinline__ void open(uint2 k, uint64_t id, uint32_t blk) {
+        key = k;
+        ctr = make_uint4((uint32_t)id, (uint32_t)(id >> 32), blk, 0u);
+        w = philox10(ctr, key);
+    }
+    // uniform_index (rng.hpp:42-55) on word 0
+    __device__ __forceinline__ uint32_t index(uint32_t n) const {
+        const uint64_t m = (uint64_t)w.x * n;
+        if ((uint32_t)m < n) return lemire_slow(w, key, ctr, n);
+        return (uint32_t)(m >> 32);
+    }
+    // uniform_real (rng.hpp:58-60) on words 1,2
+    __device__ __forceinline__ double unit() const { return unit53(w.y, w.z); }
+};
+
+// --------------------------------------------------------------- loads
+__device__ __forceinline__ NodeRec load_node(const DevGraph& g, uint32_t v) {
+    const int4 r = __ldg(reinterpret_cast<const int4*>(g.nodes) + v);
+    NodeRec n;
+    n.off = ((long long)(uint32_t)r.y << 32) | (uint32_t)r.x;
+    n.deg = (uint32_t)r.z;
+    n.type = (uint16_t)((uint32_t)r.w & 0xFFFFu);
+    n.flags = (uint16_t)((uint32_t)r.w >> 16);
+    return n;
+}
+__device__ __forceinline__ uint32_t load_id(const DevGraph& g, long long arc) { return __ldg(g.ids + arc); }
+__device__ __forceinline__ double static_w(const DevGraph& g, long long arc) {
+    return g.w ? (double)__ldg(g.w + arc) : 1.0;
+}
+
+// Adjacency test: lower_bound (graph.cpp:13-18) with early exit on a hit.
+__device__ __forceinline__ bool adj_search(const uint32_t* __restrict__ ids, long long off,
+                                           uint32_t deg, uint32_t key) {
+    const uint32_t* p = ids + off;
+    uint32_t lo = 0, len = deg;
+    while (len > 0) {
+        const uint32_t half = len >> 1;
+        const uint32_t x = __ldg(p + lo + half);
+        if (x == key) return true;
+        if (x < key) {
+            lo += half + 1;
+            len -= half + 1;
+        } else {
+            len = half;
+        }
+    }
+    return false;
+}
+
+// Exact lower_bound index; returns kNoBack when key is absent.
+__device__ __forceinline__ uint32_t index_of(const uint32_t* __restrict__ ids, long long off,
+                                             uint32_t deg, uint32_t key) {
+    const uint32_t* p = ids + off;
+    uint32_t lo = 0, len = deg;
+    while (len > 0) {
+        const uint32_t half = len >> 1;
+        if (__ldg(p + lo + half) < key) {
+            lo += half + 1;
+            len -= half + 1;
+        } else {
+            len = half;
+        }
+    }
+    return (lo < deg && __ldg(p + lo) == key) ? lo : kNoBack;
+}
+
+// ------------------------------------------------------------ models
+// State context of one transition distribution (WalkerState + what the
+// weight functor reads). For second-order states s = N(v)[affix].
+struct SCtx {
+    uint32_t v;
+    long long off;
+    uint32_t deg;
+    uint16_t vtype;
+    uint16_t vflags;
+    uint32_t s;          // previous node
+    long long off_s;
+    uint32_t deg_s;
+    uint32_t in_type;    // edge2vec: type of arc s->v
+    uint32_t req;        // metapath2vec: required type of the next node
+    bool boot;           // second-order bootstrap (affix == kNoAffix)
+};
+
+// metapath_next / required_type, models.hpp:77-85
+__device__ __forceinline__ uint32_t metapath_next(const DevModel& m, uint32_t affix) {
+    if (affix + 1 < m.mp_len) return affix + 1;
+    return (m.metapath[0] == m.metapath[m.mp_len - 1] && m.mp_len > 1) ? 1u : 0u;
+}
+
+// Graph::edge_type, graph.hpp:47-50
+__device__ __forceinline__ uint32_t edge_type_of(const DevGraph& g, long long arc, uint16_t src_type,
+                                                 uint16_t dst_type) {
+    if (g.etype) return __ldg(g.etype + arc);
+    return (uint16_t)(src_type * g.n_ntypes + dst_type);
+}
+
+// alpha class of candidate u under state c: 0 return (u == s), 1 adjacent to
+// s, 2 otherwise (models.cpp:76-80). urec: the candidate's record if already
+// loaded (lets a verified-symmetric graph search the shorter slice).
+__device__ __forceinline__ uint32_t alpha_class(const DevGraph& g, const DevModel& m, const SCtx& c,
+                                                uint32_t u, const NodeRec* urec) {
+    if (m.alpha_trivial) return 1;
+    if (u == c.s) return 0;
+    long long off = c.off_s;
+    uint32_t deg = c.deg_s, key = u;
+    if (g.verified_sym && urec && urec->deg < deg) {
+        off = urec->off;
+        deg = urec->deg;
+        key = c.s;
+    }
+    return adj_search(g.ids, off, deg, key) ? 1u : 2u;
+}
+
+__device__ __forceinline__ double alpha_value(const DevModel& m, uint32_t cls) {
+    return cls == 0 ? m.inv_p : (cls == 1 ? 1.0 : m.inv_q);
+}
+
+// Dynamic weight w' of candidate index i (node u, type utype, alpha class
+// cls) under state c: WalkModel::calculate_weight, models.cpp:82-123.
+template <int KIND>
+__device__ __forceinline__ double wprime(const DevGraph& g, const DevModel& m, const SCtx& c, uint32_t i,
+                                         uint16_t utype, uint32_t cls) {
+    const double w = static_w(g, c.off + i);
+    if (KIND == DEEPWALK) return w;
+    if (KIND == METAPATH2VEC) return utype == c.req ? w : 0.0;
+    if (c.boot) return w;
+    const double a = alpha_value(m, cls);
+    if (KIND == NODE2VEC) return __dmul_rn(a, w);
+    if (KIND == EDGE2VEC) {
+        const uint32_t out_t = edge_type_of(g, c.off + i, c.vtype, utype);
+        return __dmul_rn(__dmul_rn(a, __ldg(m.M + (size_t)c.in_type * m.M_dim + out_t)), w);
+    }
+    // FAIRWALK: a * w / group
+    const uint32_t group = __ldg(g.tcount + (size_t)c.v * g.n_ntypes + utype);
+    return __ddiv_rn(__dmul_rn(a, w), (double)group);
+}
+
+template <int KIND>
+__device__ __forceinline__ bool needs_utype() {
+    return KIND == METAPATH2VEC || KIND == FAIRWALK || KIND == EDGE2VEC;
+}
+
+// Full evaluation of candidate i (loads its id/record as needed); cls out.
+template <int KIND>
+__device__ __forceinline__ double eval_index(const DevGraph& g, const DevModel& m, const SCtx& c,
+                                             uint32_t i, uint32_t* cls_out) {
+    uint32_t cls = 0;
+    uint16_t utype = 0;
+    if (KIND != DEEPWALK) {
+        const uint32_t u = load_id(g, c.off + i);
+        if (second_order(KIND) && !c.boot && !m.alpha_trivial) {
+            if (needs_utype<KIND>() || (g.verified_sym && c.deg_s > 8 && u != c.s)) {
+                const NodeRec r = load_node(g, u);
+                utype = r.type;
+                cls = alpha_class(g, m, c, u, &r);
+            } else {
+                cls = alpha_class(g, m, c, u, nullptr);
+            }
+        } else {
+            if (needs_utype<KIND>()) utype = load_node(g, u).type;
+            if (second_order(KIND)) cls = 1;
+        }
+    }
+    *cls_out = cls;
+    return wprime<KIND>(g, m, c, i, utype, cls);
+}
+
+// accept rule, samplers.hpp:24
+__device__ __forceinline__ bool mh_accept(double wc, double wl, double u) {
+    return wl <= 0.0 || wc >= wl || __dmul_rn(u, wl) < wc;
+}
+
+__device__ __forceinline__ uint32_t pack_entry(uint32_t idx, uint32_t cls) { return idx | (cls << 30); }
+
+// Builds the state context of (v, affix) from memory (decide / init /
+// deterministic schedule; the throughput kernel keeps it in registers).
+template <int KIND>
+__device__ __forceinline__ SCtx make_ctx(const DevGraph& g, const DevModel& m, uint32_t v, uint32_t affix) {
+    SCtx c;
+    const NodeRec r = load_node(g, v);
+    c.v = v;
+    c.off = r.off;
+    c.deg = r.deg;
+    c.vtype = r.type;
+    c.vflags = r.flags;
+    c.s = 0;
+    c.off_s = 0;
+    c.deg_s = 0;
+    c.in_type = 0;
+    c.req = 0;
+    c.boot = false;
+    if (KIND == METAPATH2VEC) c.req = m.metapath[metapath_next(m, affix)];
+    if (second_order(KIND)) {
+        if (affix == kNoAffix) {
+            c.boot = true;
+        } else {
+            c.s = load_id(g, c.off + affix);
+            const NodeRec rs = load_node(g, c.s);
+            c.off_s = rs.off;
+            c.deg_s = rs.deg;
+            if (KIND == EDGE2VEC) {
+                // arc s->v sits at index rev[v->s] of N(s) (graph.cpp:13-18 lookup)
+                const uint32_t sv = g.rev ? __ldg(g.rev + c.off + affix) : index_of(g.ids, rs.off, rs.deg, v);
+                c.in_type = edge_type_of(g, rs.off + sv, rs.type, r.type);
+            }
+        }
+    }
+    return c;
+}
+
+// Slot of state (v, affix): manager.hpp:29-31 + models.cpp:163-172.
+template <int KIND>
+__device__ __forceinline__ uint64_t slot_of(const DevModel& m, const SCtx& c, uint32_t affix) {
+    if (KIND == DEEPWALK) return c.v;
+    if (KIND == METAPATH2VEC) return (uint64_t)c.v * m.num_types + c.req;
+    return (uint64_t)c.off + affix;
+}
+
+template <int KIND>
+__device__ __forceinline__ bool all_positive(const DevModel& m, const SCtx& c) {
+    if (KIND == METAPATH2VEC) return false;
+    if (KIND == EDGE2VEC && !m.M_allpos) return false;
+    return (c.vflags & NF_ALLPOS) != 0;
+}
+
+// random_positive (samplers.cpp:22-33) with the pick drawn from block `blk`.
+template <int KIND>
+__device__ bool random_positive(const DevGraph& g, const DevModel& m, const SCtx& c, uint2 key,
+                                uint64_t slot, uint32_t blk, uint32_t* out, uint32_t* cls_out,
+                                double* w_out) {
+    Draw d;
+    d.open(key, slot, blk);
+    if (all_positive<KIND>(m, c)) {
+        const uint32_t pick = d.index(c.deg);
+        *out = pick;
+        *w_out = eval_index<KIND>(g, m, c, pick, cls_out);
+        return true;
+    }
+    uint32_t positive = 0, cls;
+    for (uint32_t i = 0; i < c.deg; ++i) positive += eval_index<KIND>(g, m, c, i, &cls) > 0 ? 1u : 0u;
+    if (positive == 0) return false;
+    uint32_t pick = d.index(positive);
+    for (uint32_t i = 0; i < c.deg; ++i) {
+        const double w = eval_index<KIND>(g, m, c, i, &cls);
+        if (w > 0 && pick-- == 0) {
+            *out = i;
+            *cls_out = cls;
+            *w_out = w;
+            return true;
+        }
+    }
+    return false;
+}
+
+// mh_init (samplers.cpp:37-83) with slot-keyed Philox blocks: random -> block
+// 0; high_weight probes -> blocks 0..hw-1, fallback -> block hw; burn_in ->
+// block 0 pick, blocks 1..k transitions. Returns the packed entry or kDead.
+template <int KIND>
+__device__ uint32_t init_slot(const DevGraph& g, const DevModel& m, const DevCfg& cfg, const SCtx& c,
+                              uint64_t slot) {
+    if (c.deg == 0) return kDead;
+    const uint2 key = philox_key(cfg.seed, DOM_INIT);
+    uint32_t last, cls;
+    double wl;
+    if (cfg.init_kind == INIT_RANDOM) {
+        if (!random_positive<KIND>(g, m, c, key, slot, 0, &last, &cls, &wl)) return kDead;
+        return pack_entry(last, cls);
+    }
+    if (cfg.init_kind == INIT_HIGH_WEIGHT) {
+        double best_w = 0.0;
+        uint32_t best = 0, best_cls = 0;
+        bool found = false;
+        if (c.deg <= cfg.hw) {
+            for (uint32_t i = 0; i < c.deg; ++i) {
+                uint32_t ci;
+                const double w = eval_index<KIND>(g, m, c, i, &ci);
+                if (w > best_w) {
+                    best_w = w;
+                    best = i;
+                    best_cls = ci;
+                    found = true;
+                }
+            }
+        } else {
+            for (uint32_t probe = 0; probe < cfg.hw; ++probe) {
+                Draw d;
+                d.open(key, slot, probe);
+                const uint32_t i = d.index(c.deg);
+                uint32_t ci;
+                const double w = eval_index<KIND>(g, m, c, i, &ci);
+                if (w > best_w || (w == best_w && found && i < best)) {
+                    if (w > 0) {
+                        best_w = w;
+                        best = i;
+                        best_cls = ci;
+                        found = true;
+                    }
+                }
+            }
+            if (!found) {
+                if (!random_positive<KIND>(g, m, c, key, slot, cfg.hw, &last, &cls, &wl)) return kDead;
+                return pack_entry(last, cls);
+            }
+        }
+        return found ? pack_entry(best, best_cls) : kDead;
+    }
+    // burn-in
+    if (!random_positive<KIND>(g, m, c, key, slot, 0, &last, &cls, &wl)) return kDead;
+    for (uint32_t i = 0; i < cfg.burn_in; ++i) {
+        Draw d;
+        d.open(key, slot, 1 + i);
+        const uint32_t cand = d.index(c.deg);
+        uint32_t cc;
+        const double wc = eval_index<KIND>(g, m, c, cand, &cc);
+        if (mh_accept(wc, wl, d.unit())) {
+            last = cand;
+            cls = cc;
+            wl = wc;
+        }
+    }
+    return pack_entry(last, cls);
+}
+
+// Bootstrap step of a second-order walk: direct_sample over static weights
+// (engine.cpp:81-83, samplers.cpp:133-146). Unweighted: min(floor(u*deg),
+// deg-1), which is what the sequential r -= 1.0 loop returns exactly.
+__device__ __forceinline__ bool bootstrap_pick(const DevGraph& g, const SCtx& c, double u, uint32_t* out) {
+    if (!g.w) {
+        uint32_t i = (uint32_t)__dmul_rn(u, (double)c.deg);
+        *out = i < c.deg ? i : c.deg - 1;
+        return true;
+    }
+    const double total = __ldg(g.wtotal + c.v);
+    if (!(total > 0)) return false;
+    double r = __dmul_rn(u, total);
+    const float* w = g.w + c.off;
+    for (uint32_t i = 0; i < c.deg; ++i) {
+        r = __dsub_rn(r, (double)__ldg(w + i));
+        if (r < 0) {
+            *out = i;
+            return true;
+        }
+    }
+    for (uint32_t i = c.deg; i-- > 0;) {
+        if (__ldg(w + i) > 0) {
+            *out = i;
+            return true;
+        }
+    }
+    *out = 0;
+    return true;
+}
+
+}  // namespace mhw

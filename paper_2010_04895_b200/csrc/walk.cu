@@ -1,0 +1,840 @@
+// walk.cu -- the M-H walk kernels and the session that drives them.
+//
+// Reference path: generate_walks (engine.cpp:157-234) -> next_edge
+// (engine.cpp:75-118) -> SamplerManager::sample (manager.cpp:30-72) ->
+// mh_transition (samplers.hpp:18-27) -> calculate_weight (models.cpp:82-123)
+// -> update_state (models.cpp:125-136).
+//
+// Two schedules share the device functors of mhw_device.cuh:
+//  * throughput: one persistent kernel; each thread owns a walker for all L
+//    steps in registers; the chain table (one uint32 per state, HBM) is
+//    updated with CAS so every slot's chain is a linearisable sequential M-H
+//    chain (no lost updates); lazily initialised with slot-keyed
+//    randomness so racing initialisers agree.
+//  * deterministic: step-synchronous; same-slot contenders are folded in
+//    walker-id order; byte-reproducible and equal to the CPU oracle's
+//    (philox, step-major) mode.
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <cstring>
+
+#include "internal.h"
+#include "walk.h"
+
+namespace mhw {
+
+namespace {
+
+constexpr int kWalkBlock = 256;
+constexpr uint32_t kDeadMark = 0xFFFFFFFEu;
+
+__device__ __forceinline__ void fail_back_edge(unsigned long long* ctr, uint32_t from, uint32_t to) {
+    if (atomicCAS(&ctr[4], 0ull, 1ull) == 0ull) ctr[5] = ((unsigned long long)from << 32) | to;
+}
+
+// ------------------------------------------------------ throughput kernel
+template <int KIND>
+__global__ void __launch_bounds__(kWalkBlock) k_walk(RunParams P) {
+    const DevGraph& g = P.g;
+    const uint2 wkey = philox_key(P.cfg.seed, DOM_WALK);
+    const uint32_t K = P.cfg.K, L = P.cfg.L;
+    const unsigned lane = threadIdx.x & 31;
+    unsigned long long steps = 0, early = 0, inits = 0;
+    for (;;) {
+        // warp-aggregated work fetch (k-major item order spreads a start
+        // node's K walkers over time, limiting same-slot contention)
+        const unsigned mask = __activemask();
+        const unsigned leader = __ffs(mask) - 1;
+        unsigned long long base = 0;
+        if (lane == leader) base = atomicAdd(&P.ctr[0], (unsigned long long)__popc(mask));
+        base = __shfl_sync(mask, base, leader);
+        const uint64_t item = base + __popc(mask & ((1u << lane) - 1));
+        if (item >= P.n_items) break;
+        const uint32_t k = (uint32_t)(item / P.n_act);
+        const uint32_t j = (uint32_t)(item - (uint64_t)k * P.n_act);
+        const uint32_t v0 = __ldg(P.act + j);
+        const uint64_t row = __ldg(P.act_row + j) + k;
+        const uint64_t walker = (uint64_t)v0 * K + k;
+        uint32_t* orow = P.out + row * P.stride;
+
+        const NodeRec r0 = load_node(g, v0);
+        SCtx c;
+        c.v = v0;
+        c.off = r0.off;
+        c.deg = r0.deg;
+        c.vtype = r0.type;
+        c.vflags = r0.flags;
+        c.s = 0;
+        c.off_s = 0;
+        c.deg_s = 0;
+        c.in_type = 0;
+        c.req = 0;
+        c.boot = second_order(KIND);
+        uint32_t affix = 0;
+        uint64_t slot = v0;
+        if (KIND == METAPATH2VEC) {
+            c.req = P.m.metapath[metapath_next(P.m, 0)];
+            slot = (uint64_t)v0 * P.m.num_types + c.req;
+        }
+        uint32_t len = 1;
+        uint32_t b0 = v0, b1 = 0, b2 = 0, b3 = 0;
+        bool dead = false;
+        for (uint32_t step = 0; step < L; ++step) {
+            if (c.deg == 0) {
+                dead = true;
+                break;
+            }
+            Draw d;
+            d.open(wkey, walker, step);
+            uint32_t chosen, next;
+            NodeRec rn;
+            if (second_order(KIND) && c.boot) {
+                if (!bootstrap_pick(g, c, d.unit(), &chosen)) {
+                    dead = true;
+                    break;
+                }
+                next = load_id(g, c.off + chosen);
+                rn = load_node(g, next);
+            } else {
+                uint32_t e = __ldcg(P.chain + slot);
+                if (e == kEmpty) {
+                    const uint32_t ie = init_slot<KIND>(g, P.m, P.cfg, c, slot);
+                    const uint32_t old = atomicCAS(P.chain + slot, kEmpty, ie);
+                    if (old == kEmpty) {
+                        e = ie;
+                        ++inits;
+                    } else {
+                        e = old;
+                    }
+                }
+                if (e == kDead) {
+                    dead = true;
+                    break;
+                }
+                const uint32_t cand = d.index(c.deg);
+                const double u = d.unit();
+                const uint32_t uc = load_id(g, c.off + cand);
+                const NodeRec rc = load_node(g, uc);
+                const uint32_t cls_c = second_order(KIND) ? alpha_class(g, P.m, c, uc, &rc) : 0u;
+                const double wc = wprime<KIND>(g, P.m, c, cand, rc.type, cls_c);
+                for (;;) {
+                    const uint32_t last = e & kIdxMask, cls_l = e >> 30;
+                    uint16_t ltype = 0;
+                    if (needs_utype<KIND>()) ltype = load_node(g, load_id(g, c.off + last)).type;
+                    const double wl = wprime<KIND>(g, P.m, c, last, ltype, cls_l);
+                    if (!mh_accept(wc, wl, u) || cand == last) {
+                        chosen = last;
+                        break;
+                    }
+                    const uint32_t old = atomicCAS(P.chain + slot, e, pack_entry(cand, cls_c));
+                    if (old == e) {
+                        chosen = cand;
+                        break;
+                    }
+                    e = old;  // another walker advanced this chain: redo against it
+                }
+                if (chosen == cand) {
+                    next = uc;
+                    rn = rc;
+                } else {
+                    next = load_id(g, c.off + chosen);
+                    rn = load_node(g, next);
+                }
+            }
+            // emit: 4 ids buffered in registers, one 16-byte store
+            switch (len & 3) {
+                case 0: b0 = next; break;
+                case 1: b1 = next; break;
+                case 2: b2 = next; break;
+                default:
+                    b3 = next;
+                    *reinterpret_cast<uint4*>(orow + (len & ~3u)) = make_uint4(b0, b1, b2, b3);
+                    break;
+            }
+            ++len;
+            ++steps;
+            // update_state (models.cpp:125-136)
+            if (KIND == DEEPWALK) {
+                slot = next;
+            } else if (KIND == METAPATH2VEC) {
+                affix = metapath_next(P.m, affix);
+                c.req = P.m.metapath[metapath_next(P.m, affix)];
+                slot = (uint64_t)next * P.m.num_types + c.req;
+            } else {
+                const uint32_t back = __ldg(g.rev + c.off + chosen);
+                if (back == kNoBack) {
+                    fail_back_edge(P.ctr, next, c.v);
+                    dead = true;
+                    break;
+                }
+                if (KIND == EDGE2VEC) c.in_type = edge_type_of(g, c.off + chosen, c.vtype, rn.type);
+                c.s = c.v;
+                c.off_s = c.off;
+                c.deg_s = c.deg;
+                c.boot = false;
+                slot = (uint64_t)rn.off + back;
+            }
+            c.v = next;
+            c.off = rn.off;
+            c.deg = rn.deg;
+            c.vtype = rn.type;
+            c.vflags = rn.flags;
+        }
+        const uint32_t base4 = len & ~3u;
+        const uint32_t pend = len & 3u;
+        if (pend > 0) orow[base4] = b0;
+        if (pend > 1) orow[base4 + 1] = b1;
+        if (pend > 2) orow[base4 + 2] = b2;
+        P.lens[row] = len;
+        if (dead) ++early;
+    }
+    if (steps) atomicAdd(&P.ctr[1], steps);
+    if (early) atomicAdd(&P.ctr[2], early);
+    if (inits) atomicAdd(&P.ctr[3], inits);
+}
+
+// Rows of valid starts on isolated nodes: [v], an early termination each.
+__global__ void k_iso_rows(const uint32_t* __restrict__ iso, const uint64_t* __restrict__ iso_row,
+                           uint32_t n_iso, uint32_t K, uint32_t* __restrict__ out, uint32_t stride,
+                           uint32_t* __restrict__ lens) {
+    const uint64_t total = (uint64_t)n_iso * K;
+    for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total;
+         t += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t j = t / K, k = t - j * K;
+        const uint64_t row = iso_row[j] + k;
+        out[row * stride] = iso[j];
+        lens[row] = 1;
+    }
+}
+
+// ------------------------------------------------- deterministic schedule
+template <int KIND>
+__global__ void k_det_setup(RunParams P, DetState S) {
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < P.n_items;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t j = i / P.cfg.K, k = i - j * P.cfg.K;
+        const uint32_t v0 = P.act[j];
+        S.v[i] = v0;
+        S.aff[i] = KIND == METAPATH2VEC ? 0u : kNoAffix;
+        S.len[i] = 1;
+        S.alive[i] = 1;
+        P.out[(P.act_row[j] + k) * P.stride] = v0;
+    }
+}
+
+template <int KIND>
+__global__ void k_det_propose(RunParams P, DetState S, uint32_t step, uint64_t invalid_key) {
+    const uint2 wkey = philox_key(P.cfg.seed, DOM_WALK);
+    unsigned long long inits = 0;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < P.n_items;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        S.key[i] = invalid_key;
+        S.idx[i] = (uint32_t)i;
+        if (!S.alive[i]) continue;
+        const SCtx c = make_ctx<KIND>(P.g, P.m, S.v[i], S.aff[i]);
+        if (c.deg == 0) {
+            S.chosen[i] = kDeadMark;
+            continue;
+        }
+        const uint64_t j = i / P.cfg.K, k = i - j * P.cfg.K;
+        const uint64_t walker = (uint64_t)P.act[j] * P.cfg.K + k;
+        Draw d;
+        d.open(wkey, walker, step);
+        if (second_order(KIND) && c.boot) {
+            uint32_t ch;
+            S.chosen[i] = bootstrap_pick(P.g, c, d.unit(), &ch) ? ch : kDeadMark;
+            continue;
+        }
+        const uint64_t slot = slot_of<KIND>(P.m, c, S.aff[i]);
+        uint32_t e = __ldcg(P.chain + slot);
+        if (e == kEmpty) {
+            const uint32_t ie = init_slot<KIND>(P.g, P.m, P.cfg, c, slot);
+            if (atomicCAS(P.chain + slot, kEmpty, ie) == kEmpty) ++inits;
+        }
+        const uint32_t cand = d.index(c.deg);
+        const uint32_t uc = load_id(P.g, c.off + cand);
+        const NodeRec rc = load_node(P.g, uc);
+        const uint32_t cls = second_order(KIND) ? alpha_class(P.g, P.m, c, uc, &rc) : 0u;
+        S.cand[i] = cand;
+        S.ccls[i] = (uint8_t)cls;
+        S.wc[i] = wprime<KIND>(P.g, P.m, c, cand, rc.type, cls);
+        S.u[i] = d.unit();
+        S.key[i] = slot;
+    }
+    if (inits) atomicAdd(&P.ctr[3], inits);
+}
+
+// One thread per run of equal slots: the sequential M-H chain in walker order.
+template <int KIND>
+__global__ void k_det_fold(RunParams P, DetState S, const uint64_t* __restrict__ keys,
+                           const uint32_t* __restrict__ idx, uint64_t invalid_key) {
+    for (uint64_t p = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; p < P.n_items;
+         p += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t key = keys[p];
+        if (key == invalid_key || (p > 0 && keys[p - 1] == key)) continue;
+        uint32_t e = P.chain[key];
+        const uint32_t i0 = idx[p];
+        const SCtx c = make_ctx<KIND>(P.g, P.m, S.v[i0], S.aff[i0]);
+        const uint32_t e0 = e;
+        for (uint64_t q = p; q < P.n_items && keys[q] == key; ++q) {
+            const uint32_t i = idx[q];
+            if (e == kDead) {
+                S.chosen[i] = kDeadMark;
+                continue;
+            }
+            const uint32_t last = e & kIdxMask, cls_l = e >> 30;
+            uint16_t ltype = 0;
+            if (needs_utype<KIND>()) ltype = load_node(P.g, load_id(P.g, c.off + last)).type;
+            const double wl = wprime<KIND>(P.g, P.m, c, last, ltype, cls_l);
+            const uint32_t cand = S.cand[i];
+            if (mh_accept(S.wc[i], wl, S.u[i]) && cand != last) {
+                e = pack_entry(cand, S.ccls[i]);
+                S.chosen[i] = cand;
+            } else {
+                S.chosen[i] = last;
+            }
+        }
+        if (e != e0) P.chain[key] = e;
+    }
+}
+
+template <int KIND>
+__global__ void k_det_advance(RunParams P, DetState S) {
+    unsigned long long steps = 0, early = 0;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < P.n_items;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        if (!S.alive[i]) continue;
+        const uint32_t ch = S.chosen[i];
+        if (ch == kDeadMark) {
+            S.alive[i] = 0;
+            ++early;
+            continue;
+        }
+        const uint32_t v = S.v[i];
+        const NodeRec r = load_node(P.g, v);
+        const uint32_t next = load_id(P.g, r.off + ch);
+        const uint64_t j = i / P.cfg.K, k = i - j * P.cfg.K;
+        const uint64_t row = P.act_row[j] + k;
+        P.out[row * P.stride + S.len[i]] = next;
+        S.len[i] += 1;
+        ++steps;
+        if (KIND == DEEPWALK) {
+            S.aff[i] = kNoAffix;
+        } else if (KIND == METAPATH2VEC) {
+            S.aff[i] = metapath_next(P.m, S.aff[i]);
+        } else {
+            const uint32_t back = __ldg(P.g.rev + r.off + ch);
+            if (back == kNoBack) {
+                fail_back_edge(P.ctr, next, v);
+                S.alive[i] = 0;
+                continue;
+            }
+            S.aff[i] = back;
+        }
+        S.v[i] = next;
+    }
+    if (steps) atomicAdd(&P.ctr[1], steps);
+    if (early) atomicAdd(&P.ctr[2], early);
+}
+
+__global__ void k_det_finish(RunParams P, DetState S) {
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < P.n_items;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t j = i / P.cfg.K, k = i - j * P.cfg.K;
+        P.lens[P.act_row[j] + k] = S.len[i];
+    }
+}
+
+// --------------------------------------------------------- parity kernels
+template <int KIND>
+__global__ void k_decide(DevGraph g, DevModel m, uint64_t n, const uint32_t* __restrict__ pos,
+                         const uint32_t* __restrict__ aff, const uint32_t* __restrict__ cand,
+                         const uint32_t* __restrict__ last, const double* __restrict__ u,
+                         double* __restrict__ wc, double* __restrict__ wl, uint8_t* __restrict__ acc,
+                         unsigned* __restrict__ bad) {
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t v = pos[i], a = aff[i];
+        bool ok = v < g.n;
+        if (ok) {
+            const uint32_t deg = load_node(g, v).deg;
+            ok = cand[i] < deg && last[i] < deg;
+            if (KIND == METAPATH2VEC) ok = ok && a < m.mp_len;
+            if (second_order(KIND)) ok = ok && (a == kNoAffix || a < deg);
+        }
+        if (!ok) {
+            atomicAdd(bad, 1u);
+            acc[i] = 2;
+            continue;
+        }
+        const SCtx c = make_ctx<KIND>(g, m, v, a);
+        uint32_t cls;
+        const double x = eval_index<KIND>(g, m, c, cand[i], &cls);
+        const double y = eval_index<KIND>(g, m, c, last[i], &cls);
+        wc[i] = x;
+        wl[i] = y;
+        acc[i] = mh_accept(x, y, u[i]) ? 1 : 0;
+    }
+}
+
+template <int KIND>
+__global__ void k_init_states(DevGraph g, DevModel m, DevCfg cfg, uint64_t n, const uint32_t* __restrict__ pos,
+                              const uint32_t* __restrict__ aff, uint32_t* __restrict__ out,
+                              unsigned* __restrict__ bad) {
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t v = pos[i], a = aff[i];
+        bool ok = v < g.n;
+        if (ok) {
+            const uint32_t deg = load_node(g, v).deg;
+            if (KIND == METAPATH2VEC) ok = a < m.mp_len;
+            if (second_order(KIND)) ok = a < deg;
+        }
+        if (!ok) {
+            atomicAdd(bad, 1u);
+            out[i] = kNoAffix;
+            continue;
+        }
+        const SCtx c = make_ctx<KIND>(g, m, v, a);
+        const uint32_t e = init_slot<KIND>(g, m, cfg, c, slot_of<KIND>(m, c, a));
+        out[i] = e == kDead ? kNoAffix : (e & kIdxMask);
+    }
+}
+
+// Session setup: classify start nodes of [b, e).
+__global__ void k_classify(DevGraph g, DevModel m, uint32_t b, uint32_t e, uint8_t* __restrict__ valid,
+                           uint8_t* __restrict__ act, uint8_t* __restrict__ iso) {
+    for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < (uint64_t)(e - b);
+         t += (uint64_t)gridDim.x * blockDim.x) {
+        const NodeRec r = load_node(g, (uint32_t)(b + t));
+        const bool ok = m.kind != METAPATH2VEC || r.type == m.metapath[0];  // initial_state, models.cpp:138-144
+        valid[t] = ok;
+        act[t] = ok && r.deg > 0;
+        iso[t] = ok && r.deg == 0;
+    }
+}
+
+__global__ void k_iota_from(uint32_t* p, uint32_t n, uint32_t base) {
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (uint64_t)gridDim.x * blockDim.x)
+        p[i] = base + (uint32_t)i;
+}
+
+__global__ void k_rows_of(const uint32_t* __restrict__ nodes, uint32_t n, uint32_t b,
+                          const uint32_t* __restrict__ rank, uint32_t K, uint64_t* __restrict__ rows) {
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (uint64_t)gridDim.x * blockDim.x)
+        rows[i] = (uint64_t)rank[nodes[i] - b] * K;
+}
+
+int sms() {
+    int dev = 0, n = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    return n > 0 ? n : 148;
+}
+
+unsigned grid_for(uint64_t work, int block = 256) {
+    const uint64_t g = (work + block - 1) / block;
+    return (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(g, (uint64_t)sms() * 16));
+}
+
+template <int KIND>
+int walk_grid() {
+    int per_sm = 0;
+    MHW_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_walk<KIND>, kWalkBlock, 0));
+    return std::max(1, per_sm) * sms();
+}
+
+template <class F>
+void dispatch(int kind, F&& f) {
+    switch (kind) {
+        case DEEPWALK: f(std::integral_constant<int, DEEPWALK>{}); break;
+        case NODE2VEC: f(std::integral_constant<int, NODE2VEC>{}); break;
+        case METAPATH2VEC: f(std::integral_constant<int, METAPATH2VEC>{}); break;
+        case EDGE2VEC: f(std::integral_constant<int, EDGE2VEC>{}); break;
+        case FAIRWALK: f(std::integral_constant<int, FAIRWALK>{}); break;
+        default: invalid("unknown model kind");
+    }
+}
+
+template <class T>
+void select_flagged(const T* in, const uint8_t* flags, T* out, uint32_t n, uint32_t* count, cudaStream_t st) {
+    DBuf<int64_t> d_cnt(1);
+    size_t bytes = 0;
+    MHW_CK(cub::DeviceSelect::Flagged(nullptr, bytes, in, flags, out, d_cnt.p, (int64_t)n, st));
+    DBuf<uint8_t> temp(std::max<size_t>(bytes, 1));
+    MHW_CK(cub::DeviceSelect::Flagged(temp.p, bytes, in, flags, out, d_cnt.p, (int64_t)n, st));
+    int64_t h = 0;
+    MHW_CK(cudaMemcpyAsync(&h, d_cnt.p, sizeof(h), cudaMemcpyDeviceToHost, st));
+    MHW_CK(cudaStreamSynchronize(st));
+    *count = (uint32_t)h;
+}
+
+}  // namespace
+
+// ----------------------------------------------------------- model bind
+void model_bind(Model& mb, Graph& g, const mhw_model_desc& d) {
+    DeviceGuard dg(g.device);
+    mb.desc = d;
+    const int k = d.kind;
+    if (k < DEEPWALK || k > FAIRWALK) invalid("unknown model: " + std::to_string(k));
+    static const char* names[] = {"deepwalk", "node2vec", "metapath2vec", "edge2vec", "fairwalk"};
+    // WalkModel::bind, models.cpp:29-74
+    if (second_order(k)) {
+        if (!(d.p > 0) || !(d.q > 0)) invalid("p and q must be positive");
+        if (!g.symmetric) invalid(std::string(names[k]) + " requires a symmetric graph (load with symmetrize)");
+    }
+    if ((k == METAPATH2VEC || k == FAIRWALK || k == EDGE2VEC) && !g.has_ntypes())
+        invalid(std::string(names[k]) + " requires node types");
+    DevModel& m = mb.dev;
+    m = DevModel{};
+    m.kind = k;
+    m.inv_p = 1.0 / d.p;
+    m.inv_q = 1.0 / d.q;
+    m.alpha_trivial = (m.inv_p == 1.0 && m.inv_q == 1.0) ? 1 : 0;
+    m.num_types = g.n_ntypes;
+    if (k == METAPATH2VEC) {
+        if (d.metapath_len < 2 || !d.metapath) invalid("metapath needs at least 2 types");
+        for (uint32_t i = 0; i < d.metapath_len; ++i)
+            if (d.metapath[i] >= g.n_ntypes) invalid("metapath type " + std::to_string(d.metapath[i]) + " not in graph");
+        mb.h_metapath.assign(d.metapath, d.metapath + d.metapath_len);
+        mb.metapath.alloc(d.metapath_len);
+        MHW_CK(cudaMemcpy(mb.metapath.p, d.metapath, d.metapath_len * 2, cudaMemcpyHostToDevice));
+        m.metapath = mb.metapath.p;
+        m.mp_len = d.metapath_len;
+    }
+    if (k == EDGE2VEC) {
+        const uint32_t dim = g.etype.n ? g.n_etypes : (uint32_t)(g.n_ntypes * g.n_ntypes);
+        if (d.type_matrix_dim != dim || !d.type_matrix)
+            invalid("edge type matrix must be " + std::to_string(dim) + "x" + std::to_string(dim));
+        bool allpos = true;
+        for (uint32_t i = 0; i < dim * dim; ++i) {
+            if (d.type_matrix[i] < 0) invalid("edge type matrix entries must be non-negative");
+            if (!(d.type_matrix[i] > 0)) allpos = false;
+        }
+        mb.M.alloc((size_t)dim * dim);
+        MHW_CK(cudaMemcpy(mb.M.p, d.type_matrix, (size_t)dim * dim * sizeof(double), cudaMemcpyHostToDevice));
+        m.M = mb.M.p;
+        m.M_dim = dim;
+        m.M_allpos = allpos ? 1 : 0;
+    }
+    if (second_order(k)) {
+        graph_ensure_rev(g);
+        graph_ensure_wtotal(g);
+    }
+    if (k == FAIRWALK) graph_ensure_tcount(g);
+}
+
+// ------------------------------------------------------------- sessions
+Session::~Session() {
+    if (ev0) cudaEventDestroy(ev0);
+    if (ev1) cudaEventDestroy(ev1);
+    if (stream) cudaStreamDestroy(stream);
+}
+
+void session_create(Session& s, Graph& g, const mhw_model_desc& md, const mhw_walk_config& wc) {
+    DeviceGuard dg(g.device);
+    if (wc.walks_per_node == 0 || wc.walk_length == 0)
+        invalid("walks_per_node, walk_length and threads must be positive");
+    if (wc.sampler != 0) {
+        static const char* sn[] = {"mh", "alias", "direct", "rejection"};
+        const char* name = (wc.sampler > 0 && wc.sampler < 4) ? sn[wc.sampler] : "?";
+        invalid(std::string("sampler not supported by the GPU engine: ") + name);
+    }
+    if (wc.init_kind < 0 || wc.init_kind > 2) invalid("unknown init strategy");
+    if (wc.schedule < 0 || wc.schedule > 1) invalid("unknown schedule");
+    s.g = &g;
+    s.wc = wc;
+    model_bind(s.model, g, md);
+    const DevModel& m = s.model.dev;
+    s.cfg.seed = wc.seed;
+    s.cfg.K = wc.walks_per_node;
+    s.cfg.L = wc.walk_length;
+    s.cfg.init_kind = wc.init_kind;
+    s.cfg.burn_in = wc.burn_in_steps;
+    s.cfg.hw = wc.hw_sample_size;
+    s.node_begin = wc.node_begin;
+    s.node_end = wc.node_end ? wc.node_end : g.n;
+    if (s.node_end > g.n || s.node_begin > s.node_end) invalid("node range out of bounds");
+    s.stride = (wc.walk_length + 1 + 3) & ~3u;
+    // slot layout (manager.cpp:14-21)
+    s.slots = k_slots(m.kind, g);
+    if (s.slots > (uint64_t(1) << 40)) invalid("sampler layout too large: " + std::to_string(s.slots) + " slots");
+    MHW_CK(cudaStreamCreateWithFlags(&s.stream, cudaStreamNonBlocking));
+    MHW_CK(cudaEventCreate(&s.ev0));
+    MHW_CK(cudaEventCreate(&s.ev1));
+    cudaStream_t st = s.stream;
+    const uint32_t span = s.node_end - s.node_begin;
+    DBuf<uint8_t> valid(std::max<uint32_t>(span, 1)), act(std::max<uint32_t>(span, 1)), iso(std::max<uint32_t>(span, 1));
+    DBuf<uint32_t> rank(std::max<uint32_t>(span, 1) + 1), ids(std::max<uint32_t>(span, 1));
+    const DevGraph gv = g.view();
+    uint32_t n_valid = 0;
+    if (span) {
+        k_classify<<<grid_for(span), 256, 0, st>>>(gv, m, s.node_begin, s.node_end, valid.p, act.p, iso.p);
+        k_iota_from<<<grid_for(span), 256, 0, st>>>(ids.p, span, s.node_begin);
+        MHW_CK(cudaGetLastError());
+        size_t bytes = 0;
+        MHW_CK(cub::DeviceScan::ExclusiveSum(nullptr, bytes, valid.p, rank.p, (int64_t)span, st));
+        DBuf<uint8_t> temp(std::max<size_t>(bytes, 1));
+        MHW_CK(cub::DeviceScan::ExclusiveSum(temp.p, bytes, valid.p, rank.p, (int64_t)span, st));
+        uint32_t last_rank = 0;
+        uint8_t last_valid = 0;
+        MHW_CK(cudaMemcpyAsync(&last_rank, rank.p + span - 1, 4, cudaMemcpyDeviceToHost, st));
+        MHW_CK(cudaMemcpyAsync(&last_valid, valid.p + span - 1, 1, cudaMemcpyDeviceToHost, st));
+        MHW_CK(cudaStreamSynchronize(st));
+        n_valid = last_rank + last_valid;
+        s.act.alloc(span);
+        s.iso.alloc(span);
+        select_flagged(ids.p, act.p, s.act.p, span, &s.n_act, st);
+        select_flagged(ids.p, iso.p, s.iso.p, span, &s.n_iso, st);
+        s.act_row.alloc(std::max<uint32_t>(s.n_act, 1));
+        s.iso_row.alloc(std::max<uint32_t>(s.n_iso, 1));
+        if (s.n_act) k_rows_of<<<grid_for(s.n_act), 256, 0, st>>>(s.act.p, s.n_act, s.node_begin, rank.p, s.cfg.K, s.act_row.p);
+        if (s.n_iso) k_rows_of<<<grid_for(s.n_iso), 256, 0, st>>>(s.iso.p, s.n_iso, s.node_begin, rank.p, s.cfg.K, s.iso_row.p);
+        MHW_CK(cudaGetLastError());
+    }
+    s.rows = (uint64_t)n_valid * s.cfg.K;
+    s.skipped = (uint64_t)(span - n_valid) * s.cfg.K;
+    s.n_items = (uint64_t)s.n_act * s.cfg.K;
+    s.chain.alloc(std::max<uint64_t>(s.slots, 1));
+    s.out.alloc(std::max<uint64_t>(s.rows * s.stride, 4));
+    s.lens.alloc(std::max<uint64_t>(s.rows, 1));
+    s.ctr.alloc(8);
+    if (wc.schedule == MHW_SCHEDULE_DETERMINISTIC) {
+        const uint64_t n = std::max<uint64_t>(s.n_items, 1);
+        if (s.n_items > 0xFFFFFFFFull) invalid("deterministic schedule supports at most 2^32 walkers");
+        s.d_v.alloc(n);
+        s.d_aff.alloc(n);
+        s.d_len.alloc(n);
+        s.d_alive.alloc(n);
+        s.d_key.alloc(n);
+        s.d_key2.alloc(n);
+        s.d_idx.alloc(n);
+        s.d_idx2.alloc(n);
+        s.d_cand.alloc(n);
+        s.d_ccls.alloc(n);
+        s.d_wc.alloc(n);
+        s.d_u.alloc(n);
+        s.d_chosen.alloc(n);
+        int bits = 1;
+        while (bits < 64 && ((s.slots) >> bits) != 0) ++bits;
+        s.sort_bits = bits;
+        size_t bytes = 0;
+        MHW_CK(cub::DeviceRadixSort::SortPairs(nullptr, bytes, s.d_key.p, s.d_key2.p, s.d_idx.p, s.d_idx2.p,
+                                               (int64_t)n, 0, bits, st));
+        s.sort_temp.alloc(std::max<size_t>(bytes, 1));
+    } else {
+        dispatch(m.kind, [&](auto kc) { s.grid = walk_grid<decltype(kc)::value>(); });
+    }
+    MHW_CK(cudaStreamSynchronize(st));
+}
+
+uint64_t k_slots(int kind, const Graph& g) {
+    if (kind == DEEPWALK) return g.n;
+    if (kind == METAPATH2VEC) return (uint64_t)g.n * g.n_ntypes;
+    return g.m;
+}
+
+RunParams Session::params() const {
+    RunParams P;
+    P.g = g->view();
+    P.m = model.dev;
+    P.cfg = cfg;
+    P.act = act.p;
+    P.act_row = act_row.p;
+    P.n_act = n_act;
+    P.n_items = n_items;
+    P.chain = chain.p;
+    P.out = out.p;
+    P.stride = stride;
+    P.lens = lens.p;
+    P.ctr = ctr.p;
+    return P;
+}
+
+void session_run(Session& s, cudaStream_t user) {
+    DeviceGuard dg(s.g->device);
+    cudaStream_t st = user ? user : s.stream;
+    const RunParams P = s.params();
+    s.launches = 0;
+    MHW_CK(cudaMemsetAsync(s.chain.p, 0xFF, s.chain.bytes(), st));
+    MHW_CK(cudaMemsetAsync(s.ctr.p, 0, s.ctr.bytes(), st));
+    if (s.n_iso) {
+        k_iso_rows<<<grid_for((uint64_t)s.n_iso * s.cfg.K), 256, 0, st>>>(s.iso.p, s.iso_row.p, s.n_iso, s.cfg.K,
+                                                                          s.out.p, s.stride, s.lens.p);
+        ++s.launches;
+    }
+    MHW_CK(cudaEventRecord(s.ev0, st));
+    if (s.n_items) {
+        if (s.wc.schedule == MHW_SCHEDULE_DETERMINISTIC) {
+            DetState S;
+            S.v = s.d_v.p;
+            S.aff = s.d_aff.p;
+            S.len = s.d_len.p;
+            S.alive = s.d_alive.p;
+            S.key = s.d_key.p;
+            S.idx = s.d_idx.p;
+            S.cand = s.d_cand.p;
+            S.ccls = s.d_ccls.p;
+            S.wc = s.d_wc.p;
+            S.u = s.d_u.p;
+            S.chosen = s.d_chosen.p;
+            const uint64_t invalid_key = s.slots;
+            const unsigned gr = grid_for(s.n_items);
+            dispatch(s.model.dev.kind, [&](auto kc) {
+                constexpr int KIND = decltype(kc)::value;
+                k_det_setup<KIND><<<gr, 256, 0, st>>>(P, S);
+                ++s.launches;
+                for (uint32_t step = 0; step < s.cfg.L; ++step) {
+                    k_det_propose<KIND><<<gr, 256, 0, st>>>(P, S, step, invalid_key);
+                    size_t bytes = s.sort_temp.n;
+                    MHW_CK(cub::DeviceRadixSort::SortPairs(s.sort_temp.p, bytes, s.d_key.p, s.d_key2.p, s.d_idx.p,
+                                                           s.d_idx2.p, (int64_t)s.n_items, 0, s.sort_bits, st));
+                    k_det_fold<KIND><<<gr, 256, 0, st>>>(P, S, s.d_key2.p, s.d_idx2.p, invalid_key);
+                    k_det_advance<KIND><<<gr, 256, 0, st>>>(P, S);
+                    s.launches += 3;
+                }
+                k_det_finish<<<gr, 256, 0, st>>>(P, S);
+                ++s.launches;
+            });
+        } else {
+            dispatch(s.model.dev.kind, [&](auto kc) {
+                constexpr int KIND = decltype(kc)::value;
+                k_walk<KIND><<<s.grid, kWalkBlock, 0, st>>>(P);
+            });
+            ++s.launches;
+        }
+        MHW_CK(cudaGetLastError());
+    }
+    MHW_CK(cudaEventRecord(s.ev1, st));
+}
+
+void session_stats(Session& s, mhw_walk_stats& out) {
+    DeviceGuard dg(s.g->device);
+    MHW_CK(cudaEventSynchronize(s.ev1));
+    unsigned long long h[8];
+    MHW_CK(cudaMemcpy(h, s.ctr.p, sizeof(h), cudaMemcpyDeviceToHost));
+    if (h[4]) {
+        const uint32_t from = (uint32_t)(h[5] >> 32), to = (uint32_t)h[5];
+        invalid("second-order walk on asymmetric adjacency: no back edge " + std::to_string(from) + "->" +
+                std::to_string(to));
+    }
+    float ms = 0.f;
+    MHW_CK(cudaEventElapsedTime(&ms, s.ev0, s.ev1));
+    out.walks = s.rows;
+    out.early_terminations = h[2] + (uint64_t)s.n_iso * s.cfg.K;
+    out.skipped_starts = s.skipped;
+    out.steps = h[1];
+    out.slot_inits = h[3];
+    out.walk_seconds = ms * 1e-3;
+    out.init_seconds = 0.0;
+    out.steps_per_sec = ms > 0 ? (double)h[1] / (ms * 1e-3) : 0.0;
+}
+
+void session_download(Session& s, uint32_t* nodes, uint32_t* lens, cudaStream_t user) {
+    DeviceGuard dg(s.g->device);
+    cudaStream_t st = user ? user : s.stream;
+    if (s.rows) {
+        if (nodes) MHW_CK(cudaMemcpyAsync(nodes, s.out.p, s.rows * s.stride * 4, cudaMemcpyDeviceToHost, st));
+        if (lens) MHW_CK(cudaMemcpyAsync(lens, s.lens.p, s.rows * 4, cudaMemcpyDeviceToHost, st));
+    }
+    MHW_CK(cudaStreamSynchronize(st));
+}
+
+// ------------------------------------------------------------ parity API
+void run_decide(Graph& g, const mhw_model_desc& md, uint64_t n, const uint32_t* pos, const uint32_t* aff,
+                const uint32_t* cand, const uint32_t* last, const double* u, double* wc, double* wl,
+                uint8_t* acc) {
+    DeviceGuard dg(g.device);
+    Model mb;
+    model_bind(mb, g, md);
+    if (!n) return;
+    cudaStream_t st = g.stream;
+    DBuf<uint32_t> dpos(n), daff(n), dc(n), dl(n);
+    DBuf<double> du(n), dwc(n), dwl(n);
+    DBuf<uint8_t> dacc(n);
+    DBuf<unsigned> bad(1);
+    MHW_CK(cudaMemcpyAsync(dpos.p, pos, n * 4, cudaMemcpyHostToDevice, st));
+    MHW_CK(cudaMemcpyAsync(daff.p, aff, n * 4, cudaMemcpyHostToDevice, st));
+    MHW_CK(cudaMemcpyAsync(dc.p, cand, n * 4, cudaMemcpyHostToDevice, st));
+    MHW_CK(cudaMemcpyAsync(dl.p, last, n * 4, cudaMemcpyHostToDevice, st));
+    MHW_CK(cudaMemcpyAsync(du.p, u, n * 8, cudaMemcpyHostToDevice, st));
+    MHW_CK(cudaMemsetAsync(bad.p, 0, 4, st));
+    const DevGraph gv = g.view();
+    dispatch(md.kind, [&](auto kc) {
+        constexpr int KIND = decltype(kc)::value;
+        k_decide<KIND><<<grid_for(n), 256, 0, st>>>(gv, mb.dev, n, dpos.p, daff.p, dc.p, dl.p, du.p, dwc.p, dwl.p,
+                                                   dacc.p, bad.p);
+    });
+    MHW_CK(cudaGetLastError());
+    unsigned hbad = 0;
+    MHW_CK(cudaMemcpyAsync(wc, dwc.p, n * 8, cudaMemcpyDeviceToHost, st));
+    MHW_CK(cudaMemcpyAsync(wl, dwl.p, n * 8, cudaMemcpyDeviceToHost, st));
+    MHW_CK(cudaMemcpyAsync(acc, dacc.p, n, cudaMemcpyDeviceToHost, st));
+    MHW_CK(cudaMemcpyAsync(&hbad, bad.p, 4, cudaMemcpyDeviceToHost, st));
+    MHW_CK(cudaStreamSynchronize(st));
+    if (hbad) invalid(std::to_string(hbad) + " decide triples reference states or indices outside the graph");
+}
+
+void run_init_states(Graph& g, const mhw_model_desc& md, const mhw_walk_config& wc, uint64_t n,
+                     const uint32_t* pos, const uint32_t* aff, uint32_t* last) {
+    DeviceGuard dg(g.device);
+    Model mb;
+    model_bind(mb, g, md);
+    if (!n) return;
+    DevCfg cfg;
+    cfg.seed = wc.seed;
+    cfg.K = wc.walks_per_node;
+    cfg.L = wc.walk_length;
+    cfg.init_kind = wc.init_kind;
+    cfg.burn_in = wc.burn_in_steps;
+    cfg.hw = wc.hw_sample_size;
+    cudaStream_t st = g.stream;
+    DBuf<uint32_t> dpos(n), daff(n), dout(n);
+    DBuf<unsigned> bad(1);
+    MHW_CK(cudaMemcpyAsync(dpos.p, pos, n * 4, cudaMemcpyHostToDevice, st));
+    MHW_CK(cudaMemcpyAsync(daff.p, aff, n * 4, cudaMemcpyHostToDevice, st));
+    MHW_CK(cudaMemsetAsync(bad.p, 0, 4, st));
+    const DevGraph gv = g.view();
+    dispatch(md.kind, [&](auto kc) {
+        constexpr int KIND = decltype(kc)::value;
+        k_init_states<KIND><<<grid_for(n), 256, 0, st>>>(gv, mb.dev, cfg, n, dpos.p, daff.p, dout.p, bad.p);
+    });
+    MHW_CK(cudaGetLastError());
+    unsigned hbad = 0;
+    MHW_CK(cudaMemcpyAsync(last, dout.p, n * 4, cudaMemcpyDeviceToHost, st));
+    MHW_CK(cudaMemcpyAsync(&hbad, bad.p, 4, cudaMemcpyDeviceToHost, st));
+    MHW_CK(cudaStreamSynchronize(st));
+    if (hbad) invalid(std::to_string(hbad) + " states outside the graph");
+}
+
+void partition_nodes(Graph& g, const mhw_model_desc& md, int parts, uint32_t* cuts) {
+    DeviceGuard dg(g.device);
+    if (parts <= 0) invalid("parts must be positive");
+    Model mb;
+    model_bind(mb, g, md);
+    cudaStream_t st = g.stream;
+    const uint32_t n = g.n;
+    cuts[0] = 0;
+    for (int i = 1; i <= parts; ++i) cuts[i] = n;
+    if (!n) return;
+    DBuf<uint8_t> valid(n), act(n), iso(n);
+    DBuf<uint32_t> ids(n), list(n);
+    k_classify<<<grid_for(n), 256, 0, st>>>(g.view(), mb.dev, 0, n, valid.p, act.p, iso.p);
+    k_iota_from<<<grid_for(n), 256, 0, st>>>(ids.p, n, 0);
+    MHW_CK(cudaGetLastError());
+    uint32_t n_act = 0;
+    select_flagged(ids.p, act.p, list.p, n, &n_act, st);
+    std::vector<uint32_t> h(n_act);
+    if (n_act) MHW_CK(cudaMemcpy(h.data(), list.p, n_act * 4, cudaMemcpyDeviceToHost));
+    // cut i starts at the active node of rank floor(i * n_act / parts)
+    for (int i = 1; i < parts; ++i) {
+        const uint64_t r = (uint64_t)i * n_act / parts;
+        cuts[i] = r < n_act ? h[r] : n;
+        if (cuts[i] < cuts[i - 1]) cuts[i] = cuts[i - 1];
+    }
+}
+
+}  // namespace mhw

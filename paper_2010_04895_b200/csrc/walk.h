@@ -1,0 +1,83 @@
+// walk.h -- walk session (one generate_walks over a start-node range on one
+// device) and the kernel parameter blocks.
+#pragma once
+
+#include "internal.h"
+
+namespace mhw {
+
+struct RunParams {
+    DevGraph g;
+    DevModel m;
+    DevCfg cfg;
+    const uint32_t* act;      // active start nodes (valid start, degree > 0)
+    const uint64_t* act_row;  // first corpus row of each active start node
+    uint32_t n_act;
+    uint64_t n_items;         // n_act * K walkers
+    uint32_t* chain;          // one packed Last word per state slot
+    uint32_t* out;            // rows x stride walk buffer
+    uint32_t stride;
+    uint32_t* lens;
+    unsigned long long* ctr;  // [0] work counter [1] steps [2] early [3] inits [4] error [5] error arc
+};
+
+struct DetState {
+    uint32_t* v;
+    uint32_t* aff;
+    uint32_t* len;
+    uint8_t* alive;
+    uint64_t* key;
+    uint32_t* idx;
+    uint32_t* cand;
+    uint8_t* ccls;
+    double* wc;
+    double* u;
+    uint32_t* chosen;
+};
+
+struct Session {
+    Graph* g = nullptr;
+    Model model;
+    DevCfg cfg{};
+    mhw_walk_config wc{};
+    uint32_t node_begin = 0, node_end = 0;
+    DBuf<uint32_t> act, iso;
+    DBuf<uint64_t> act_row, iso_row;
+    uint32_t n_act = 0, n_iso = 0;
+    uint64_t n_items = 0, rows = 0, skipped = 0, slots = 0;
+    uint32_t stride = 0;
+    DBuf<uint32_t> chain, out, lens;
+    DBuf<unsigned long long> ctr;
+    // deterministic schedule scratch
+    DBuf<uint32_t> d_v, d_aff, d_len, d_idx, d_idx2, d_cand, d_chosen;
+    DBuf<uint8_t> d_alive, d_ccls, sort_temp;
+    DBuf<uint64_t> d_key, d_key2;
+    DBuf<double> d_wc, d_u;
+    int sort_bits = 1;
+    int grid = 0;
+    uint32_t launches = 0;
+    cudaStream_t stream = nullptr;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+
+    Session() = default;
+    Session(const Session&) = delete;
+    Session& operator=(const Session&) = delete;
+    ~Session();
+    RunParams params() const;
+};
+
+uint64_t k_slots(int kind, const Graph& g);
+void session_create(Session& s, Graph& g, const mhw_model_desc& md, const mhw_walk_config& wc);
+void session_run(Session& s, cudaStream_t stream);
+void session_stats(Session& s, mhw_walk_stats& out);
+void session_download(Session& s, uint32_t* nodes, uint32_t* lens, cudaStream_t stream);
+void run_decide(Graph& g, const mhw_model_desc& md, uint64_t n, const uint32_t* pos, const uint32_t* aff,
+                const uint32_t* cand, const uint32_t* last, const double* u, double* wc, double* wl,
+                uint8_t* acc);
+void run_init_states(Graph& g, const mhw_model_desc& md, const mhw_walk_config& wc, uint64_t n,
+                     const uint32_t* pos, const uint32_t* aff, uint32_t* last);
+void partition_nodes(Graph& g, const mhw_model_desc& md, int parts, uint32_t* cuts);
+
+}  // namespace mhw
+
+struct mhw_session : mhw::Session {};

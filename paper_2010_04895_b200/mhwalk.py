@@ -1,0 +1,510 @@
+"""Python mirror of the reference's walk-path API (namespace mhwalk of
+/root/reference/proj) over the C ABI of libmhw.so.
+
+Same names, argument meanings and error classes as the reference:
+  Graph            graph.hpp:15-55      (device-resident CSR handle)
+  load_edge_list   graph.hpp:65 / graph.cpp:70-100
+  ModelKind        models.hpp:13         WalkModel  models.hpp:40-92
+  InitStrategy     samplers.hpp:29-34    SamplerKind engine.hpp:12
+  WalkConfig       engine.hpp:19-26      RunStats   engine.hpp:28-36
+  WalkCorpus       engine.hpp:38-41      generate_walks engine.hpp:47
+  write_corpus / read_corpus  engine.hpp:50-52
+  ParseError / ValidationError / IoError  errors.hpp:8-21
+WalkConfig.threads == 1 selects the deterministic schedule (the GPU
+counterpart of the reference's single-thread byte determinism,
+engine.hpp:43-46); any other value selects the throughput schedule.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import enum
+import json
+import os
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib as L
+
+
+class MhwError(RuntimeError):
+    code = 4
+
+
+class IoError(MhwError):
+    code = 1
+
+
+class ValidationError(MhwError):
+    code = 2
+
+
+class ParseError(ValidationError):
+    code = 2
+
+
+class CudaError(MhwError):
+    code = 4
+
+
+def _check(rc: int):
+    if rc == 0:
+        return
+    msg = L.lib().mhw_last_error().decode()
+    if rc == 1:
+        raise IoError(msg)
+    if rc == 2:
+        raise ValidationError(msg)
+    raise CudaError(msg)
+
+
+def _ptr(a):
+    return None if a is None else C.c_void_p(a.ctypes.data)
+
+
+class ModelKind(enum.IntEnum):
+    deepwalk = 0
+    node2vec = 1
+    metapath2vec = 2
+    edge2vec = 3
+    fairwalk = 4
+
+
+def model_kind_from_string(name: str) -> ModelKind:
+    try:
+        return ModelKind[name]
+    except KeyError:
+        raise ValidationError(f"unknown model: {name}") from None
+
+
+class InitKind(enum.IntEnum):
+    random = 0
+    high_weight = 1
+    burn_in = 2
+
+
+def init_kind_from_string(name: str) -> InitKind:
+    key = name.replace("-", "_")
+    try:
+        return InitKind[key]
+    except KeyError:
+        raise ValidationError(f"unknown init strategy: {name}") from None
+
+
+class SamplerKind(enum.IntEnum):
+    mh = 0
+    alias = 1
+    direct = 2
+    rejection = 3
+
+
+class Schedule(enum.IntEnum):
+    throughput = 0
+    deterministic = 1
+
+
+kNoAffix = 0xFFFFFFFF
+
+
+@dataclass
+class InitStrategy:
+    kind: InitKind = InitKind.random
+    burn_in_steps: int = 100
+    hw_sample_size: int = 32
+
+
+@dataclass
+class WalkModel:
+    kind: ModelKind = ModelKind.deepwalk
+    p: float = 1.0
+    q: float = 1.0
+    metapath: list = field(default_factory=list)
+    type_matrix: list | np.ndarray | None = None
+
+    def second_order(self) -> bool:
+        return self.kind in (ModelKind.node2vec, ModelKind.edge2vec, ModelKind.fairwalk)
+
+    def _desc(self):
+        d = L.ModelDescC()
+        keep = []
+        d.kind, d.p, d.q = int(self.kind), float(self.p), float(self.q)
+        if self.metapath:
+            mp = np.ascontiguousarray(self.metapath, dtype=np.uint16)
+            keep.append(mp)
+            d.metapath, d.metapath_len = mp.ctypes.data, len(mp)
+        if self.type_matrix is not None:
+            M = np.ascontiguousarray(self.type_matrix, dtype=np.float64)
+            if M.ndim != 2 or M.shape[0] != M.shape[1]:
+                raise ValidationError("edge type matrix is not square")
+            keep.append(M)
+            d.type_matrix, d.type_matrix_dim = M.ctypes.data, M.shape[0]
+        return d, keep
+
+
+@dataclass
+class WalkConfig:
+    walks_per_node: int = 10
+    walk_length: int = 80
+    threads: int = 1
+    seed: int = 0
+    sampler_kind: SamplerKind = SamplerKind.mh
+    init: InitStrategy = field(default_factory=InitStrategy)
+    schedule: Schedule | None = None   # None: derived from threads
+    node_begin: int = 0
+    node_end: int = 0
+
+    def _c(self):
+        c = L.WalkConfigC()
+        if self.threads == 0:
+            raise ValidationError("walks_per_node, walk_length and threads must be positive")
+        c.walks_per_node, c.walk_length, c.seed = self.walks_per_node, self.walk_length, self.seed
+        c.sampler = int(self.sampler_kind)
+        c.init_kind = int(self.init.kind)
+        c.burn_in_steps, c.hw_sample_size = self.init.burn_in_steps, self.init.hw_sample_size
+        sched = self.schedule
+        if sched is None:
+            sched = Schedule.deterministic if self.threads == 1 else Schedule.throughput
+        c.schedule = int(sched)
+        c.node_begin, c.node_end = self.node_begin, self.node_end
+        return c
+
+
+@dataclass
+class RunStats:
+    walks: int = 0
+    early_terminations: int = 0
+    skipped_starts: int = 0
+    steps: int = 0
+    steps_per_sec: float = 0.0
+    init_seconds: float = 0.0
+    walk_seconds: float = 0.0
+    slot_inits: int = 0
+
+    @classmethod
+    def _from(cls, s: L.WalkStatsC):
+        return cls(s.walks, s.early_terminations, s.skipped_starts, s.steps, s.steps_per_sec, s.init_seconds,
+                   s.walk_seconds, s.slot_inits)
+
+
+class WalkCorpus:
+    """Padded corpus: rows[r, :lengths[r]] is walk r (reference corpus order)."""
+
+    def __init__(self, rows: np.ndarray, lengths: np.ndarray, stats: RunStats):
+        self.rows, self.lengths, self.stats = rows, lengths, stats
+
+    @property
+    def walks(self):
+        return [self.rows[r, :self.lengths[r]] for r in range(len(self.lengths))]
+
+    def __len__(self):
+        return len(self.lengths)
+
+
+class Graph:
+    """Device-resident CSR (one replica on one device)."""
+
+    def __init__(self, handle, device=0):
+        self._h = C.c_void_p(handle)
+        self.device = device
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            try:
+                L.lib().mhw_graph_free(h)
+            except Exception:
+                pass
+            self._h = None
+
+    @property
+    def handle(self):
+        return self._h
+
+    # ------------------------------------------------------------ builders
+    @classmethod
+    def from_csr(cls, offsets, neighbors, weights=None, node_types=None, edge_types=None, symmetric=True,
+                 num_node_types=0, num_edge_types=0, device=0) -> "Graph":
+        off = np.ascontiguousarray(offsets, dtype=np.int64)
+        nb = np.ascontiguousarray(neighbors, dtype=np.int32)
+        w = None if weights is None else np.ascontiguousarray(weights, dtype=np.float32)
+        nt = None if node_types is None else np.ascontiguousarray(node_types, dtype=np.uint16)
+        et = None if edge_types is None else np.ascontiguousarray(edge_types, dtype=np.uint16)
+        v = L.GraphView()
+        v.node_count, v.arc_count = len(off) - 1, len(nb)
+        v.offsets, v.neighbors = off.ctypes.data, (nb.ctypes.data if len(nb) else None)
+        v.weights = None if w is None else w.ctypes.data
+        v.node_types = None if nt is None else nt.ctypes.data
+        v.edge_types = None if et is None else et.ctypes.data
+        v.num_node_types, v.num_edge_types, v.symmetric = num_node_types, num_edge_types, int(symmetric)
+        h = C.c_void_p()
+        _check(L.lib().mhw_graph_upload(C.byref(v), device, C.byref(h)))
+        return cls(h.value, device)
+
+    @classmethod
+    def from_host(cls, hg, device=0, weighted=True) -> "Graph":
+        """From an oracle.HostGraph-like object (offsets/nbr/w/ntype/etype)."""
+        return cls.from_csr(hg.offsets.astype(np.int64), hg.nbr.astype(np.int32),
+                            hg.w.astype(np.float32) if weighted else None, hg.ntype, hg.etype, hg.symmetric,
+                            hg.n_ntypes, hg.n_etypes, device)
+
+    @classmethod
+    def from_edges(cls, src, dst, weights=None, symmetrize=False, node_count=0, device=0) -> "Graph":
+        s = np.ascontiguousarray(src, dtype=np.uint32)
+        d = np.ascontiguousarray(dst, dtype=np.uint32)
+        w = None if weights is None else np.ascontiguousarray(weights, dtype=np.float32)
+        h = C.c_void_p()
+        _check(L.lib().mhw_graph_from_edges(len(s), _ptr(s), _ptr(d), _ptr(w), int(symmetrize), node_count,
+                                            device, C.byref(h)))
+        return cls(h.value, device)
+
+    @classmethod
+    def rmat(cls, scale, edge_factor=16, a=0.57, b=0.19, c=0.19, seed=1, weighted=False, weight_lo=1.0,
+             weight_hi=10.0, edge_types=0, device=0) -> "Graph":
+        h = C.c_void_p()
+        _check(L.lib().mhw_graph_generate_rmat(scale, edge_factor, a, b, c, seed, int(weighted), weight_lo,
+                                               weight_hi, edge_types, device, C.byref(h)))
+        return cls(h.value, device)
+
+    @classmethod
+    def hetero(cls, node_count, seed=1, weight_lo=1.0, weight_hi=5.0, device=0) -> "Graph":
+        h = C.c_void_p()
+        _check(L.lib().mhw_graph_generate_hetero(node_count, seed, weight_lo, weight_hi, device, C.byref(h)))
+        return cls(h.value, device)
+
+    # ------------------------------------------------------------- queries
+    def info(self) -> dict:
+        i = L.GraphInfoC()
+        _check(L.lib().mhw_graph_info_get(self._h, C.byref(i)))
+        return {k: getattr(i, k) for k, _ in L.GraphInfoC._fields_}
+
+    def node_count(self) -> int:
+        return self.info()["node_count"]
+
+    def arc_count(self) -> int:
+        return self.info()["arc_count"]
+
+    def download(self) -> dict:
+        inf = self.info()
+        n, m = inf["node_count"], inf["arc_count"]
+        off = np.zeros(n + 1, dtype=np.int64)
+        nb = np.zeros(max(m, 1), dtype=np.int32)
+        w = np.zeros(max(m, 1), dtype=np.float32)
+        nt = np.zeros(max(n, 1), dtype=np.uint16) if inf["num_node_types"] else None
+        et = np.zeros(max(m, 1), dtype=np.uint16) if inf["num_edge_types"] else None
+        _check(L.lib().mhw_graph_download(self._h, _ptr(off), _ptr(nb), _ptr(w), _ptr(nt), _ptr(et)))
+        return dict(offsets=off, neighbors=nb[:m], weights=w[:m] if inf["weighted"] else None,
+                    node_types=None if nt is None else nt[:n], edge_types=None if et is None else et[:m],
+                    num_node_types=inf["num_node_types"], num_edge_types=inf["num_edge_types"])
+
+    def set_node_types(self, types, num_types=0):
+        t = np.ascontiguousarray(types, dtype=np.uint16)
+        _check(L.lib().mhw_graph_set_node_types(self._h, _ptr(t), num_types))
+
+    def set_edge_types(self, types, num_types=0):
+        t = np.ascontiguousarray(types, dtype=np.uint16)
+        _check(L.lib().mhw_graph_set_edge_types(self._h, _ptr(t), num_types))
+
+    def replicate(self, device) -> "Graph":
+        h = C.c_void_p()
+        _check(L.lib().mhw_graph_replicate(self._h, device, C.byref(h)))
+        return Graph(h.value, device)
+
+
+def load_edge_list(path, weighted=False, symmetrize=False, device=0) -> Graph:
+    """load_edge_list (graph.cpp:70-100): "src dst [weight]" lines, '#'
+    comments; ParseError with the line number, negative weight ->
+    ValidationError, unreadable file -> IoError."""
+    try:
+        f = open(path, "r")
+    except OSError:
+        raise IoError(f"cannot open edge list: {path}") from None
+    src, dst, ws = [], [], []
+    with f:
+        for lineno, line in enumerate(f, 1):
+            s = line.split("#", 1)[0]
+            if not s.strip():
+                continue
+            parts = s.split()
+            try:
+                a, b = int(parts[0]), int(parts[1])
+                if a < 0 or b < 0:
+                    raise ValueError
+            except (ValueError, IndexError):
+                raise ParseError(f'{path}:{lineno}: expected "src dst [weight]"') from None
+            w = 1.0
+            if weighted:
+                try:
+                    w = float(parts[2])
+                except (ValueError, IndexError):
+                    raise ParseError(f"{path}:{lineno}: missing edge weight") from None
+                if w < 0:
+                    raise ValidationError(f"{path}:{lineno}: negative edge weight")
+            src.append(a)
+            dst.append(b)
+            ws.append(w)
+    return Graph.from_edges(src, dst, ws if weighted else None, symmetrize=symmetrize, device=device)
+
+
+def generate_walks(graph: Graph, model: WalkModel, config: WalkConfig) -> WalkCorpus:
+    """generate_walks (engine.cpp:157-234) on the GPU."""
+    d, keep = model._desc()
+    c = config._c()
+    h = C.c_void_p()
+    _check(L.lib().mhw_generate_walks(graph.handle, C.byref(d), C.byref(c), C.byref(h)))
+    lib = L.lib()
+    try:
+        rows, stride = lib.mhw_walks_count(h), lib.mhw_walks_stride(h)
+        st = L.WalkStatsC()
+        _check(lib.mhw_walks_stats(h, C.byref(st)))
+        nodes = np.zeros((rows, stride), dtype=np.uint32)
+        lens = np.zeros(rows, dtype=np.uint32)
+        if rows:
+            C.memmove(nodes.ctypes.data, lib.mhw_walks_nodes(h), rows * stride * 4)
+            C.memmove(lens.ctypes.data, lib.mhw_walks_lengths(h), rows * 4)
+    finally:
+        lib.mhw_walks_free(h)
+    return WalkCorpus(nodes, lens, RunStats._from(st))
+
+
+def generate_walks_multi(replicas: list, model: WalkModel, config: WalkConfig) -> WalkCorpus:
+    d, keep = model._desc()
+    c = config._c()
+    arr = (C.c_void_p * len(replicas))(*[g.handle.value for g in replicas])
+    h = C.c_void_p()
+    _check(L.lib().mhw_generate_walks_multi(C.cast(arr, C.c_void_p), len(replicas), C.byref(d), C.byref(c),
+                                            C.byref(h)))
+    lib = L.lib()
+    try:
+        rows, stride = lib.mhw_walks_count(h), lib.mhw_walks_stride(h)
+        st = L.WalkStatsC()
+        _check(lib.mhw_walks_stats(h, C.byref(st)))
+        nodes = np.zeros((rows, stride), dtype=np.uint32)
+        lens = np.zeros(rows, dtype=np.uint32)
+        if rows:
+            C.memmove(nodes.ctypes.data, lib.mhw_walks_nodes(h), rows * stride * 4)
+            C.memmove(lens.ctypes.data, lib.mhw_walks_lengths(h), rows * 4)
+    finally:
+        lib.mhw_walks_free(h)
+    return WalkCorpus(nodes, lens, RunStats._from(st))
+
+
+def partition_nodes(graph: Graph, model: WalkModel, parts: int) -> np.ndarray:
+    d, keep = model._desc()
+    cuts = np.zeros(parts + 1, dtype=np.uint32)
+    _check(L.lib().mhw_partition_nodes(graph.handle, C.byref(d), parts, _ptr(cuts)))
+    return cuts
+
+
+def write_corpus(corpus: WalkCorpus, path: str):
+    """write_corpus (engine.cpp:236-259): one walk per line + stats sidecar."""
+    try:
+        with open(path, "w") as f:
+            for r in range(len(corpus.lengths)):
+                f.write(" ".join(map(str, corpus.rows[r, :corpus.lengths[r]].tolist())))
+                f.write("\n")
+    except OSError:
+        raise IoError(f"cannot open for writing: {path}") from None
+    s = corpus.stats
+    with open(path + ".stats.jsonl", "w") as f:
+        f.write(json.dumps(dict(walks=s.walks, early_terminations=s.early_terminations,
+                                skipped_starts=s.skipped_starts, steps=s.steps, steps_per_sec=s.steps_per_sec,
+                                init_seconds=s.init_seconds, walk_seconds=s.walk_seconds)) + "\n")
+
+
+def read_corpus(path: str) -> list:
+    """read_corpus (engine.cpp:261-275)."""
+    if not os.path.exists(path):
+        raise IoError(f"cannot open corpus: {path}")
+    out = []
+    with open(path) as f:
+        for line in f:
+            w = [int(x) for x in line.split()]
+            if w:
+                out.append(w)
+    return out
+
+
+# --------------------------------------------------------- parity helpers
+def decide(graph: Graph, model: WalkModel, position, affixture, candidate, last, u):
+    """(state, cand, last, u) -> (w'(cand), w'(last), accept) on the GPU."""
+    d, keep = model._desc()
+    arrs = [np.ascontiguousarray(x, dtype=np.uint32) for x in (position, affixture, candidate, last)]
+    uu = np.ascontiguousarray(u, dtype=np.float64)
+    n = len(uu)
+    wc, wl = np.zeros(max(n, 1)), np.zeros(max(n, 1))
+    acc = np.zeros(max(n, 1), dtype=np.uint8)
+    _check(L.lib().mhw_decide(graph.handle, C.byref(d), n, *[_ptr(a) for a in arrs], _ptr(uu), _ptr(wc),
+                              _ptr(wl), _ptr(acc)))
+    return wc[:n], wl[:n], acc[:n]
+
+
+def alias_tables(graph: Graph):
+    m = graph.arc_count()
+    prob = np.zeros(max(m, 1))
+    alias = np.zeros(max(m, 1), dtype=np.uint32)
+    _check(L.lib().mhw_alias_tables(graph.handle, _ptr(prob), _ptr(alias)))
+    return prob[:m], alias[:m]
+
+
+def init_states(graph: Graph, model: WalkModel, config: WalkConfig, position, affixture):
+    d, keep = model._desc()
+    c = config._c()
+    pos = np.ascontiguousarray(position, dtype=np.uint32)
+    aff = np.ascontiguousarray(affixture, dtype=np.uint32)
+    out = np.zeros(max(len(pos), 1), dtype=np.uint32)
+    _check(L.lib().mhw_init_states(graph.handle, C.byref(d), C.byref(c), len(pos), _ptr(pos), _ptr(aff),
+                                   _ptr(out)))
+    return out[:len(pos)]
+
+
+class Session:
+    """Device-resident repeated generate_walks (benchmarks)."""
+
+    def __init__(self, graph: Graph, model: WalkModel, config: WalkConfig):
+        self._d, self._keep = model._desc()
+        self._c = config._c()
+        self.graph = graph
+        h = C.c_void_p()
+        _check(L.lib().mhw_session_create(graph.handle, C.byref(self._d), C.byref(self._c), C.byref(h)))
+        self._h = h
+        rows, stride = C.c_uint64(), C.c_uint32()
+        dn, dl = C.c_void_p(), C.c_void_p()
+        _check(L.lib().mhw_session_buffers(h, C.byref(dn), C.byref(dl), C.byref(rows), C.byref(stride)))
+        self.rows, self.stride = rows.value, stride.value
+        self.d_nodes, self.d_lengths = dn.value, dl.value
+
+    def run(self, stream: int | None = None):
+        _check(L.lib().mhw_session_run(self._h, C.c_void_p(stream) if stream else None))
+
+    def stats(self) -> RunStats:
+        st = L.WalkStatsC()
+        _check(L.lib().mhw_session_stats(self._h, C.byref(st)))
+        return RunStats._from(st)
+
+    def launches(self) -> int:
+        return L.lib().mhw_session_launches(self._h)
+
+    def download(self, nodes=None, lengths=None, stream: int | None = None):
+        if nodes is None:
+            nodes = np.zeros((self.rows, self.stride), dtype=np.uint32)
+        if lengths is None:
+            lengths = np.zeros(self.rows, dtype=np.uint32)
+        _check(L.lib().mhw_session_download(self._h, C.c_void_p(nodes.ctypes.data) if self.rows else None,
+                                            C.c_void_p(lengths.ctypes.data) if self.rows else None,
+                                            C.c_void_p(stream) if stream else None))
+        return nodes, lengths
+
+    def close(self):
+        if self._h is not None and self._h.value:
+            L.lib().mhw_session_free(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def device_count() -> int:
+    return L.lib().mhw_device_count()
