@@ -109,6 +109,14 @@ typedef struct mhw_walk_config {
     int32_t schedule;          /* mhw_schedule */
     uint32_t node_begin;
     uint32_t node_end;
+    /* Node-keyed models (deepwalk, metapath2vec): nodes of degree >= this get
+     * up to 64 independent chains per state, picked by walker id (0 = 256,
+     * 0xFFFFFFFF = one chain per state exactly as SamplerManager). */
+    uint32_t chain_replica_degree;
+    /* Second-order slot initialisation: 0 auto, 1 lazy (first query, as
+     * manager.cpp:35-56), 2 eager (all slots before the walk; identical
+     * values because init randomness is keyed by the slot). */
+    int32_t init_mode;
 } mhw_walk_config;
 
 /* Replaces mhwalk::RunStats (engine.hpp:28-36). init_seconds is not
@@ -120,6 +128,7 @@ typedef struct mhw_walk_stats {
     uint64_t skipped_starts;
     uint64_t steps;
     uint64_t slot_inits;
+    uint64_t chain_retries;   /* CAS retries on contended chain slots */
     double steps_per_sec;
     double init_seconds;
     double walk_seconds;

@@ -671,6 +671,36 @@ static inline uint64_t slot_index(const og_graph* g, const og_model* m, uint32_t
     }
 }
 
+/* Engine chain layout: node-keyed states of hub nodes (degree >= D) own
+ * R = 2^(floor(log2(deg/D))+1) <= 64 chains; walker w uses chain
+ * (w * golden >> 40) & (R-1); chains 1..R-1 live after the n*G base slots. */
+typedef struct {
+    uint32_t D;
+    uint32_t* group;   /* n+1 exclusive prefix of (R-1) */
+    uint64_t base;     /* n*G */
+    uint32_t G;
+} replica_layout_t;
+
+static uint32_t chain_replicas(uint32_t deg, uint32_t D) {
+    if (D == OG_NO_REPLICAS || deg < D) return 1;
+    uint32_t q = deg / D, lg = 0;
+    while (q >>= 1) ++lg;
+    const uint32_t r = 2u << lg;
+    return r < 64 ? r : 64;
+}
+
+static uint64_t engine_slot(const og_graph* g, const og_model* m, const replica_layout_t* rl, uint32_t v,
+                            uint32_t affix, uint64_t walker) {
+    const uint64_t base = slot_index(g, m, v, affix);
+    if (m->kind != OG_DEEPWALK && m->kind != OG_METAPATH2VEC) return base;
+    const uint32_t R = chain_replicas(deg_of(g, v), rl->D);
+    if (R == 1) return base;
+    const uint32_t r = (uint32_t)((walker * 0x9E3779B97F4A7C15ULL) >> 40) & (R - 1);
+    if (r == 0) return base;
+    const uint32_t t = m->kind == OG_METAPATH2VEC ? required_type(m, affix) : 0;
+    return rl->base + ((uint64_t)rl->group[v] + r - 1) * rl->G + t;
+}
+
 int og_init_philox(const og_graph* g, const og_model* m, const og_config* c, uint32_t v,
                    uint32_t affix, uint64_t slot, uint32_t* last) {
     st_t s = {g, m, v, affix, deg_of(g, v)};
@@ -702,8 +732,8 @@ typedef struct {
 /* One walker step = WalkerContext::next_edge (engine.cpp:75-87) + the push and
  * update_state of engine.cpp:201-204. Returns 1 stepped, 0 dead end, -1 error. */
 static int walker_step(const og_graph* g, const og_model* m, const og_config* c, chain_t* ch,
-                       walker_t* w, uint32_t step, uint32_t stride, uint32_t* rows,
-                       og_stats* st, char* err, size_t errlen) {
+                       const replica_layout_t* rl, walker_t* w, uint32_t step, uint32_t stride,
+                       uint32_t* rows, og_stats* st, char* err, size_t errlen) {
     const uint32_t v = w->v;
     const uint32_t deg = deg_of(g, v);
     if (deg == 0) return 0;
@@ -722,7 +752,7 @@ static int walker_step(const og_graph* g, const og_model* m, const og_config* c,
         edge = og_direct_sample_u(deg, ws, draw_real(&d));
     } else {
         /* SamplerManager::sample, manager.cpp:30-72 */
-        const uint64_t slot = slot_index(g, m, v, w->affix);
+        const uint64_t slot = engine_slot(g, m, rl, v, w->affix, w->walker);
         st_t s = {g, m, v, w->affix, deg};
         if (ch->status[slot] == ST_EMPTY) {
             init_src_t src;
@@ -777,8 +807,21 @@ int og_generate_walks(const og_graph* g, const og_model* m, const og_config* c, 
         return OG_ERR_INVALID;
     }
     if (stride < c->L + 1) { snprintf(err, errlen, "row stride too small"); return OG_ERR_INVALID; }
-    const uint64_t slots = og_slot_count(g, m);
-    if (slots > ((uint64_t)1 << 40)) { snprintf(err, errlen, "sampler layout too large"); return OG_ERR_INVALID; }
+    uint64_t slots = og_slot_count(g, m);
+    replica_layout_t rl;
+    rl.D = c->replica_degree;
+    rl.G = m->kind == OG_METAPATH2VEC ? m->num_types : 1;
+    rl.base = slots;
+    rl.group = NULL;
+    if ((m->kind == OG_DEEPWALK || m->kind == OG_METAPATH2VEC) && rl.D != OG_NO_REPLICAS) {
+        if (rl.D == 0) rl.D = 256;
+        rl.group = (uint32_t*)calloc((size_t)g->n + 1, sizeof(uint32_t));
+        for (uint32_t v = 0; v < g->n; ++v) rl.group[v + 1] = rl.group[v] + chain_replicas(deg_of(g, v), rl.D) - 1;
+        slots += (uint64_t)rl.group[g->n] * rl.G;
+    } else {
+        rl.D = OG_NO_REPLICAS;
+    }
+    if (slots > ((uint64_t)1 << 40)) { snprintf(err, errlen, "sampler layout too large"); free(rl.group); return OG_ERR_INVALID; }
     chain_t ch;
     ch.status = (uint8_t*)calloc(slots ? slots : 1, 1);
     ch.last = (uint32_t*)calloc(slots ? slots : 1, sizeof(uint32_t));
@@ -802,7 +845,7 @@ int og_generate_walks(const og_graph* g, const og_model* m, const og_config* c, 
             rows[w.row * stride] = w.v;
             w.len = 1;
             for (uint32_t step = 0; step < c->L; ++step) {
-                const int r = walker_step(g, m, c, &ch, &w, step, stride, rows, stats, err, errlen);
+                const int r = walker_step(g, m, c, &ch, &rl, &w, step, stride, rows, stats, err, errlen);
                 if (r < 0) { rc = OG_ERR_INVALID; break; }
                 if (r == 0) { stats->early++; break; }
             }
@@ -833,7 +876,7 @@ int og_generate_walks(const og_graph* g, const og_model* m, const og_config* c, 
             for (uint64_t i = 0; i < nw; ++i) {
                 walker_t* w = &ws[i];
                 if (!w->alive) continue;
-                const int r = walker_step(g, m, c, &ch, w, step, stride, rows, stats, err, errlen);
+                const int r = walker_step(g, m, c, &ch, &rl, w, step, stride, rows, stats, err, errlen);
                 if (r < 0) { rc = OG_ERR_INVALID; break; }
                 if (r == 0) { stats->early++; w->alive = 0; }
             }
@@ -845,86 +888,6 @@ int og_generate_walks(const og_graph* g, const og_model* m, const og_config* c, 
     *n_rows = row;
     free(ch.status);
     free(ch.last);
+    free(rl.group);
     return rc;
-}
-
-/* ===================================================== threaded baseline */
-
-typedef struct {
-    const og_graph* g;
-    const og_model* m;
-    const og_config* c;
-    chain_t* ch;
-    uint64_t begin, stride, count;
-    og_stats st;
-    uint32_t* row;
-} mt_arg_t;
-
-static void* mt_worker(void* p) {
-    mt_arg_t* a = (mt_arg_t*)p;
-    char err[256];
-    memset(&a->st, 0, sizeof(a->st));
-    for (uint64_t j = 0; j < a->count; ++j) {
-        const uint64_t idx = a->begin + j * a->stride;
-        walker_t w;
-        w.v = (uint32_t)(idx / a->c->K);
-        w.walker = idx;
-        xo_walker(&w.xo, a->c->seed, w.v, idx % a->c->K);
-        if (a->m->kind == OG_METAPATH2VEC) {
-            if (a->g->ntype[w.v] != a->m->metapath[0]) { a->st.skipped++; continue; }
-            w.affix = 0;
-        } else {
-            w.affix = OG_NO_AFFIX;
-        }
-        w.row = 0;
-        w.len = 1;
-        for (uint32_t step = 0; step < a->c->L; ++step) {
-            w.len = 1;
-            const int r = walker_step(a->g, a->m, a->c, a->ch, &w, step, 0, a->row, &a->st, err, sizeof err);
-            if (r <= 0) { a->st.early++; break; }
-        }
-        a->st.walks++;
-    }
-    return NULL;
-}
-
-int og_walks_sample_mt(const og_graph* g, const og_model* m, const og_config* c,
-                       uint64_t walker_begin, uint64_t walker_stride, uint64_t walker_count,
-                       uint32_t threads, og_stats* stats, double* seconds) {
-    const uint64_t slots = og_slot_count(g, m);
-    chain_t ch;
-    ch.status = (uint8_t*)calloc(slots ? slots : 1, 1);
-    ch.last = (uint32_t*)calloc(slots ? slots : 1, sizeof(uint32_t));
-    if (threads == 0) threads = 1;
-    mt_arg_t* args = (mt_arg_t*)calloc(threads, sizeof(mt_arg_t));
-    pthread_t* th = (pthread_t*)calloc(threads, sizeof(pthread_t));
-    uint32_t* scratch = (uint32_t*)calloc(threads, sizeof(uint32_t) * 4);
-    struct timespec t0, t1;
-    clock_gettime(CLOCK_MONOTONIC, &t0);
-    for (uint32_t t = 0; t < threads; ++t) {
-        const uint64_t b = walker_count * t / threads, e = walker_count * (t + 1) / threads;
-        args[t].g = g; args[t].m = m; args[t].c = c; args[t].ch = &ch;
-        args[t].begin = walker_begin + b * walker_stride;
-        args[t].stride = walker_stride;
-        args[t].count = e - b;
-        args[t].row = scratch + 4 * t;
-        pthread_create(&th[t], NULL, mt_worker, &args[t]);
-    }
-    memset(stats, 0, sizeof(*stats));
-    for (uint32_t t = 0; t < threads; ++t) {
-        pthread_join(th[t], NULL);
-        stats->walks += args[t].st.walks;
-        stats->early += args[t].st.early;
-        stats->skipped += args[t].st.skipped;
-        stats->steps += args[t].st.steps;
-        stats->init_calls += args[t].st.init_calls;
-    }
-    clock_gettime(CLOCK_MONOTONIC, &t1);
-    *seconds = (double)(t1.tv_sec - t0.tv_sec) + 1e-9 * (double)(t1.tv_nsec - t0.tv_nsec);
-    free(args);
-    free(th);
-    free(scratch);
-    free(ch.status);
-    free(ch.last);
-    return OG_OK;
 }

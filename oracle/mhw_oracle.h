@@ -72,7 +72,12 @@ typedef struct {
     uint32_t hw_sample_size;
     int rng;
     int order;
+    /* node-keyed chain replicas at hubs (engine layout, DESIGN.md "Chain
+     * table"); OG_NO_REPLICAS = one chain per state like SamplerManager */
+    uint32_t replica_degree;
 } og_config;
+
+#define OG_NO_REPLICAS 0xFFFFFFFFu
 
 typedef struct {
     uint64_t walks, early, skipped, steps, init_calls;
@@ -130,12 +135,6 @@ uint64_t og_slot_count(const og_graph* g, const og_model* m);
 int og_generate_walks(const og_graph* g, const og_model* m, const og_config* c, uint32_t stride,
                       uint32_t* rows, uint32_t* lens, uint64_t* n_rows, og_stats* stats,
                       char* err, size_t errlen);
-
-/* Multithreaded CPU baseline of the same engine (philox, step-free chain races as
- * in the reference contract). Used only by bench.py's cpu_baseline leg. */
-int og_walks_sample_mt(const og_graph* g, const og_model* m, const og_config* c,
-                       uint64_t walker_begin, uint64_t walker_stride, uint64_t walker_count,
-                       uint32_t threads, og_stats* stats, double* seconds);
 
 #ifdef __cplusplus
 }

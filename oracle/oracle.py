@@ -63,7 +63,7 @@ class _OgModel(C.Structure):
 class _OgConfig(C.Structure):
     _fields_ = [("K", C.c_uint32), ("L", C.c_uint32), ("seed", C.c_uint64), ("init_kind", C.c_int),
                 ("burn_in_steps", C.c_uint32), ("hw_sample_size", C.c_uint32), ("rng", C.c_int),
-                ("order", C.c_int)]
+                ("order", C.c_int), ("replica_degree", C.c_uint32)]
 
 
 class _OgStats(C.Structure):
@@ -138,6 +138,9 @@ class WalkCfg:
     init_kind: int = INIT_RANDOM
     burn_in_steps: int = 100
     hw_sample_size: int = 32
+    # engine chain layout: hub replicas for node-keyed models (0 = 256);
+    # NO_REPLICAS = one chain per state, the reference's SamplerManager
+    replica_degree: int = 0xFFFFFFFF
 
 
 class OracleError(RuntimeError):
@@ -182,9 +185,6 @@ class Oracle:
         L.og_generate_walks.argtypes = [C.POINTER(_OgGraph), C.POINTER(_OgModel), C.POINTER(_OgConfig),
                                         C.c_uint32, _u32p, _u32p, _u64p, C.POINTER(_OgStats),
                                         C.c_char_p, C.c_size_t]
-        L.og_walks_sample_mt.argtypes = [C.POINTER(_OgGraph), C.POINTER(_OgModel), C.POINTER(_OgConfig),
-                                         C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint32,
-                                         C.POINTER(_OgStats), _dp]
 
     # ---------------------------------------------------------------- rng
     def philox(self, ctr, key):
@@ -302,6 +302,7 @@ class Oracle:
         c.K, c.L, c.seed = cfg.K, cfg.L, cfg.seed
         c.init_kind, c.burn_in_steps, c.hw_sample_size = cfg.init_kind, cfg.burn_in_steps, cfg.hw_sample_size
         c.rng, c.order = rng, order
+        c.replica_degree = cfg.replica_degree
         return c
 
     def generate_walks(self, g, md, cfg: WalkCfg, rng=RNG_XOSHIRO, order=ORDER_WALKER, stride=None):
@@ -332,15 +333,6 @@ class Oracle:
         ok = self.lib.og_init_philox(C.byref(gs), C.byref(ms), C.byref(c), v, affix, slot, C.byref(out))
         return out.value if ok else None
 
-    def walks_sample_mt(self, g, md, cfg, begin, stride, count, threads):
-        gs, ms, keep = self.bind(g, md)
-        c = self._cfg(cfg, RNG_PHILOX, ORDER_WALKER)
-        st = _OgStats()
-        sec = C.c_double()
-        self.lib.og_walks_sample_mt(C.byref(gs), C.byref(ms), C.byref(c), begin, stride, count,
-                                    threads, C.byref(st), C.byref(sec))
-        return dict(walks=st.walks, early_terminations=st.early, skipped_starts=st.skipped,
-                    steps=st.steps), sec.value
 
 
 class RefLib:

@@ -26,12 +26,12 @@ class WalkConfigC(C.Structure):
     _fields_ = [("walks_per_node", C.c_uint32), ("walk_length", C.c_uint32), ("seed", C.c_uint64),
                 ("sampler", C.c_int32), ("init_kind", C.c_int32), ("burn_in_steps", C.c_uint32),
                 ("hw_sample_size", C.c_uint32), ("schedule", C.c_int32), ("node_begin", C.c_uint32),
-                ("node_end", C.c_uint32)]
+                ("node_end", C.c_uint32), ("chain_replica_degree", C.c_uint32), ("init_mode", C.c_int32)]
 
 
 class WalkStatsC(C.Structure):
     _fields_ = [("walks", C.c_uint64), ("early_terminations", C.c_uint64), ("skipped_starts", C.c_uint64),
-                ("steps", C.c_uint64), ("slot_inits", C.c_uint64), ("steps_per_sec", C.c_double),
+                ("steps", C.c_uint64), ("slot_inits", C.c_uint64), ("chain_retries", C.c_uint64), ("steps_per_sec", C.c_double),
                 ("init_seconds", C.c_double), ("walk_seconds", C.c_double)]
 
 

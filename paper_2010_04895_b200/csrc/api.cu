@@ -295,6 +295,7 @@ mhw_status mhw_generate_walks_multi(const mhw_graph* const* replicas, int32_t n_
             t.skipped_starts += st[i].skipped_starts;
             t.steps += st[i].steps;
             t.slot_inits += st[i].slot_inits;
+            t.chain_retries += st[i].chain_retries;
             wall = std::max(wall, st[i].walk_seconds);
         }
         // skipped starts outside [b, e) are not walkers of this call

@@ -81,7 +81,42 @@ struct DevCfg {
     int init_kind;
     uint32_t burn_in;
     uint32_t hw;
+    // node-keyed chain replication at hubs
+    uint32_t rep_deg;            // nodes with degree >= rep_deg get replicas
+    uint64_t rep_base_slot;      // first slot of the replica region (= n * G)
+    const uint32_t* rep_group;   // per node: first replica group (hubs only)
 };
+
+constexpr uint32_t kNoReplicas = 0xFFFFFFFFu;
+constexpr uint32_t kDefaultRepDeg = 256;
+constexpr uint32_t kMaxReplicas = 64;
+
+// Chains per node-keyed state: 1 below rep_deg, else 2^(floor(log2(deg /
+// rep_deg)) + 1) capped at 64 -- about 2*deg/rep_deg concurrent chains, so a
+// hub's visitors spread over independent exact M-H chains.
+__host__ __device__ __forceinline__ uint32_t chain_replicas(uint32_t deg, uint32_t rep_deg) {
+    if (rep_deg == kNoReplicas || deg < rep_deg) return 1;
+    uint32_t q = deg / rep_deg, lg = 0;
+    while (q >>= 1) ++lg;
+    const uint32_t r = 2u << lg;
+    return r < kMaxReplicas ? r : kMaxReplicas;
+}
+
+__host__ __device__ __forceinline__ uint32_t walker_replica(uint64_t walker, uint32_t R) {
+    return (uint32_t)((walker * 0x9E3779B97F4A7C15ull) >> 40) & (R - 1);
+}
+
+// Slot of node-keyed state (v, t) for `walker`: G slots per node (1 for
+// deepwalk, num_types for metapath2vec), replicas after the n*G base slots.
+__device__ __forceinline__ uint64_t node_slot(const DevCfg& cfg, uint32_t G, uint32_t v, uint32_t deg,
+                                              uint32_t t, uint64_t walker) {
+    const uint64_t base = (uint64_t)v * G + t;
+    const uint32_t R = chain_replicas(deg, cfg.rep_deg);
+    if (R == 1) return base;
+    const uint32_t r = walker_replica(walker, R);
+    if (r == 0) return base;
+    return cfg.rep_base_slot + ((uint64_t)__ldg(cfg.rep_group + v) + r - 1) * G + t;
+}
 
 // ------------------------------------------------------------------ Philox
 // Philox4x32-10 (Salmon et al., SC'11): 10 rounds, Weyl key schedule.
@@ -347,11 +382,13 @@ __device__ __forceinline__ SCtx make_ctx(const DevGraph& g, const DevModel& m, u
     return c;
 }
 
-// Slot of state (v, affix): manager.hpp:29-31 + models.cpp:163-172.
+// Slot of state (v, affix) used by `walker`: manager.hpp:29-31 +
+// models.cpp:163-172, with hub replicas for node-keyed models.
 template <int KIND>
-__device__ __forceinline__ uint64_t slot_of(const DevModel& m, const SCtx& c, uint32_t affix) {
-    if (KIND == DEEPWALK) return c.v;
-    if (KIND == METAPATH2VEC) return (uint64_t)c.v * m.num_types + c.req;
+__device__ __forceinline__ uint64_t slot_of(const DevModel& m, const DevCfg& cfg, const SCtx& c, uint32_t affix,
+                                            uint64_t walker) {
+    if (KIND == DEEPWALK) return node_slot(cfg, 1, c.v, c.deg, 0, walker);
+    if (KIND == METAPATH2VEC) return node_slot(cfg, m.num_types, c.v, c.deg, c.req, walker);
     return (uint64_t)c.off + affix;
 }
 

@@ -17,6 +17,7 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 
 #include "internal.h"
@@ -33,14 +34,22 @@ __device__ __forceinline__ void fail_back_edge(unsigned long long* ctr, uint32_t
     if (atomicCAS(&ctr[4], 0ull, 1ull) == 0ull) ctr[5] = ((unsigned long long)from << 32) | to;
 }
 
-// ------------------------------------------------------ throughput kernel
+// Lazy slot initialisation out of line: keeps the rarely taken init code
+// (count/select loops, burn-in) from inflating the walk kernel's registers.
 template <int KIND>
-__global__ void __launch_bounds__(kWalkBlock) k_walk(RunParams P) {
+__device__ __noinline__ uint32_t init_slot_ool(const DevGraph g, const DevModel m, const DevCfg cfg, const SCtx c,
+                                               uint64_t slot) {
+    return init_slot<KIND>(g, m, cfg, c, slot);
+}
+
+// ------------------------------------------------------ throughput kernel
+template <int KIND, int MINB>
+__global__ void __launch_bounds__(kWalkBlock, MINB) k_walk(RunParams P) {
     const DevGraph& g = P.g;
     const uint2 wkey = philox_key(P.cfg.seed, DOM_WALK);
     const uint32_t K = P.cfg.K, L = P.cfg.L;
     const unsigned lane = threadIdx.x & 31;
-    unsigned long long steps = 0, early = 0, inits = 0;
+    unsigned long long steps = 0, early = 0, inits = 0, retries = 0;
     for (;;) {
         // warp-aggregated work fetch (k-major item order spreads a start
         // node's K walkers over time, limiting same-slot contention)
@@ -72,11 +81,9 @@ __global__ void __launch_bounds__(kWalkBlock) k_walk(RunParams P) {
         c.req = 0;
         c.boot = second_order(KIND);
         uint32_t affix = 0;
-        uint64_t slot = v0;
-        if (KIND == METAPATH2VEC) {
-            c.req = P.m.metapath[metapath_next(P.m, 0)];
-            slot = (uint64_t)v0 * P.m.num_types + c.req;
-        }
+        uint64_t slot = 0;
+        if (KIND == METAPATH2VEC) c.req = P.m.metapath[metapath_next(P.m, 0)];
+        if (!second_order(KIND)) slot = slot_of<KIND>(P.m, P.cfg, c, 0, walker);
         uint32_t len = 1;
         uint32_t b0 = v0, b1 = 0, b2 = 0, b3 = 0;
         bool dead = false;
@@ -99,7 +106,7 @@ __global__ void __launch_bounds__(kWalkBlock) k_walk(RunParams P) {
             } else {
                 uint32_t e = __ldcg(P.chain + slot);
                 if (e == kEmpty) {
-                    const uint32_t ie = init_slot<KIND>(g, P.m, P.cfg, c, slot);
+                    const uint32_t ie = init_slot_ool<KIND>(g, P.m, P.cfg, c, slot);
                     const uint32_t old = atomicCAS(P.chain + slot, kEmpty, ie);
                     if (old == kEmpty) {
                         e = ie;
@@ -133,6 +140,7 @@ __global__ void __launch_bounds__(kWalkBlock) k_walk(RunParams P) {
                         break;
                     }
                     e = old;  // another walker advanced this chain: redo against it
+                    ++retries;
                 }
                 if (chosen == cand) {
                     next = uc;
@@ -156,11 +164,11 @@ __global__ void __launch_bounds__(kWalkBlock) k_walk(RunParams P) {
             ++steps;
             // update_state (models.cpp:125-136)
             if (KIND == DEEPWALK) {
-                slot = next;
+                slot = node_slot(P.cfg, 1, next, rn.deg, 0, walker);
             } else if (KIND == METAPATH2VEC) {
                 affix = metapath_next(P.m, affix);
                 c.req = P.m.metapath[metapath_next(P.m, affix)];
-                slot = (uint64_t)next * P.m.num_types + c.req;
+                slot = node_slot(P.cfg, P.m.num_types, next, rn.deg, c.req, walker);
             } else {
                 const uint32_t back = __ldg(g.rev + c.off + chosen);
                 if (back == kNoBack) {
@@ -192,6 +200,39 @@ __global__ void __launch_bounds__(kWalkBlock) k_walk(RunParams P) {
     if (steps) atomicAdd(&P.ctr[1], steps);
     if (early) atomicAdd(&P.ctr[2], early);
     if (inits) atomicAdd(&P.ctr[3], inits);
+    if (retries) atomicAdd(&P.ctr[6], retries);
+}
+
+// Eager chain-table initialisation of every arc-keyed slot (second-order
+// models). Result-identical to the lazy path (init randomness is keyed by the
+// slot), but runs with full warps and neighbouring threads share the node v.
+template <int KIND>
+__global__ void __launch_bounds__(256) k_init_all(RunParams P) {
+    const DevGraph& g = P.g;
+    unsigned long long inits = 0;
+    for (uint64_t a = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; a < g.m;
+         a += (uint64_t)gridDim.x * blockDim.x) {
+        // node of arc a: the last v with nodes[v].off <= a (skips isolated nodes)
+        uint32_t lo = 0, hi = g.n;
+        while (hi - lo > 1) {
+            const uint32_t mid = (lo + hi) >> 1;
+            if ((uint64_t)__ldg(&g.nodes[mid].off) <= a) lo = mid;
+            else hi = mid;
+        }
+        const NodeRec r = load_node(g, lo);
+        const uint32_t affix = (uint32_t)(a - (uint64_t)r.off);
+        const SCtx c = make_ctx<KIND>(g, P.m, lo, affix);
+        P.chain[a] = init_slot<KIND>(g, P.m, P.cfg, c, a);
+        ++inits;
+    }
+    if (inits) atomicAdd(&P.ctr[3], inits);
+}
+
+// Replica groups per node (chain_replicas - 1).
+__global__ void k_rep_counts(DevGraph g, uint32_t D, uint32_t* __restrict__ cnt) {
+    for (uint64_t v = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; v < g.n;
+         v += (uint64_t)gridDim.x * blockDim.x)
+        cnt[v] = chain_replicas(load_node(g, (uint32_t)v).deg, D) - 1;
 }
 
 // Rows of valid starts on isolated nodes: [v], an early termination each.
@@ -246,7 +287,7 @@ __global__ void k_det_propose(RunParams P, DetState S, uint32_t step, uint64_t i
             S.chosen[i] = bootstrap_pick(P.g, c, d.unit(), &ch) ? ch : kDeadMark;
             continue;
         }
-        const uint64_t slot = slot_of<KIND>(P.m, c, S.aff[i]);
+        const uint64_t slot = slot_of<KIND>(P.m, P.cfg, c, S.aff[i], walker);
         uint32_t e = __ldcg(P.chain + slot);
         if (e == kEmpty) {
             const uint32_t ie = init_slot<KIND>(P.g, P.m, P.cfg, c, slot);
@@ -397,7 +438,7 @@ __global__ void k_init_states(DevGraph g, DevModel m, DevCfg cfg, uint64_t n, co
             continue;
         }
         const SCtx c = make_ctx<KIND>(g, m, v, a);
-        const uint32_t e = init_slot<KIND>(g, m, cfg, c, slot_of<KIND>(m, c, a));
+        const uint32_t e = init_slot<KIND>(g, m, cfg, c, slot_of<KIND>(m, cfg, c, a, 0));
         out[i] = e == kDead ? kNoAffix : (e & kIdxMask);
     }
 }
@@ -440,11 +481,29 @@ unsigned grid_for(uint64_t work, int block = 256) {
     return (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(g, (uint64_t)sms() * 16));
 }
 
-template <int KIND>
+template <int KIND, int MINB>
 int walk_grid() {
     int per_sm = 0;
-    MHW_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_walk<KIND>, kWalkBlock, 0));
+    MHW_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_walk<KIND, MINB>, kWalkBlock, 0));
     return std::max(1, per_sm) * sms();
+}
+
+// Occupancy variant of the walk kernel (blocks of 256 per SM the register
+// allocation must allow); MHW_WALK_MINB selects it at session creation.
+int walk_minb() {
+    const char* e = std::getenv("MHW_WALK_MINB");
+    const int v = e ? std::atoi(e) : 4;
+    return (v == 4 || v == 6 || v == 8) ? v : 1;
+}
+
+template <int KIND, class F>
+void with_minb(int minb, F&& f) {
+    switch (minb) {
+        case 4: f(std::integral_constant<int, 4>{}); break;
+        case 6: f(std::integral_constant<int, 6>{}); break;
+        case 8: f(std::integral_constant<int, 8>{}); break;
+        default: f(std::integral_constant<int, 1>{}); break;
+    }
 }
 
 template <class F>
@@ -559,13 +618,38 @@ void session_create(Session& s, Graph& g, const mhw_model_desc& md, const mhw_wa
     s.node_end = wc.node_end ? wc.node_end : g.n;
     if (s.node_end > g.n || s.node_begin > s.node_end) invalid("node range out of bounds");
     s.stride = (wc.walk_length + 1 + 3) & ~3u;
-    // slot layout (manager.cpp:14-21)
-    s.slots = k_slots(m.kind, g);
-    if (s.slots > (uint64_t(1) << 40)) invalid("sampler layout too large: " + std::to_string(s.slots) + " slots");
     MHW_CK(cudaStreamCreateWithFlags(&s.stream, cudaStreamNonBlocking));
     MHW_CK(cudaEventCreate(&s.ev0));
     MHW_CK(cudaEventCreate(&s.ev1));
     cudaStream_t st = s.stream;
+    // slot layout (manager.cpp:14-21): base slots, then hub replicas for
+    // node-keyed models
+    s.slots = k_slots(m.kind, g);
+    s.cfg.rep_deg = kNoReplicas;
+    s.cfg.rep_base_slot = s.slots;
+    s.cfg.rep_group = nullptr;
+    if (!second_order(m.kind) && wc.chain_replica_degree != kNoReplicas && g.n) {
+        const uint32_t D = wc.chain_replica_degree ? wc.chain_replica_degree : kDefaultRepDeg;
+        if (g.max_deg >= D) {
+            DBuf<uint32_t> cnt(g.n + 1);
+            s.rep_group.alloc(g.n + 1);
+            MHW_CK(cudaMemsetAsync(cnt.p, 0, (g.n + 1) * 4, st));
+            k_rep_counts<<<grid_for(g.n), 256, 0, st>>>(g.view(), D, cnt.p);
+            MHW_CK(cudaGetLastError());
+            size_t bytes = 0;
+            MHW_CK(cub::DeviceScan::ExclusiveSum(nullptr, bytes, cnt.p, s.rep_group.p, (int64_t)g.n + 1, st));
+            DBuf<uint8_t> temp(std::max<size_t>(bytes, 1));
+            MHW_CK(cub::DeviceScan::ExclusiveSum(temp.p, bytes, cnt.p, s.rep_group.p, (int64_t)g.n + 1, st));
+            uint32_t groups = 0;
+            MHW_CK(cudaMemcpyAsync(&groups, s.rep_group.p + g.n, 4, cudaMemcpyDeviceToHost, st));
+            MHW_CK(cudaStreamSynchronize(st));
+            const uint64_t G = m.kind == METAPATH2VEC ? g.n_ntypes : 1;
+            s.cfg.rep_deg = D;
+            s.cfg.rep_group = s.rep_group.p;
+            s.slots += (uint64_t)groups * G;
+        }
+    }
+    if (s.slots > (uint64_t(1) << 40)) invalid("sampler layout too large: " + std::to_string(s.slots) + " slots");
     const uint32_t span = s.node_end - s.node_begin;
     DBuf<uint8_t> valid(std::max<uint32_t>(span, 1)), act(std::max<uint32_t>(span, 1)), iso(std::max<uint32_t>(span, 1));
     DBuf<uint32_t> rank(std::max<uint32_t>(span, 1) + 1), ids(std::max<uint32_t>(span, 1));
@@ -626,7 +710,16 @@ void session_create(Session& s, Graph& g, const mhw_model_desc& md, const mhw_wa
                                                (int64_t)n, 0, bits, st));
         s.sort_temp.alloc(std::max<size_t>(bytes, 1));
     } else {
-        dispatch(m.kind, [&](auto kc) { s.grid = walk_grid<decltype(kc)::value>(); });
+        s.minb = walk_minb();
+        dispatch(m.kind, [&](auto kc) {
+            with_minb<decltype(kc)::value>(s.minb, [&](auto mb) {
+                s.grid = walk_grid<decltype(kc)::value, decltype(mb)::value>();
+            });
+        });
+        // Eager slot init when walks will touch most arc-keyed slots anyway
+        // (identical chain values: init randomness is slot-keyed).
+        const bool dense = (double)s.n_items * s.cfg.L >= 8.0 * (double)s.slots;
+        s.eager_init = second_order(m.kind) && (wc.init_mode == 2 || (wc.init_mode == 0 && dense));
     }
     MHW_CK(cudaStreamSynchronize(st));
 }
@@ -702,7 +795,15 @@ void session_run(Session& s, cudaStream_t user) {
         } else {
             dispatch(s.model.dev.kind, [&](auto kc) {
                 constexpr int KIND = decltype(kc)::value;
-                k_walk<KIND><<<s.grid, kWalkBlock, 0, st>>>(P);
+                if constexpr (second_order(KIND)) {
+                    if (s.eager_init) {
+                        k_init_all<KIND><<<grid_for(s.g->m), 256, 0, st>>>(P);
+                        ++s.launches;
+                    }
+                }
+                with_minb<KIND>(s.minb, [&](auto mb) {
+                    k_walk<KIND, decltype(mb)::value><<<s.grid, kWalkBlock, 0, st>>>(P);
+                });
             });
             ++s.launches;
         }
@@ -728,6 +829,7 @@ void session_stats(Session& s, mhw_walk_stats& out) {
     out.skipped_starts = s.skipped;
     out.steps = h[1];
     out.slot_inits = h[3];
+    out.chain_retries = h[6];
     out.walk_seconds = ms * 1e-3;
     out.init_seconds = 0.0;
     out.steps_per_sec = ms > 0 ? (double)h[1] / (ms * 1e-3) : 0.0;
@@ -791,6 +893,9 @@ void run_init_states(Graph& g, const mhw_model_desc& md, const mhw_walk_config& 
     cfg.init_kind = wc.init_kind;
     cfg.burn_in = wc.burn_in_steps;
     cfg.hw = wc.hw_sample_size;
+    cfg.rep_deg = kNoReplicas;  // states are queried without a walker: base slots
+    cfg.rep_base_slot = 0;
+    cfg.rep_group = nullptr;
     cudaStream_t st = g.stream;
     DBuf<uint32_t> dpos(n), daff(n), dout(n);
     DBuf<unsigned> bad(1);

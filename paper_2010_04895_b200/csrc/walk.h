@@ -46,7 +46,7 @@ struct Session {
     uint32_t n_act = 0, n_iso = 0;
     uint64_t n_items = 0, rows = 0, skipped = 0, slots = 0;
     uint32_t stride = 0;
-    DBuf<uint32_t> chain, out, lens;
+    DBuf<uint32_t> chain, out, lens, rep_group;
     DBuf<unsigned long long> ctr;
     // deterministic schedule scratch
     DBuf<uint32_t> d_v, d_aff, d_len, d_idx, d_idx2, d_cand, d_chosen;
@@ -55,6 +55,8 @@ struct Session {
     DBuf<double> d_wc, d_u;
     int sort_bits = 1;
     int grid = 0;
+    bool eager_init = false;
+    int minb = 1;
     uint32_t launches = 0;
     cudaStream_t stream = nullptr;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;

@@ -152,6 +152,8 @@ class WalkConfig:
     schedule: Schedule | None = None   # None: derived from threads
     node_begin: int = 0
     node_end: int = 0
+    chain_replica_degree: int = 0      # 0: 256; 0xFFFFFFFF: one chain per state
+    init_mode: int = 0                 # 0 auto, 1 lazy, 2 eager
 
     def _c(self):
         c = L.WalkConfigC()
@@ -166,6 +168,7 @@ class WalkConfig:
             sched = Schedule.deterministic if self.threads == 1 else Schedule.throughput
         c.schedule = int(sched)
         c.node_begin, c.node_end = self.node_begin, self.node_end
+        c.chain_replica_degree, c.init_mode = self.chain_replica_degree, self.init_mode
         return c
 
 
@@ -179,11 +182,12 @@ class RunStats:
     init_seconds: float = 0.0
     walk_seconds: float = 0.0
     slot_inits: int = 0
+    chain_retries: int = 0
 
     @classmethod
     def _from(cls, s: L.WalkStatsC):
         return cls(s.walks, s.early_terminations, s.skipped_starts, s.steps, s.steps_per_sec, s.init_seconds,
-                   s.walk_seconds, s.slot_inits)
+                   s.walk_seconds, s.slot_inits, s.chain_retries)
 
 
 class WalkCorpus:

@@ -29,6 +29,7 @@ def walk_model(md: O.ModelDesc):
 
 def walk_config(cfg: O.WalkCfg, threads=1, **kw):
     from paper_2010_04895_b200 import InitKind, InitStrategy, WalkConfig
+    kw.setdefault("chain_replica_degree", cfg.replica_degree)
     return WalkConfig(walks_per_node=cfg.K, walk_length=cfg.L, threads=threads, seed=cfg.seed,
                       init=InitStrategy(InitKind(cfg.init_kind), cfg.burn_in_steps, cfg.hw_sample_size), **kw)
 

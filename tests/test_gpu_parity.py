@@ -59,6 +59,24 @@ def test_deterministic_walks_equal_oracle(mhw, oracle, kind, init):
         ost["walks"], ost["early_terminations"], ost["skipped_starts"], ost["steps"])
 
 
+@pytest.mark.parametrize("kind", [O.DEEPWALK, O.METAPATH2VEC])
+@pytest.mark.parametrize("rep", [4, 16])
+def test_deterministic_hub_replicas_equal_oracle(mhw, oracle, kind, rep):
+    """Node-keyed chains replicated at hubs (degree >= rep): same layout and
+    walker->replica map on both sides, corpus byte-identical."""
+    rng = O.XoRng(21)
+    g = O.preferential_attachment(300, 3, rng)
+    O.assign_random_types(g, 2, rng)
+    g.w = np.array([float(np.float32(0.5 + rng.uniform_real())) for _ in range(g.m)])
+    # symmetric weights are not needed for first-order models
+    md = model_desc(kind, g)
+    cfg = O.WalkCfg(K=6, L=30, seed=3, init_kind=O.INIT_BURN_IN, burn_in_steps=5, replica_degree=rep)
+    orow, olen, ost = oracle.generate_walks(g, md, cfg, rng=O.RNG_PHILOX, order=O.ORDER_STEP)
+    corpus = mhw.generate_walks(device_graph(g), walk_model(md), walk_config(cfg))
+    assert corpus_equal(orow, olen, corpus.rows, corpus.lengths)
+    assert corpus.stats.slot_inits == ost["init_calls"]
+
+
 @pytest.mark.parametrize("kind", KINDS)
 def test_deterministic_unweighted_and_isolated(mhw, oracle, kind):
     """Unweighted graph (bootstrap closed form) with isolated nodes."""
