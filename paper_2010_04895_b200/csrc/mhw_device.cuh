@@ -19,6 +19,7 @@ namespace mhw {
 constexpr uint32_t kNoAffix = 0xFFFFFFFFu;   // models.hpp:17
 constexpr uint32_t kEmpty = 0xFFFFFFFFu;     // chain slot never initialised
 constexpr uint32_t kDead = 0xFFFFFFFEu;      // chain slot is a dead end
+constexpr uint32_t kLocked = 0xFFFFFFFDu;    // chain slot held by a walker mid-transition
 constexpr uint32_t kIdxMask = 0x3FFFFFFFu;   // low 30 bits: Last index
 constexpr uint32_t kMaxDegree = 0x3FFFFFF0u; // degrees must fit the index field
 constexpr uint32_t kNoBack = 0xFFFFFFFFu;    // rev[] entry of an arc without back arc

@@ -30,6 +30,12 @@ namespace {
 constexpr int kWalkBlock = 256;
 constexpr uint32_t kDeadMark = 0xFFFFFFFEu;
 
+// Releases a chain slot taken with atomicExch(kLocked): publishes the new
+// chain state with a release store at GPU scope.
+__device__ __forceinline__ void chain_release(uint32_t* p, uint32_t v) {
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
 __device__ __forceinline__ void fail_back_edge(unsigned long long* ctr, uint32_t from, uint32_t to) {
     if (atomicCAS(&ctr[4], 0ull, 1ull) == 0ull) ctr[5] = ((unsigned long long)from << 32) | to;
 }
@@ -104,18 +110,28 @@ __global__ void __launch_bounds__(kWalkBlock, MINB) k_walk(RunParams P) {
                 next = load_id(g, c.off + chosen);
                 rn = load_node(g, next);
             } else {
-                uint32_t e = __ldcg(P.chain + slot);
+                // Take the slot: the chain word itself is the lock. The
+                // transition (proposal evaluation + decision) happens while
+                // holding it, so the order of transitions on a chain never
+                // depends on proposals or decisions -> every slot runs an
+                // exact sequential M-H chain (manager.cpp:63-71 semantics
+                // without lost updates).
+                uint32_t e = atomicExch(P.chain + slot, kLocked);
+                if (e == kLocked) {
+                    unsigned ns = 32;
+                    do {
+                        ++retries;
+                        __nanosleep(ns);
+                        ns = ns < 512 ? ns * 2 : 512;
+                        e = atomicExch(P.chain + slot, kLocked);
+                    } while (e == kLocked);
+                }
                 if (e == kEmpty) {
-                    const uint32_t ie = init_slot_ool<KIND>(g, P.m, P.cfg, c, slot);
-                    const uint32_t old = atomicCAS(P.chain + slot, kEmpty, ie);
-                    if (old == kEmpty) {
-                        e = ie;
-                        ++inits;
-                    } else {
-                        e = old;
-                    }
+                    e = init_slot_ool<KIND>(g, P.m, P.cfg, c, slot);
+                    ++inits;
                 }
                 if (e == kDead) {
+                    chain_release(P.chain + slot, kDead);
                     dead = true;
                     break;
                 }
@@ -125,23 +141,13 @@ __global__ void __launch_bounds__(kWalkBlock, MINB) k_walk(RunParams P) {
                 const NodeRec rc = load_node(g, uc);
                 const uint32_t cls_c = second_order(KIND) ? alpha_class(g, P.m, c, uc, &rc) : 0u;
                 const double wc = wprime<KIND>(g, P.m, c, cand, rc.type, cls_c);
-                for (;;) {
-                    const uint32_t last = e & kIdxMask, cls_l = e >> 30;
-                    uint16_t ltype = 0;
-                    if (needs_utype<KIND>()) ltype = load_node(g, load_id(g, c.off + last)).type;
-                    const double wl = wprime<KIND>(g, P.m, c, last, ltype, cls_l);
-                    if (!mh_accept(wc, wl, u) || cand == last) {
-                        chosen = last;
-                        break;
-                    }
-                    const uint32_t old = atomicCAS(P.chain + slot, e, pack_entry(cand, cls_c));
-                    if (old == e) {
-                        chosen = cand;
-                        break;
-                    }
-                    e = old;  // another walker advanced this chain: redo against it
-                    ++retries;
-                }
+                const uint32_t last = e & kIdxMask, cls_l = e >> 30;
+                uint16_t ltype = 0;
+                if (needs_utype<KIND>()) ltype = load_node(g, load_id(g, c.off + last)).type;
+                const double wl = wprime<KIND>(g, P.m, c, last, ltype, cls_l);
+                const bool acc = mh_accept(wc, wl, u) && cand != last;
+                chain_release(P.chain + slot, acc ? pack_entry(cand, cls_c) : e);
+                chosen = acc ? cand : last;
                 if (chosen == cand) {
                     next = uc;
                     rn = rc;
