@@ -110,7 +110,7 @@ typedef struct mhw_walk_config {
     uint32_t node_begin;
     uint32_t node_end;
     /* Node-keyed models (deepwalk, metapath2vec): nodes of degree >= this get
-     * up to 64 independent chains per state, picked by walker id (0 = 256,
+     * up to 256 independent chains per state, picked by walker id (0 = 128,
      * 0xFFFFFFFF = one chain per state exactly as SamplerManager). */
     uint32_t chain_replica_degree;
     /* Second-order slot initialisation: 0 auto, 1 lazy (first query, as

@@ -672,7 +672,7 @@ static inline uint64_t slot_index(const og_graph* g, const og_model* m, uint32_t
 }
 
 /* Engine chain layout: node-keyed states of hub nodes (degree >= D) own
- * R = 2^(floor(log2(deg/D))+1) <= 64 chains; walker w uses chain
+ * R = 2^(floor(log2(deg/D))+1) <= 256 chains; walker w uses chain
  * (w * golden >> 40) & (R-1); chains 1..R-1 live after the n*G base slots. */
 typedef struct {
     uint32_t D;
@@ -686,7 +686,7 @@ static uint32_t chain_replicas(uint32_t deg, uint32_t D) {
     uint32_t q = deg / D, lg = 0;
     while (q >>= 1) ++lg;
     const uint32_t r = 2u << lg;
-    return r < 64 ? r : 64;
+    return r < 256 ? r : 256;
 }
 
 static uint64_t engine_slot(const og_graph* g, const og_model* m, const replica_layout_t* rl, uint32_t v,
@@ -814,7 +814,7 @@ int og_generate_walks(const og_graph* g, const og_model* m, const og_config* c, 
     rl.base = slots;
     rl.group = NULL;
     if ((m->kind == OG_DEEPWALK || m->kind == OG_METAPATH2VEC) && rl.D != OG_NO_REPLICAS) {
-        if (rl.D == 0) rl.D = 256;
+        if (rl.D == 0) rl.D = 128;
         rl.group = (uint32_t*)calloc((size_t)g->n + 1, sizeof(uint32_t));
         for (uint32_t v = 0; v < g->n; ++v) rl.group[v + 1] = rl.group[v] + chain_replicas(deg_of(g, v), rl.D) - 1;
         slots += (uint64_t)rl.group[g->n] * rl.G;

@@ -33,6 +33,7 @@ DevGraph Graph::view() const {
     d.rev = rev.n ? rev.p : nullptr;
     d.wtotal = wtotal.n ? wtotal.p : nullptr;
     d.tcount = tcount.n ? tcount.p : nullptr;
+    d.htab = htab.n ? htab.p : nullptr;
     d.n_ntypes = n_ntypes;
     d.n_etypes = n_etypes;
     d.verified_sym = verified_sym ? 1 : 0;
@@ -41,7 +42,7 @@ DevGraph Graph::view() const {
 
 uint64_t Graph::device_bytes() const {
     return nodes.bytes() + ids.bytes() + w.bytes() + ntype.bytes() + etype.bytes() + rev.bytes() +
-           wtotal.bytes() + tcount.bytes();
+           wtotal.bytes() + tcount.bytes() + htab.bytes();
 }
 
 namespace {
@@ -126,6 +127,29 @@ __global__ void k_rev(DevGraph g, uint32_t* __restrict__ rev, unsigned* __restri
             miss |= b == kNoBack;
         }
         if (__any_sync(0xffffffffu, miss) && lane == 0) atomicAdd(missing, 1u);
+    }
+}
+
+// Warp per node: insert N(v) into v's adjacency hash set (degree >= kHashMinDeg).
+__global__ void k_hash_build(DevGraph g, uint32_t* __restrict__ tab) {
+    const unsigned lane = threadIdx.x & 31;
+    const uint64_t wid = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    for (uint64_t v = wid; v < g.n; v += nw) {
+        const NodeRec r = load_node(g, (uint32_t)v);
+        if (r.deg < kHashMinDeg) continue;
+        const uint32_t nb = hash_buckets(r.deg);
+        uint32_t* base = tab + 8 * hash_base(r.off, (uint32_t)v);
+        for (uint32_t i = lane; i < r.deg; i += 32) {
+            const uint32_t key = load_id(g, r.off + i);
+            uint32_t b = hash_bucket(key, nb);
+            for (;;) {
+                bool done = false;
+                for (int s = 0; s < 8 && !done; ++s) done = atomicCAS(base + 8 * b + s, kHashEmpty, key) == kHashEmpty;
+                if (done) break;
+                b = b + 1 == nb ? 0 : b + 1;
+            }
+        }
     }
 }
 
@@ -485,6 +509,7 @@ void graph_finalize(Graph& g, const int64_t* d_off, const uint16_t* d_ntypes) {
     g.rev.reset();
     g.wtotal.reset();
     g.tcount.reset();
+    g.htab.reset();
     g.verified_sym = false;
 }
 
@@ -731,6 +756,7 @@ void graph_replicate(const Graph& s, Graph& d, int device) {
     copy_buf(s.rev, s.device, d.rev, device, d.stream);
     copy_buf(s.wtotal, s.device, d.wtotal, device, d.stream);
     copy_buf(s.tcount, s.device, d.tcount, device, d.stream);
+    copy_buf(s.htab, s.device, d.htab, device, d.stream);
     MHW_CK(cudaStreamSynchronize(d.stream));
     d.n = s.n;
     d.m = s.m;
@@ -779,6 +805,17 @@ void graph_ensure_rev(Graph& g) {
     MHW_CK(cudaMemcpyAsync(&h, missing.p, sizeof(h), cudaMemcpyDeviceToHost, g.stream));
     MHW_CK(cudaStreamSynchronize(g.stream));
     g.verified_sym = h == 0;
+}
+
+void graph_ensure_hash(Graph& g) {
+    if (g.htab.n || !g.m || g.max_deg < kHashMinDeg) return;
+    DeviceGuard dg(g.device);
+    const uint64_t buckets = (g.m >> 2) + g.n + 1;
+    g.htab.alloc(8 * buckets);
+    MHW_CK(cudaMemsetAsync(g.htab.p, 0xFF, g.htab.bytes(), g.stream));
+    k_hash_build<<<grid_for((uint64_t)g.n * 32), kBlock, 0, g.stream>>>(g.view(), g.htab.p);
+    MHW_CK(cudaGetLastError());
+    MHW_CK(cudaStreamSynchronize(g.stream));
 }
 
 void graph_ensure_wtotal(Graph& g) {

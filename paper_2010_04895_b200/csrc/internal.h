@@ -90,6 +90,7 @@ struct Graph {
     DBuf<uint32_t> rev;      // lazily built
     DBuf<double> wtotal;     // lazily built
     DBuf<uint32_t> tcount;   // lazily built
+    DBuf<uint32_t> htab;     // adjacency hash sets, lazily built
     uint16_t n_ntypes = 0, n_etypes = 0;
     bool symmetric = false;
     bool verified_sym = false;
@@ -120,6 +121,7 @@ void graph_download(const Graph& g, int64_t* offsets, int32_t* nbr, float* w, ui
 void graph_ensure_rev(Graph& g);
 void graph_ensure_wtotal(Graph& g);
 void graph_ensure_tcount(Graph& g);
+void graph_ensure_hash(Graph& g);
 void graph_alias_tables(Graph& g, double* prob, uint32_t* alias);
 
 // Bound model (host validation of WalkModel::bind, models.cpp:29-74).

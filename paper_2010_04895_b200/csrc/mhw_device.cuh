@@ -59,10 +59,49 @@ struct DevGraph {
     const uint32_t* __restrict__ rev;     // index of v in N(u) for arc v->u
     const double* __restrict__ wtotal;    // sequential fp64 slice sums
     const uint32_t* __restrict__ tcount;  // fairwalk type counts, n * n_ntypes
+    const uint32_t* __restrict__ htab;    // adjacency hash sets (nullptr: not built)
     uint16_t n_ntypes;
     uint16_t n_etypes;
     int verified_sym;                     // every arc has its back arc
 };
+
+// ------------------------------------------------- adjacency hash sets
+// Nodes of degree >= kHashMinDeg get an exact hash set of their neighbour
+// ids: ceil(deg/4) buckets of 8 u32 keys (one 32-byte sector, load <= 0.5),
+// linear probing over buckets. Node v's buckets start at bucket
+// (off_v >> 2) + v, so no per-node metadata is needed (the bases of
+// consecutive nodes never overlap: floor((o+d)/4) + 1 >= floor(o/4) + ceil(d/4)).
+constexpr uint32_t kHashMinDeg = 32;
+constexpr uint32_t kHashEmpty = 0xFFFFFFFFu;
+
+__host__ __device__ __forceinline__ uint64_t hash_base(long long off, uint32_t v) {
+    return ((uint64_t)off >> 2) + v;
+}
+__host__ __device__ __forceinline__ uint32_t hash_buckets(uint32_t deg) { return (deg + 3) >> 2; }
+__host__ __device__ __forceinline__ uint32_t hash_bucket(uint32_t key, uint32_t nb) {
+    uint32_t h = key;  // murmur3 fmix32
+    h ^= h >> 16;
+    h *= 0x85EBCA6Bu;
+    h ^= h >> 13;
+    h *= 0xC2B2AE35u;
+    h ^= h >> 16;
+    return (uint32_t)(((uint64_t)h * nb) >> 32);
+}
+
+__device__ __forceinline__ bool hash_contains(const uint32_t* __restrict__ tab, long long off, uint32_t v,
+                                              uint32_t deg, uint32_t key) {
+    const uint32_t nb = hash_buckets(deg);
+    const uint4* base = reinterpret_cast<const uint4*>(tab) + 2 * hash_base(off, v);
+    uint32_t b = hash_bucket(key, nb);
+    for (;;) {
+        const uint4 x = __ldg(base + 2 * b), y = __ldg(base + 2 * b + 1);
+        if (x.x == key || x.y == key || x.z == key || x.w == key || y.x == key || y.y == key || y.z == key ||
+            y.w == key)
+            return true;
+        if (y.w == kHashEmpty) return false;  // slots fill in order: a free last slot ends the probe
+        b = b + 1 == nb ? 0 : b + 1;
+    }
+}
 
 struct DevModel {
     int kind;
@@ -89,11 +128,11 @@ struct DevCfg {
 };
 
 constexpr uint32_t kNoReplicas = 0xFFFFFFFFu;
-constexpr uint32_t kDefaultRepDeg = 256;
-constexpr uint32_t kMaxReplicas = 64;
+constexpr uint32_t kDefaultRepDeg = 128;
+constexpr uint32_t kMaxReplicas = 256;
 
 // Chains per node-keyed state: 1 below rep_deg, else 2^(floor(log2(deg /
-// rep_deg)) + 1) capped at 64 -- about 2*deg/rep_deg concurrent chains, so a
+// rep_deg)) + 1) capped at 256 -- about 2*deg/rep_deg concurrent chains, so a
 // hub's visitors spread over independent exact M-H chains.
 __host__ __device__ __forceinline__ uint32_t chain_replicas(uint32_t deg, uint32_t rep_deg) {
     if (rep_deg == kNoReplicas || deg < rep_deg) return 1;
@@ -276,14 +315,31 @@ __device__ __forceinline__ uint32_t alpha_class(const DevGraph& g, const DevMode
                                                 uint32_t u, const NodeRec* urec) {
     if (m.alpha_trivial) return 1;
     if (u == c.s) return 0;
-    long long off = c.off_s;
-    uint32_t deg = c.deg_s, key = u;
-    if (g.verified_sym && urec && urec->deg < deg) {
-        off = urec->off;
-        deg = urec->deg;
-        key = c.s;
+    // is_adjacent(s, u): u in N(s), or s in N(u) when every arc has its
+    // back arc. Cheapest structure first: a <= 8-entry slice (one sector),
+    // else a hash set (one sector), else binary search of the shorter slice.
+    uint32_t node_a = c.s, deg_a = c.deg_s, key_a = u;  // shorter slice
+    long long off_a = c.off_s;
+    uint32_t node_b = 0, deg_b = 0, key_b = 0;           // longer slice
+    long long off_b = 0;
+    const bool both = g.verified_sym && urec;
+    if (both) {
+        node_b = u;
+        off_b = urec->off;
+        deg_b = urec->deg;
+        key_b = c.s;
+        if (deg_b < deg_a) {
+            uint32_t t = node_a; node_a = node_b; node_b = t;
+            t = deg_a; deg_a = deg_b; deg_b = t;
+            t = key_a; key_a = key_b; key_b = t;
+            const long long o = off_a; off_a = off_b; off_b = o;
+        }
     }
-    return adj_search(g.ids, off, deg, key) ? 1u : 2u;
+    if (deg_a > 8 && g.htab) {
+        if (deg_a >= kHashMinDeg) return hash_contains(g.htab, off_a, node_a, deg_a, key_a) ? 1u : 2u;
+        if (both && deg_b >= kHashMinDeg) return hash_contains(g.htab, off_b, node_b, deg_b, key_b) ? 1u : 2u;
+    }
+    return adj_search(g.ids, off_a, deg_a, key_a) ? 1u : 2u;
 }
 
 __device__ __forceinline__ double alpha_value(const DevModel& m, uint32_t cls) {

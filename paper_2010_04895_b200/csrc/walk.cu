@@ -116,7 +116,17 @@ __global__ void __launch_bounds__(kWalkBlock, MINB) k_walk(RunParams P) {
                 // depends on proposals or decisions -> every slot runs an
                 // exact sequential M-H chain (manager.cpp:63-71 semantics
                 // without lost updates).
+                // The exchange is issued before any candidate-dependent work
+                // (its timing cannot depend on the proposal); the candidate
+                // evaluation overlaps its latency, and the chain state it
+                // returns is only consumed by the decision.
                 uint32_t e = atomicExch(P.chain + slot, kLocked);
+                const uint32_t cand = d.index(c.deg);
+                const double u = d.unit();
+                const uint32_t uc = load_id(g, c.off + cand);
+                const NodeRec rc = load_node(g, uc);
+                const uint32_t cls_c = second_order(KIND) ? alpha_class(g, P.m, c, uc, &rc) : 0u;
+                const double wc = wprime<KIND>(g, P.m, c, cand, rc.type, cls_c);
                 if (e == kLocked) {
                     unsigned ns = 32;
                     do {
@@ -135,12 +145,6 @@ __global__ void __launch_bounds__(kWalkBlock, MINB) k_walk(RunParams P) {
                     dead = true;
                     break;
                 }
-                const uint32_t cand = d.index(c.deg);
-                const double u = d.unit();
-                const uint32_t uc = load_id(g, c.off + cand);
-                const NodeRec rc = load_node(g, uc);
-                const uint32_t cls_c = second_order(KIND) ? alpha_class(g, P.m, c, uc, &rc) : 0u;
-                const double wc = wprime<KIND>(g, P.m, c, cand, rc.type, cls_c);
                 const uint32_t last = e & kIdxMask, cls_l = e >> 30;
                 uint16_t ltype = 0;
                 if (needs_utype<KIND>()) ltype = load_node(g, load_id(g, c.off + last)).type;
@@ -588,6 +592,7 @@ void model_bind(Model& mb, Graph& g, const mhw_model_desc& d) {
     if (second_order(k)) {
         graph_ensure_rev(g);
         graph_ensure_wtotal(g);
+        if (!m.alpha_trivial) graph_ensure_hash(g);
     }
     if (k == FAIRWALK) graph_ensure_tcount(g);
 }

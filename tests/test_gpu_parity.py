@@ -42,6 +42,47 @@ def test_decide_bit_exact(mhw, oracle, kind, weighted):
     assert np.array_equal(oacc, gacc)
 
 
+def rmat_host(oracle, scale=11, seed=9, types=3):
+    lo, hi = oracle.rmat_pairs(scale, 16, seed=seed)
+    w = oracle.pair_weights(seed, lo, hi, 1.0, 10.0).astype(np.float64)
+    hg = oracle.build_csr(lo, hi, w, symmetrize=True, n_nodes=1 << scale)
+    hg.ntype = np.random.default_rng(seed).integers(0, types, hg.n).astype(np.uint16)
+    hg.n_ntypes = types
+    return hg
+
+
+@pytest.mark.parametrize("kind", [O.NODE2VEC, O.EDGE2VEC, O.FAIRWALK])
+def test_decide_bit_exact_on_hubs(mhw, oracle, kind):
+    """Hub-heavy R-MAT graph: alpha goes through the adjacency hash sets
+    (degree >= 32) and the shorter-slice search; decisions stay bit-exact."""
+    hg = rmat_host(oracle)
+    assert np.diff(hg.offsets).max() >= 256
+    md = model_desc(kind, hg, p=0.4, q=2.5, M=np.random.default_rng(2).uniform(0.5, 2.0, (9, 9)))
+    pos, aff, cand, last, u = random_triples(hg, md, 50000, seed=kind)
+    # bias half of the states onto the top hubs
+    deg = np.diff(hg.offsets).astype(np.int64)
+    hubs = np.argsort(deg)[-32:]
+    pos[::2] = hubs[np.arange(len(pos[::2])) % 32]
+    d = deg[pos]
+    cand, last = cand % d, last % d
+    aff = np.where(aff == O.NO_AFFIX, aff, aff % d)
+    owc, owl, oacc = oracle.decide(hg, md, pos, aff, cand, last, u)
+    gwc, gwl, gacc = mhw.decide(device_graph(hg), walk_model(md), pos, aff, cand, last, u)
+    assert np.array_equal(owc.view(np.uint64), gwc.view(np.uint64))
+    assert np.array_equal(owl.view(np.uint64), gwl.view(np.uint64))
+    assert np.array_equal(oacc, gacc)
+
+
+@pytest.mark.parametrize("kind", [O.NODE2VEC, O.EDGE2VEC, O.FAIRWALK])
+def test_deterministic_walks_on_hubs_equal_oracle(mhw, oracle, kind):
+    hg = rmat_host(oracle, scale=10, seed=4)
+    md = model_desc(kind, hg, p=0.25, q=4.0, M=np.random.default_rng(3).uniform(0.5, 2.0, (9, 9)))
+    cfg = O.WalkCfg(K=2, L=40, seed=8, init_kind=O.INIT_BURN_IN, burn_in_steps=10)
+    orow, olen, _ = oracle.generate_walks(hg, md, cfg, rng=O.RNG_PHILOX, order=O.ORDER_STEP)
+    corpus = mhw.generate_walks(device_graph(hg), walk_model(md), walk_config(cfg))
+    assert corpus_equal(orow, olen, corpus.rows, corpus.lengths)
+
+
 @pytest.mark.parametrize("kind", KINDS)
 @pytest.mark.parametrize("init", INITS)
 def test_deterministic_walks_equal_oracle(mhw, oracle, kind, init):
