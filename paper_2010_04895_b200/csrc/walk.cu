@@ -30,10 +30,11 @@ namespace {
 constexpr int kWalkBlock = 256;
 constexpr uint32_t kDeadMark = 0xFFFFFFFEu;
 
-// Releases a chain slot taken with atomicExch(kLocked): publishes the new
-// chain state with a release store at GPU scope.
+// Releases a chain slot taken with atomicExch(kLocked). The lock protects
+// only the chain word itself, so a relaxed GPU-scope store suffices (no
+// other data is published; a release store would add a full fence).
 __device__ __forceinline__ void chain_release(uint32_t* p, uint32_t v) {
-    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+    asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
 __device__ __forceinline__ void fail_back_edge(unsigned long long* ctr, uint32_t from, uint32_t to) {
@@ -49,8 +50,8 @@ __device__ __noinline__ uint32_t init_slot_ool(const DevGraph g, const DevModel 
 }
 
 // ------------------------------------------------------ throughput kernel
-template <int KIND, int MINB>
-__global__ void __launch_bounds__(kWalkBlock, MINB) k_walk(RunParams P) {
+template <int KIND, int REGS>
+__global__ void __launch_bounds__(kWalkBlock) __maxnreg__(REGS) k_walk(RunParams P) {
     const DevGraph& g = P.g;
     const uint2 wkey = philox_key(P.cfg.seed, DOM_WALK);
     const uint32_t K = P.cfg.K, L = P.cfg.L;
@@ -498,21 +499,23 @@ int walk_grid() {
     return std::max(1, per_sm) * sms();
 }
 
-// Occupancy variant of the walk kernel (blocks of 256 per SM the register
-// allocation must allow); MHW_WALK_MINB selects it at session creation.
-int walk_minb() {
-    const char* e = std::getenv("MHW_WALK_MINB");
-    const int v = e ? std::atoi(e) : 4;
-    return (v == 4 || v == 6 || v == 8) ? v : 1;
+// Register-cap variant of the walk kernel (occupancy vs spills trade-off,
+// measured in profiles/); MHW_WALK_REGS selects it at session creation.
+// Defaults from the sweep in profiles/: deepwalk 80 (4.84 vs 5.27 ms on cfg1),
+// second-order models uncapped (no spills; 65.7 vs 69-71 ms on cfg2).
+int walk_minb(int kind) {
+    const char* e = std::getenv("MHW_WALK_REGS");
+    const int v = e ? std::atoi(e) : (kind == DEEPWALK ? 80 : 255);
+    return (v == 80 || v == 96 || v == 112) ? v : 255;
 }
 
 template <int KIND, class F>
-void with_minb(int minb, F&& f) {
-    switch (minb) {
-        case 4: f(std::integral_constant<int, 4>{}); break;
-        case 6: f(std::integral_constant<int, 6>{}); break;
-        case 8: f(std::integral_constant<int, 8>{}); break;
-        default: f(std::integral_constant<int, 1>{}); break;
+void with_minb(int regs, F&& f) {
+    switch (regs) {
+        case 80: f(std::integral_constant<int, 80>{}); break;
+        case 96: f(std::integral_constant<int, 96>{}); break;
+        case 112: f(std::integral_constant<int, 112>{}); break;
+        default: f(std::integral_constant<int, 255>{}); break;
     }
 }
 
@@ -721,7 +724,7 @@ void session_create(Session& s, Graph& g, const mhw_model_desc& md, const mhw_wa
                                                (int64_t)n, 0, bits, st));
         s.sort_temp.alloc(std::max<size_t>(bytes, 1));
     } else {
-        s.minb = walk_minb();
+        s.minb = walk_minb(m.kind);
         dispatch(m.kind, [&](auto kc) {
             with_minb<decltype(kc)::value>(s.minb, [&](auto mb) {
                 s.grid = walk_grid<decltype(kc)::value, decltype(mb)::value>();
