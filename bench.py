@@ -361,7 +361,7 @@ def run_mine(args, cfg):
             "setup_seconds": t_setup,
         }
     # ---- e2e through the public C ABI with host buffers
-    e2e = run_e2e(args, cfg, g, model, wcfg, dev, dist)
+    e2e = None if args.no_e2e else run_e2e(args, cfg, g, model, wcfg, dev, dist)
     if rank == 0:
         line["e2e"] = e2e
         if world == 1 and not args.no_cpu_baseline:
@@ -458,6 +458,7 @@ def main():
     ap.add_argument("--config", default="cfg2", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="mine", choices=["mine", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true", help="skip the host-buffer e2e leg")
     args = ap.parse_args()
     cfg = dict(CONFIGS[args.config])
     cfg["name"] = args.config
