@@ -50,7 +50,9 @@ __device__ __noinline__ uint32_t init_slot_ool(const DevGraph g, const DevModel 
 }
 
 // ------------------------------------------------------ throughput kernel
-template <int KIND, int REGS>
+// LAZY = false: every slot was initialised by k_init_all before the launch,
+// so the lazy-init call (and the registers the call ABI pins) is compiled out.
+template <int KIND, int REGS, bool LAZY>
 __global__ void __launch_bounds__(kWalkBlock) __maxnreg__(REGS) k_walk(RunParams P) {
     const DevGraph& g = P.g;
     const uint2 wkey = philox_key(P.cfg.seed, DOM_WALK);
@@ -138,8 +140,13 @@ __global__ void __launch_bounds__(kWalkBlock) __maxnreg__(REGS) k_walk(RunParams
                     } while (e == kLocked);
                 }
                 if (e == kEmpty) {
-                    e = init_slot_ool<KIND>(g, P.m, P.cfg, c, slot);
-                    ++inits;
+                    if constexpr (LAZY) {
+                        e = init_slot<KIND>(g, P.m, P.cfg, c, slot);
+                        ++inits;
+                    } else {
+                        e = kDead;  // unreachable: eager init filled every slot
+                        fail_back_edge(P.ctr, 0xFFFFFFFFu, 0xFFFFFFFFu);
+                    }
                 }
                 if (e == kDead) {
                     chain_release(P.chain + slot, kDead);
@@ -492,10 +499,10 @@ unsigned grid_for(uint64_t work, int block = 256) {
     return (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(g, (uint64_t)sms() * 16));
 }
 
-template <int KIND, int MINB>
+template <int KIND, int MINB, bool LAZY>
 int walk_grid() {
     int per_sm = 0;
-    MHW_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_walk<KIND, MINB>, kWalkBlock, 0));
+    MHW_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_walk<KIND, MINB, LAZY>, kWalkBlock, 0));
     return std::max(1, per_sm) * sms();
 }
 
@@ -506,7 +513,7 @@ int walk_grid() {
 int walk_minb(int kind) {
     const char* e = std::getenv("MHW_WALK_REGS");
     const int v = e ? std::atoi(e) : (kind == DEEPWALK ? 80 : 255);
-    return (v == 80 || v == 96 || v == 112) ? v : 255;
+    return (v == 64 || v == 80 || v == 96) ? v : 255;
 }
 
 template <int KIND, class F>
@@ -514,7 +521,7 @@ void with_minb(int regs, F&& f) {
     switch (regs) {
         case 80: f(std::integral_constant<int, 80>{}); break;
         case 96: f(std::integral_constant<int, 96>{}); break;
-        case 112: f(std::integral_constant<int, 112>{}); break;
+        case 64: f(std::integral_constant<int, 64>{}); break;
         default: f(std::integral_constant<int, 255>{}); break;
     }
 }
@@ -724,16 +731,17 @@ void session_create(Session& s, Graph& g, const mhw_model_desc& md, const mhw_wa
                                                (int64_t)n, 0, bits, st));
         s.sort_temp.alloc(std::max<size_t>(bytes, 1));
     } else {
-        s.minb = walk_minb(m.kind);
-        dispatch(m.kind, [&](auto kc) {
-            with_minb<decltype(kc)::value>(s.minb, [&](auto mb) {
-                s.grid = walk_grid<decltype(kc)::value, decltype(mb)::value>();
-            });
-        });
         // Eager slot init when walks will touch most arc-keyed slots anyway
         // (identical chain values: init randomness is slot-keyed).
         const bool dense = (double)s.n_items * s.cfg.L >= 8.0 * (double)s.slots;
         s.eager_init = second_order(m.kind) && (wc.init_mode == 2 || (wc.init_mode == 0 && dense));
+        s.minb = walk_minb(m.kind);
+        dispatch(m.kind, [&](auto kc) {
+            with_minb<decltype(kc)::value>(s.minb, [&](auto mb) {
+                if (s.eager_init) s.grid = walk_grid<decltype(kc)::value, decltype(mb)::value, false>();
+                else s.grid = walk_grid<decltype(kc)::value, decltype(mb)::value, true>();
+            });
+        });
     }
     MHW_CK(cudaStreamSynchronize(st));
 }
@@ -816,7 +824,8 @@ void session_run(Session& s, cudaStream_t user) {
                     }
                 }
                 with_minb<KIND>(s.minb, [&](auto mb) {
-                    k_walk<KIND, decltype(mb)::value><<<s.grid, kWalkBlock, 0, st>>>(P);
+                    if (s.eager_init) k_walk<KIND, decltype(mb)::value, false><<<s.grid, kWalkBlock, 0, st>>>(P);
+                    else k_walk<KIND, decltype(mb)::value, true><<<s.grid, kWalkBlock, 0, st>>>(P);
                 });
             });
             ++s.launches;
