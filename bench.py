@@ -399,12 +399,13 @@ def run_e2e(args, cfg, g, model, wcfg, dev, dist):
     lib = L.lib()
     rows, stride = C.c_uint64(), C.c_uint32()
     mhw.mhwalk._check(lib.mhw_walk_rows(g.handle, C.byref(md), C.byref(c), C.byref(rows), C.byref(stride)))
-    out = torch.empty(rows.value * stride.value, dtype=torch.int32).pin_memory()
-    lens = torch.empty(max(rows.value, 1), dtype=torch.int32).pin_memory()
+    # packed corpus: walk r = nodes[offsets[r] .. offsets[r+1])
+    cap = rows.value * (cfg["L"] + 1)
+    out = torch.empty(max(cap, 1), dtype=torch.int32).pin_memory()
+    offs = torch.empty(rows.value + 1, dtype=torch.int64).pin_memory()
     h2d = sum(x.numel() * x.element_size() for x in (off, nb, w, nt, et) if x is not None)
-    d2h = out.numel() * 4 + rows.value * 4
     steps_e2e = max(1, min(args.steps, 3))
-    times, steps = [], 0
+    times, steps, d2h = [], 0, 0
     for i in range(1 + steps_e2e):
         if dist:
             dist.barrier()
@@ -413,11 +414,13 @@ def run_e2e(args, cfg, g, model, wcfg, dev, dist):
         mhw.mhwalk._check(lib.mhw_graph_upload(C.byref(view), dev, C.byref(h)))
         st = L.WalkStatsC()
         try:
-            mhw.mhwalk._check(lib.mhw_generate_walks_into(h, C.byref(md), C.byref(c), C.c_void_p(out.data_ptr()),
-                                                          C.c_void_p(lens.data_ptr()), rows.value, C.byref(st)))
+            mhw.mhwalk._check(lib.mhw_generate_walks_packed(h, C.byref(md), C.byref(c), C.c_void_p(out.data_ptr()),
+                                                            cap, C.c_void_p(offs.data_ptr()), rows.value + 1,
+                                                            C.byref(st)))
         finally:
             lib.mhw_graph_free(h)
         dt = time.perf_counter() - t0
+        d2h = (st.walks + st.steps) * 4 + (rows.value + 1) * 8
         if i >= 1:
             times.append(dt)
             steps += st.steps
@@ -432,7 +435,7 @@ def run_e2e(args, cfg, g, model, wcfg, dev, dist):
         t_job, steps_job = t_local, float(steps)
     return {"value": steps_job / t_job, "unit": "steps/s", "h2d_bytes_per_step": int(h2d),
             "d2h_bytes_per_step": int(d2h), "steps": steps_e2e,
-            "path": "mhw_graph_upload + mhw_generate_walks_into (pinned host buffers), wall clock"}
+            "path": "mhw_graph_upload + mhw_generate_walks_packed (pinned host buffers), wall clock"}
 
 
 def cpu_baseline(cfg, g):

@@ -222,6 +222,15 @@ MHW_API mhw_status mhw_generate_walks_into(const mhw_graph* g, const mhw_model_d
                                    uint32_t* h_lengths, uint64_t capacity_rows,
                                    mhw_walk_stats* stats);
 
+/* generate_walks into a packed host corpus: walk r is
+ * h_nodes[h_offsets[r] .. h_offsets[r+1]) (h_offsets has rows + 1 entries).
+ * The padded device rows are compacted on the device first, so the D2H
+ * carries only the sum of walk lengths. */
+MHW_API mhw_status mhw_generate_walks_packed(const mhw_graph* g, const mhw_model_desc* model,
+                                     const mhw_walk_config* config, uint32_t* h_nodes,
+                                     uint64_t capacity_nodes, uint64_t* h_offsets,
+                                     uint64_t capacity_rows, mhw_walk_stats* stats);
+
 MHW_API uint64_t mhw_walks_count(const mhw_walks* w);
 MHW_API uint32_t mhw_walks_stride(const mhw_walks* w);
 MHW_API const uint32_t* mhw_walks_nodes(const mhw_walks* w);   /* count x stride, row r = walk r */

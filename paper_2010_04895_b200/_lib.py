@@ -68,6 +68,8 @@ SIGNATURES = {
                                   C.POINTER(C.c_uint32)]),
     "mhw_generate_walks_into": (C.c_int32, [_P, C.POINTER(ModelDescC), C.POINTER(WalkConfigC), _P, _P,
                                             C.c_uint64, C.POINTER(WalkStatsC)]),
+    "mhw_generate_walks_packed": (C.c_int32, [_P, C.POINTER(ModelDescC), C.POINTER(WalkConfigC), _P, C.c_uint64,
+                                              _P, C.c_uint64, C.POINTER(WalkStatsC)]),
     "mhw_walks_count": (C.c_uint64, [_P]),
     "mhw_walks_stride": (C.c_uint32, [_P]),
     "mhw_walks_nodes": (_P, [_P]),

@@ -398,6 +398,28 @@ mhw_status mhw_generate_walks_into(const mhw_graph* g, const mhw_model_desc* mod
     return guard([&] { run_into(g, model, config, h_nodes, h_lengths, capacity_rows, stats, nullptr); });
 }
 
+mhw_status mhw_generate_walks_packed(const mhw_graph* g, const mhw_model_desc* model,
+                                     const mhw_walk_config* config, uint32_t* h_nodes, uint64_t capacity_nodes,
+                                     uint64_t* h_offsets, uint64_t capacity_rows, mhw_walk_stats* stats) {
+    return guard([&] {
+        need(g, "graph");
+        need(model, "model");
+        need(config, "config");
+        need(h_nodes, "h_nodes");
+        need(h_offsets, "h_offsets");
+        auto* gg = const_cast<mhw_graph*>(g);
+        mhw::DeviceGuard dg(gg->device);
+        mhw_session s;
+        mhw::session_create(s, *gg, *model, *config);
+        if (capacity_rows < s.rows + 1) mhw::invalid("offset buffer too small for the corpus");
+        mhw::session_run(s, nullptr);
+        mhw_walk_stats st{};
+        mhw::session_stats(s, st);
+        mhw::session_download_packed(s, h_nodes, capacity_nodes, h_offsets, capacity_rows, nullptr, nullptr);
+        if (stats) *stats = st;
+    });
+}
+
 mhw_status mhw_session_create(const mhw_graph* g, const mhw_model_desc* model, const mhw_walk_config* config,
                               mhw_session** out) {
     return guard([&] {

@@ -130,26 +130,83 @@ __global__ void k_rev(DevGraph g, uint32_t* __restrict__ rev, unsigned* __restri
     }
 }
 
-// Warp per node: insert N(v) into v's adjacency hash set (degree >= kHashMinDeg).
+// Source node of arc a: the last v with nodes[v].off <= a (isolated nodes
+// share their successor's offset and are skipped by "last").
+__device__ __forceinline__ uint32_t arc_source(const DevGraph& g, uint64_t a) {
+    uint32_t lo = 0, hi = g.n;
+    while (hi - lo > 1) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if ((uint64_t)__ldg(&g.nodes[mid].off) <= a) lo = mid;
+        else hi = mid;
+    }
+    return lo;
+}
+
+// Thread per arc: insert u into the hash set of its source (degree >=
+// kHashMinDeg). Arc-parallel so hubs do not serialise on one warp; the
+// bucket is read once and only the first free slot is CAS-ed.
 __global__ void k_hash_build(DevGraph g, uint32_t* __restrict__ tab) {
+    for (uint64_t a = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; a < g.m;
+         a += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t v = arc_source(g, a);
+        const NodeRec r = load_node(g, v);
+        if (r.deg < kHashMinDeg) continue;
+        const uint32_t nb = hash_buckets(r.deg);
+        uint32_t* base = tab + 8 * hash_base(r.off, v);
+        const uint32_t key = load_id(g, a);
+        uint32_t b = hash_bucket(key, nb);
+        for (;;) {
+            uint32_t* bk = base + 8 * b;
+            int s = 0;
+            while (s < 8) {
+                const uint32_t cur = __ldcg(bk + s);
+                if (cur != kHashEmpty) {
+                    ++s;
+                    continue;
+                }
+                if (atomicCAS(bk + s, kHashEmpty, key) == kHashEmpty) break;
+                // lost the race for slot s: it is now taken, look further
+                ++s;
+            }
+            if (s < 8) break;
+            b = b + 1 == nb ? 0 : b + 1;
+        }
+    }
+}
+
+// rev[] by sorting: keys (dst << bits | src) of every arc. For a symmetric
+// CSR the k-th arc in (dst, src) order is the reverse of CSR arc k.
+__global__ void k_rev_keys(DevGraph g, int bits, uint64_t* __restrict__ keys, uint32_t* __restrict__ vals) {
     const unsigned lane = threadIdx.x & 31;
     const uint64_t wid = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
     for (uint64_t v = wid; v < g.n; v += nw) {
         const NodeRec r = load_node(g, (uint32_t)v);
-        if (r.deg < kHashMinDeg) continue;
-        const uint32_t nb = hash_buckets(r.deg);
-        uint32_t* base = tab + 8 * hash_base(r.off, (uint32_t)v);
         for (uint32_t i = lane; i < r.deg; i += 32) {
-            const uint32_t key = load_id(g, r.off + i);
-            uint32_t b = hash_bucket(key, nb);
-            for (;;) {
-                bool done = false;
-                for (int s = 0; s < 8 && !done; ++s) done = atomicCAS(base + 8 * b + s, kHashEmpty, key) == kHashEmpty;
-                if (done) break;
-                b = b + 1 == nb ? 0 : b + 1;
-            }
+            keys[r.off + i] = ((uint64_t)load_id(g, r.off + i) << bits) | v;
+            vals[r.off + i] = i;  // index of the arc within its source slice
         }
+    }
+}
+
+// Sorted position k holds arc (v -> u) with key (u, v): if CSR arc k is
+// (u -> v) then v sits at index k - off(u) of N(u).
+__global__ void k_rev_scatter(DevGraph g, int bits, const uint64_t* __restrict__ keys,
+                              const uint32_t* __restrict__ vals, uint32_t* __restrict__ rev,
+                              unsigned* __restrict__ mismatch) {
+    const uint64_t mask = (bits >= 64) ? ~0ull : ((1ull << bits) - 1);
+    for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < g.m;
+         k += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t key = keys[k];
+        const uint32_t u = (uint32_t)(key >> bits), v = (uint32_t)(key & mask);
+        const NodeRec ru = load_node(g, u);
+        const NodeRec rv = load_node(g, v);
+        const bool ok = (uint64_t)ru.off <= k && k < (uint64_t)ru.off + ru.deg && load_id(g, k) == v;
+        if (!ok) {
+            atomicAdd(mismatch, 1u);
+            continue;
+        }
+        rev[rv.off + vals[k]] = (uint32_t)(k - (uint64_t)ru.off);
     }
 }
 
@@ -795,15 +852,37 @@ void graph_download(const Graph& g, int64_t* offsets, int32_t* nbr, float* w, ui
 void graph_ensure_rev(Graph& g) {
     if (g.rev.n || !g.m) return;
     DeviceGuard dg(g.device);
+    cudaStream_t st = g.stream;
     g.rev.alloc(g.m);
-    DBuf<unsigned> missing(1);
-    MHW_CK(cudaMemsetAsync(missing.p, 0, sizeof(unsigned), g.stream));
     DevGraph v = g.view();
-    k_rev<<<grid_for((uint64_t)g.n * 32), kBlock, 0, g.stream>>>(v, g.rev.p, missing.p);
-    MHW_CK(cudaGetLastError());
-    unsigned h = 0;
-    MHW_CK(cudaMemcpyAsync(&h, missing.p, sizeof(h), cudaMemcpyDeviceToHost, g.stream));
-    MHW_CK(cudaStreamSynchronize(g.stream));
+    int bits = 1;
+    while (bits < 32 && ((uint64_t)g.n >> bits) != 0) ++bits;
+    unsigned h = 1;
+    {
+        // one radix sort of (dst, src) keys; valid when the CSR is symmetric
+        DBuf<uint64_t> k1(g.m), k2(g.m);
+        DBuf<uint32_t> v1(g.m), v2(g.m);
+        DBuf<unsigned> mismatch(1);
+        MHW_CK(cudaMemsetAsync(mismatch.p, 0, sizeof(unsigned), st));
+        k_rev_keys<<<grid_for((uint64_t)g.n * 32), kBlock, 0, st>>>(v, bits, k1.p, v1.p);
+        size_t bytes = 0;
+        MHW_CK(cub::DeviceRadixSort::SortPairs(nullptr, bytes, k1.p, k2.p, v1.p, v2.p, (int64_t)g.m, 0, 2 * bits, st));
+        DBuf<uint8_t> temp(std::max<size_t>(bytes, 1));
+        MHW_CK(cub::DeviceRadixSort::SortPairs(temp.p, bytes, k1.p, k2.p, v1.p, v2.p, (int64_t)g.m, 0, 2 * bits, st));
+        k_rev_scatter<<<grid_for(g.m), kBlock, 0, st>>>(v, bits, k2.p, v2.p, g.rev.p, mismatch.p);
+        MHW_CK(cudaGetLastError());
+        MHW_CK(cudaMemcpyAsync(&h, mismatch.p, sizeof(h), cudaMemcpyDeviceToHost, st));
+        MHW_CK(cudaStreamSynchronize(st));
+    }
+    if (h != 0) {
+        // not symmetric: per-arc search, missing back arcs become kNoBack
+        DBuf<unsigned> missing(1);
+        MHW_CK(cudaMemsetAsync(missing.p, 0, sizeof(unsigned), st));
+        k_rev<<<grid_for((uint64_t)g.n * 32), kBlock, 0, st>>>(v, g.rev.p, missing.p);
+        MHW_CK(cudaGetLastError());
+        MHW_CK(cudaMemcpyAsync(&h, missing.p, sizeof(h), cudaMemcpyDeviceToHost, st));
+        MHW_CK(cudaStreamSynchronize(st));
+    }
     g.verified_sym = h == 0;
 }
 
@@ -813,7 +892,7 @@ void graph_ensure_hash(Graph& g) {
     const uint64_t buckets = (g.m >> 2) + g.n + 1;
     g.htab.alloc(8 * buckets);
     MHW_CK(cudaMemsetAsync(g.htab.p, 0xFF, g.htab.bytes(), g.stream));
-    k_hash_build<<<grid_for((uint64_t)g.n * 32), kBlock, 0, g.stream>>>(g.view(), g.htab.p);
+    k_hash_build<<<grid_for(g.m), kBlock, 0, g.stream>>>(g.view(), g.htab.p);
     MHW_CK(cudaGetLastError());
     MHW_CK(cudaStreamSynchronize(g.stream));
 }

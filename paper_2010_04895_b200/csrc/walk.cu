@@ -246,6 +246,27 @@ __global__ void __launch_bounds__(256) k_init_all(RunParams P) {
     if (inits) atomicAdd(&P.ctr[3], inits);
 }
 
+// Packed corpus: widen lengths for the 64-bit offset scan, then one warp per
+// row copies the row (coalesced on both sides).
+__global__ void k_len64(const uint32_t* __restrict__ lens, uint64_t rows, uint64_t* __restrict__ out) {
+    for (uint64_t r = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; r <= rows;
+         r += (uint64_t)gridDim.x * blockDim.x)
+        out[r] = r < rows ? lens[r] : 0;
+}
+
+__global__ void k_pack(const uint32_t* __restrict__ src, uint32_t stride, const uint64_t* __restrict__ off,
+                       uint64_t rows, uint32_t* __restrict__ dst) {
+    const unsigned lane = threadIdx.x & 31;
+    const uint64_t wid = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    for (uint64_t r = wid; r < rows; r += nw) {
+        const uint64_t o = off[r];
+        const uint32_t len = (uint32_t)(off[r + 1] - o);
+        const uint32_t* s = src + r * stride;
+        for (uint32_t i = lane; i < len; i += 32) dst[o + i] = s[i];
+    }
+}
+
 // Replica groups per node (chain_replicas - 1).
 __global__ void k_rep_counts(DevGraph g, uint32_t D, uint32_t* __restrict__ cnt) {
     for (uint64_t v = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; v < g.n;
@@ -866,6 +887,33 @@ void session_download(Session& s, uint32_t* nodes, uint32_t* lens, cudaStream_t 
         if (lens) MHW_CK(cudaMemcpyAsync(lens, s.lens.p, s.rows * 4, cudaMemcpyDeviceToHost, st));
     }
     MHW_CK(cudaStreamSynchronize(st));
+}
+
+// Packs the last run's corpus (rows of length lens[r]) into nodes[off[r] ..
+// off[r+1]) and copies nodes + offsets to the host.
+void session_download_packed(Session& s, uint32_t* h_nodes, uint64_t cap_nodes, uint64_t* h_offsets,
+                             uint64_t cap_rows, uint64_t* n_nodes, cudaStream_t user) {
+    DeviceGuard dg(s.g->device);
+    cudaStream_t st = user ? user : s.stream;
+    const uint64_t rows = s.rows;
+    if (cap_rows < rows + 1) invalid("offset buffer too small for the corpus");
+    DBuf<uint64_t> len64(rows + 1), off(rows + 1);
+    k_len64<<<grid_for(rows + 1), 256, 0, st>>>(s.lens.p, rows, len64.p);
+    size_t bytes = 0;
+    MHW_CK(cub::DeviceScan::ExclusiveSum(nullptr, bytes, len64.p, off.p, (int64_t)rows + 1, st));
+    DBuf<uint8_t> temp(std::max<size_t>(bytes, 1));
+    MHW_CK(cub::DeviceScan::ExclusiveSum(temp.p, bytes, len64.p, off.p, (int64_t)rows + 1, st));
+    uint64_t total = 0;
+    MHW_CK(cudaMemcpyAsync(&total, off.p + rows, 8, cudaMemcpyDeviceToHost, st));
+    MHW_CK(cudaStreamSynchronize(st));
+    if (cap_nodes < total) invalid("node buffer too small for the corpus");
+    DBuf<uint32_t> packed(std::max<uint64_t>(total, 1));
+    if (rows) k_pack<<<grid_for(rows * 32), 256, 0, st>>>(s.out.p, s.stride, off.p, rows, packed.p);
+    MHW_CK(cudaGetLastError());
+    if (total) MHW_CK(cudaMemcpyAsync(h_nodes, packed.p, total * 4, cudaMemcpyDeviceToHost, st));
+    MHW_CK(cudaMemcpyAsync(h_offsets, off.p, (rows + 1) * 8, cudaMemcpyDeviceToHost, st));
+    MHW_CK(cudaStreamSynchronize(st));
+    if (n_nodes) *n_nodes = total;
 }
 
 // ------------------------------------------------------------ parity API

@@ -370,6 +370,23 @@ def generate_walks(graph: Graph, model: WalkModel, config: WalkConfig) -> WalkCo
     return WalkCorpus(nodes, lens, RunStats._from(st))
 
 
+def generate_walks_packed(graph: Graph, model: WalkModel, config: WalkConfig):
+    """generate_walks into a packed corpus: (nodes, offsets, RunStats) with
+    walk r = nodes[offsets[r]:offsets[r+1]] (compacted on the device)."""
+    d, keep = model._desc()
+    c = config._c()
+    lib = L.lib()
+    rows, stride = C.c_uint64(), C.c_uint32()
+    _check(lib.mhw_walk_rows(graph.handle, C.byref(d), C.byref(c), C.byref(rows), C.byref(stride)))
+    cap = max(rows.value * (config.walk_length + 1), 1)
+    nodes = np.zeros(cap, dtype=np.uint32)
+    offsets = np.zeros(rows.value + 1, dtype=np.uint64)
+    st = L.WalkStatsC()
+    _check(lib.mhw_generate_walks_packed(graph.handle, C.byref(d), C.byref(c), _ptr(nodes), cap, _ptr(offsets),
+                                         rows.value + 1, C.byref(st)))
+    return nodes[:int(offsets[-1])], offsets, RunStats._from(st)
+
+
 def generate_walks_multi(replicas: list, model: WalkModel, config: WalkConfig) -> WalkCorpus:
     d, keep = model._desc()
     c = config._c()

@@ -158,6 +158,24 @@ def test_throughput_walks_valid(mhw, kind):
     assert corpus.stats.steps == int(np.sum(corpus.lengths - 1))
 
 
+def test_packed_corpus_equals_padded(mhw, oracle):
+    """mhw_generate_walks_packed (device compaction + D2H) == the padded corpus."""
+    from paper_2010_04895_b200.mhwalk import generate_walks_packed
+    g = typed_random_graph(61, 150, 5.0, weighted=True, types=2)
+    rng = O.XoRng(1)
+    md = model_desc(O.NODE2VEC, g, p=0.25, q=4.0)
+    cfg = O.WalkCfg(K=3, L=30, seed=5, init_kind=O.INIT_BURN_IN, burn_in_steps=10)
+    dg = device_graph(g)
+    padded = mhw.generate_walks(dg, walk_model(md), walk_config(cfg, threads=1))
+    nodes, offsets, st = generate_walks_packed(dg, walk_model(md), walk_config(cfg, threads=1))
+    assert len(offsets) == len(padded) + 1
+    assert np.array_equal(np.diff(offsets), padded.lengths)
+    for r in range(len(padded)):
+        assert np.array_equal(nodes[offsets[r]:offsets[r + 1]], padded.rows[r, :padded.lengths[r]])
+    assert st.steps == padded.stats.steps
+    assert rng is not None
+
+
 def test_alias_tables_bit_exact(mhw, oracle):
     """Per-node alias tables == alias_build (samplers.cpp:95-131) bit for bit."""
     g = typed_random_graph(41, 500, 10.0, weighted=True)
