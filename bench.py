@@ -434,7 +434,7 @@ def run_e2e(args, cfg, g, model, wcfg, dev, dist):
     else:
         t_job, steps_job = t_local, float(steps)
     return {"value": steps_job / t_job, "unit": "steps/s", "h2d_bytes_per_step": int(h2d),
-            "d2h_bytes_per_step": int(d2h), "steps": steps_e2e,
+            "d2h_bytes_per_step": int(d2h), "steps": steps_e2e, "ms_per_step": [round(1e3 * x, 2) for x in times],
             "path": "mhw_graph_upload + mhw_generate_walks_packed (pinned host buffers), wall clock"}
 
 

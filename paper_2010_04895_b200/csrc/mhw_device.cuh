@@ -315,6 +315,9 @@ __device__ __forceinline__ uint32_t alpha_class(const DevGraph& g, const DevMode
                                                 uint32_t u, const NodeRec* urec) {
     if (m.alpha_trivial) return 1;
     if (u == c.s) return 0;
+    // s's own hash set needs nothing about u: probe it without waiting for
+    // the candidate's node record (shorter dependency chain per step).
+    if (g.htab && c.deg_s >= kHashMinDeg) return hash_contains(g.htab, c.off_s, c.s, c.deg_s, u) ? 1u : 2u;
     // is_adjacent(s, u): u in N(s), or s in N(u) when every arc has its
     // back arc. Cheapest structure first: a <= 8-entry slice (one sector),
     // else a hash set (one sector), else binary search of the shorter slice.
@@ -367,7 +370,7 @@ __device__ __forceinline__ double wprime(const DevGraph& g, const DevModel& m, c
 }
 
 template <int KIND>
-__device__ __forceinline__ bool needs_utype() {
+__host__ __device__ constexpr bool needs_utype() {
     return KIND == METAPATH2VEC || KIND == FAIRWALK || KIND == EDGE2VEC;
 }
 

@@ -103,7 +103,7 @@ __global__ void __launch_bounds__(kWalkBlock) __maxnreg__(REGS) k_walk(RunParams
             }
             Draw d;
             d.open(wkey, walker, step);
-            uint32_t chosen, next;
+            uint32_t chosen, next, back_c = 0, back_l = 0;
             NodeRec rn;
             if (second_order(KIND) && c.boot) {
                 if (!bootstrap_pick(g, c, d.unit(), &chosen)) {
@@ -112,6 +112,7 @@ __global__ void __launch_bounds__(kWalkBlock) __maxnreg__(REGS) k_walk(RunParams
                 }
                 next = load_id(g, c.off + chosen);
                 rn = load_node(g, next);
+                back_c = __ldg(g.rev + c.off + chosen);
             } else {
                 // Take the slot: the chain word itself is the lock. The
                 // transition (proposal evaluation + decision) happens while
@@ -154,19 +155,33 @@ __global__ void __launch_bounds__(kWalkBlock) __maxnreg__(REGS) k_walk(RunParams
                     break;
                 }
                 const uint32_t last = e & kIdxMask, cls_l = e >> 30;
-                uint16_t ltype = 0;
-                if (needs_utype<KIND>()) ltype = load_node(g, load_id(g, c.off + last)).type;
-                const double wl = wprime<KIND>(g, P.m, c, last, ltype, cls_l);
+                // The last sample's id and record are fetched before the
+                // decision where w'(last) needs its type anyway, and for
+                // deepwalk (cheap, L2-resident graphs; measured win). For
+                // node2vec/edge2vec the extra sectors cost more than the
+                // shorter rejection path saves (profiles/, round 1).
+                constexpr bool kSpec = needs_utype<KIND>() || KIND == DEEPWALK;
+                uint32_t ul = 0;
+                NodeRec rl{};
+                if (kSpec) {
+                    ul = load_id(g, c.off + last);
+                    rl = load_node(g, ul);
+                }
+                const double wl = wprime<KIND>(g, P.m, c, last, rl.type, cls_l);
                 const bool acc = mh_accept(wc, wl, u) && cand != last;
                 chain_release(P.chain + slot, acc ? pack_entry(cand, cls_c) : e);
                 chosen = acc ? cand : last;
-                if (chosen == cand) {
+                if (acc || cand == last) {
                     next = uc;
                     rn = rc;
+                } else if (kSpec) {
+                    next = ul;
+                    rn = rl;
                 } else {
-                    next = load_id(g, c.off + chosen);
+                    next = load_id(g, c.off + last);
                     rn = load_node(g, next);
                 }
+                if (second_order(KIND)) back_c = __ldg(g.rev + c.off + chosen);
             }
             // emit: 4 ids buffered in registers, one 16-byte store
             switch (len & 3) {
@@ -188,7 +203,7 @@ __global__ void __launch_bounds__(kWalkBlock) __maxnreg__(REGS) k_walk(RunParams
                 c.req = P.m.metapath[metapath_next(P.m, affix)];
                 slot = node_slot(P.cfg, P.m.num_types, next, rn.deg, c.req, walker);
             } else {
-                const uint32_t back = __ldg(g.rev + c.off + chosen);
+                const uint32_t back = back_c;  // rev[off(v) + chosen], fetched above
                 if (back == kNoBack) {
                     fail_back_edge(P.ctr, next, c.v);
                     dead = true;
