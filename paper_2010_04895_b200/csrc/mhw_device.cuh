@@ -345,6 +345,12 @@ __device__ __forceinline__ uint32_t alpha_class(const DevGraph& g, const DevMode
     return adj_search(g.ids, off_a, deg_a, key_a) ? 1u : 2u;
 }
 
+// Does alpha_class look at the candidate's record? Only when s has no hash
+// set and its slice is longer than one sector (then N(u) may be shorter).
+__device__ __forceinline__ bool needs_urec_for_alpha(const DevGraph& g, const SCtx& c) {
+    return g.verified_sym && c.deg_s > 8 && (c.deg_s < kHashMinDeg || !g.htab);
+}
+
 __device__ __forceinline__ double alpha_value(const DevModel& m, uint32_t cls) {
     return cls == 0 ? m.inv_p : (cls == 1 ? 1.0 : m.inv_q);
 }
@@ -383,7 +389,7 @@ __device__ __forceinline__ double eval_index(const DevGraph& g, const DevModel& 
     if (KIND != DEEPWALK) {
         const uint32_t u = load_id(g, c.off + i);
         if (second_order(KIND) && !c.boot && !m.alpha_trivial) {
-            if (needs_utype<KIND>() || (g.verified_sym && c.deg_s > 8 && u != c.s)) {
+            if (needs_utype<KIND>() || (needs_urec_for_alpha(g, c) && u != c.s)) {
                 const NodeRec r = load_node(g, u);
                 utype = r.type;
                 cls = alpha_class(g, m, c, u, &r);

@@ -128,8 +128,15 @@ __global__ void __launch_bounds__(kWalkBlock) __maxnreg__(REGS) k_walk(RunParams
                 const uint32_t cand = d.index(c.deg);
                 const double u = d.unit();
                 const uint32_t uc = load_id(g, c.off + cand);
-                const NodeRec rc = load_node(g, uc);
-                const uint32_t cls_c = second_order(KIND) ? alpha_class(g, P.m, c, uc, &rc) : 0u;
+                // the candidate's record is needed before the decision only
+                // for its type or for the alpha slice choice; otherwise it is
+                // fetched after an acceptance (it is the next node then)
+                const bool rc_early = needs_utype<KIND>() ||
+                                      (second_order(KIND) && !P.m.alpha_trivial && needs_urec_for_alpha(g, c));
+                NodeRec rc{};
+                if (rc_early) rc = load_node(g, uc);
+                const uint32_t cls_c =
+                    second_order(KIND) ? alpha_class(g, P.m, c, uc, rc_early ? &rc : nullptr) : 0u;
                 const double wc = wprime<KIND>(g, P.m, c, cand, rc.type, cls_c);
                 if (e == kLocked) {
                     unsigned ns = 32;
@@ -173,7 +180,7 @@ __global__ void __launch_bounds__(kWalkBlock) __maxnreg__(REGS) k_walk(RunParams
                 chosen = acc ? cand : last;
                 if (acc || cand == last) {
                     next = uc;
-                    rn = rc;
+                    rn = rc_early ? rc : load_node(g, uc);
                 } else if (kSpec) {
                     next = ul;
                     rn = rl;
