@@ -242,6 +242,13 @@ MHW_API void mhw_walks_free(mhw_walks* w);
  * line, space separated, plus <path>.stats.jsonl. */
 MHW_API mhw_status mhw_walks_write(const mhw_walks* w, const char* path);
 
+/* generate_walks + write_corpus with the text formatted on the device
+ * (integer-to-text kernels, chunked pinned D2H overlapping fwrite); same
+ * bytes as write_corpus (engine.cpp:236-259) plus <path>.stats.jsonl. */
+MHW_API mhw_status mhw_generate_walks_to_file(const mhw_graph* g, const mhw_model_desc* model,
+                                              const mhw_walk_config* config, const char* path,
+                                              mhw_walk_stats* stats);
+
 /* Balanced walker partition: cut points of [0, n) into `parts` contiguous
  * start-node ranges with equal active-walker counts.
  * cuts has parts + 1 entries. */
@@ -264,6 +271,8 @@ MHW_API mhw_status mhw_session_buffers(mhw_session* s, uint32_t** d_nodes, uint3
 /* D2H of the corpus into caller buffers (pinned for full speed). */
 MHW_API mhw_status mhw_session_download(mhw_session* s, uint32_t* h_nodes, uint32_t* h_lengths,
                                 void* stream);
+/* Writes the last run's corpus like mhw_generate_walks_to_file. */
+MHW_API mhw_status mhw_session_write_corpus(mhw_session* s, const char* path);
 /* Number of kernels the last mhw_session_run enqueued. */
 MHW_API uint32_t mhw_session_launches(const mhw_session* s);
 MHW_API void mhw_session_free(mhw_session* s);

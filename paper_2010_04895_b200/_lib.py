@@ -70,6 +70,9 @@ SIGNATURES = {
                                             C.c_uint64, C.POINTER(WalkStatsC)]),
     "mhw_generate_walks_packed": (C.c_int32, [_P, C.POINTER(ModelDescC), C.POINTER(WalkConfigC), _P, C.c_uint64,
                                               _P, C.c_uint64, C.POINTER(WalkStatsC)]),
+    "mhw_generate_walks_to_file": (C.c_int32, [_P, C.POINTER(ModelDescC), C.POINTER(WalkConfigC), C.c_char_p,
+                                               C.POINTER(WalkStatsC)]),
+    "mhw_session_write_corpus": (C.c_int32, [_P, C.c_char_p]),
     "mhw_walks_count": (C.c_uint64, [_P]),
     "mhw_walks_stride": (C.c_uint32, [_P]),
     "mhw_walks_nodes": (_P, [_P]),

@@ -13,7 +13,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libmhw.so")
 OBJ = os.path.join(PKG, "_obj")
-SOURCES = ["graph.cu", "walk.cu", "api.cu"]
+SOURCES = ["graph.cu", "walk.cu", "corpus.cu", "api.cu"]
 HEADERS = ["mhw_device.cuh", "internal.h", "walk.h"]
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")

@@ -420,6 +420,35 @@ mhw_status mhw_generate_walks_packed(const mhw_graph* g, const mhw_model_desc* m
     });
 }
 
+mhw_status mhw_generate_walks_to_file(const mhw_graph* g, const mhw_model_desc* model,
+                                      const mhw_walk_config* config, const char* path, mhw_walk_stats* stats) {
+    return guard([&] {
+        need(g, "graph");
+        need(model, "model");
+        need(config, "config");
+        need(path, "path");
+        auto* gg = const_cast<mhw_graph*>(g);
+        mhw::DeviceGuard dg(gg->device);
+        mhw_session s;
+        mhw::session_create(s, *gg, *model, *config);
+        mhw::session_run(s, nullptr);
+        mhw_walk_stats st{};
+        mhw::session_stats(s, st);
+        mhw::session_write_corpus(s, path, st);
+        if (stats) *stats = st;
+    });
+}
+
+mhw_status mhw_session_write_corpus(mhw_session* s, const char* path) {
+    return guard([&] {
+        need(s, "session");
+        need(path, "path");
+        mhw_walk_stats st{};
+        mhw::session_stats(*s, st);
+        mhw::session_write_corpus(*s, path, st);
+    });
+}
+
 mhw_status mhw_session_create(const mhw_graph* g, const mhw_model_desc* model, const mhw_walk_config* config,
                               mhw_session** out) {
     return guard([&] {

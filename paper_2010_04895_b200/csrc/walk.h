@@ -73,6 +73,7 @@ void session_create(Session& s, Graph& g, const mhw_model_desc& md, const mhw_wa
 void session_run(Session& s, cudaStream_t stream);
 void session_stats(Session& s, mhw_walk_stats& out);
 void session_download(Session& s, uint32_t* nodes, uint32_t* lens, cudaStream_t stream);
+void session_write_corpus(Session& s, const char* path, const mhw_walk_stats& st);
 void session_download_packed(Session& s, uint32_t* h_nodes, uint64_t cap_nodes, uint64_t* h_offsets,
                              uint64_t cap_rows, uint64_t* n_nodes, cudaStream_t stream);
 void run_decide(Graph& g, const mhw_model_desc& md, uint64_t n, const uint32_t* pos, const uint32_t* aff,

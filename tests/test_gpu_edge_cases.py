@@ -1,0 +1,137 @@
+"""Edge cases of the walk path on the GPU: empty and tiny graphs, walk
+length 1, start-node ranges, dead ends, asymmetric adjacency behind a
+symmetric flag (update_state's error, models.cpp:131-133), and the
+one-chain-per-state layout switch."""
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+from tests.helpers import corpus_equal, device_graph, model_desc, typed_random_graph, walk_config, walk_model
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def mhw():
+    import paper_2010_04895_b200 as m
+    assert m.device_count() > 0
+    return m
+
+
+def test_empty_graph(mhw):
+    g = mhw.Graph.from_csr(np.array([0]), np.array([], dtype=np.int32))
+    assert g.node_count() == 0 and g.arc_count() == 0
+    for threads in (1, 8):
+        c = mhw.generate_walks(g, mhw.WalkModel(), mhw.WalkConfig(threads=threads))
+        assert len(c) == 0 and c.stats.steps == 0
+
+
+def test_walk_length_one_and_single_walk(mhw, oracle):
+    g = typed_random_graph(5, 50, 4.0)
+    for kind in range(5):
+        md = model_desc(kind, g)
+        cfg = O.WalkCfg(K=1, L=1, seed=3)
+        orow, olen, _ = oracle.generate_walks(g, md, cfg, rng=O.RNG_PHILOX, order=O.ORDER_STEP)
+        c = mhw.generate_walks(device_graph(g), walk_model(md), walk_config(cfg))
+        assert corpus_equal(orow, olen, c.rows, c.lengths)
+        assert c.rows.shape[1] == 4  # L+1 = 2 padded to 4 (16-byte rows)
+
+
+def test_node_range_rows_are_the_corpus_slice(mhw, oracle):
+    """A start-node range yields exactly those walkers' rows, in corpus order
+    (the per-GPU shard of a multi-GPU run)."""
+    g = typed_random_graph(9, 120, 5.0)
+    md = model_desc(O.DEEPWALK, g)
+    dg, m = device_graph(g), walk_model(md)
+    full = mhw.generate_walks(dg, m, mhw.WalkConfig(walks_per_node=3, walk_length=5, threads=8, seed=2))
+    part = mhw.generate_walks(dg, m, mhw.WalkConfig(walks_per_node=3, walk_length=5, threads=8, seed=2,
+                                                    node_begin=40, node_end=90))
+    assert len(part) == 50 * 3
+    assert np.array_equal(part.rows[:, 0], full.rows[40 * 3:90 * 3, 0])
+    with pytest.raises(mhw.ValidationError, match="node range"):
+        mhw.generate_walks(dg, m, mhw.WalkConfig(node_begin=5, node_end=500))
+
+
+def test_asymmetric_adjacency_raises_like_update_state(mhw):
+    """Flagged symmetric but missing back arcs: the walk fails with the
+    reference's ValidationError message (models.cpp:131-133)."""
+    # 0 -> 1, 1 -> 2, 2 -> 0 only (a directed triangle), flagged symmetric
+    g = O.make_graph(3, [(0, 1, 1.0), (1, 2, 1.0), (2, 0, 1.0)], symmetric=True)
+    dg = device_graph(g)
+    assert not dg.info()["verified_symmetric"]
+    for threads in (1, 8):
+        with pytest.raises(mhw.ValidationError, match="asymmetric adjacency: no back edge"):
+            mhw.generate_walks(dg, walk_model(model_desc(O.NODE2VEC, g)),
+                               mhw.WalkConfig(walks_per_node=1, walk_length=5, threads=threads))
+
+
+def test_dead_end_state_terminates_early(mhw, oracle):
+    """metapath2vec on a node whose neighbours lack the required type: dead
+    end (nullopt from mh_init) -> early termination, walk kept."""
+    g = O.make_graph(3, [(0, 1, 1.0), (1, 0, 1.0), (1, 2, 1.0), (2, 1, 1.0)])
+    g.ntype, g.n_ntypes = np.array([0, 1, 1], dtype=np.uint16), 2
+    md = model_desc(O.METAPATH2VEC, g, metapath=(0, 1, 2 - 1, 0))
+    for threads in (1, 8):
+        c = mhw.generate_walks(device_graph(g), walk_model(md),
+                               mhw.WalkConfig(walks_per_node=2, walk_length=10, threads=threads, seed=1))
+        cfg = O.WalkCfg(K=2, L=10, seed=1)
+        orow, olen, ost = oracle.generate_walks(g, md, cfg, rng=O.RNG_PHILOX, order=O.ORDER_STEP)
+        assert list(c.lengths) == list(olen)
+        assert c.stats.early_terminations == ost["early_terminations"]
+
+
+def test_one_chain_per_state_layout(mhw, oracle):
+    """chain_replica_degree = 0xFFFFFFFF is SamplerManager's layout exactly."""
+    rng = O.XoRng(21)
+    g = O.preferential_attachment(200, 3, rng)
+    md = model_desc(O.DEEPWALK, g)
+    cfg = O.WalkCfg(K=4, L=20, seed=3)  # replica_degree default: none
+    orow, olen, ost = oracle.generate_walks(g, md, cfg, rng=O.RNG_PHILOX, order=O.ORDER_STEP)
+    c = mhw.generate_walks(device_graph(g), walk_model(md), walk_config(cfg))
+    assert corpus_equal(orow, olen, c.rows, c.lengths)
+    assert c.stats.slot_inits <= g.n
+
+
+@pytest.mark.parametrize("L", [1, 7, 80])
+def test_device_corpus_text_equals_write_corpus(mhw, tmp_path, L):
+    """Text formatted on the GPU (mhw_generate_walks_to_file) == write_corpus
+    of the same corpus (deterministic schedule, so both runs agree)."""
+    import ctypes as C
+    from paper_2010_04895_b200 import _lib as L_
+    rng = O.XoRng(8)
+    g = O.random_graph(2000, 4.0, True, rng, ensure_connected=False)   # isolated nodes too
+    md = model_desc(O.DEEPWALK, g)
+    cfgw = walk_config(O.WalkCfg(K=3, L=L, seed=4))
+    dg, m = device_graph(g), walk_model(md)
+    corpus = mhw.generate_walks(dg, m, cfgw)
+    want = str(tmp_path / "want.txt")
+    mhw.write_corpus(corpus, want)
+    got = str(tmp_path / "got.txt")
+    d, keep = m._desc()
+    st = L_.WalkStatsC()
+    assert L_.lib().mhw_generate_walks_to_file(dg.handle, C.byref(d), C.byref(cfgw._c()), got.encode(), C.byref(st)) == 0
+    assert open(got, "rb").read() == open(want, "rb").read()
+    assert st.steps == corpus.stats.steps
+
+
+def test_walks_write_matches_write_corpus_format(mhw, tmp_path):
+    """mhw_walks_write (C, host) == write_corpus's format (engine.cpp:236-247)."""
+    import ctypes as C
+    from paper_2010_04895_b200 import _lib as L
+    g = typed_random_graph(4, 40, 3.0)
+    md = model_desc(O.NODE2VEC, g)
+    d, keep = walk_model(md)._desc()
+    c = walk_config(O.WalkCfg(K=2, L=7, seed=5))._c()
+    h = C.c_void_p()
+    lib = L.lib()
+    assert lib.mhw_generate_walks(device_graph(g).handle, C.byref(d), C.byref(c), C.byref(h)) == 0
+    p = str(tmp_path / "c.txt")
+    assert lib.mhw_walks_write(h, p.encode()) == 0
+    rows = lib.mhw_walks_count(h)
+    stride = lib.mhw_walks_stride(h)
+    nodes = np.ctypeslib.as_array(C.cast(lib.mhw_walks_nodes(h), C.POINTER(C.c_uint32)), shape=(rows * stride,))
+    lens = np.ctypeslib.as_array(C.cast(lib.mhw_walks_lengths(h), C.POINTER(C.c_uint32)), shape=(rows,))
+    want = "".join(" ".join(str(int(x)) for x in nodes[r * stride:r * stride + lens[r]]) + "\n" for r in range(rows))
+    lib.mhw_walks_free(h)
+    assert open(p).read() == want
+    assert open(p + ".stats.jsonl").read().startswith("{")
