@@ -287,6 +287,16 @@ MHW_API mhw_status mhw_decide(const mhw_graph* g, const mhw_model_desc* model, u
                       const uint32_t* candidate, const uint32_t* last, const double* u,
                       double* w_cand, double* w_last, uint8_t* accept);
 
+/* The `check` audit (tools/mhwalk.cpp:183-264) on the GPU: for each state,
+ * random init then `draws` M-H transitions counting the chain's states, and
+ * KL(empirical || exact normalised w') (analysis.cpp:34-45) into kl[j] (NaN
+ * when the target has no mass or init dead-ends). counts (optional) receives
+ * the per-candidate visit counts, deg(position[j]) entries per state in order.
+ * A caller reproduces cmd_check's exit code as max(kl) < tolerance ? 0 : 3. */
+MHW_API mhw_status mhw_check(const mhw_graph* g, const mhw_model_desc* model, uint64_t seed,
+                             uint64_t count, const uint32_t* position, const uint32_t* affixture,
+                             uint64_t draws, double* kl, uint64_t* counts);
+
 /* Per-node static-weight alias tables, alias_build (samplers.cpp:95-131),
  * into host arrays of arc_count entries (node v's table at offsets[v]). */
 MHW_API mhw_status mhw_alias_tables(const mhw_graph* g, double* prob, uint32_t* alias);

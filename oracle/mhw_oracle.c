@@ -13,6 +13,7 @@
 #include <stdio.h>
 #include <stdlib.h>
 #include <string.h>
+#include <math.h>
 #include <time.h>
 
 /* ================================================================== RNG */
@@ -710,6 +711,61 @@ int og_init_philox(const og_graph* g, const og_model* m, const og_config* c, uin
     og_philox_key(c->seed, DOM_INIT, src.key);
     src.slot = slot;
     return mh_init(&s, c, &src, last);
+}
+
+/* ================================================================= check */
+
+#define DOM_CHECK 0xC4EC0005u
+
+/* cmd_check's per-state audit (tools/mhwalk.cpp:222-247): exact target =
+ * normalised w', random init, `draws` M-H transitions counting the chain's
+ * states, KL(empirical || target) (analysis.cpp:34-45). Engine layout: init
+ * keyed by slot = state index j, transition d from Philox block (j, d) of the
+ * check domain. kl[j] = NaN when the target has no mass or init dead-ends. */
+void og_check(const og_graph* g, const og_model* m, uint64_t seed, uint64_t n_states, const uint32_t* pos,
+              const uint32_t* affix, uint64_t draws, uint64_t* counts, double* kl) {
+    og_config c;
+    memset(&c, 0, sizeof c);
+    c.seed = seed;
+    c.init_kind = OG_INIT_RANDOM;
+    c.burn_in_steps = 100;
+    c.hw_sample_size = 32;
+    c.rng = OG_RNG_PHILOX;
+    uint32_t key[2];
+    og_philox_key(seed, DOM_CHECK, key);
+    uint64_t base = 0;
+    for (uint64_t j = 0; j < n_states; ++j) {
+        const uint32_t v = pos[j], a = affix[j];
+        const uint32_t deg = deg_of(g, v);
+        uint64_t* cnt = counts + base;
+        base += deg;
+        for (uint32_t i = 0; i < deg; ++i) cnt[i] = 0;
+        kl[j] = __builtin_nan("");
+        double* w = (double*)malloc((deg ? deg : 1) * sizeof(double));
+        double total = 0.0;
+        for (uint32_t i = 0; i < deg; ++i) {
+            w[i] = og_weight(g, m, v, a, i);
+            total += w[i];
+        }
+        uint32_t last;
+        if (total > 0 && og_init_philox(g, m, &c, v, a, j, &last)) {
+            st_t s = {g, m, v, a, deg};
+            for (uint64_t d = 0; d < draws; ++d) {
+                draw_t dr;
+                draw_open(&dr, 1, NULL, key, j, (uint32_t)d);
+                last = mh_transition(&s, last, &dr);
+                cnt[last]++;
+            }
+            double k = 0.0;
+            for (uint32_t i = 0; i < deg; ++i) {
+                const double p = (double)cnt[i] / (double)draws;
+                if (p == 0.0) continue;
+                k += p * log(p / (w[i] / total));
+            }
+            kl[j] = k;
+        }
+        free(w);
+    }
 }
 
 /* ================================================================ engine */

@@ -129,6 +129,11 @@ int og_init_philox(const og_graph* g, const og_model* m, const og_config* c, uin
                    uint32_t affix, uint64_t slot, uint32_t* last);
 uint64_t og_slot_count(const og_graph* g, const og_model* m);
 
+/* Per-state chain audit of cmd_check (tools/mhwalk.cpp:222-247) under the
+ * engine's Philox layout; counts has sum(deg(pos[j])) entries. */
+void og_check(const og_graph* g, const og_model* m, uint64_t seed, uint64_t n_states, const uint32_t* pos,
+              const uint32_t* affix, uint64_t draws, uint64_t* counts, double* kl);
+
 /* ------------------------------------------------------------- engine */
 /* generate_walks (engine.cpp:157-234). rows: (n*K) x stride, lens: n*K.
  * Returns status; err holds the message. */

@@ -176,6 +176,8 @@ class Oracle:
         L.og_decide.argtypes = [C.POINTER(_OgGraph), C.POINTER(_OgModel), C.c_uint64, _u32p, _u32p,
                                 _u32p, _u32p, _dp, _dp, _dp, _u8p]
         L.og_alias_build.argtypes = [C.c_uint32, _dp, _dp, _u32p]
+        L.og_check.argtypes = [C.POINTER(_OgGraph), C.POINTER(_OgModel), C.c_uint64, C.c_uint64, _u32p, _u32p,
+                               C.c_uint64, _u64p, _dp]
         L.og_direct_sample_u.argtypes = [C.c_uint32, _dp, C.c_double]
         L.og_direct_sample_u.restype = C.c_uint32
         L.og_slot_count.argtypes = [C.POINTER(_OgGraph), C.POINTER(_OgModel)]
@@ -325,6 +327,18 @@ class Oracle:
         stats = dict(walks=st.walks, early_terminations=st.early, skipped_starts=st.skipped,
                      steps=st.steps, init_calls=st.init_calls)
         return rows[:k], lens[:k], stats
+
+    def check(self, g, md, seed, pos, affix, draws):
+        """og_check: per-state (kl, counts) of cmd_check's chain audit."""
+        gs, ms, keep = self.bind(g, md)
+        pos = np.ascontiguousarray(pos, dtype=np.uint32)
+        aff = np.ascontiguousarray(affix, dtype=np.uint32)
+        deg = np.diff(g.offsets).astype(np.int64)[pos]
+        counts = np.zeros(max(int(deg.sum()), 1), dtype=np.uint64)
+        kl = np.zeros(len(pos))
+        self.lib.og_check(C.byref(gs), C.byref(ms), seed, len(pos), _ptr(pos, _u32p), _ptr(aff, _u32p), draws,
+                          _ptr(counts, _u64p), _ptr(kl, _dp))
+        return kl, counts[:int(deg.sum())]
 
     def init_philox(self, g, md, cfg: WalkCfg, v, affix, slot):
         gs, ms, keep = self.bind(g, md)

@@ -527,6 +527,21 @@ mhw_status mhw_decide(const mhw_graph* g, const mhw_model_desc* model, uint64_t 
     });
 }
 
+mhw_status mhw_check(const mhw_graph* g, const mhw_model_desc* model, uint64_t seed, uint64_t count,
+                     const uint32_t* position, const uint32_t* affixture, uint64_t draws, double* kl,
+                     uint64_t* counts) {
+    return guard([&] {
+        need(g, "graph");
+        need(model, "model");
+        if (count) {
+            need(position, "position");
+            need(affixture, "affixture");
+            need(kl, "kl");
+        }
+        mhw::run_check(*const_cast<mhw_graph*>(g), *model, seed, count, position, affixture, draws, kl, counts);
+    });
+}
+
 mhw_status mhw_alias_tables(const mhw_graph* g, double* prob, uint32_t* alias) {
     return guard([&] {
         need(g, "graph");

@@ -504,6 +504,89 @@ __global__ void k_init_states(DevGraph g, DevModel m, DevCfg cfg, uint64_t n, co
     }
 }
 
+// cmd_check's per-state chain audit (tools/mhwalk.cpp:222-247), one warp per
+// state: the warp evaluates the state's w' table once, then runs the chain 32
+// draws at a time -- lanes draw and look up their proposals in parallel, the
+// fold over the 32 is done by every lane in lockstep through shuffles, each
+// lane records the chain state after its own draw. Same Philox layout as
+// og_check: init keyed by slot = state index, draw d from block (j, d).
+constexpr uint32_t DOM_CHECK = 0xC4EC0005u;
+
+template <int KIND>
+__global__ void k_check(DevGraph g, DevModel m, DevCfg cfg, uint64_t n, const uint32_t* __restrict__ pos,
+                        const uint32_t* __restrict__ aff, const uint64_t* __restrict__ base, uint64_t draws,
+                        double* __restrict__ W, unsigned long long* __restrict__ counts, double* __restrict__ kl) {
+    const unsigned lane = threadIdx.x & 31;
+    const uint64_t wid = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    const uint2 key = philox_key(cfg.seed, DOM_CHECK);
+    for (uint64_t j = wid; j < n; j += nw) {
+        const SCtx c = make_ctx<KIND>(g, m, pos[j], aff[j]);
+        double* w = W + base[j];
+        unsigned long long* cnt = counts + base[j];
+        for (uint32_t i = lane; i < c.deg; i += 32) {
+            uint32_t cls;
+            w[i] = eval_index<KIND>(g, m, c, i, &cls);
+            cnt[i] = 0;
+        }
+        __syncwarp();
+        double total = 0.0;
+        for (uint32_t i = 0; i < c.deg; ++i) total = __dadd_rn(total, w[i]);
+        if (!(total > 0)) {
+            if (lane == 0) kl[j] = __longlong_as_double(0x7FF8000000000000ll);
+            continue;
+        }
+        const uint32_t e = init_slot<KIND>(g, m, cfg, c, j);  // every lane: same value
+        if (e == kDead) {
+            if (lane == 0) kl[j] = __longlong_as_double(0x7FF8000000000000ll);
+            continue;
+        }
+        uint32_t last = e & kIdxMask;
+        double wl = w[last];
+        for (uint64_t d0 = 0; d0 < draws; d0 += 32) {
+            const uint64_t d = d0 + lane;
+            uint32_t cand = 0;
+            double wc = 0.0, u = 1.0;
+            if (d < draws) {
+                Draw dr;
+                dr.open(key, j, (uint32_t)d);
+                cand = dr.index(c.deg);
+                u = dr.unit();
+                wc = w[cand];
+            }
+            const uint32_t steps = draws - d0 < 32 ? (uint32_t)(draws - d0) : 32u;
+            uint32_t mine = 0;
+            for (uint32_t t = 0; t < steps; ++t) {
+                const uint32_t ct = __shfl_sync(0xffffffffu, cand, t);
+                const double wct = __shfl_sync(0xffffffffu, wc, t);
+                const double ut = __shfl_sync(0xffffffffu, u, t);
+                if (mh_accept(wct, wl, ut)) {
+                    last = ct;
+                    wl = wct;
+                }
+                if (t == lane) mine = last;
+            }
+            if (lane < steps) atomicAdd(cnt + mine, 1ull);
+        }
+        __syncwarp();
+        if (lane == 0) {
+            double k = 0.0;
+            for (uint32_t i = 0; i < c.deg; ++i) {
+                const double p = (double)cnt[i] / (double)draws;
+                if (p == 0.0) continue;
+                k += p * log(p / (w[i] / total));
+            }
+            kl[j] = k;
+        }
+    }
+}
+
+__global__ void k_state_degrees(DevGraph g, const uint32_t* __restrict__ pos, uint64_t n, uint64_t* __restrict__ d) {
+    for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j <= n;
+         j += (uint64_t)gridDim.x * blockDim.x)
+        d[j] = j < n ? load_node(g, pos[j]).deg : 0;
+}
+
 // Session setup: classify start nodes of [b, e).
 __global__ void k_classify(DevGraph g, DevModel m, uint32_t b, uint32_t e, uint8_t* __restrict__ valid,
                            uint8_t* __restrict__ act, uint8_t* __restrict__ iso) {
@@ -1006,6 +1089,49 @@ void run_init_states(Graph& g, const mhw_model_desc& md, const mhw_walk_config& 
     MHW_CK(cudaMemcpyAsync(&hbad, bad.p, 4, cudaMemcpyDeviceToHost, st));
     MHW_CK(cudaStreamSynchronize(st));
     if (hbad) invalid(std::to_string(hbad) + " states outside the graph");
+}
+
+void run_check(Graph& g, const mhw_model_desc& md, uint64_t seed, uint64_t n, const uint32_t* pos,
+               const uint32_t* aff, uint64_t draws, double* kl, uint64_t* counts) {
+    DeviceGuard dg(g.device);
+    Model mb;
+    model_bind(mb, g, md);
+    if (!n) return;
+    if (!draws) invalid("draws must be positive");
+    for (uint64_t j = 0; j < n; ++j)
+        if (pos[j] >= g.n) invalid("state position outside the graph");
+    DevCfg cfg{};
+    cfg.seed = seed;
+    cfg.init_kind = INIT_RANDOM;  // cmd_check uses the default InitStrategy (tools/mhwalk.cpp:235)
+    cfg.burn_in = 100;
+    cfg.hw = 32;
+    cfg.rep_deg = kNoReplicas;
+    cudaStream_t st = g.stream;
+    DBuf<uint32_t> dpos(n), daff(n);
+    DBuf<uint64_t> deg(n + 1), base(n + 1);
+    DBuf<double> dkl(n);
+    MHW_CK(cudaMemcpyAsync(dpos.p, pos, n * 4, cudaMemcpyHostToDevice, st));
+    MHW_CK(cudaMemcpyAsync(daff.p, aff, n * 4, cudaMemcpyHostToDevice, st));
+    k_state_degrees<<<grid_for(n + 1), 256, 0, st>>>(g.view(), dpos.p, n, deg.p);
+    size_t bytes = 0;
+    MHW_CK(cub::DeviceScan::ExclusiveSum(nullptr, bytes, deg.p, base.p, (int64_t)n + 1, st));
+    DBuf<uint8_t> temp(std::max<size_t>(bytes, 1));
+    MHW_CK(cub::DeviceScan::ExclusiveSum(temp.p, bytes, deg.p, base.p, (int64_t)n + 1, st));
+    uint64_t total = 0;
+    MHW_CK(cudaMemcpyAsync(&total, base.p + n, 8, cudaMemcpyDeviceToHost, st));
+    MHW_CK(cudaStreamSynchronize(st));
+    DBuf<double> W(std::max<uint64_t>(total, 1));
+    DBuf<unsigned long long> cnt(std::max<uint64_t>(total, 1));
+    const DevGraph gv = g.view();
+    dispatch(md.kind, [&](auto kc) {
+        constexpr int KIND = decltype(kc)::value;
+        k_check<KIND><<<grid_for(n * 32), 256, 0, st>>>(gv, mb.dev, cfg, n, dpos.p, daff.p, base.p, draws, W.p,
+                                                        cnt.p, dkl.p);
+    });
+    MHW_CK(cudaGetLastError());
+    MHW_CK(cudaMemcpyAsync(kl, dkl.p, n * 8, cudaMemcpyDeviceToHost, st));
+    if (counts && total) MHW_CK(cudaMemcpyAsync(counts, cnt.p, total * 8, cudaMemcpyDeviceToHost, st));
+    MHW_CK(cudaStreamSynchronize(st));
 }
 
 void partition_nodes(Graph& g, const mhw_model_desc& md, int parts, uint32_t* cuts) {

@@ -82,6 +82,8 @@ void run_decide(Graph& g, const mhw_model_desc& md, uint64_t n, const uint32_t* 
 void run_init_states(Graph& g, const mhw_model_desc& md, const mhw_walk_config& wc, uint64_t n,
                      const uint32_t* pos, const uint32_t* aff, uint32_t* last);
 void partition_nodes(Graph& g, const mhw_model_desc& md, int parts, uint32_t* cuts);
+void run_check(Graph& g, const mhw_model_desc& md, uint64_t seed, uint64_t n, const uint32_t* pos,
+               const uint32_t* aff, uint64_t draws, double* kl, uint64_t* counts);
 
 }  // namespace mhw
 

@@ -459,6 +459,32 @@ def decide(graph: Graph, model: WalkModel, position, affixture, candidate, last,
     return wc[:n], wl[:n], acc[:n]
 
 
+def check(graph: Graph, model: WalkModel, position, affixture, draws: int, seed: int = 0,
+          tolerance: float | None = None):
+    """cmd_check (tools/mhwalk.cpp:222-264) on the GPU: per-state KL of a
+    `draws`-long M-H chain against the exact target. Returns (kl, counts,
+    exit_code) with exit_code = 0 if max KL < tolerance else 3 (None without
+    a tolerance)."""
+    d, keep = model._desc()
+    pos = np.ascontiguousarray(position, dtype=np.uint32)
+    aff = np.ascontiguousarray(affixture, dtype=np.uint32)
+    n = len(pos)
+    kl = np.zeros(max(n, 1))
+    total = 0
+    if n:
+        offs = graph.download()["offsets"]
+        total = int(np.sum(offs[pos.astype(np.int64) + 1] - offs[pos.astype(np.int64)]))
+    counts = np.zeros(max(total, 1), dtype=np.uint64)
+    _check(L.lib().mhw_check(graph.handle, C.byref(d), seed, n, _ptr(pos), _ptr(aff), draws, _ptr(kl),
+                             _ptr(counts)))
+    kl = kl[:n]
+    code = None
+    if tolerance is not None:
+        valid = kl[~np.isnan(kl)]
+        code = 0 if (valid.max() if len(valid) else 0.0) < tolerance else 3
+    return kl, counts[:total], code
+
+
 def alias_tables(graph: Graph):
     m = graph.arc_count()
     prob = np.zeros(max(m, 1))

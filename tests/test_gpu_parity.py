@@ -176,6 +176,30 @@ def test_packed_corpus_equals_padded(mhw, oracle):
     assert rng is not None
 
 
+@pytest.mark.parametrize("kind", KINDS)
+def test_check_audit_equals_oracle(mhw, oracle, kind):
+    """`check` (tools/mhwalk.cpp:222-247) on the GPU: per-state chain visit
+    counts identical to og_check, KL within 1e-12, and below the reference's
+    chain-correctness bound (acceptance.cpp:44-63: KL < 0.005 at 1e6 draws)."""
+    g = typed_random_graph(71 + kind, 200, 8.0, weighted=True, types=2)
+    md = model_desc(kind, g, p=0.4, q=2.5)
+    pos, aff, _, _, _ = random_triples(g, md, 64, seed=kind)
+    if kind in (O.NODE2VEC, O.EDGE2VEC, O.FAIRWALK):
+        deg = np.diff(g.offsets).astype(np.int64)[pos]
+        aff = np.where(aff == O.NO_AFFIX, 0, aff) % deg
+    if kind == O.METAPATH2VEC:  # states must have the metapath position's type
+        keep = g.ntype[pos] == np.array(md.metapath)[aff]
+        pos, aff = pos[keep], aff[keep]
+    okl, ocnt = oracle.check(g, md, 99, pos, aff, 100000)
+    from paper_2010_04895_b200.mhwalk import check
+    gkl, gcnt, code = check(device_graph(g), walk_model(md), pos, aff, 100000, seed=99, tolerance=0.005)
+    assert np.array_equal(ocnt, gcnt)
+    both = ~np.isnan(okl)
+    assert np.array_equal(both, ~np.isnan(gkl))
+    assert np.allclose(okl[both], gkl[both], rtol=1e-12, atol=1e-15)
+    assert code == 0
+
+
 def test_alias_tables_bit_exact(mhw, oracle):
     """Per-node alias tables == alias_build (samplers.cpp:95-131) bit for bit."""
     g = typed_random_graph(41, 500, 10.0, weighted=True)
