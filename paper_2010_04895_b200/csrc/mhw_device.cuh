@@ -60,10 +60,28 @@ struct DevGraph {
     const double* __restrict__ wtotal;    // sequential fp64 slice sums
     const uint32_t* __restrict__ tcount;  // fairwalk type counts, n * n_ntypes
     const uint32_t* __restrict__ htab;    // adjacency hash sets (nullptr: not built)
+    const uint4* __restrict__ arc;        // arc records (nullptr: not built)
     uint16_t n_ntypes;
     uint16_t n_etypes;
     int verified_sym;                     // every arc has its back arc
 };
+
+// ------------------------------------------------------------ arc records
+// For graphs with < 2^32 arcs, arc a = (v -> u) has a 16-byte record
+// {u, deg(u) | NF_ALLPOS(u) << 31, off(u), aux} with aux = rev[a] (index of v
+// in N(u), second-order models) or the fp32 weight bits of a (first-order):
+// one load yields everything the next walker state needs.
+constexpr int ARC_AUX_REV = 1;
+constexpr int ARC_AUX_WEIGHT = 2;
+
+__device__ __forceinline__ NodeRec arc_node(uint4 a) {
+    NodeRec r;
+    r.off = (long long)a.z;
+    r.deg = a.y & 0x7FFFFFFFu;
+    r.type = 0;
+    r.flags = (a.y >> 31) ? NF_ALLPOS : 0;
+    return r;
+}
 
 // ------------------------------------------------- adjacency hash sets
 // Nodes of degree >= kHashMinDeg get an exact hash set of their neighbour

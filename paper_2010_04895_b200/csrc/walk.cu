@@ -52,7 +52,9 @@ __device__ __noinline__ uint32_t init_slot_ool(const DevGraph g, const DevModel 
 // ------------------------------------------------------ throughput kernel
 // LAZY = false: every slot was initialised by k_init_all before the launch,
 // so the lazy-init call (and the registers the call ABI pins) is compiled out.
-template <int KIND, int REGS, bool LAZY>
+// AR = true: arc records (deepwalk: aux = weight, node2vec: aux = rev) replace
+// the id / node-record / weight / reverse-arc loads of a step.
+template <int KIND, int REGS, bool LAZY, bool AR>
 __global__ void __launch_bounds__(kWalkBlock) __maxnreg__(REGS) k_walk(RunParams P) {
     const DevGraph& g = P.g;
     const uint2 wkey = philox_key(P.cfg.seed, DOM_WALK);
@@ -110,9 +112,16 @@ __global__ void __launch_bounds__(kWalkBlock) __maxnreg__(REGS) k_walk(RunParams
                     dead = true;
                     break;
                 }
-                next = load_id(g, c.off + chosen);
-                rn = load_node(g, next);
-                back_c = __ldg(g.rev + c.off + chosen);
+                if constexpr (AR) {
+                    const uint4 a = __ldg(g.arc + c.off + chosen);
+                    next = a.x;
+                    rn = arc_node(a);
+                    back_c = a.w;
+                } else {
+                    next = load_id(g, c.off + chosen);
+                    rn = load_node(g, next);
+                    back_c = __ldg(g.rev + c.off + chosen);
+                }
             } else {
                 // Take the slot: the chain word itself is the lock. The
                 // transition (proposal evaluation + decision) happens while
@@ -127,17 +136,28 @@ __global__ void __launch_bounds__(kWalkBlock) __maxnreg__(REGS) k_walk(RunParams
                 uint32_t e = atomicExch(P.chain + slot, kLocked);
                 const uint32_t cand = d.index(c.deg);
                 const double u = d.unit();
-                const uint32_t uc = load_id(g, c.off + cand);
-                // the candidate's record is needed before the decision only
-                // for its type or for the alpha slice choice; otherwise it is
-                // fetched after an acceptance (it is the next node then)
-                const bool rc_early = needs_utype<KIND>() ||
-                                      (second_order(KIND) && !P.m.alpha_trivial && needs_urec_for_alpha(g, c));
+                uint32_t uc;
+                uint4 ac = make_uint4(0, 0, 0, 0);
                 NodeRec rc{};
-                if (rc_early) rc = load_node(g, uc);
+                bool rc_early;
+                if constexpr (AR) {
+                    ac = __ldg(g.arc + c.off + cand);
+                    uc = ac.x;
+                    rc = arc_node(ac);
+                    rc_early = true;
+                } else {
+                    uc = load_id(g, c.off + cand);
+                    // the candidate's record is needed before the decision
+                    // only for its type or for the alpha slice choice;
+                    // otherwise it is fetched after an acceptance
+                    rc_early = needs_utype<KIND>() ||
+                               (second_order(KIND) && !P.m.alpha_trivial && needs_urec_for_alpha(g, c));
+                    if (rc_early) rc = load_node(g, uc);
+                }
                 const uint32_t cls_c =
                     second_order(KIND) ? alpha_class(g, P.m, c, uc, rc_early ? &rc : nullptr) : 0u;
-                const double wc = wprime<KIND>(g, P.m, c, cand, rc.type, cls_c);
+                const double wc = (AR && KIND == DEEPWALK) ? (double)__uint_as_float(ac.w)
+                                                          : wprime<KIND>(g, P.m, c, cand, rc.type, cls_c);
                 if (e == kLocked) {
                     unsigned ns = 32;
                     do {
@@ -170,25 +190,40 @@ __global__ void __launch_bounds__(kWalkBlock) __maxnreg__(REGS) k_walk(RunParams
                 constexpr bool kSpec = needs_utype<KIND>() || KIND == DEEPWALK;
                 uint32_t ul = 0;
                 NodeRec rl{};
+                uint4 al = make_uint4(0, 0, 0, 0);
                 if (kSpec) {
-                    ul = load_id(g, c.off + last);
-                    rl = load_node(g, ul);
+                    if constexpr (AR) {
+                        al = __ldg(g.arc + c.off + last);
+                        ul = al.x;
+                        rl = arc_node(al);
+                    } else {
+                        ul = load_id(g, c.off + last);
+                        rl = load_node(g, ul);
+                    }
                 }
-                const double wl = wprime<KIND>(g, P.m, c, last, rl.type, cls_l);
+                const double wl = (AR && KIND == DEEPWALK) ? (double)__uint_as_float(al.w)
+                                                          : wprime<KIND>(g, P.m, c, last, rl.type, cls_l);
                 const bool acc = mh_accept(wc, wl, u) && cand != last;
                 chain_release(P.chain + slot, acc ? pack_entry(cand, cls_c) : e);
                 chosen = acc ? cand : last;
-                if (acc || cand == last) {
-                    next = uc;
-                    rn = rc_early ? rc : load_node(g, uc);
-                } else if (kSpec) {
-                    next = ul;
-                    rn = rl;
+                if constexpr (AR) {
+                    const uint4 an = (acc || cand == last) ? ac : (kSpec ? al : __ldg(g.arc + c.off + last));
+                    next = an.x;
+                    rn = arc_node(an);
+                    back_c = an.w;
                 } else {
-                    next = load_id(g, c.off + last);
-                    rn = load_node(g, next);
+                    if (acc || cand == last) {
+                        next = uc;
+                        rn = rc_early ? rc : load_node(g, uc);
+                    } else if (kSpec) {
+                        next = ul;
+                        rn = rl;
+                    } else {
+                        next = load_id(g, c.off + last);
+                        rn = load_node(g, next);
+                    }
+                    if (second_order(KIND)) back_c = __ldg(g.rev + c.off + chosen);
                 }
-                if (second_order(KIND)) back_c = __ldg(g.rev + c.off + chosen);
             }
             // emit: 4 ids buffered in registers, one 16-byte store
             switch (len & 3) {
@@ -625,13 +660,6 @@ unsigned grid_for(uint64_t work, int block = 256) {
     return (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(g, (uint64_t)sms() * 16));
 }
 
-template <int KIND, int MINB, bool LAZY>
-int walk_grid() {
-    int per_sm = 0;
-    MHW_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_walk<KIND, MINB, LAZY>, kWalkBlock, 0));
-    return std::max(1, per_sm) * sms();
-}
-
 // Register-cap variant of the walk kernel (occupancy vs spills trade-off,
 // measured in profiles/); MHW_WALK_REGS selects it at session creation.
 // Defaults from the sweep in profiles/: deepwalk 80 (4.84 vs 5.27 ms on cfg1),
@@ -639,17 +667,34 @@ int walk_grid() {
 int walk_minb(int kind) {
     const char* e = std::getenv("MHW_WALK_REGS");
     const int v = e ? std::atoi(e) : (kind == DEEPWALK ? 80 : 255);
-    return (v == 64 || v == 80 || v == 96) ? v : 255;
+    return v == 80 ? 80 : 255;
 }
 
+// Calls f(REGS, LAZY, AR) with the compile-time variant of the session.
 template <int KIND, class F>
-void with_minb(int regs, F&& f) {
-    switch (regs) {
-        case 80: f(std::integral_constant<int, 80>{}); break;
-        case 96: f(std::integral_constant<int, 96>{}); break;
-        case 64: f(std::integral_constant<int, 64>{}); break;
-        default: f(std::integral_constant<int, 255>{}); break;
+void with_variant(int regs, bool lazy, bool ar, F&& f) {
+    using T = std::true_type;
+    using N = std::false_type;
+    auto by_regs = [&](auto lz, auto a) {
+        if (regs == 80) f(std::integral_constant<int, 80>{}, lz, a);
+        else f(std::integral_constant<int, 255>{}, lz, a);
+    };
+    if constexpr (KIND == DEEPWALK || KIND == NODE2VEC) {
+        if (ar) {
+            if (lazy) by_regs(T{}, T{});
+            else by_regs(N{}, T{});
+            return;
+        }
     }
+    if (lazy) by_regs(T{}, N{});
+    else by_regs(N{}, N{});
+}
+
+template <int KIND, int REGS, bool LAZY, bool AR>
+int walk_grid() {
+    int per_sm = 0;
+    MHW_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_walk<KIND, REGS, LAZY, AR>, kWalkBlock, 0));
+    return std::max(1, per_sm) * sms();
 }
 
 template <class F>
@@ -862,10 +907,15 @@ void session_create(Session& s, Graph& g, const mhw_model_desc& md, const mhw_wa
         const bool dense = (double)s.n_items * s.cfg.L >= 8.0 * (double)s.slots;
         s.eager_init = second_order(m.kind) && (wc.init_mode == 2 || (wc.init_mode == 0 && dense));
         s.minb = walk_minb(m.kind);
+        // arc records (after the session buffers, so the memory check sees them)
+        const char* ar_env = std::getenv("MHW_ARC_RECORDS");
+        const bool want_ar = !(ar_env && ar_env[0] == '0');
+        if (want_ar && (m.kind == DEEPWALK || m.kind == NODE2VEC))
+            s.use_ar = graph_ensure_arcrec(g, m.kind == NODE2VEC ? ARC_AUX_REV : ARC_AUX_WEIGHT);
         dispatch(m.kind, [&](auto kc) {
-            with_minb<decltype(kc)::value>(s.minb, [&](auto mb) {
-                if (s.eager_init) s.grid = walk_grid<decltype(kc)::value, decltype(mb)::value, false>();
-                else s.grid = walk_grid<decltype(kc)::value, decltype(mb)::value, true>();
+            constexpr int KIND = decltype(kc)::value;
+            with_variant<KIND>(s.minb, !s.eager_init, s.use_ar, [&](auto rg, auto lz, auto ar) {
+                s.grid = walk_grid<KIND, decltype(rg)::value, decltype(lz)::value, decltype(ar)::value>();
             });
         });
     }
@@ -949,9 +999,9 @@ void session_run(Session& s, cudaStream_t user) {
                         ++s.launches;
                     }
                 }
-                with_minb<KIND>(s.minb, [&](auto mb) {
-                    if (s.eager_init) k_walk<KIND, decltype(mb)::value, false><<<s.grid, kWalkBlock, 0, st>>>(P);
-                    else k_walk<KIND, decltype(mb)::value, true><<<s.grid, kWalkBlock, 0, st>>>(P);
+                with_variant<KIND>(s.minb, !s.eager_init, s.use_ar, [&](auto rg, auto lz, auto ar) {
+                    k_walk<KIND, decltype(rg)::value, decltype(lz)::value, decltype(ar)::value>
+                        <<<s.grid, kWalkBlock, 0, st>>>(P);
                 });
             });
             ++s.launches;

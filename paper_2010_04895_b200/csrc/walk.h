@@ -56,6 +56,7 @@ struct Session {
     int sort_bits = 1;
     int grid = 0;
     bool eager_init = false;
+    bool use_ar = false;     // arc-record walk kernel variant
     int minb = 1;
     uint32_t launches = 0;
     cudaStream_t stream = nullptr;
