@@ -270,14 +270,21 @@ def run_mine(args, cfg):
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     dist = None
+    n_dev = torch.cuda.device_count()
+    dev = local % max(n_dev, 1)
+    torch.cuda.set_device(dev)
+    host_coll = False
     if world > 1:
         import torch.distributed as dist
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    else:
-        torch.cuda.set_device(local)
-    dev = local
+        if n_dev >= world:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+        else:
+            # fewer GPUs than ranks (path check on one GPU): the barrier and
+            # the max-over-ranks reduction go over gloo; no kernel of one rank
+            # ever waits on another rank
+            dist.init_process_group("gloo")
+            host_coll = True
     t0 = time.time()
     g = build_graph(cfg, device=dev)
     model = make_model(cfg)
@@ -318,7 +325,8 @@ def run_mine(args, cfg):
     steps_total = st.steps * args.steps
     t_local = sum(ms) * 1e-3
     kernel_ms = st.walk_seconds * 1e3
-    t = torch.tensor([t_local, steps_total, launches], dtype=torch.float64, device=dev)
+    args.coll_device = "cpu" if host_coll else dev
+    t = torch.tensor([t_local, steps_total, launches], dtype=torch.float64, device=args.coll_device)
     if dist:
         tmax = t.clone()
         dist.all_reduce(tmax[:1], op=dist.ReduceOp.MAX)
@@ -426,7 +434,7 @@ def run_e2e(args, cfg, g, model, wcfg, dev, dist):
             steps += st.steps
     t_local = float(np.sum(times))
     if dist:
-        tt = torch.tensor([t_local, float(steps)], dtype=torch.float64, device=dev)
+        tt = torch.tensor([t_local, float(steps)], dtype=torch.float64, device=args.coll_device)
         tmax = tt.clone()
         dist.all_reduce(tmax[:1], op=dist.ReduceOp.MAX)
         dist.all_reduce(tt[1:], op=dist.ReduceOp.SUM)

@@ -24,6 +24,11 @@ view = L.GraphView()
 view.node_count, view.arc_count = len(d["offsets"]) - 1, len(d["neighbors"])
 view.offsets, view.neighbors = off.data_ptr(), nb.data_ptr()
 view.weights = w.data_ptr() if w is not None else None
+nt = pin(d["node_types"]) if d["node_types"] is not None else None
+et = pin(d["edge_types"]) if d["edge_types"] is not None else None
+view.node_types = nt.data_ptr() if nt is not None else None
+view.edge_types = et.data_ptr() if et is not None else None
+view.num_node_types, view.num_edge_types = d["num_node_types"], d["num_edge_types"]
 view.symmetric = 1
 md, keep = model._desc()
 c = wcfg._c()
