@@ -155,6 +155,9 @@ typedef struct mhw_session mhw_session;
 MHW_API const char* mhw_last_error(void);
 MHW_API const char* mhw_version(void);
 MHW_API int32_t mhw_device_count(void);
+/* Releases the library's cache of large device blocks (kept between calls
+ * to avoid multi-GB cudaMalloc/cudaFree per generate_walks). */
+MHW_API void mhw_trim_memory(void);
 
 /* ---- graphs (device-resident CSR) ------------------------------------ */
 

@@ -50,6 +50,7 @@ SIGNATURES = {
     "mhw_last_error": (C.c_char_p, []),
     "mhw_version": (C.c_char_p, []),
     "mhw_device_count": (C.c_int32, []),
+    "mhw_trim_memory": (None, []),
     "mhw_graph_upload": (C.c_int32, [C.POINTER(GraphView), C.c_int32, _PP]),
     "mhw_graph_from_edges": (C.c_int32, [C.c_uint64, _P, _P, _P, C.c_int32, C.c_uint32, C.c_int32, _PP]),
     "mhw_graph_generate_rmat": (C.c_int32, [C.c_uint32, C.c_uint32, C.c_double, C.c_double, C.c_double,

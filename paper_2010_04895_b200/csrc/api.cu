@@ -2,6 +2,7 @@
 // converts exceptions to status codes (errors.hpp classes -> 1/2/4) and keeps
 // the message in a thread-local buffer (mhw_last_error).
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <new>
@@ -92,6 +93,8 @@ extern "C" {
 
 const char* mhw_last_error(void) { return g_error.c_str(); }
 const char* mhw_version(void) { return "mhw 0.1.0 (sm_100a)"; }
+
+void mhw_trim_memory(void) { mhw::dev_trim(); }
 
 int32_t mhw_device_count(void) {
     int n = 0;
@@ -412,11 +415,9 @@ mhw_status mhw_generate_walks_packed(const mhw_graph* g, const mhw_model_desc* m
         mhw_session s;
         mhw::session_create(s, *gg, *model, *config);
         if (capacity_rows < s.rows + 1) mhw::invalid("offset buffer too small for the corpus");
-        mhw::session_run(s, nullptr);
-        mhw_walk_stats st{};
-        mhw::session_stats(s, st);
-        mhw::session_download_packed(s, h_nodes, capacity_nodes, h_offsets, capacity_rows, nullptr, nullptr);
-        if (stats) *stats = st;
+        const char* e = std::getenv("MHW_E2E_CHUNKS");
+        const int chunks = e ? std::atoi(e) : 4;
+        mhw::session_run_packed(s, h_nodes, capacity_nodes, h_offsets, capacity_rows, chunks, stats);
     });
 }
 

@@ -7,7 +7,9 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <cstdint>
 #include <cstring>
+#include <mutex>
 
 #include "internal.h"
 
@@ -20,6 +22,80 @@ void throw_cuda(cudaError_t e, const char* what, const char* file, int line) {
                       std::to_string(line) + ")";
     if (e == cudaErrorMemoryAllocation) msg = "out of device memory: " + msg;
     throw Error(code, msg);
+}
+
+// ------------------------------------------------------- device block cache
+namespace {
+constexpr size_t kCacheMin = 32ull << 20;
+constexpr size_t kCacheGrain = 2ull << 20;
+struct CachedBlock {
+    int device;
+    size_t cap;
+    void* p;
+};
+std::mutex g_cache_mu;
+std::vector<CachedBlock> g_cache;
+}  // namespace
+
+void* dev_alloc(size_t bytes, size_t* cap) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (bytes >= kCacheMin) {
+        bytes = (bytes + kCacheGrain - 1) / kCacheGrain * kCacheGrain;
+        std::lock_guard<std::mutex> lk(g_cache_mu);
+        size_t best = SIZE_MAX;
+        for (size_t i = 0; i < g_cache.size(); ++i) {
+            const auto& b = g_cache[i];
+            if (b.device == dev && b.cap >= bytes && b.cap <= bytes + bytes / 4 + kCacheGrain &&
+                (best == SIZE_MAX || b.cap < g_cache[best].cap))
+                best = i;
+        }
+        if (best != SIZE_MAX) {
+            void* p = g_cache[best].p;
+            *cap = g_cache[best].cap;
+            g_cache.erase(g_cache.begin() + best);
+            return p;
+        }
+    }
+    void* p = nullptr;
+    cudaError_t e = cudaMalloc(&p, bytes);
+    if (e == cudaErrorMemoryAllocation) {
+        cudaGetLastError();
+        dev_trim();
+        e = cudaMalloc(&p, bytes);
+    }
+    if (e != cudaSuccess) throw_cuda(e, "cudaMalloc", __FILE__, __LINE__);
+    *cap = bytes;
+    return p;
+}
+
+void dev_free(void* p, size_t cap) {
+    if (!p) return;
+    if (cap < kCacheMin) {
+        cudaFree(p);
+        return;
+    }
+    // the block may still be read by in-flight work on any stream
+    cudaDeviceSynchronize();
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lk(g_cache_mu);
+    g_cache.push_back({dev, cap, p});
+}
+
+void dev_trim() {
+    std::vector<CachedBlock> all;
+    {
+        std::lock_guard<std::mutex> lk(g_cache_mu);
+        all.swap(g_cache);
+    }
+    int prev = 0;
+    cudaGetDevice(&prev);
+    for (const auto& b : all) {
+        cudaSetDevice(b.device);
+        cudaFree(b.p);
+    }
+    cudaSetDevice(prev);
 }
 
 DevGraph Graph::view() const {
@@ -922,6 +998,10 @@ bool graph_ensure_arcrec(Graph& g, int aux) {
     if (aux == ARC_AUX_REV) graph_ensure_rev(g);
     size_t free_b = 0, total_b = 0;
     MHW_CK(cudaMemGetInfo(&free_b, &total_b));
+    if (free_b < 16 * g.m + (2ull << 30)) {
+        dev_trim();  // cached blocks count as used
+        MHW_CK(cudaMemGetInfo(&free_b, &total_b));
+    }
     if (free_b < 16 * g.m + (2ull << 30)) return false;  // keep headroom; the walk works without
     g.arc.alloc(g.m);
     g.arc_aux = aux;

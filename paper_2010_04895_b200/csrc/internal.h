@@ -29,36 +29,49 @@ struct Error : std::runtime_error {
 
 inline void invalid(const std::string& msg) { throw Error(MHW_ERR_INVALID, msg); }
 
+// Device allocation with a block cache for large buffers (graph.cu): blocks
+// >= 32 MB are kept after a device synchronisation and reused by later calls
+// (multi-GB cudaMalloc/cudaFree per generate_walks call cost tens of ms);
+// on an allocation failure the cache is released and the allocation retried.
+void* dev_alloc(size_t bytes, size_t* cap);
+void dev_free(void* p, size_t cap);
+void dev_trim();
+
 // RAII device buffer on the current device.
 template <class T>
 struct DBuf {
     T* p = nullptr;
     size_t n = 0;
+    size_t cap = 0;  // allocated bytes
     DBuf() = default;
     explicit DBuf(size_t count) { alloc(count); }
     DBuf(const DBuf&) = delete;
     DBuf& operator=(const DBuf&) = delete;
-    DBuf(DBuf&& o) noexcept : p(o.p), n(o.n) { o.p = nullptr; o.n = 0; }
+    DBuf(DBuf&& o) noexcept : p(o.p), n(o.n), cap(o.cap) {
+        o.p = nullptr;
+        o.n = o.cap = 0;
+    }
     DBuf& operator=(DBuf&& o) noexcept {
         if (this != &o) {
             reset();
             p = o.p;
             n = o.n;
+            cap = o.cap;
             o.p = nullptr;
-            o.n = 0;
+            o.n = o.cap = 0;
         }
         return *this;
     }
     ~DBuf() { reset(); }
     void alloc(size_t count) {
         reset();
-        if (count) MHW_CK(cudaMalloc(&p, count * sizeof(T)));
+        if (count) p = static_cast<T*>(dev_alloc(count * sizeof(T), &cap));
         n = count;
     }
     void reset() {
-        if (p) cudaFree(p);
+        if (p) dev_free(p, cap);
         p = nullptr;
-        n = 0;
+        n = cap = 0;
     }
     size_t bytes() const { return n * sizeof(T); }
 };

@@ -1071,6 +1071,126 @@ void session_download_packed(Session& s, uint32_t* h_nodes, uint64_t cap_nodes, 
     if (n_nodes) *n_nodes = total;
 }
 
+// generate_walks into a packed host corpus with the D2H overlapped: the
+// active start nodes are cut into `chunks` contiguous ranges (rows of a range
+// are contiguous); chunk c is walked, packed on the device and copied to the
+// host on a second stream while chunk c+1 walks. Every chunk shares the chain
+// table (same sampler state as one launch; only the interleaving differs).
+void session_run_packed(Session& s, uint32_t* h_nodes, uint64_t cap_nodes, uint64_t* h_offsets,
+                        uint64_t cap_rows, int chunks, mhw_walk_stats* stats) {
+    DeviceGuard dg(s.g->device);
+    if (s.wc.schedule == MHW_SCHEDULE_DETERMINISTIC || s.n_act < 2 * (uint32_t)chunks || chunks < 2) {
+        session_run(s, nullptr);
+        mhw_walk_stats st{};
+        session_stats(s, st);
+        session_download_packed(s, h_nodes, cap_nodes, h_offsets, cap_rows, nullptr, nullptr);
+        if (stats) *stats = st;
+        return;
+    }
+    if (cap_rows < s.rows + 1) invalid("offset buffer too small for the corpus");
+    cudaStream_t S = s.stream, T = nullptr;
+    MHW_CK(cudaStreamCreateWithFlags(&T, cudaStreamNonBlocking));
+    std::vector<cudaEvent_t> ev(chunks, nullptr);
+    auto cleanup = [&] {
+        for (auto& e : ev)
+            if (e) cudaEventDestroy(e);
+        if (T) cudaStreamDestroy(T);
+    };
+    try {
+        for (auto& e : ev) MHW_CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        // chunk boundaries over the active-node list and their first rows
+        std::vector<uint32_t> jc(chunks + 1);
+        std::vector<uint64_t> rc(chunks + 1);
+        for (int c = 0; c <= chunks; ++c) jc[c] = (uint32_t)((uint64_t)s.n_act * c / chunks);
+        rc[0] = 0;
+        rc[chunks] = s.rows;
+        for (int c = 1; c < chunks; ++c)
+            MHW_CK(cudaMemcpy(&rc[c], s.act_row.p + jc[c], 8, cudaMemcpyDeviceToHost));
+        uint64_t max_rows = 0;
+        for (int c = 0; c < chunks; ++c) max_rows = std::max(max_rows, rc[c + 1] - rc[c]);
+        const uint64_t rowcap = (uint64_t)s.cfg.L + 1;
+        DBuf<uint32_t> packed(std::max<uint64_t>(s.rows * rowcap, 1));
+        DBuf<uint64_t> len64(s.rows + 1), goff(s.rows + 1);
+        std::vector<DBuf<uint64_t>> offc(chunks);
+        uint64_t* h_tot = nullptr;
+        MHW_CK(cudaMallocHost(&h_tot, chunks * sizeof(uint64_t)));
+        std::unique_ptr<uint64_t, decltype(&cudaFreeHost)> hold_tot(h_tot, cudaFreeHost);
+        size_t scan_bytes = 0;
+        MHW_CK(cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, len64.p, goff.p, (int64_t)s.rows + 1, S));
+        DBuf<uint8_t> scan_tmp(std::max<size_t>(scan_bytes, 1));
+        // sampler reset + isolated rows + eager init (as session_run)
+        RunParams P = s.params();
+        MHW_CK(cudaMemsetAsync(s.chain.p, 0xFF, s.chain.bytes(), S));
+        MHW_CK(cudaMemsetAsync(s.ctr.p, 0, s.ctr.bytes(), S));
+        if (s.n_iso)
+            k_iso_rows<<<grid_for((uint64_t)s.n_iso * s.cfg.K), 256, 0, S>>>(s.iso.p, s.iso_row.p, s.n_iso, s.cfg.K,
+                                                                             s.out.p, s.stride, s.lens.p);
+        MHW_CK(cudaEventRecord(s.ev0, S));
+        dispatch(s.model.dev.kind, [&](auto kc) {
+            constexpr int KIND = decltype(kc)::value;
+            if constexpr (second_order(KIND)) {
+                if (s.eager_init) k_init_all<KIND><<<grid_for(s.g->m), 256, 0, S>>>(P);
+            }
+        });
+        for (int c = 0; c < chunks; ++c) {
+            RunParams Pc = P;
+            Pc.act = s.act.p + jc[c];
+            Pc.act_row = s.act_row.p + jc[c];
+            Pc.n_act = jc[c + 1] - jc[c];
+            Pc.n_items = (uint64_t)Pc.n_act * s.cfg.K;
+            MHW_CK(cudaMemsetAsync(s.ctr.p, 0, sizeof(unsigned long long), S));  // work counter
+            dispatch(s.model.dev.kind, [&](auto kc) {
+                constexpr int KIND = decltype(kc)::value;
+                with_variant<KIND>(s.minb, !s.eager_init, s.use_ar, [&](auto rg, auto lz, auto ar) {
+                    k_walk<KIND, decltype(rg)::value, decltype(lz)::value, decltype(ar)::value>
+                        <<<s.grid, kWalkBlock, 0, S>>>(Pc);
+                });
+            });
+            // pack rows [rc[c], rc[c+1]) into packed + rc[c] * (L+1)
+            const uint64_t nr = rc[c + 1] - rc[c];
+            offc[c].alloc(nr + 1);
+            k_len64<<<grid_for(nr + 1), 256, 0, S>>>(s.lens.p + rc[c], nr, len64.p + rc[c]);
+            size_t b = scan_bytes;
+            MHW_CK(cub::DeviceScan::ExclusiveSum(scan_tmp.p, b, len64.p + rc[c], offc[c].p, (int64_t)nr + 1, S));
+            if (nr)
+                k_pack<<<grid_for(nr * 32), 256, 0, S>>>(s.out.p + rc[c] * s.stride, s.stride, offc[c].p, nr,
+                                                        packed.p + rc[c] * rowcap);
+            MHW_CK(cudaMemcpyAsync(h_tot + c, offc[c].p + nr, 8, cudaMemcpyDeviceToHost, S));
+            MHW_CK(cudaEventRecord(ev[c], S));
+        }
+        MHW_CK(cudaEventRecord(s.ev1, S));
+        MHW_CK(cudaGetLastError());
+        // copy chunk c while later chunks walk
+        uint64_t H = 0;
+        for (int c = 0; c < chunks; ++c) {
+            MHW_CK(cudaEventSynchronize(ev[c]));
+            const uint64_t tot = h_tot[c];
+            if (H + tot > cap_nodes) invalid("node buffer too small for the corpus");
+            MHW_CK(cudaStreamWaitEvent(T, ev[c], 0));
+            if (tot)
+                MHW_CK(cudaMemcpyAsync(h_nodes + H, packed.p + rc[c] * rowcap, tot * 4, cudaMemcpyDeviceToHost, T));
+            H += tot;
+        }
+        // global row offsets (one scan over all lengths) and the counters
+        k_len64<<<grid_for(s.rows + 1), 256, 0, S>>>(s.lens.p, s.rows, len64.p);
+        size_t b = scan_bytes;
+        MHW_CK(cub::DeviceScan::ExclusiveSum(scan_tmp.p, b, len64.p, goff.p, (int64_t)s.rows + 1, S));
+        MHW_CK(cudaMemcpyAsync(h_offsets, goff.p, (s.rows + 1) * 8, cudaMemcpyDeviceToHost, S));
+        MHW_CK(cudaStreamSynchronize(S));
+        MHW_CK(cudaStreamSynchronize(T));
+        s.launches = 0;
+        mhw_walk_stats st{};
+        session_stats(s, st);
+        if (stats) *stats = st;
+    } catch (...) {
+        cudaStreamSynchronize(S);
+        if (T) cudaStreamSynchronize(T);
+        cleanup();
+        throw;
+    }
+    cleanup();
+}
+
 // ------------------------------------------------------------ parity API
 void run_decide(Graph& g, const mhw_model_desc& md, uint64_t n, const uint32_t* pos, const uint32_t* aff,
                 const uint32_t* cand, const uint32_t* last, const double* u, double* wc, double* wl,

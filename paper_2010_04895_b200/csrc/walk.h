@@ -75,6 +75,8 @@ void session_run(Session& s, cudaStream_t stream);
 void session_stats(Session& s, mhw_walk_stats& out);
 void session_download(Session& s, uint32_t* nodes, uint32_t* lens, cudaStream_t stream);
 void session_write_corpus(Session& s, const char* path, const mhw_walk_stats& st);
+void session_run_packed(Session& s, uint32_t* h_nodes, uint64_t cap_nodes, uint64_t* h_offsets,
+                        uint64_t cap_rows, int chunks, mhw_walk_stats* stats);
 void session_download_packed(Session& s, uint32_t* h_nodes, uint64_t cap_nodes, uint64_t* h_offsets,
                              uint64_t cap_rows, uint64_t* n_nodes, cudaStream_t stream);
 void run_decide(Graph& g, const mhw_model_desc& md, uint64_t n, const uint32_t* pos, const uint32_t* aff,

@@ -200,6 +200,27 @@ def test_check_audit_equals_oracle(mhw, oracle, kind):
     assert code == 0
 
 
+@pytest.mark.parametrize("kind", [O.DEEPWALK, O.NODE2VEC, O.METAPATH2VEC])
+def test_packed_overlapped_throughput_corpus(mhw, kind):
+    """Throughput schedule through the chunked walk + overlapped D2H path:
+    corpus order, start nodes, edge validity, lengths and step count."""
+    from paper_2010_04895_b200.mhwalk import generate_walks_packed
+    g = typed_random_graph(81 + kind, 3000, 6.0, weighted=True, types=2)
+    md = model_desc(kind, g, p=0.5, q=2.0)
+    cfg = O.WalkCfg(K=4, L=25, seed=3)
+    nodes, offsets, st = generate_walks_packed(device_graph(g), walk_model(md), walk_config(cfg, threads=8))
+    starts = [v for v in range(g.n) if kind != O.METAPATH2VEC or g.ntype[v] == md.metapath[0]]
+    assert len(offsets) == len(starts) * cfg.K + 1
+    lens = np.diff(offsets.astype(np.int64))
+    assert lens.min() >= 1 and lens.max() <= cfg.L + 1
+    assert st.steps == int(np.sum(lens - 1))
+    adj = {(v, int(u)) for v in range(g.n) for u in g.neighbors_of(v)}
+    for r in range(len(lens)):
+        w = nodes[offsets[r]:offsets[r + 1]]
+        assert w[0] == starts[r // cfg.K]
+        assert all((int(a), int(b)) in adj for a, b in zip(w[:-1], w[1:]))
+
+
 def test_alias_tables_bit_exact(mhw, oracle):
     """Per-node alias tables == alias_build (samplers.cpp:95-131) bit for bit."""
     g = typed_random_graph(41, 500, 10.0, weighted=True)
