@@ -183,6 +183,24 @@ MHW_API mhw_status mhw_graph_generate_rmat(uint32_t scale, uint32_t edge_factor,
 MHW_API mhw_status mhw_graph_generate_hetero(uint32_t node_count, uint64_t seed, float weight_lo,
                                      float weight_hi, int32_t device, mhw_graph** out);
 
+/* Text ingestion (graph.cpp:70-177): "src dst [weight]" lines, '#'
+ * comments, parsed by all host cores with the reference loader's acceptance
+ * rules and messages (first bad line in file order: "path:LINE: expected
+ * \"src dst [weight]\"", "missing edge weight", "negative edge weight";
+ * unreadable file -> MHW_ERR_IO), then build_csr on the device. */
+MHW_API mhw_status mhw_graph_load_edge_list(const char* path, int32_t weighted, int32_t symmetrize,
+                                            int32_t device, mhw_graph** out);
+MHW_API mhw_status mhw_graph_load_node_types(mhw_graph* g, const char* path);
+MHW_API mhw_status mhw_graph_load_edge_types(mhw_graph* g, const char* path);
+/* The parse alone, on the host (no device needed): the reference's raw edge
+ * vector before build_csr (reverse arcs interleaved when symmetrize, decided
+ * on the untruncated ids, graph.cpp:94-97), library-allocated arrays released
+ * with mhw_free_host. */
+MHW_API mhw_status mhw_parse_edge_list(const char* path, int32_t weighted, int32_t symmetrize,
+                                       uint64_t* edge_count, uint32_t** src, uint32_t** dst,
+                                       double** weights);
+MHW_API void mhw_free_host(void* p);
+
 /* load_node_types / load_edge_types (graph.cpp:102-177) from arrays. */
 MHW_API mhw_status mhw_graph_set_node_types(mhw_graph* g, const uint16_t* types, uint16_t num_types);
 MHW_API mhw_status mhw_graph_set_edge_types(mhw_graph* g, const uint16_t* types, uint16_t num_types);

@@ -7,5 +7,6 @@ from .mhwalk import (  # noqa: F401
     CudaError, Graph, InitKind, InitStrategy, IoError, ModelKind, ParseError, RunStats, SamplerKind,
     Schedule, Session, ValidationError, WalkConfig, WalkCorpus, WalkModel, alias_tables, decide,
     device_count, generate_walks, generate_walks_multi, init_kind_from_string, init_states, kNoAffix,
-    load_edge_list, model_kind_from_string, partition_nodes, read_corpus, write_corpus,
+    load_edge_list, load_edge_types, load_node_types, model_kind_from_string, partition_nodes, read_corpus,
+    write_corpus,
 )

@@ -57,6 +57,11 @@ SIGNATURES = {
                                             C.c_uint64, C.c_int32, C.c_float, C.c_float, C.c_uint32,
                                             C.c_int32, _PP]),
     "mhw_graph_generate_hetero": (C.c_int32, [C.c_uint32, C.c_uint64, C.c_float, C.c_float, C.c_int32, _PP]),
+    "mhw_graph_load_edge_list": (C.c_int32, [C.c_char_p, C.c_int32, C.c_int32, C.c_int32, _PP]),
+    "mhw_graph_load_node_types": (C.c_int32, [_P, C.c_char_p]),
+    "mhw_graph_load_edge_types": (C.c_int32, [_P, C.c_char_p]),
+    "mhw_parse_edge_list": (C.c_int32, [C.c_char_p, C.c_int32, C.c_int32, C.POINTER(C.c_uint64), _PP, _PP, _PP]),
+    "mhw_free_host": (None, [_P]),
     "mhw_graph_set_node_types": (C.c_int32, [_P, _P, C.c_uint16]),
     "mhw_graph_set_edge_types": (C.c_int32, [_P, _P, C.c_uint16]),
     "mhw_graph_replicate": (C.c_int32, [_P, C.c_int32, _PP]),

@@ -13,8 +13,8 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libmhw.so")
 OBJ = os.path.join(PKG, "_obj")
-SOURCES = ["graph.cu", "walk.cu", "corpus.cu", "api.cu"]
-HEADERS = ["mhw_device.cuh", "internal.h", "walk.h"]
+SOURCES = ["graph.cu", "walk.cu", "corpus.cu", "loader.cu", "api.cu"]
+HEADERS = ["mhw_device.cuh", "internal.h", "walk.h", "loader.h"]
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -35,16 +35,23 @@ def _stale(target: str, deps: list[str]) -> bool:
 def build(force: bool = False, verbose: bool = False) -> str:
     os.makedirs(OBJ, exist_ok=True)
     hdrs = [os.path.join(CSRC, h) for h in HEADERS] + [os.path.join(ROOT, "include", "mhw.h")]
-    objs = []
+    objs, cmds = [], []
     for src in SOURCES:
         s = os.path.join(CSRC, src)
         o = os.path.join(OBJ, src.replace(".cu", ".o"))
         objs.append(o)
         if force or _stale(o, [s, *hdrs]):
-            cmd = [NVCC, *ARCH, *FLAGS, "-c", s, "-o", o]
-            if verbose:
-                print(" ".join(cmd), flush=True)
-            subprocess.run(cmd, check=True)
+            cmds.append([NVCC, *ARCH, *FLAGS, "-c", s, "-o", o])
+    # translation units compile in parallel
+    from concurrent.futures import ThreadPoolExecutor
+
+    def run(cmd):
+        if verbose:
+            print(" ".join(cmd), flush=True)
+        subprocess.run(cmd, check=True)
+
+    with ThreadPoolExecutor(max_workers=max(1, min(len(cmds), os.cpu_count() or 1))) as ex:
+        list(ex.map(run, cmds))
     if force or _stale(LIB, objs):
         # export only the C ABI: the visibility flag hides everything else,
         # the mhw_* symbols are re-exported by the version script.

@@ -11,6 +11,7 @@
 #include <vector>
 
 #include "internal.h"
+#include "loader.h"
 #include "walk.h"
 
 struct mhw_walks {
@@ -143,6 +144,73 @@ mhw_status mhw_graph_generate_hetero(uint32_t node_count, uint64_t seed, float w
     return build_graph(device, out, [&](mhw::Graph& g) {
         if (!(weight_lo >= 0 && weight_hi >= weight_lo)) mhw::invalid("bad weight range");
         mhw::graph_generate_hetero(g, node_count, seed, weight_lo, weight_hi);
+    });
+}
+
+mhw_status mhw_parse_edge_list(const char* path, int32_t weighted, int32_t symmetrize, uint64_t* n_edges,
+                               uint32_t** src, uint32_t** dst, double** weights) {
+    return guard([&] {
+        need(path, "path");
+        need(n_edges, "n_edges");
+        need(src, "src");
+        need(dst, "dst");
+        need(weights, "weights");
+        std::vector<uint32_t> s, d;
+        std::vector<double> w;
+        mhw::parse_edge_list(path, weighted != 0, symmetrize != 0, s, d, w);
+        const size_t n = s.size();
+        auto* ps = static_cast<uint32_t*>(std::malloc(std::max<size_t>(n, 1) * 4));
+        auto* pd = static_cast<uint32_t*>(std::malloc(std::max<size_t>(n, 1) * 4));
+        auto* pw = static_cast<double*>(std::malloc(std::max<size_t>(n, 1) * 8));
+        if (!ps || !pd || !pw) {
+            std::free(ps);
+            std::free(pd);
+            std::free(pw);
+            throw std::bad_alloc();
+        }
+        if (n) {
+            std::memcpy(ps, s.data(), n * 4);
+            std::memcpy(pd, d.data(), n * 4);
+            std::memcpy(pw, w.data(), n * 8);
+        }
+        *n_edges = n;
+        *src = ps;
+        *dst = pd;
+        *weights = pw;
+    });
+}
+
+void mhw_free_host(void* p) { std::free(p); }
+
+mhw_status mhw_graph_load_edge_list(const char* path, int32_t weighted, int32_t symmetrize, int32_t device,
+                                    mhw_graph** out) {
+    // parse first (host): file and format errors take precedence, as in the
+    // reference where loading precedes any walk
+    std::vector<uint32_t> s, d;
+    std::vector<double> w;
+    const mhw_status rc = guard([&] {
+        need(path, "path");
+        mhw::parse_edge_list(path, weighted != 0, symmetrize != 0, s, d, w);
+    });
+    if (rc != MHW_OK) return rc;
+    return build_graph(device, out, [&](mhw::Graph& g) { mhw::build_parsed(g, s, d, w, weighted != 0, symmetrize != 0); });
+}
+
+mhw_status mhw_graph_load_node_types(mhw_graph* g, const char* path) {
+    return guard([&] {
+        need(g, "graph");
+        need(path, "path");
+        mhw::DeviceGuard dg(g->device);
+        mhw::load_node_types(*g, path);
+    });
+}
+
+mhw_status mhw_graph_load_edge_types(mhw_graph* g, const char* path) {
+    return guard([&] {
+        need(g, "graph");
+        need(path, "path");
+        mhw::DeviceGuard dg(g->device);
+        mhw::load_edge_types(*g, path);
     });
 }
 

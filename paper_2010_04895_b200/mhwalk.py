@@ -315,38 +315,29 @@ class Graph:
 
 
 def load_edge_list(path, weighted=False, symmetrize=False, device=0) -> Graph:
-    """load_edge_list (graph.cpp:70-100): "src dst [weight]" lines, '#'
-    comments; ParseError with the line number, negative weight ->
-    ValidationError, unreadable file -> IoError."""
-    try:
-        f = open(path, "r")
-    except OSError:
-        raise IoError(f"cannot open edge list: {path}") from None
-    src, dst, ws = [], [], []
-    with f:
-        for lineno, line in enumerate(f, 1):
-            s = line.split("#", 1)[0]
-            if not s.strip():
-                continue
-            parts = s.split()
-            try:
-                a, b = int(parts[0]), int(parts[1])
-                if a < 0 or b < 0:
-                    raise ValueError
-            except (ValueError, IndexError):
-                raise ParseError(f'{path}:{lineno}: expected "src dst [weight]"') from None
-            w = 1.0
-            if weighted:
-                try:
-                    w = float(parts[2])
-                except (ValueError, IndexError):
-                    raise ParseError(f"{path}:{lineno}: missing edge weight") from None
-                if w < 0:
-                    raise ValidationError(f"{path}:{lineno}: negative edge weight")
-            src.append(a)
-            dst.append(b)
-            ws.append(w)
-    return Graph.from_edges(src, dst, ws if weighted else None, symmetrize=symmetrize, device=device)
+    """load_edge_list (graph.cpp:70-100) through the native multi-threaded
+    parser + device build_csr: "src dst [weight]" lines, '#' comments;
+    ParseError / ValidationError with "path:LINE: ..." messages, IoError for
+    an unreadable file."""
+    h = C.c_void_p()
+    rc = L.lib().mhw_graph_load_edge_list(str(path).encode(), int(weighted), int(symmetrize), device, C.byref(h))
+    if rc == 2:
+        msg = L.lib().mhw_last_error().decode()
+        if "negative" in msg:
+            raise ValidationError(msg)
+        raise ParseError(msg)
+    _check(rc)
+    return Graph(h.value, device)
+
+
+def load_node_types(graph: Graph, path):
+    """load_node_types (graph.cpp:102-135)."""
+    _check(L.lib().mhw_graph_load_node_types(graph.handle, str(path).encode()))
+
+
+def load_edge_types(graph: Graph, path):
+    """load_edge_types (graph.cpp:137-177); symmetric graphs type both directions."""
+    _check(L.lib().mhw_graph_load_edge_types(graph.handle, str(path).encode()))
 
 
 def generate_walks(graph: Graph, model: WalkModel, config: WalkConfig) -> WalkCorpus:
