@@ -111,7 +111,8 @@ def make_config(cfg, node_begin=0, node_end=0):
     import paper_2010_04895_b200 as mhw
     return mhw.WalkConfig(walks_per_node=cfg["K"], walk_length=cfg["L"], threads=8, seed=WALK_SEED,
                           init=mhw.InitStrategy(mhw.InitKind[cfg["init"]], cfg.get("burn_in", 100), 32),
-                          schedule=mhw.Schedule.throughput, node_begin=node_begin, node_end=node_end)
+                          schedule=mhw.Schedule.throughput, node_begin=node_begin, node_end=node_end,
+                          chain_replica_degree=int(os.environ.get("MHW_REP_DEG", "0")))
 
 
 class Clocks:

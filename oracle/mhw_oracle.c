@@ -686,8 +686,8 @@ static uint32_t chain_replicas(uint32_t deg, uint32_t D) {
     if (D == OG_NO_REPLICAS || deg < D) return 1;
     uint32_t q = deg / D, lg = 0;
     while (q >>= 1) ++lg;
-    const uint32_t r = 2u << lg;
-    return r < 256 ? r : 256;
+    const uint32_t r = lg < 16 ? 2u << lg : 65536u;
+    return r < 65536 ? r : 65536;
 }
 
 static uint64_t engine_slot(const og_graph* g, const og_model* m, const replica_layout_t* rl, uint32_t v,
@@ -870,7 +870,29 @@ int og_generate_walks(const og_graph* g, const og_model* m, const og_config* c, 
     rl.base = slots;
     rl.group = NULL;
     if ((m->kind == OG_DEEPWALK || m->kind == OG_METAPATH2VEC) && rl.D != OG_NO_REPLICAS) {
-        if (rl.D == 0) rl.D = 128;
+        if (rl.D == 0) {
+            /* automatic layout (walk.cu session_create): metapath2vec 128;
+             * deepwalk the smallest power-of-two D whose replica region
+             * holds at most 8M chain words */
+            rl.D = 128;
+            if (m->kind == OG_DEEPWALK) {
+                uint64_t hist[33] = {0};
+                for (uint32_t v = 0; v < g->n; ++v) {
+                    uint32_t d = deg_of(g, v), b = 0;
+                    if (!d) continue;
+                    while (d >>= 1) ++b;
+                    ++hist[b];
+                }
+                for (uint32_t lg = 0; lg < 31; ++lg) {
+                    uint64_t t = 0;
+                    for (uint32_t b = lg; b < 33; ++b) {
+                        const uint64_t r = b - lg < 16 ? (uint64_t)2 << (b - lg) : 65536;
+                        t += hist[b] * ((r < 65536 ? r : 65536) - 1);
+                    }
+                    if (t <= ((uint64_t)8 << 20)) { rl.D = 1u << lg; break; }
+                }
+            }
+        }
         rl.group = (uint32_t*)calloc((size_t)g->n + 1, sizeof(uint32_t));
         for (uint32_t v = 0; v < g->n; ++v) rl.group[v + 1] = rl.group[v] + chain_replicas(deg_of(g, v), rl.D) - 1;
         slots += (uint64_t)rl.group[g->n] * rl.G;

@@ -141,23 +141,26 @@ struct DevCfg {
     uint32_t hw;
     // node-keyed chain replication at hubs
     uint32_t rep_deg;            // nodes with degree >= rep_deg get replicas
+    uint32_t rep_max;            // replica cap (power of two)
     uint64_t rep_base_slot;      // first slot of the replica region (= n * G)
     const uint32_t* rep_group;   // per node: first replica group (hubs only)
 };
 
 constexpr uint32_t kNoReplicas = 0xFFFFFFFFu;
 constexpr uint32_t kDefaultRepDeg = 128;
-constexpr uint32_t kMaxReplicas = 256;
+constexpr uint32_t kMaxReplicas = 65536;
+constexpr uint64_t kAutoReplicaSlots = uint64_t(8) << 20;  // auto D budget (32 MB of chain words)
 
 // Chains per node-keyed state: 1 below rep_deg, else 2^(floor(log2(deg /
-// rep_deg)) + 1) capped at 256 -- about 2*deg/rep_deg concurrent chains, so a
+// rep_deg)) + 1) capped at 65536 -- about 2*deg/rep_deg concurrent chains, so a
 // hub's visitors spread over independent exact M-H chains.
-__host__ __device__ __forceinline__ uint32_t chain_replicas(uint32_t deg, uint32_t rep_deg) {
+__host__ __device__ __forceinline__ uint32_t chain_replicas(uint32_t deg, uint32_t rep_deg,
+                                                             uint32_t rep_max = kMaxReplicas) {
     if (rep_deg == kNoReplicas || deg < rep_deg) return 1;
     uint32_t q = deg / rep_deg, lg = 0;
     while (q >>= 1) ++lg;
-    const uint32_t r = 2u << lg;
-    return r < kMaxReplicas ? r : kMaxReplicas;
+    const uint32_t r = lg < 31 ? 2u << lg : 0x80000000u;
+    return r < rep_max ? r : rep_max;
 }
 
 __host__ __device__ __forceinline__ uint32_t walker_replica(uint64_t walker, uint32_t R) {
@@ -169,7 +172,7 @@ __host__ __device__ __forceinline__ uint32_t walker_replica(uint64_t walker, uin
 __device__ __forceinline__ uint64_t node_slot(const DevCfg& cfg, uint32_t G, uint32_t v, uint32_t deg,
                                               uint32_t t, uint64_t walker) {
     const uint64_t base = (uint64_t)v * G + t;
-    const uint32_t R = chain_replicas(deg, cfg.rep_deg);
+    const uint32_t R = chain_replicas(deg, cfg.rep_deg, cfg.rep_max);
     if (R == 1) return base;
     const uint32_t r = walker_replica(walker, R);
     if (r == 0) return base;

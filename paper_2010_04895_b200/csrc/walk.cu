@@ -324,11 +324,27 @@ __global__ void k_pack(const uint32_t* __restrict__ src, uint32_t stride, const 
     }
 }
 
+// Histogram of floor(log2 deg) over nodes of degree >= 1 (33 bins): with a
+// power-of-two D, chain_replicas(d, D) depends on floor(log2 d) alone, so the
+// host sizes the replica region for any D from it.
+__global__ void k_deg_log2_hist(DevGraph g, unsigned long long* __restrict__ hist) {
+    __shared__ unsigned int h[33];
+    if (threadIdx.x < 33) h[threadIdx.x] = 0;
+    __syncthreads();
+    for (uint64_t v = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; v < g.n;
+         v += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t d = load_node(g, (uint32_t)v).deg;
+        if (d) atomicAdd(&h[31 - __clz(d)], 1u);
+    }
+    __syncthreads();
+    if (threadIdx.x < 33 && h[threadIdx.x]) atomicAdd(hist + threadIdx.x, (unsigned long long)h[threadIdx.x]);
+}
+
 // Replica groups per node (chain_replicas - 1).
-__global__ void k_rep_counts(DevGraph g, uint32_t D, uint32_t* __restrict__ cnt) {
+__global__ void k_rep_counts(DevGraph g, uint32_t D, uint32_t cap, uint32_t* __restrict__ cnt) {
     for (uint64_t v = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; v < g.n;
          v += (uint64_t)gridDim.x * blockDim.x)
-        cnt[v] = chain_replicas(load_node(g, (uint32_t)v).deg, D) - 1;
+        cnt[v] = chain_replicas(load_node(g, (uint32_t)v).deg, D, cap) - 1;
 }
 
 // Rows of valid starts on isolated nodes: [v], an early termination each.
@@ -818,15 +834,50 @@ void session_create(Session& s, Graph& g, const mhw_model_desc& md, const mhw_wa
     // node-keyed models
     s.slots = k_slots(m.kind, g);
     s.cfg.rep_deg = kNoReplicas;
+    s.cfg.rep_max = kMaxReplicas;
     s.cfg.rep_base_slot = s.slots;
     s.cfg.rep_group = nullptr;
-    if (!second_order(m.kind) && wc.chain_replica_degree != kNoReplicas && g.n) {
-        const uint32_t D = wc.chain_replica_degree ? wc.chain_replica_degree : kDefaultRepDeg;
+    if (!second_order(m.kind) && wc.chain_replica_degree != kNoReplicas && g.n && g.max_deg) {
+        const uint64_t G = m.kind == METAPATH2VEC ? g.n_ntypes : 1;
+        // replica groups for power-of-two D from the log2-degree histogram
+        DBuf<unsigned long long> hist(33);
+        MHW_CK(cudaMemsetAsync(hist.p, 0, 33 * 8, st));
+        k_deg_log2_hist<<<grid_for(g.n), 256, 0, st>>>(g.view(), hist.p);
+        MHW_CK(cudaGetLastError());
+        unsigned long long hh[33];
+        MHW_CK(cudaMemcpyAsync(hh, hist.p, sizeof hh, cudaMemcpyDeviceToHost, st));
+        MHW_CK(cudaStreamSynchronize(st));
+        auto groups_for = [&](uint32_t lgD) {
+            uint64_t t = 0;
+            for (uint32_t b = lgD; b < 33; ++b) {
+                const uint64_t r = std::min<uint64_t>(uint64_t(2) << (b - lgD), s.cfg.rep_max);
+                t += hh[b] * (r - 1);
+            }
+            return t;
+        };
+        uint32_t D = wc.chain_replica_degree;
+        if (!D) {
+            // auto: metapath2vec keeps kDefaultRepDeg (its inits scan typed
+            // neighbours, so extra chains cost more than the contention they
+            // remove); deepwalk takes the smallest power-of-two D whose
+            // replica region fits kAutoReplicaSlots (L2-resident chain table)
+            D = kDefaultRepDeg;
+            if (m.kind == DEEPWALK)
+                for (uint32_t lg = 0; lg < 31; ++lg)
+                    if (groups_for(lg) * G <= kAutoReplicaSlots) { D = 1u << lg; break; }
+        }
+        if ((D & (D - 1)) == 0) {
+            uint32_t lg = 0;
+            while ((1u << lg) != D) ++lg;
+            if (groups_for(lg) > 0xFFFFFFFEull)
+                invalid("sampler layout too large: chain_replica_degree " + std::to_string(D) + " gives " +
+                        std::to_string(groups_for(lg)) + " replica groups");
+        }
         if (g.max_deg >= D) {
             DBuf<uint32_t> cnt(g.n + 1);
             s.rep_group.alloc(g.n + 1);
             MHW_CK(cudaMemsetAsync(cnt.p, 0, (g.n + 1) * 4, st));
-            k_rep_counts<<<grid_for(g.n), 256, 0, st>>>(g.view(), D, cnt.p);
+            k_rep_counts<<<grid_for(g.n), 256, 0, st>>>(g.view(), D, s.cfg.rep_max, cnt.p);
             MHW_CK(cudaGetLastError());
             size_t bytes = 0;
             MHW_CK(cub::DeviceScan::ExclusiveSum(nullptr, bytes, cnt.p, s.rep_group.p, (int64_t)g.n + 1, st));
@@ -835,7 +886,6 @@ void session_create(Session& s, Graph& g, const mhw_model_desc& md, const mhw_wa
             uint32_t groups = 0;
             MHW_CK(cudaMemcpyAsync(&groups, s.rep_group.p + g.n, 4, cudaMemcpyDeviceToHost, st));
             MHW_CK(cudaStreamSynchronize(st));
-            const uint64_t G = m.kind == METAPATH2VEC ? g.n_ntypes : 1;
             s.cfg.rep_deg = D;
             s.cfg.rep_group = s.rep_group.p;
             s.slots += (uint64_t)groups * G;

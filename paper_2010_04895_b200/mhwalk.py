@@ -152,7 +152,7 @@ class WalkConfig:
     schedule: Schedule | None = None   # None: derived from threads
     node_begin: int = 0
     node_end: int = 0
-    chain_replica_degree: int = 0      # 0: 256; 0xFFFFFFFF: one chain per state
+    chain_replica_degree: int = 0      # 0: auto; 0xFFFFFFFF: one chain per state
     init_mode: int = 0                 # 0 auto, 1 lazy, 2 eager
 
     def _c(self):

@@ -101,7 +101,7 @@ def test_deterministic_walks_equal_oracle(mhw, oracle, kind, init):
 
 
 @pytest.mark.parametrize("kind", [O.DEEPWALK, O.METAPATH2VEC])
-@pytest.mark.parametrize("rep", [4, 16])
+@pytest.mark.parametrize("rep", [0, 1, 4, 16])
 def test_deterministic_hub_replicas_equal_oracle(mhw, oracle, kind, rep):
     """Node-keyed chains replicated at hubs (degree >= rep): same layout and
     walker->replica map on both sides, corpus byte-identical."""

@@ -326,12 +326,14 @@ def test_throughput_transitions_pass_chain_chi_square(mhw, oracle, kind):
     assert ok_c, "control: " + msg_c
 
 
-def test_hub_replicas_pass_chain_chi_square(mhw, oracle):
-    """Deepwalk on a hub-heavy graph with replicated hub chains."""
+@pytest.mark.parametrize("rep", [8, 1, 0])
+def test_hub_replicas_pass_chain_chi_square(mhw, oracle, rep):
+    """Deepwalk on a hub-heavy graph with replicated hub chains (8, every
+    node (1), and the automatic layout (0))."""
     rng = O.XoRng(12)
     g = O.preferential_attachment(60, 3, rng)
     md = model_desc(O.DEEPWALK, g)
-    cfg = O.WalkCfg(K=300, L=80, seed=5, replica_degree=8)
+    cfg = O.WalkCfg(K=300, L=80, seed=5, replica_degree=rep)
     c = mhw.generate_walks(device_graph(g), walk_model(md), walk_config(cfg, threads=8))
     ok, msg = gate(audit(g, oracle, md, c.rows, c.lengths, min_visits=5000))
     assert ok, msg
