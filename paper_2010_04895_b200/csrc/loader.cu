@@ -58,7 +58,6 @@ inline bool blank_or_comment(const char* b, const char* e) {
 // istream >> long long: skip whitespace, optional sign, digits (overflow fails).
 inline bool read_ll(const char*& p, const char* e, long long& out) {
     while (p < e && is_space(*p)) ++p;
-    const char* s = p;
     bool neg = false;
     if (p < e && (*p == '+' || *p == '-')) {
         neg = *p == '-';
@@ -72,7 +71,6 @@ inline bool read_ll(const char*& p, const char* e, long long& out) {
         v = v * 10 + d;
         ++p;
     }
-    (void)s;
     out = neg ? -(long long)v : (long long)v;
     return true;
 }

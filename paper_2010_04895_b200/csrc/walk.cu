@@ -52,11 +52,16 @@ __device__ __noinline__ uint32_t init_slot_ool(const DevGraph g, const DevModel 
 // ------------------------------------------------------ throughput kernel
 // LAZY = false: every slot was initialised by k_init_all before the launch,
 // so the lazy-init call (and the registers the call ABI pins) is compiled out.
-// AR = true: arc records (deepwalk: aux = weight, node2vec: aux = rev) replace
-// the id / node-record / weight / reverse-arc loads of a step.
+// AR = true: arc records replace the id / node-record / weight loads of a
+// step. deepwalk: graph records, aux = weight. node2vec: the session's
+// records, aux = the chain word of the state entered through that arc
+// (colocated chains: the chain word a step locks sits in the sector the
+// previous step loaded as its candidate record, so the lock is an L2 hit).
 template <int KIND, int REGS, bool LAZY, bool AR>
 __global__ void __launch_bounds__(kWalkBlock) __maxnreg__(REGS) k_walk(RunParams P) {
     const DevGraph& g = P.g;
+    constexpr bool CC = AR && KIND == NODE2VEC;
+    const uint4* const arcs = CC ? P.ac : g.arc;
     const uint2 wkey = philox_key(P.cfg.seed, DOM_WALK);
     const uint32_t K = P.cfg.K, L = P.cfg.L;
     const unsigned lane = threadIdx.x & 31;
@@ -93,6 +98,7 @@ __global__ void __launch_bounds__(kWalkBlock) __maxnreg__(REGS) k_walk(RunParams
         c.boot = second_order(KIND);
         uint32_t affix = 0;
         uint64_t slot = 0;
+        uint64_t loc = 0;  // CC: forward arc s->v holding the chain word of state (s, v)
         if (KIND == METAPATH2VEC) c.req = P.m.metapath[metapath_next(P.m, 0)];
         if (!second_order(KIND)) slot = slot_of<KIND>(P.m, P.cfg, c, 0, walker);
         uint32_t len = 1;
@@ -105,7 +111,7 @@ __global__ void __launch_bounds__(kWalkBlock) __maxnreg__(REGS) k_walk(RunParams
             }
             Draw d;
             d.open(wkey, walker, step);
-            uint32_t chosen, next, back_c = 0, back_l = 0;
+            uint32_t chosen, next, back_c = 0;
             NodeRec rn;
             if (second_order(KIND) && c.boot) {
                 if (!bootstrap_pick(g, c, d.unit(), &chosen)) {
@@ -113,10 +119,10 @@ __global__ void __launch_bounds__(kWalkBlock) __maxnreg__(REGS) k_walk(RunParams
                     break;
                 }
                 if constexpr (AR) {
-                    const uint4 a = __ldg(g.arc + c.off + chosen);
+                    const uint4 a = __ldg(arcs + c.off + chosen);
                     next = a.x;
                     rn = arc_node(a);
-                    back_c = a.w;
+                    if (!CC) back_c = a.w;
                 } else {
                     next = load_id(g, c.off + chosen);
                     rn = load_node(g, next);
@@ -133,7 +139,8 @@ __global__ void __launch_bounds__(kWalkBlock) __maxnreg__(REGS) k_walk(RunParams
                 // (its timing cannot depend on the proposal); the candidate
                 // evaluation overlaps its latency, and the chain state it
                 // returns is only consumed by the decision.
-                uint32_t e = atomicExch(P.chain + slot, kLocked);
+                uint32_t* const cw = CC ? reinterpret_cast<uint32_t*>(P.ac + loc) + 3 : P.chain + slot;
+                uint32_t e = atomicExch(cw, kLocked);
                 const uint32_t cand = d.index(c.deg);
                 const double u = d.unit();
                 uint32_t uc;
@@ -141,7 +148,7 @@ __global__ void __launch_bounds__(kWalkBlock) __maxnreg__(REGS) k_walk(RunParams
                 NodeRec rc{};
                 bool rc_early;
                 if constexpr (AR) {
-                    ac = __ldg(g.arc + c.off + cand);
+                    ac = __ldg(arcs + c.off + cand);
                     uc = ac.x;
                     rc = arc_node(ac);
                     rc_early = true;
@@ -164,11 +171,13 @@ __global__ void __launch_bounds__(kWalkBlock) __maxnreg__(REGS) k_walk(RunParams
                         ++retries;
                         __nanosleep(ns);
                         ns = ns < 512 ? ns * 2 : 512;
-                        e = atomicExch(P.chain + slot, kLocked);
+                        e = atomicExch(cw, kLocked);
                     } while (e == kLocked);
                 }
                 if (e == kEmpty) {
                     if constexpr (LAZY) {
+                        // CC: slot id of (s, v) = off(v) + index of s in N(v)
+                        if (CC) slot = (uint64_t)c.off + __ldg(g.rev + loc);
                         e = init_slot<KIND>(g, P.m, P.cfg, c, slot);
                         ++inits;
                     } else {
@@ -177,7 +186,7 @@ __global__ void __launch_bounds__(kWalkBlock) __maxnreg__(REGS) k_walk(RunParams
                     }
                 }
                 if (e == kDead) {
-                    chain_release(P.chain + slot, kDead);
+                    chain_release(cw, kDead);
                     dead = true;
                     break;
                 }
@@ -193,7 +202,7 @@ __global__ void __launch_bounds__(kWalkBlock) __maxnreg__(REGS) k_walk(RunParams
                 uint4 al = make_uint4(0, 0, 0, 0);
                 if (kSpec) {
                     if constexpr (AR) {
-                        al = __ldg(g.arc + c.off + last);
+                        al = __ldg(arcs + c.off + last);
                         ul = al.x;
                         rl = arc_node(al);
                     } else {
@@ -204,13 +213,13 @@ __global__ void __launch_bounds__(kWalkBlock) __maxnreg__(REGS) k_walk(RunParams
                 const double wl = (AR && KIND == DEEPWALK) ? (double)__uint_as_float(al.w)
                                                           : wprime<KIND>(g, P.m, c, last, rl.type, cls_l);
                 const bool acc = mh_accept(wc, wl, u) && cand != last;
-                chain_release(P.chain + slot, acc ? pack_entry(cand, cls_c) : e);
+                chain_release(cw, acc ? pack_entry(cand, cls_c) : e);
                 chosen = acc ? cand : last;
                 if constexpr (AR) {
-                    const uint4 an = (acc || cand == last) ? ac : (kSpec ? al : __ldg(g.arc + c.off + last));
+                    const uint4 an = (acc || cand == last) ? ac : (kSpec ? al : __ldg(arcs + c.off + last));
                     next = an.x;
                     rn = arc_node(an);
-                    back_c = an.w;
+                    if (!CC) back_c = an.w;
                 } else {
                     if (acc || cand == last) {
                         next = uc;
@@ -245,18 +254,23 @@ __global__ void __launch_bounds__(kWalkBlock) __maxnreg__(REGS) k_walk(RunParams
                 c.req = P.m.metapath[metapath_next(P.m, affix)];
                 slot = node_slot(P.cfg, P.m.num_types, next, rn.deg, c.req, walker);
             } else {
-                const uint32_t back = back_c;  // rev[off(v) + chosen], fetched above
+                // rev[off(v) + chosen], fetched above (CC: only checked on a
+                // graph not verified symmetric; the chain word is located by
+                // the forward arc itself)
+                uint32_t back = back_c;
+                if (CC) back = g.verified_sym ? 0u : __ldg(g.rev + c.off + chosen);
                 if (back == kNoBack) {
                     fail_back_edge(P.ctr, next, c.v);
                     dead = true;
                     break;
                 }
                 if (KIND == EDGE2VEC) c.in_type = edge_type_of(g, c.off + chosen, c.vtype, rn.type);
+                if (CC) loc = (uint64_t)c.off + chosen;
                 c.s = c.v;
                 c.off_s = c.off;
                 c.deg_s = c.deg;
                 c.boot = false;
-                slot = (uint64_t)rn.off + back;
+                if (!CC) slot = (uint64_t)rn.off + back;
             }
             c.v = next;
             c.off = rn.off;
@@ -297,10 +311,33 @@ __global__ void __launch_bounds__(256) k_init_all(RunParams P) {
         const NodeRec r = load_node(g, lo);
         const uint32_t affix = (uint32_t)(a - (uint64_t)r.off);
         const SCtx c = make_ctx<KIND>(g, P.m, lo, affix);
-        P.chain[a] = init_slot<KIND>(g, P.m, P.cfg, c, a);
+        const uint32_t e = init_slot<KIND>(g, P.m, P.cfg, c, a);
+        if (P.ac) {
+            // colocated: the word lives in the record of the forward arc s->v
+            const uint32_t sv = __ldg(g.rev + a);  // index of v in N(s)
+            if (sv != kNoBack) reinterpret_cast<uint32_t*>(P.ac + c.off_s + sv)[3] = e;
+        } else {
+            P.chain[a] = e;
+        }
         ++inits;
     }
     if (inits) atomicAdd(&P.ctr[3], inits);
+}
+
+// Session arc records for colocated chains: {id, deg | allpos << 31, off,
+// chain word}; k_ac_reset empties the chain words before a lazy run.
+__global__ void k_arc_chain(DevGraph g, uint4* __restrict__ out) {
+    for (uint64_t a = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; a < g.m;
+         a += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t u = load_id(g, a);
+        const NodeRec r = load_node(g, u);
+        out[a] = make_uint4(u, r.deg | ((r.flags & NF_ALLPOS) ? 0x80000000u : 0u), (uint32_t)r.off, kEmpty);
+    }
+}
+
+__global__ void k_ac_reset(uint4* __restrict__ ac, uint64_t m) {
+    for (uint64_t a = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; a < m; a += (uint64_t)gridDim.x * blockDim.x)
+        reinterpret_cast<uint32_t*>(ac + a)[3] = kEmpty;
 }
 
 // Packed corpus: widen lengths for the 64-bit offset scan, then one warp per
@@ -924,11 +961,11 @@ void session_create(Session& s, Graph& g, const mhw_model_desc& md, const mhw_wa
     s.rows = (uint64_t)n_valid * s.cfg.K;
     s.skipped = (uint64_t)(span - n_valid) * s.cfg.K;
     s.n_items = (uint64_t)s.n_act * s.cfg.K;
-    s.chain.alloc(std::max<uint64_t>(s.slots, 1));
     s.out.alloc(std::max<uint64_t>(s.rows * s.stride, 4));
     s.lens.alloc(std::max<uint64_t>(s.rows, 1));
     s.ctr.alloc(8);
     if (wc.schedule == MHW_SCHEDULE_DETERMINISTIC) {
+        s.chain.alloc(std::max<uint64_t>(s.slots, 1));
         const uint64_t n = std::max<uint64_t>(s.n_items, 1);
         if (s.n_items > 0xFFFFFFFFull) invalid("deterministic schedule supports at most 2^32 walkers");
         s.d_v.alloc(n);
@@ -960,8 +997,24 @@ void session_create(Session& s, Graph& g, const mhw_model_desc& md, const mhw_wa
         // arc records (after the session buffers, so the memory check sees them)
         const char* ar_env = std::getenv("MHW_ARC_RECORDS");
         const bool want_ar = !(ar_env && ar_env[0] == '0');
-        if (want_ar && (m.kind == DEEPWALK || m.kind == NODE2VEC))
-            s.use_ar = graph_ensure_arcrec(g, m.kind == NODE2VEC ? ARC_AUX_REV : ARC_AUX_WEIGHT);
+        if (want_ar && m.kind == NODE2VEC && g.m && g.m < (1ull << 32)) {
+            // colocated chains: the session's arc records carry the chain words
+            size_t free_b = 0, total_b = 0;
+            MHW_CK(cudaMemGetInfo(&free_b, &total_b));
+            if (free_b < 16 * g.m + (2ull << 30)) {
+                dev_trim();
+                MHW_CK(cudaMemGetInfo(&free_b, &total_b));
+            }
+            if (free_b >= 16 * g.m + (2ull << 30)) {
+                s.ac.alloc(g.m);
+                k_arc_chain<<<grid_for(g.m), 256, 0, st>>>(g.view(), s.ac.p);
+                MHW_CK(cudaGetLastError());
+                s.use_ar = true;
+            }
+        }
+        if (!s.ac.n) s.chain.alloc(std::max<uint64_t>(s.slots, 1));
+        else s.chain.alloc(1);
+        if (want_ar && m.kind == DEEPWALK) s.use_ar = graph_ensure_arcrec(g, ARC_AUX_WEIGHT);
         dispatch(m.kind, [&](auto kc) {
             constexpr int KIND = decltype(kc)::value;
             with_variant<KIND>(s.minb, !s.eager_init, s.use_ar, [&](auto rg, auto lz, auto ar) {
@@ -988,6 +1041,7 @@ RunParams Session::params() const {
     P.n_act = n_act;
     P.n_items = n_items;
     P.chain = chain.p;
+    P.ac = ac.n ? ac.p : nullptr;
     P.out = out.p;
     P.stride = stride;
     P.lens = lens.p;
@@ -1002,6 +1056,10 @@ void session_run(Session& s, cudaStream_t user) {
     s.launches = 0;
     MHW_CK(cudaMemsetAsync(s.chain.p, 0xFF, s.chain.bytes(), st));
     MHW_CK(cudaMemsetAsync(s.ctr.p, 0, s.ctr.bytes(), st));
+    if (s.ac.n && (!s.eager_init || !s.g->verified_sym)) {
+        k_ac_reset<<<grid_for(s.ac.n), 256, 0, st>>>(s.ac.p, s.ac.n);
+        ++s.launches;
+    }
     if (s.n_iso) {
         k_iso_rows<<<grid_for((uint64_t)s.n_iso * s.cfg.K), 256, 0, st>>>(s.iso.p, s.iso_row.p, s.n_iso, s.cfg.K,
                                                                           s.out.p, s.stride, s.lens.p);
@@ -1172,6 +1230,8 @@ void session_run_packed(Session& s, uint32_t* h_nodes, uint64_t cap_nodes, uint6
         RunParams P = s.params();
         MHW_CK(cudaMemsetAsync(s.chain.p, 0xFF, s.chain.bytes(), S));
         MHW_CK(cudaMemsetAsync(s.ctr.p, 0, s.ctr.bytes(), S));
+        if (s.ac.n && (!s.eager_init || !s.g->verified_sym))
+            k_ac_reset<<<grid_for(s.ac.n), 256, 0, S>>>(s.ac.p, s.ac.n);
         if (s.n_iso)
             k_iso_rows<<<grid_for((uint64_t)s.n_iso * s.cfg.K), 256, 0, S>>>(s.iso.p, s.iso_row.p, s.n_iso, s.cfg.K,
                                                                              s.out.p, s.stride, s.lens.p);

@@ -15,6 +15,8 @@ struct RunParams {
     uint32_t n_act;
     uint64_t n_items;         // n_act * K walkers
     uint32_t* chain;          // one packed Last word per state slot
+    uint4* ac;                // node2vec throughput: arc records whose .w is the chain
+                              // word of the state entered through that arc (else null)
     uint32_t* out;            // rows x stride walk buffer
     uint32_t stride;
     uint32_t* lens;
@@ -47,6 +49,7 @@ struct Session {
     uint64_t n_items = 0, rows = 0, skipped = 0, slots = 0;
     uint32_t stride = 0;
     DBuf<uint32_t> chain, out, lens, rep_group;
+    DBuf<uint4> ac;          // arc records + colocated chain words (node2vec throughput)
     DBuf<unsigned long long> ctr;
     // deterministic schedule scratch
     DBuf<uint32_t> d_v, d_aff, d_len, d_idx, d_idx2, d_cand, d_chosen;

@@ -5,7 +5,12 @@ import sys
 
 rows = list(csv.reader(open(sys.argv[1])))
 hdr = rows[1]
-data = [dict(zip(hdr, r)) for r in rows[2:] if len(r) == len(hdr)]
+data = []
+for r in rows[2:]:
+    if r and r[0] == "Kernel Name":
+        break  # first kernel of the capture only
+    if len(r) == len(hdr) and r != hdr:
+        data.append(dict(zip(hdr, r)))
 num = lambda d, k: float(d.get(k, "0").replace(",", "") or 0)
 tot_s = sum(num(d, "Warp Stall Sampling (All Samples)") for d in data)
 tot_l2 = sum(num(d, "L2 Theoretical Sectors Global") for d in data)
