@@ -112,7 +112,8 @@ def make_config(cfg, node_begin=0, node_end=0):
     return mhw.WalkConfig(walks_per_node=cfg["K"], walk_length=cfg["L"], threads=8, seed=WALK_SEED,
                           init=mhw.InitStrategy(mhw.InitKind[cfg["init"]], cfg.get("burn_in", 100), 32),
                           schedule=mhw.Schedule.throughput, node_begin=node_begin, node_end=node_end,
-                          chain_replica_degree=int(os.environ.get("MHW_REP_DEG", "0")))
+                          chain_replica_degree=int(os.environ.get("MHW_REP_DEG", "0")),
+                          sampler_kind=mhw.SamplerKind[cfg.get("sampler", "mh")])
 
 
 class Clocks:
@@ -355,6 +356,8 @@ def run_mine(args, cfg):
         roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                 "traffic": traffic, "peak_source": peak_kind, "sectors_per_step": S, "E_sigma": es,
                 "kernel": "k_walk<%s>" % cfg["model"], "kernel_ms": kernel_ms}
+        if cfg.get("sampler", "mh") != "mh":
+            roof = None  # the canonical sector count is the M-H path's
         line = {
             "metric": METRIC, "value": value, "unit": "steps/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1e3 * t_job / args.steps, "higher_is_better": True,
@@ -363,6 +366,7 @@ def run_mine(args, cfg):
             "config": {"workload": cfg["workload"], "config": cfg["name"], "nodes": info["node_count"],
                        "arcs": info["arc_count"], "walks": st.walks, "steps_per_run": st.steps,
                        "slot_inits": st.slot_inits, "chain_retries": st.chain_retries,
+                       "sampler": cfg.get("sampler", "mh"), "rejection_trials": st.rejection_trials,
                        "seed": SEED, "walk_seed": WALK_SEED,
                        "l2": "explicit 256 MB L2 flush between timed steps (also inputs > L2)",
                        "parallelism": f"walker ranges x{world}, CSR replicated"},
@@ -472,9 +476,14 @@ def main():
     ap.add_argument("--impl", default="mine", choices=["mine", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true", help="skip the host-buffer e2e leg")
+    ap.add_argument("--sampler", default="mh", choices=["mh", "alias", "direct", "rejection"],
+                    help="exact baseline samplers of next_edge (engine.cpp:88-116) for comparison")
     args = ap.parse_args()
     cfg = dict(CONFIGS[args.config])
     cfg["name"] = args.config
+    cfg["sampler"] = args.sampler
+    if args.sampler != "mh":
+        args.no_cpu_baseline = True  # the CPU arm times the M-H path
     if args.impl == "reference":
         run_reference(args, cfg)
     else:

@@ -51,8 +51,10 @@ typedef enum {
 /* InitStrategy::Kind order, samplers.hpp:30 */
 typedef enum { MHW_INIT_RANDOM = 0, MHW_INIT_HIGH_WEIGHT = 1, MHW_INIT_BURN_IN = 2 } mhw_init_kind;
 
-/* SamplerKind order, engine.hpp:12. Only MHW_SAMPLER_MH is the product path;
- * the baseline samplers are rejected with MHW_ERR_INVALID. */
+/* SamplerKind order, engine.hpp:14. MHW_SAMPLER_MH is the product path; the
+ * exact baselines of next_edge (engine.cpp:88-116) run one warp per walker
+ * (alias: per-state tables, 12 B x sum of state degrees of device memory or
+ * MHW_ERR_INVALID; direct: inverse CDF; rejection: static alias proposal). */
 typedef enum {
     MHW_SAMPLER_MH = 0,
     MHW_SAMPLER_ALIAS = 1,
@@ -134,6 +136,7 @@ typedef struct mhw_walk_stats {
     double steps_per_sec;
     double init_seconds;
     double walk_seconds;
+    uint64_t rejection_trials; /* rejection sampler: proposals drawn */
 } mhw_walk_stats;
 
 typedef struct mhw_graph_info {

@@ -112,6 +112,7 @@ void og_philox_key(uint64_t seed, uint32_t domain, uint32_t key[2]) {
 #define DOM_WEIGHT 0x3E1647u
 #define DOM_ETYPE  0x7E7E0003u
 #define DOM_HETERO 0x4E7E0004u
+#define DOM_REJECT 0x2E1EC705u
 
 /* One "transition block": the draws of one M-H transition / one init pick.
  * xoshiro: sequential stream (reference). philox: block (id, blk) gives
@@ -139,6 +140,14 @@ static void draw_open(draw_t* d, int philox, xo_t* xo, const uint32_t key[2], ui
     d->ctr[3] = 0;
     og_philox4x32_10(d->ctr, d->key, d->w);
     d->rpos = 3;
+}
+/* block (id, blk) with sub-counter ctr[3] = sub (rejection trials) */
+static void draw_open_sub(draw_t* d, int philox, xo_t* xo, const uint32_t key[2], uint64_t id,
+                          uint32_t blk, uint32_t sub) {
+    draw_open(d, philox, xo, key, id, blk);
+    if (!philox) return;
+    d->ctr[3] = sub;
+    og_philox4x32_10(d->ctr, d->key, d->w);
 }
 static uint32_t draw_retry_word(draw_t* d) {
     if (d->rpos == 4) {
@@ -673,7 +682,7 @@ static inline uint64_t slot_index(const og_graph* g, const og_model* m, uint32_t
 }
 
 /* Engine chain layout: node-keyed states of hub nodes (degree >= D) own
- * R = 2^(floor(log2(deg/D))+1) <= 256 chains; walker w uses chain
+ * R = 2^(floor(log2(deg/D))+1) <= 65536 chains; walker w uses chain
  * (w * golden >> 40) & (R-1); chains 1..R-1 live after the n*G base slots. */
 typedef struct {
     uint32_t D;
@@ -787,8 +796,119 @@ typedef struct {
 
 /* One walker step = WalkerContext::next_edge (engine.cpp:75-87) + the push and
  * update_state of engine.cpp:201-204. Returns 1 stepped, 0 dead end, -1 error. */
+/* ---- exact baseline samplers (WalkerContext::next_edge, engine.cpp:88-116) */
+typedef struct {
+    double* wbuf;                  /* max_deg dynamic weights */
+    uint8_t* astat;                /* alias: per reference slot, 0 none 1 built */
+    double** aprob;
+    uint32_t** aalias;
+    uint8_t* pstat;                /* rejection: per node static proposal */
+    double** pprob;
+    uint32_t** palias;
+    double bound;
+} baseline_t;
+
+/* rejection_bound, engine.cpp:39-58 */
+static double rejection_bound(const og_model* m) {
+    double alpha_max = 1.0;
+    if (1.0 / m->p > alpha_max) alpha_max = 1.0 / m->p;
+    if (1.0 / m->q > alpha_max) alpha_max = 1.0 / m->q;
+    switch (m->kind) {
+    case OG_DEEPWALK:
+    case OG_METAPATH2VEC: return 1.0;
+    case OG_NODE2VEC:
+    case OG_FAIRWALK: return alpha_max;
+    default: {
+        double m_max = 0.0;
+        for (uint32_t i = 0; i < m->M_dim * m->M_dim; ++i) if (m->M[i] > m_max) m_max = m->M[i];
+        return alpha_max * m_max;
+    }
+    }
+}
+
+/* dynamic_weights (engine.cpp:120-127); returns the std::accumulate total */
+static double dyn_weights(const og_graph* g, const og_model* m, uint32_t v, uint32_t affix, double* w) {
+    const uint32_t deg = deg_of(g, v);
+    double total = 0.0;
+    for (uint32_t i = 0; i < deg; ++i) {
+        w[i] = og_weight(g, m, v, affix, i);
+        total += w[i];
+    }
+    return total;
+}
+
+/* alias_sample, samplers.hpp:65-68 */
+static uint32_t alias_draw(const double* prob, const uint32_t* alias, uint32_t n, draw_t* d) {
+    const uint32_t i = draw_index(d, n);
+    return draw_real(d) < prob[i] ? i : alias[i];
+}
+
+/* One next_edge of the alias / direct / rejection sampler. Philox layout:
+ * direct -> unit of the walk block; alias -> index + unit of the walk block;
+ * rejection trial t -> block (walker, step) of DOM_REJECT with sub-counter
+ * t<<16 (index + unit of the proposal), then sub (t<<16)|0x8000 (the accept
+ * unit). 1 stepped, 0 dead end, -1 error. */
+static int baseline_step(const og_graph* g, const og_model* m, const og_config* c, baseline_t* bt,
+                         const walker_t* w, uint32_t step, draw_t* d, uint32_t* edge, og_stats* st,
+                         char* err, size_t errlen) {
+    const uint32_t v = w->v, deg = deg_of(g, v);
+    const int philox = c->rng == OG_RNG_PHILOX;
+    if (c->sampler == OG_SAMPLER_DIRECT) {
+        if (dyn_weights(g, m, v, w->affix, bt->wbuf) <= 0) return 0;
+        *edge = og_direct_sample_u(deg, bt->wbuf, draw_real(d));
+        return 1;
+    }
+    if (c->sampler == OG_SAMPLER_ALIAS) {
+        const uint64_t slot = slot_index(g, m, v, w->affix);
+        if (!bt->astat[slot]) {
+            if (dyn_weights(g, m, v, w->affix, bt->wbuf) <= 0) return 0;
+            bt->aprob[slot] = (double*)malloc(deg * sizeof(double));
+            bt->aalias[slot] = (uint32_t*)malloc(deg * sizeof(uint32_t));
+            if (og_alias_build(deg, bt->wbuf, bt->aprob[slot], bt->aalias[slot]) != OG_OK) {
+                snprintf(err, errlen, "alias_build: negative weight");
+                return -1;
+            }
+            bt->astat[slot] = 1;
+        }
+        *edge = alias_draw(bt->aprob[slot], bt->aalias[slot], deg, d);
+        return 1;
+    }
+    /* rejection: static proposal per node (engine.cpp:136-146) */
+    const double* ws = g->w + g->offsets[v];
+    if (!bt->pstat[v]) {
+        double total = 0.0;
+        for (uint32_t i = 0; i < deg; ++i) total += ws[i];
+        if (total <= 0) return 0;
+        bt->pprob[v] = (double*)malloc(deg * sizeof(double));
+        bt->palias[v] = (uint32_t*)malloc(deg * sizeof(uint32_t));
+        og_alias_build(deg, ws, bt->pprob[v], bt->palias[v]);
+        bt->pstat[v] = 1;
+    }
+    if (dyn_weights(g, m, v, w->affix, bt->wbuf) <= 0) return 0;
+    /* rejection_sample, samplers.cpp:148-170 */
+    for (uint32_t i = 0; i < deg; ++i) {
+        if (bt->wbuf[i] > bt->bound * ws[i]) {
+            snprintf(err, errlen, "rejection_sample: envelope violated at index %u", i);
+            return -1;
+        }
+    }
+    uint32_t rkey[2];
+    og_philox_key(c->seed, DOM_REJECT, rkey);
+    for (uint32_t t = 0;; ++t) {
+        st->trials++;
+        draw_t a;
+        draw_open_sub(&a, philox, d->xo, rkey, w->walker, step, t << 16);
+        const uint32_t i = alias_draw(bt->pprob[v], bt->palias[v], deg, &a);
+        const double accept = bt->wbuf[i] / (bt->bound * ws[i]);
+        if (accept >= 1.0) { *edge = i; return 1; }
+        draw_t b;
+        draw_open_sub(&b, philox, d->xo, rkey, w->walker, step, (t << 16) | 0x8000u);
+        if (draw_real(&b) < accept) { *edge = i; return 1; }
+    }
+}
+
 static int walker_step(const og_graph* g, const og_model* m, const og_config* c, chain_t* ch,
-                       const replica_layout_t* rl, walker_t* w, uint32_t step, uint32_t stride,
+                       const replica_layout_t* rl, baseline_t* bt, walker_t* w, uint32_t step, uint32_t stride,
                        uint32_t* rows, og_stats* st, char* err, size_t errlen) {
     const uint32_t v = w->v;
     const uint32_t deg = deg_of(g, v);
@@ -806,6 +926,9 @@ static int walker_step(const og_graph* g, const og_model* m, const og_config* c,
         for (uint32_t i = 0; i < deg; ++i) total += ws[i];
         if (total <= 0) return 0;
         edge = og_direct_sample_u(deg, ws, draw_real(&d));
+    } else if (c->sampler != OG_SAMPLER_MH) {
+        const int r = baseline_step(g, m, c, bt, w, step, &d, &edge, st, err, errlen);
+        if (r <= 0) return r;
     } else {
         /* SamplerManager::sample, manager.cpp:30-72 */
         const uint64_t slot = engine_slot(g, m, rl, v, w->affix, w->walker);
@@ -903,6 +1026,21 @@ int og_generate_walks(const og_graph* g, const og_model* m, const og_config* c, 
     chain_t ch;
     ch.status = (uint8_t*)calloc(slots ? slots : 1, 1);
     ch.last = (uint32_t*)calloc(slots ? slots : 1, sizeof(uint32_t));
+    baseline_t bt;
+    memset(&bt, 0, sizeof(bt));
+    if (c->sampler != OG_SAMPLER_MH) {
+        uint32_t max_deg = 1;
+        for (uint32_t v = 0; v < g->n; ++v) if (deg_of(g, v) > max_deg) max_deg = deg_of(g, v);
+        const uint64_t rs = og_slot_count(g, m);
+        bt.wbuf = (double*)malloc(max_deg * sizeof(double));
+        bt.astat = (uint8_t*)calloc(rs ? rs : 1, 1);
+        bt.aprob = (double**)calloc(rs ? rs : 1, sizeof(double*));
+        bt.aalias = (uint32_t**)calloc(rs ? rs : 1, sizeof(uint32_t*));
+        bt.pstat = (uint8_t*)calloc(g->n ? g->n : 1, 1);
+        bt.pprob = (double**)calloc(g->n ? g->n : 1, sizeof(double*));
+        bt.palias = (uint32_t**)calloc(g->n ? g->n : 1, sizeof(uint32_t*));
+        bt.bound = rejection_bound(m);
+    }
     const uint64_t total = (uint64_t)g->n * c->K;
     int rc = OG_OK;
     uint64_t row = 0;
@@ -923,7 +1061,7 @@ int og_generate_walks(const og_graph* g, const og_model* m, const og_config* c, 
             rows[w.row * stride] = w.v;
             w.len = 1;
             for (uint32_t step = 0; step < c->L; ++step) {
-                const int r = walker_step(g, m, c, &ch, &rl, &w, step, stride, rows, stats, err, errlen);
+                const int r = walker_step(g, m, c, &ch, &rl, &bt, &w, step, stride, rows, stats, err, errlen);
                 if (r < 0) { rc = OG_ERR_INVALID; break; }
                 if (r == 0) { stats->early++; break; }
             }
@@ -954,7 +1092,7 @@ int og_generate_walks(const og_graph* g, const og_model* m, const og_config* c, 
             for (uint64_t i = 0; i < nw; ++i) {
                 walker_t* w = &ws[i];
                 if (!w->alive) continue;
-                const int r = walker_step(g, m, c, &ch, &rl, w, step, stride, rows, stats, err, errlen);
+                const int r = walker_step(g, m, c, &ch, &rl, &bt, w, step, stride, rows, stats, err, errlen);
                 if (r < 0) { rc = OG_ERR_INVALID; break; }
                 if (r == 0) { stats->early++; w->alive = 0; }
             }
@@ -967,5 +1105,12 @@ int og_generate_walks(const og_graph* g, const og_model* m, const og_config* c, 
     free(ch.status);
     free(ch.last);
     free(rl.group);
+    if (c->sampler != OG_SAMPLER_MH) {
+        const uint64_t rs = og_slot_count(g, m);
+        for (uint64_t i = 0; i < rs; ++i) { free(bt.aprob[i]); free(bt.aalias[i]); }
+        for (uint32_t v = 0; v < g->n; ++v) { free(bt.pprob[v]); free(bt.palias[v]); }
+        free(bt.wbuf); free(bt.astat); free(bt.aprob); free(bt.aalias);
+        free(bt.pstat); free(bt.pprob); free(bt.palias);
+    }
     return rc;
 }

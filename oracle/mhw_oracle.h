@@ -75,12 +75,18 @@ typedef struct {
     /* node-keyed chain replicas at hubs (engine layout, DESIGN.md "Chain
      * table"); OG_NO_REPLICAS = one chain per state like SamplerManager */
     uint32_t replica_degree;
+    /* SamplerKind (engine.hpp:14): mh, or the exact baselines of
+     * WalkerContext::next_edge (engine.cpp:88-116) */
+    int sampler;
 } og_config;
+
+enum { OG_SAMPLER_MH = 0, OG_SAMPLER_ALIAS = 1, OG_SAMPLER_DIRECT = 2, OG_SAMPLER_REJECTION = 3 };
 
 #define OG_NO_REPLICAS 0xFFFFFFFFu
 
 typedef struct {
     uint64_t walks, early, skipped, steps, init_calls;
+    uint64_t trials;  /* rejection sampler: proposals drawn */
 } og_stats;
 
 /* ------------------------------------------------------------------ RNG */

@@ -26,6 +26,7 @@ DEEPWALK, NODE2VEC, METAPATH2VEC, EDGE2VEC, FAIRWALK = range(5)
 MODEL_NAMES = ["deepwalk", "node2vec", "metapath2vec", "edge2vec", "fairwalk"]
 INIT_RANDOM, INIT_HIGH_WEIGHT, INIT_BURN_IN = range(3)
 RNG_XOSHIRO, RNG_PHILOX = 0, 1
+SAMPLER_MH, SAMPLER_ALIAS, SAMPLER_DIRECT, SAMPLER_REJECTION = range(4)
 ORDER_WALKER, ORDER_STEP = 0, 1
 NO_AFFIX = 0xFFFFFFFF
 
@@ -63,12 +64,12 @@ class _OgModel(C.Structure):
 class _OgConfig(C.Structure):
     _fields_ = [("K", C.c_uint32), ("L", C.c_uint32), ("seed", C.c_uint64), ("init_kind", C.c_int),
                 ("burn_in_steps", C.c_uint32), ("hw_sample_size", C.c_uint32), ("rng", C.c_int),
-                ("order", C.c_int), ("replica_degree", C.c_uint32)]
+                ("order", C.c_int), ("replica_degree", C.c_uint32), ("sampler", C.c_int)]
 
 
 class _OgStats(C.Structure):
     _fields_ = [("walks", C.c_uint64), ("early", C.c_uint64), ("skipped", C.c_uint64),
-                ("steps", C.c_uint64), ("init_calls", C.c_uint64)]
+                ("steps", C.c_uint64), ("init_calls", C.c_uint64), ("trials", C.c_uint64)]
 
 
 @dataclass
@@ -141,6 +142,8 @@ class WalkCfg:
     # engine chain layout: hub replicas for node-keyed models (0 = 256);
     # NO_REPLICAS = one chain per state, the reference's SamplerManager
     replica_degree: int = 0xFFFFFFFF
+    # SamplerKind (engine.hpp:14): 0 mh, 1 alias, 2 direct, 3 rejection
+    sampler: int = 0
 
 
 class OracleError(RuntimeError):
@@ -305,6 +308,7 @@ class Oracle:
         c.init_kind, c.burn_in_steps, c.hw_sample_size = cfg.init_kind, cfg.burn_in_steps, cfg.hw_sample_size
         c.rng, c.order = rng, order
         c.replica_degree = cfg.replica_degree
+        c.sampler = cfg.sampler
         return c
 
     def generate_walks(self, g, md, cfg: WalkCfg, rng=RNG_XOSHIRO, order=ORDER_WALKER, stride=None):
@@ -325,7 +329,7 @@ class Oracle:
             raise OracleError(rc, err.value.decode())
         k = nrows.value
         stats = dict(walks=st.walks, early_terminations=st.early, skipped_starts=st.skipped,
-                     steps=st.steps, init_calls=st.init_calls)
+                     steps=st.steps, init_calls=st.init_calls, trials=st.trials)
         return rows[:k], lens[:k], stats
 
     def check(self, g, md, seed, pos, affix, draws):
@@ -380,7 +384,7 @@ class RefLib:
         L.ref_slot_count.restype = C.c_uint64
         L.ref_alias_build.argtypes = [C.c_uint32, _dp, _dp, _u32p]
         L.ref_generate_walks.argtypes = [C.c_void_p, C.c_void_p, C.c_uint32, C.c_uint32, C.c_uint32,
-                                         C.c_uint64, C.c_int, C.c_uint32, C.c_uint32, C.c_uint32,
+                                         C.c_uint64, C.c_int, C.c_uint32, C.c_uint32, C.c_int, C.c_uint32,
                                          _u32p, _u32p, _u64p, _u64p, _dp]
         L.ref_walk_sample.argtypes = [C.c_void_p, C.c_void_p, C.c_uint32, C.c_uint32, C.c_uint32,
                                       C.c_uint64, C.c_int, C.c_uint32, C.c_uint32, C.c_uint64,
@@ -482,7 +486,7 @@ class _RefModel:
         st = np.zeros(4, dtype=np.uint64)
         tm = np.zeros(3)
         rc = L.ref_generate_walks(self.g.h, self.h, cfg.K, cfg.L, threads, cfg.seed, cfg.init_kind,
-                                  cfg.burn_in_steps, cfg.hw_sample_size, stride, _ptr(rows, _u32p),
+                                  cfg.burn_in_steps, cfg.hw_sample_size, cfg.sampler, stride, _ptr(rows, _u32p),
                                   _ptr(lens, _u32p), C.byref(nrows), _ptr(st, _u64p), _ptr(tm, _dp))
         self.g.ref._check(rc)
         stats = dict(walks=int(st[0]), early_terminations=int(st[1]), skipped_starts=int(st[2]),

@@ -172,7 +172,7 @@ int ref_alias_build(uint32_t n, const double* w, double* prob, uint32_t* alias) 
 
 // ---- engine: unmodified generate_walks (engine.cpp:157-234)
 int ref_generate_walks(void* gp, void* mp, uint32_t K, uint32_t L, uint32_t threads, uint64_t seed,
-                       int init_kind, uint32_t burn_in, uint32_t hw, uint32_t stride,
+                       int init_kind, uint32_t burn_in, uint32_t hw, int sampler, uint32_t stride,
                        uint32_t* rows, uint32_t* lens, uint64_t* n_rows, uint64_t* stats,
                        double* times) {
     return guarded([&] {
@@ -181,7 +181,7 @@ int ref_generate_walks(void* gp, void* mp, uint32_t K, uint32_t L, uint32_t thre
         cfg.walk_length = L;
         cfg.threads = threads;
         cfg.seed = seed;
-        cfg.sampler_kind = SamplerKind::mh;
+        cfg.sampler_kind = static_cast<SamplerKind>(sampler);
         cfg.init.kind = static_cast<InitStrategy::Kind>(init_kind);
         cfg.init.burn_in_steps = burn_in;
         cfg.init.hw_sample_size = hw;

@@ -32,7 +32,7 @@ class WalkConfigC(C.Structure):
 class WalkStatsC(C.Structure):
     _fields_ = [("walks", C.c_uint64), ("early_terminations", C.c_uint64), ("skipped_starts", C.c_uint64),
                 ("steps", C.c_uint64), ("slot_inits", C.c_uint64), ("chain_retries", C.c_uint64), ("steps_per_sec", C.c_double),
-                ("init_seconds", C.c_double), ("walk_seconds", C.c_double)]
+                ("init_seconds", C.c_double), ("walk_seconds", C.c_double), ("rejection_trials", C.c_uint64)]
 
 
 class GraphInfoC(C.Structure):

@@ -13,7 +13,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libmhw.so")
 OBJ = os.path.join(PKG, "_obj")
-SOURCES = ["graph.cu", "walk.cu", "corpus.cu", "loader.cu", "api.cu"]
+SOURCES = ["graph.cu", "walk.cu", "exact.cu", "corpus.cu", "loader.cu", "api.cu"]
 HEADERS = ["mhw_device.cuh", "internal.h", "walk.h", "loader.h"]
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")

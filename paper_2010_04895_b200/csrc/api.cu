@@ -12,6 +12,7 @@
 
 #include "internal.h"
 #include "loader.h"
+#include "exact.h"
 #include "walk.h"
 
 struct mhw_walks {
@@ -367,6 +368,7 @@ mhw_status mhw_generate_walks_multi(const mhw_graph* const* replicas, int32_t n_
             t.steps += st[i].steps;
             t.slot_inits += st[i].slot_inits;
             t.chain_retries += st[i].chain_retries;
+            t.rejection_trials += st[i].rejection_trials;
             wall = std::max(wall, st[i].walk_seconds);
         }
         // skipped starts outside [b, e) are not walkers of this call

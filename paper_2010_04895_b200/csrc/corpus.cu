@@ -12,6 +12,7 @@
 #include <string>
 
 #include "internal.h"
+#include "exact.h"
 #include "walk.h"
 
 namespace mhw {

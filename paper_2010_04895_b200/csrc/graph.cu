@@ -1030,6 +1030,15 @@ void graph_ensure_tcount(Graph& g) {
     MHW_CK(cudaStreamSynchronize(g.stream));
 }
 
+void graph_alias_device(Graph& g, double* prob, uint32_t* alias) {
+    DeviceGuard dg(g.device);
+    if (!g.m) return;
+    DBuf<uint32_t> scratch(g.m);
+    k_alias<<<grid_for(g.n, 64), 64, 0, g.stream>>>(g.view(), prob, alias, scratch.p);
+    MHW_CK(cudaGetLastError());
+    MHW_CK(cudaStreamSynchronize(g.stream));
+}
+
 void graph_alias_tables(Graph& g, double* prob, uint32_t* alias) {
     DeviceGuard dg(g.device);
     if (!g.m) return;

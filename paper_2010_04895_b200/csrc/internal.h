@@ -139,6 +139,8 @@ void graph_ensure_tcount(Graph& g);
 void graph_ensure_hash(Graph& g);
 bool graph_ensure_arcrec(Graph& g, int aux);
 void graph_alias_tables(Graph& g, double* prob, uint32_t* alias);
+// Same tables left on the device (prob, alias: m entries each).
+void graph_alias_device(Graph& g, double* prob, uint32_t* alias);
 
 // Bound model (host validation of WalkModel::bind, models.cpp:29-74).
 struct Model {

@@ -238,6 +238,12 @@ struct Draw {
         ctr = make_uint4((uint32_t)id, (uint32_t)(id >> 32), blk, 0u);
         w = philox10(ctr, key);
     }
+    // block (id, blk) with sub-counter ctr.w = sub (rejection trials)
+    __device__ __forceinline__ void open_sub(uint2 k, uint64_t id, uint32_t blk, uint32_t sub) {
+        key = k;
+        ctr = make_uint4((uint32_t)id, (uint32_t)(id >> 32), blk, sub);
+        w = philox10(ctr, key);
+    }
     // uniform_index (rng.hpp:42-55) on word 0
     __device__ __forceinline__ uint32_t index(uint32_t n) const {
         const uint64_t m = (uint64_t)w.x * n;

@@ -20,6 +20,7 @@
 #include <cstdlib>
 #include <cstring>
 
+#include "exact.h"
 #include "internal.h"
 #include "walk.h"
 
@@ -842,11 +843,7 @@ void session_create(Session& s, Graph& g, const mhw_model_desc& md, const mhw_wa
     DeviceGuard dg(g.device);
     if (wc.walks_per_node == 0 || wc.walk_length == 0)
         invalid("walks_per_node, walk_length and threads must be positive");
-    if (wc.sampler != 0) {
-        static const char* sn[] = {"mh", "alias", "direct", "rejection"};
-        const char* name = (wc.sampler > 0 && wc.sampler < 4) ? sn[wc.sampler] : "?";
-        invalid(std::string("sampler not supported by the GPU engine: ") + name);
-    }
+    if (wc.sampler < 0 || wc.sampler > 3) invalid("unknown sampler kind");
     if (wc.init_kind < 0 || wc.init_kind > 2) invalid("unknown init strategy");
     if (wc.schedule < 0 || wc.schedule > 1) invalid("unknown schedule");
     s.g = &g;
@@ -964,7 +961,13 @@ void session_create(Session& s, Graph& g, const mhw_model_desc& md, const mhw_wa
     s.out.alloc(std::max<uint64_t>(s.rows * s.stride, 4));
     s.lens.alloc(std::max<uint64_t>(s.rows, 1));
     s.ctr.alloc(8);
-    if (wc.schedule == MHW_SCHEDULE_DETERMINISTIC) {
+    if (wc.sampler != MHW_SAMPLER_MH) {
+        // exact baselines: no chains; Philox-keyed draws make any schedule
+        // deterministic
+        s.chain.alloc(1);
+        s.ex = std::make_unique<ExactState>();
+        exact_create(s);
+    } else if (wc.schedule == MHW_SCHEDULE_DETERMINISTIC) {
         s.chain.alloc(std::max<uint64_t>(s.slots, 1));
         const uint64_t n = std::max<uint64_t>(s.n_items, 1);
         if (s.n_items > 0xFFFFFFFFull) invalid("deterministic schedule supports at most 2^32 walkers");
@@ -1067,7 +1070,10 @@ void session_run(Session& s, cudaStream_t user) {
     }
     MHW_CK(cudaEventRecord(s.ev0, st));
     if (s.n_items) {
-        if (s.wc.schedule == MHW_SCHEDULE_DETERMINISTIC) {
+        if (s.ex) {
+            exact_launch(s, P, st);
+            ++s.launches;
+        } else if (s.wc.schedule == MHW_SCHEDULE_DETERMINISTIC) {
             DetState S;
             S.v = s.d_v.p;
             S.aff = s.d_aff.p;
@@ -1137,6 +1143,7 @@ void session_stats(Session& s, mhw_walk_stats& out) {
     out.steps = h[1];
     out.slot_inits = h[3];
     out.chain_retries = h[6];
+    out.rejection_trials = h[7];
     out.walk_seconds = ms * 1e-3;
     out.init_seconds = 0.0;
     out.steps_per_sec = ms > 0 ? (double)h[1] / (ms * 1e-3) : 0.0;
@@ -1187,7 +1194,7 @@ void session_download_packed(Session& s, uint32_t* h_nodes, uint64_t cap_nodes, 
 void session_run_packed(Session& s, uint32_t* h_nodes, uint64_t cap_nodes, uint64_t* h_offsets,
                         uint64_t cap_rows, int chunks, mhw_walk_stats* stats) {
     DeviceGuard dg(s.g->device);
-    if (s.wc.schedule == MHW_SCHEDULE_DETERMINISTIC || s.n_act < 2 * (uint32_t)chunks || chunks < 2) {
+    if (s.ex || s.wc.schedule == MHW_SCHEDULE_DETERMINISTIC || s.n_act < 2 * (uint32_t)chunks || chunks < 2) {
         session_run(s, nullptr);
         mhw_walk_stats st{};
         session_stats(s, st);

@@ -2,6 +2,8 @@
 // device) and the kernel parameter blocks.
 #pragma once
 
+#include <memory>
+
 #include "internal.h"
 
 namespace mhw {
@@ -37,6 +39,8 @@ struct DetState {
     uint32_t* chosen;
 };
 
+struct ExactState;
+
 struct Session {
     Graph* g = nullptr;
     Model model;
@@ -50,6 +54,7 @@ struct Session {
     uint32_t stride = 0;
     DBuf<uint32_t> chain, out, lens, rep_group;
     DBuf<uint4> ac;          // arc records + colocated chain words (node2vec throughput)
+    std::unique_ptr<ExactState> ex;  // alias / direct / rejection baselines (exact.cu)
     DBuf<unsigned long long> ctr;
     // deterministic schedule scratch
     DBuf<uint32_t> d_v, d_aff, d_len, d_idx, d_idx2, d_cand, d_chosen;

@@ -183,11 +183,12 @@ class RunStats:
     walk_seconds: float = 0.0
     slot_inits: int = 0
     chain_retries: int = 0
+    rejection_trials: int = 0
 
     @classmethod
     def _from(cls, s: L.WalkStatsC):
         return cls(s.walks, s.early_terminations, s.skipped_starts, s.steps, s.steps_per_sec, s.init_seconds,
-                   s.walk_seconds, s.slot_inits, s.chain_retries)
+                   s.walk_seconds, s.slot_inits, s.chain_retries, s.rejection_trials)
 
 
 class WalkCorpus:

@@ -28,8 +28,9 @@ def walk_model(md: O.ModelDesc):
 
 
 def walk_config(cfg: O.WalkCfg, threads=1, **kw):
-    from paper_2010_04895_b200 import InitKind, InitStrategy, WalkConfig
+    from paper_2010_04895_b200 import InitKind, InitStrategy, SamplerKind, WalkConfig
     kw.setdefault("chain_replica_degree", cfg.replica_degree)
+    kw.setdefault("sampler_kind", SamplerKind(cfg.sampler))
     return WalkConfig(walks_per_node=cfg.K, walk_length=cfg.L, threads=threads, seed=cfg.seed,
                       init=InitStrategy(InitKind(cfg.init_kind), cfg.burn_in_steps, cfg.hw_sample_size), **kw)
 

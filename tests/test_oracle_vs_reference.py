@@ -28,6 +28,28 @@ def test_corpus_byte_identical(oracle, ref, seed, kind):
         assert st["steps"] == rs["steps"] and st["early_terminations"] == rs["early_terminations"]
 
 
+@pytest.mark.parametrize("sampler", [O.SAMPLER_ALIAS, O.SAMPLER_DIRECT, O.SAMPLER_REJECTION])
+@pytest.mark.parametrize("seed", [1, 2])
+@pytest.mark.parametrize("kind", KINDS)
+def test_baseline_sampler_corpus_byte_identical(oracle, ref, seed, kind, sampler):
+    """The exact baselines of next_edge (engine.cpp:88-116): alias tables per
+    state slot, direct inverse-CDF, rejection under a static alias proposal
+    with the rejection_bound envelope -- same corpus as generate_walks."""
+    rng = O.XoRng(2000 + seed)
+    g = O.random_graph(50 + 20 * seed, 4.0 + seed, seed != 2, rng, ensure_connected=seed != 1)
+    O.assign_random_types(g, 2 + seed % 2, rng)
+    md = model_desc(kind, g, p=0.5 + 0.2 * seed, q=2.0 / seed, metapath=(0, 1, 0) if seed % 2 else (0, 1))
+    if kind == O.EDGE2VEC:
+        md.type_matrix = np.random.default_rng(seed).uniform(0.1, 1.1, md.type_matrix.shape)
+    cfg = O.WalkCfg(K=3, L=15, seed=seed * 11, sampler=sampler)
+    rows, lens, st = oracle.generate_walks(g, md, cfg)
+    rr, rl, rs = ref.graph(g).model(md).generate_walks(cfg, threads=1, n_nodes=g.n)
+    assert np.array_equal(lens, rl)
+    for i in range(len(lens)):
+        assert np.array_equal(rows[i, :lens[i]], rr[i, :rl[i]])
+    assert st["steps"] == rs["steps"] and st["early_terminations"] == rs["early_terminations"]
+
+
 @pytest.mark.parametrize("kind", KINDS)
 def test_decisions_bit_exact(oracle, ref, kind):
     rng = O.XoRng(77 + kind)
