@@ -83,6 +83,17 @@ int main() {
             }
         }
     }
+    {   // every sampler kind emits edge-valid walks (test_engine.cpp:88-98)
+        Rng rng(5);
+        Graph g = oracles::random_graph(60, 5.0, true, rng);
+        for (auto kind : {SamplerKind::mh, SamplerKind::alias, SamplerKind::direct, SamplerKind::rejection}) {
+            WalkModel m = make_bound(ModelKind::node2vec, g, 0.5, 2.0);
+            WalkConfig config{.walks_per_node = 2, .walk_length = 15, .seed = 6, .sampler_kind = kind};
+            WalkCorpus c = mhwalk_gpu::generate_walks(g, m, config);
+            CHECK(c.walks.size() == 120);
+            CHECK(walks_valid(g, c));
+        }
+    }
     {   // metapath walks follow the metapath cyclically
         Rng rng(7);
         Graph g = oracles::random_graph(80, 8.0, false, rng);
