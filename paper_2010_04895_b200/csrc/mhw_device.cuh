@@ -48,6 +48,10 @@ constexpr uint16_t NF_ALLPOS = 1;  // every static weight of the slice is > 0
 __host__ __device__ constexpr bool second_order(int k) {
     return k == NODE2VEC || k == EDGE2VEC || k == FAIRWALK;
 }
+// models whose weight functor reads the candidate's node type
+__host__ __device__ constexpr bool typed_kind(int k) {
+    return k == METAPATH2VEC || k == EDGE2VEC || k == FAIRWALK;
+}
 
 struct DevGraph {
     uint32_t n;
@@ -384,22 +388,29 @@ __device__ __forceinline__ double alpha_value(const DevModel& m, uint32_t cls) {
 
 // Dynamic weight w' of candidate index i (node u, type utype, alpha class
 // cls) under state c: WalkModel::calculate_weight, models.cpp:82-123.
+// The same from the candidate's static weight w, node type utype and edge
+// type out_t (edge2vec) already in registers (typed arc records).
 template <int KIND>
-__device__ __forceinline__ double wprime(const DevGraph& g, const DevModel& m, const SCtx& c, uint32_t i,
-                                         uint16_t utype, uint32_t cls) {
-    const double w = static_w(g, c.off + i);
+__device__ __forceinline__ double wprime_v(const DevGraph& g, const DevModel& m, const SCtx& c, double w,
+                                           uint16_t utype, uint32_t out_t, uint32_t cls) {
     if (KIND == DEEPWALK) return w;
     if (KIND == METAPATH2VEC) return utype == c.req ? w : 0.0;
     if (c.boot) return w;
     const double a = alpha_value(m, cls);
     if (KIND == NODE2VEC) return __dmul_rn(a, w);
-    if (KIND == EDGE2VEC) {
-        const uint32_t out_t = edge_type_of(g, c.off + i, c.vtype, utype);
-        return __dmul_rn(__dmul_rn(a, __ldg(m.M + (size_t)c.in_type * m.M_dim + out_t)), w);
-    }
+    if (KIND == EDGE2VEC) return __dmul_rn(__dmul_rn(a, __ldg(m.M + (size_t)c.in_type * m.M_dim + out_t)), w);
     // FAIRWALK: a * w / group
     const uint32_t group = __ldg(g.tcount + (size_t)c.v * g.n_ntypes + utype);
     return __ddiv_rn(__dmul_rn(a, w), (double)group);
+}
+
+template <int KIND>
+__device__ __forceinline__ double wprime(const DevGraph& g, const DevModel& m, const SCtx& c, uint32_t i,
+                                         uint16_t utype, uint32_t cls) {
+    const double w = static_w(g, c.off + i);
+    uint32_t out_t = 0;
+    if (KIND == EDGE2VEC && !c.boot) out_t = edge_type_of(g, c.off + i, c.vtype, utype);
+    return wprime_v<KIND>(g, m, c, w, utype, out_t, cls);
 }
 
 template <int KIND>

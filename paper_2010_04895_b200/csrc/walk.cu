@@ -53,16 +53,28 @@ __device__ __noinline__ uint32_t init_slot_ool(const DevGraph g, const DevModel 
 // ------------------------------------------------------ throughput kernel
 // LAZY = false: every slot was initialised by k_init_all before the launch,
 // so the lazy-init call (and the registers the call ABI pins) is compiled out.
-// AR = true: arc records replace the id / node-record / weight loads of a
-// step. deepwalk: graph records, aux = weight. node2vec: the session's
-// records, aux = the chain word of the state entered through that arc
-// (colocated chains: the chain word a step locks sits in the sector the
-// previous step loaded as its candidate record, so the lock is an L2 hit).
+// AR = true: arc records replace the id / node-record / weight / type loads
+// of a step. deepwalk: graph records, aux = weight. Other models: the
+// session's records (ArcRec in walk.h); for second-order models their aux
+// word is the chain word of the state entered through that arc (colocated
+// chains: the word a step locks sits in the sector the previous step loaded
+// as its candidate record, so the lock is an L2 hit).
 template <int KIND, int REGS, bool LAZY, bool AR>
 __global__ void __launch_bounds__(kWalkBlock) __maxnreg__(REGS) k_walk(RunParams P) {
     const DevGraph& g = P.g;
-    constexpr bool CC = AR && KIND == NODE2VEC;
-    const uint4* const arcs = CC ? P.ac : g.arc;
+    constexpr bool TYPED = AR && needs_utype<KIND>();
+    constexpr bool CC = AR && second_order(KIND);
+    constexpr uint32_t RS = TYPED ? 2u : 1u;  // uint4 words per record
+    const uint4* const arcs = (AR && KIND != DEEPWALK) ? P.ac : g.arc;
+    auto load_rec = [&](uint64_t arc, uint4& b) {
+        if (TYPED) b = __ldg(arcs + RS * arc + 1);
+        return __ldg(arcs + RS * arc);
+    };
+    auto rec_node = [&](const uint4& a, const uint4& b) {
+        NodeRec r = arc_node(a);
+        if (TYPED) r.type = (uint16_t)(b.y & 0xFFFFu);
+        return r;
+    };
     const uint2 wkey = philox_key(P.cfg.seed, DOM_WALK);
     const uint32_t K = P.cfg.K, L = P.cfg.L;
     const unsigned lane = threadIdx.x & 31;
@@ -114,15 +126,16 @@ __global__ void __launch_bounds__(kWalkBlock) __maxnreg__(REGS) k_walk(RunParams
             d.open(wkey, walker, step);
             uint32_t chosen, next, back_c = 0;
             NodeRec rn;
+            uint4 bn = make_uint4(0, 0, 0, 0);  // typed word of the chosen record
             if (second_order(KIND) && c.boot) {
                 if (!bootstrap_pick(g, c, d.unit(), &chosen)) {
                     dead = true;
                     break;
                 }
                 if constexpr (AR) {
-                    const uint4 a = __ldg(arcs + c.off + chosen);
+                    const uint4 a = load_rec(c.off + chosen, bn);
                     next = a.x;
-                    rn = arc_node(a);
+                    rn = rec_node(a, bn);
                     if (!CC) back_c = a.w;
                 } else {
                     next = load_id(g, c.off + chosen);
@@ -140,18 +153,18 @@ __global__ void __launch_bounds__(kWalkBlock) __maxnreg__(REGS) k_walk(RunParams
                 // (its timing cannot depend on the proposal); the candidate
                 // evaluation overlaps its latency, and the chain state it
                 // returns is only consumed by the decision.
-                uint32_t* const cw = CC ? reinterpret_cast<uint32_t*>(P.ac + loc) + 3 : P.chain + slot;
+                uint32_t* const cw = CC ? reinterpret_cast<uint32_t*>(P.ac + RS * loc) + 3 : P.chain + slot;
                 uint32_t e = atomicExch(cw, kLocked);
                 const uint32_t cand = d.index(c.deg);
                 const double u = d.unit();
                 uint32_t uc;
-                uint4 ac = make_uint4(0, 0, 0, 0);
+                uint4 ac = make_uint4(0, 0, 0, 0), bc = make_uint4(0, 0, 0, 0);
                 NodeRec rc{};
                 bool rc_early;
                 if constexpr (AR) {
-                    ac = __ldg(arcs + c.off + cand);
+                    ac = load_rec(c.off + cand, bc);
                     uc = ac.x;
-                    rc = arc_node(ac);
+                    rc = rec_node(ac, bc);
                     rc_early = true;
                 } else {
                     uc = load_id(g, c.off + cand);
@@ -164,8 +177,10 @@ __global__ void __launch_bounds__(kWalkBlock) __maxnreg__(REGS) k_walk(RunParams
                 }
                 const uint32_t cls_c =
                     second_order(KIND) ? alpha_class(g, P.m, c, uc, rc_early ? &rc : nullptr) : 0u;
-                const double wc = (AR && KIND == DEEPWALK) ? (double)__uint_as_float(ac.w)
-                                                          : wprime<KIND>(g, P.m, c, cand, rc.type, cls_c);
+                double wc;
+                if (AR && KIND == DEEPWALK) wc = (double)__uint_as_float(ac.w);
+                else if (TYPED) wc = wprime_v<KIND>(g, P.m, c, (double)__uint_as_float(bc.x), rc.type, bc.y >> 16, cls_c);
+                else wc = wprime<KIND>(g, P.m, c, cand, rc.type, cls_c);
                 if (e == kLocked) {
                     unsigned ns = 32;
                     do {
@@ -200,26 +215,38 @@ __global__ void __launch_bounds__(kWalkBlock) __maxnreg__(REGS) k_walk(RunParams
                 constexpr bool kSpec = needs_utype<KIND>() || KIND == DEEPWALK;
                 uint32_t ul = 0;
                 NodeRec rl{};
-                uint4 al = make_uint4(0, 0, 0, 0);
+                uint4 al = make_uint4(0, 0, 0, 0), bl = make_uint4(0, 0, 0, 0);
                 if (kSpec) {
                     if constexpr (AR) {
-                        al = __ldg(arcs + c.off + last);
+                        al = load_rec(c.off + last, bl);
                         ul = al.x;
-                        rl = arc_node(al);
+                        rl = rec_node(al, bl);
                     } else {
                         ul = load_id(g, c.off + last);
                         rl = load_node(g, ul);
                     }
                 }
-                const double wl = (AR && KIND == DEEPWALK) ? (double)__uint_as_float(al.w)
-                                                          : wprime<KIND>(g, P.m, c, last, rl.type, cls_l);
+                double wl;
+                if (AR && KIND == DEEPWALK) wl = (double)__uint_as_float(al.w);
+                else if (TYPED) wl = wprime_v<KIND>(g, P.m, c, (double)__uint_as_float(bl.x), rl.type, bl.y >> 16, cls_l);
+                else wl = wprime<KIND>(g, P.m, c, last, rl.type, cls_l);
                 const bool acc = mh_accept(wc, wl, u) && cand != last;
                 chain_release(cw, acc ? pack_entry(cand, cls_c) : e);
                 chosen = acc ? cand : last;
                 if constexpr (AR) {
-                    const uint4 an = (acc || cand == last) ? ac : (kSpec ? al : __ldg(arcs + c.off + last));
+                    const bool take_c = acc || cand == last;
+                    uint4 an;
+                    if (take_c) {
+                        an = ac;
+                        bn = bc;
+                    } else if (kSpec) {
+                        an = al;
+                        bn = bl;
+                    } else {
+                        an = load_rec(c.off + last, bn);
+                    }
                     next = an.x;
-                    rn = arc_node(an);
+                    rn = rec_node(an, bn);
                     if (!CC) back_c = an.w;
                 } else {
                     if (acc || cand == last) {
@@ -265,7 +292,8 @@ __global__ void __launch_bounds__(kWalkBlock) __maxnreg__(REGS) k_walk(RunParams
                     dead = true;
                     break;
                 }
-                if (KIND == EDGE2VEC) c.in_type = edge_type_of(g, c.off + chosen, c.vtype, rn.type);
+                if (KIND == EDGE2VEC)
+                    c.in_type = TYPED ? (bn.y >> 16) : edge_type_of(g, c.off + chosen, c.vtype, rn.type);
                 if (CC) loc = (uint64_t)c.off + chosen;
                 c.s = c.v;
                 c.off_s = c.off;
@@ -315,8 +343,9 @@ __global__ void __launch_bounds__(256) k_init_all(RunParams P) {
         const uint32_t e = init_slot<KIND>(g, P.m, P.cfg, c, a);
         if (P.ac) {
             // colocated: the word lives in the record of the forward arc s->v
+            constexpr uint32_t RS = needs_utype<KIND>() ? 2u : 1u;
             const uint32_t sv = __ldg(g.rev + a);  // index of v in N(s)
-            if (sv != kNoBack) reinterpret_cast<uint32_t*>(P.ac + c.off_s + sv)[3] = e;
+            if (sv != kNoBack) reinterpret_cast<uint32_t*>(P.ac + RS * (c.off_s + sv))[3] = e;
         } else {
             P.chain[a] = e;
         }
@@ -325,20 +354,34 @@ __global__ void __launch_bounds__(256) k_init_all(RunParams P) {
     if (inits) atomicAdd(&P.ctr[3], inits);
 }
 
-// Session arc records for colocated chains: {id, deg | allpos << 31, off,
-// chain word}; k_ac_reset empties the chain words before a lazy run.
-__global__ void k_arc_chain(DevGraph g, uint4* __restrict__ out) {
-    for (uint64_t a = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; a < g.m;
-         a += (uint64_t)gridDim.x * blockDim.x) {
-        const uint32_t u = load_id(g, a);
-        const NodeRec r = load_node(g, u);
-        out[a] = make_uint4(u, r.deg | ((r.flags & NF_ALLPOS) ? 0x80000000u : 0u), (uint32_t)r.off, kEmpty);
+// Session arc records (walk.h ArcRec): word 0 = {id u, deg(u) | allpos << 31,
+// off(u), chain word (second order) }, typed models add word 1 = {fp32
+// weight, type(u) | edge_type(arc) << 16, 0, 0}. Warp per source node (its
+// type gives the computed edge type, graph.hpp:47-50). k_ac_reset empties the
+// chain words before a lazy run.
+__global__ void k_arc_chain(DevGraph g, uint4* __restrict__ out, uint32_t rs) {
+    const unsigned lane = threadIdx.x & 31;
+    const uint64_t wid = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    for (uint64_t v = wid; v < g.n; v += nw) {
+        const NodeRec rv = load_node(g, (uint32_t)v);
+        for (uint32_t i = lane; i < rv.deg; i += 32) {
+            const uint64_t a = (uint64_t)rv.off + i;
+            const uint32_t u = load_id(g, a);
+            const NodeRec r = load_node(g, u);
+            out[rs * a] = make_uint4(u, r.deg | ((r.flags & NF_ALLPOS) ? 0x80000000u : 0u), (uint32_t)r.off, kEmpty);
+            if (rs == 2) {
+                const float w = g.w ? __ldg(g.w + a) : 1.0f;
+                const uint32_t et = edge_type_of(g, a, rv.type, r.type);
+                out[rs * a + 1] = make_uint4(__float_as_uint(w), (uint32_t)r.type | (et << 16), 0u, 0u);
+            }
+        }
     }
 }
 
-__global__ void k_ac_reset(uint4* __restrict__ ac, uint64_t m) {
+__global__ void k_ac_reset(uint4* __restrict__ ac, uint64_t m, uint32_t rs) {
     for (uint64_t a = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; a < m; a += (uint64_t)gridDim.x * blockDim.x)
-        reinterpret_cast<uint32_t*>(ac + a)[3] = kEmpty;
+        reinterpret_cast<uint32_t*>(ac + rs * a)[3] = kEmpty;
 }
 
 // Packed corpus: widen lengths for the 64-bit offset scan, then one warp per
@@ -733,7 +776,7 @@ void with_variant(int regs, bool lazy, bool ar, F&& f) {
         if (regs == 80) f(std::integral_constant<int, 80>{}, lz, a);
         else f(std::integral_constant<int, 255>{}, lz, a);
     };
-    if constexpr (KIND == DEEPWALK || KIND == NODE2VEC) {
+    {
         if (ar) {
             if (lazy) by_regs(T{}, T{});
             else by_regs(N{}, T{});
@@ -1000,22 +1043,25 @@ void session_create(Session& s, Graph& g, const mhw_model_desc& md, const mhw_wa
         // arc records (after the session buffers, so the memory check sees them)
         const char* ar_env = std::getenv("MHW_ARC_RECORDS");
         const bool want_ar = !(ar_env && ar_env[0] == '0');
-        if (want_ar && m.kind == NODE2VEC && g.m && g.m < (1ull << 32)) {
-            // colocated chains: the session's arc records carry the chain words
+        if (want_ar && m.kind != DEEPWALK && g.m && g.m < (1ull << 32)) {
+            // session arc records (typed models: 32 B with weight and types);
+            // second-order models keep their chain words in them
+            s.rec_words = typed_kind(m.kind) ? 2 : 1;
+            const uint64_t need = 16ull * s.rec_words * g.m;
             size_t free_b = 0, total_b = 0;
             MHW_CK(cudaMemGetInfo(&free_b, &total_b));
-            if (free_b < 16 * g.m + (2ull << 30)) {
+            if (free_b < need + (2ull << 30)) {
                 dev_trim();
                 MHW_CK(cudaMemGetInfo(&free_b, &total_b));
             }
-            if (free_b >= 16 * g.m + (2ull << 30)) {
-                s.ac.alloc(g.m);
-                k_arc_chain<<<grid_for(g.m), 256, 0, st>>>(g.view(), s.ac.p);
+            if (free_b >= need + (2ull << 30)) {
+                s.ac.alloc(g.m * s.rec_words);
+                k_arc_chain<<<grid_for(g.n * 32ull), 256, 0, st>>>(g.view(), s.ac.p, s.rec_words);
                 MHW_CK(cudaGetLastError());
                 s.use_ar = true;
             }
         }
-        if (!s.ac.n) s.chain.alloc(std::max<uint64_t>(s.slots, 1));
+        if (!s.ac.n || !second_order(m.kind)) s.chain.alloc(std::max<uint64_t>(s.slots, 1));
         else s.chain.alloc(1);
         if (want_ar && m.kind == DEEPWALK) s.use_ar = graph_ensure_arcrec(g, ARC_AUX_WEIGHT);
         dispatch(m.kind, [&](auto kc) {
@@ -1059,8 +1105,8 @@ void session_run(Session& s, cudaStream_t user) {
     s.launches = 0;
     MHW_CK(cudaMemsetAsync(s.chain.p, 0xFF, s.chain.bytes(), st));
     MHW_CK(cudaMemsetAsync(s.ctr.p, 0, s.ctr.bytes(), st));
-    if (s.ac.n && (!s.eager_init || !s.g->verified_sym)) {
-        k_ac_reset<<<grid_for(s.ac.n), 256, 0, st>>>(s.ac.p, s.ac.n);
+    if (s.ac.n && second_order(s.model.dev.kind) && (!s.eager_init || !s.g->verified_sym)) {
+        k_ac_reset<<<grid_for(s.g->m), 256, 0, st>>>(s.ac.p, s.g->m, s.rec_words);
         ++s.launches;
     }
     if (s.n_iso) {
@@ -1237,8 +1283,8 @@ void session_run_packed(Session& s, uint32_t* h_nodes, uint64_t cap_nodes, uint6
         RunParams P = s.params();
         MHW_CK(cudaMemsetAsync(s.chain.p, 0xFF, s.chain.bytes(), S));
         MHW_CK(cudaMemsetAsync(s.ctr.p, 0, s.ctr.bytes(), S));
-        if (s.ac.n && (!s.eager_init || !s.g->verified_sym))
-            k_ac_reset<<<grid_for(s.ac.n), 256, 0, S>>>(s.ac.p, s.ac.n);
+        if (s.ac.n && second_order(s.model.dev.kind) && (!s.eager_init || !s.g->verified_sym))
+            k_ac_reset<<<grid_for(s.g->m), 256, 0, S>>>(s.ac.p, s.g->m, s.rec_words);
         if (s.n_iso)
             k_iso_rows<<<grid_for((uint64_t)s.n_iso * s.cfg.K), 256, 0, S>>>(s.iso.p, s.iso_row.p, s.n_iso, s.cfg.K,
                                                                              s.out.p, s.stride, s.lens.p);

@@ -53,7 +53,8 @@ struct Session {
     uint64_t n_items = 0, rows = 0, skipped = 0, slots = 0;
     uint32_t stride = 0;
     DBuf<uint32_t> chain, out, lens, rep_group;
-    DBuf<uint4> ac;          // arc records + colocated chain words (node2vec throughput)
+    DBuf<uint4> ac;          // session arc records (+ colocated chain words, second order)
+    uint32_t rec_words = 1;  // uint4 words per record: 2 for typed models
     std::unique_ptr<ExactState> ex;  // alias / direct / rejection baselines (exact.cu)
     DBuf<unsigned long long> ctr;
     // deterministic schedule scratch

@@ -70,12 +70,14 @@ def test_every_model_emits_edge_valid_walks(mhw, threads):          # :76-86
         assert valid(g, c)
 
 
-def test_baseline_sampler_kinds_are_rejected(mhw):                    # :88-98 (baselines OUT OF SCOPE)
-    g = O.triangle()
-    for kind in (mhw.SamplerKind.alias, mhw.SamplerKind.direct, mhw.SamplerKind.rejection):
-        with pytest.raises(mhw.ValidationError, match="sampler not supported"):
-            mhw.generate_walks(device_graph(g), walk_model(model_desc(O.NODE2VEC, g)),
-                               mhw.WalkConfig(sampler_kind=kind))
+def test_every_sampler_kind_emits_edge_valid_walks(mhw):              # :88-98
+    rng = O.XoRng(5)
+    g = O.random_graph(60, 5.0, True, rng)
+    dg = device_graph(g)
+    for kind in mhw.SamplerKind:
+        c = mhw.generate_walks(dg, walk_model(model_desc(O.NODE2VEC, g, 0.5, 2.0)),
+                               mhw.WalkConfig(walks_per_node=2, walk_length=15, seed=6, sampler_kind=kind))
+        assert len(c) == 120 and valid(g, c)
 
 
 @pytest.mark.parametrize("threads", [1, 8])
