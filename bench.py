@@ -417,9 +417,9 @@ def run_e2e(args, cfg, g, model, wcfg, dev, dist):
     out = torch.empty(max(cap, 1), dtype=torch.int32).pin_memory()
     offs = torch.empty(rows.value + 1, dtype=torch.int64).pin_memory()
     h2d = sum(x.numel() * x.element_size() for x in (off, nb, w, nt, et) if x is not None)
-    steps_e2e = max(1, min(args.steps, 3))
+    steps_e2e = max(1, min(args.steps, 5))
     times, steps, d2h = [], 0, 0
-    e2e_warm = 2
+    e2e_warm = max(3, args.warmup)
     for i in range(e2e_warm + steps_e2e):
         if dist:
             dist.barrier()

@@ -1,6 +1,7 @@
 // api.cu -- the extern "C" boundary (include/mhw.h). Every entry point
 // converts exceptions to status codes (errors.hpp classes -> 1/2/4) and keeps
 // the message in a thread-local buffer (mhw_last_error).
+#include <chrono>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -482,12 +483,21 @@ mhw_status mhw_generate_walks_packed(const mhw_graph* g, const mhw_model_desc* m
         need(h_offsets, "h_offsets");
         auto* gg = const_cast<mhw_graph*>(g);
         mhw::DeviceGuard dg(gg->device);
+        const bool trace = std::getenv("MHW_TRACE") != nullptr;
+        const auto t0 = std::chrono::steady_clock::now();
         mhw_session s;
         mhw::session_create(s, *gg, *model, *config);
+        const auto t1 = std::chrono::steady_clock::now();
         if (capacity_rows < s.rows + 1) mhw::invalid("offset buffer too small for the corpus");
         const char* e = std::getenv("MHW_E2E_CHUNKS");
-        const int chunks = e ? std::atoi(e) : 4;
+        const int chunks = e ? std::atoi(e) : 16;
         mhw::session_run_packed(s, h_nodes, capacity_nodes, h_offsets, capacity_rows, chunks, stats);
+        if (trace) {
+            const auto t2 = std::chrono::steady_clock::now();
+            std::fprintf(stderr, "[mhw] packed: create %.2f ms, run+copy %.2f ms\n",
+                         std::chrono::duration<double, std::milli>(t1 - t0).count(),
+                         std::chrono::duration<double, std::milli>(t2 - t1).count());
+        }
     });
 }
 

@@ -17,6 +17,8 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 
@@ -764,7 +766,7 @@ unsigned grid_for(uint64_t work, int block = 256) {
 int walk_minb(int kind) {
     const char* e = std::getenv("MHW_WALK_REGS");
     const int v = e ? std::atoi(e) : (kind == DEEPWALK ? 80 : 255);
-    return v == 80 ? 80 : 255;
+    return v == 64 ? 64 : (v == 80 ? 80 : 255);
 }
 
 // Calls f(REGS, LAZY, AR) with the compile-time variant of the session.
@@ -774,6 +776,7 @@ void with_variant(int regs, bool lazy, bool ar, F&& f) {
     using N = std::false_type;
     auto by_regs = [&](auto lz, auto a) {
         if (regs == 80) f(std::integral_constant<int, 80>{}, lz, a);
+        else if (regs == 64) f(std::integral_constant<int, 64>{}, lz, a);
         else f(std::integral_constant<int, 255>{}, lz, a);
     };
     {
@@ -1249,6 +1252,10 @@ void session_run_packed(Session& s, uint32_t* h_nodes, uint64_t cap_nodes, uint6
         return;
     }
     if (cap_rows < s.rows + 1) invalid("offset buffer too small for the corpus");
+    const bool trace = std::getenv("MHW_TRACE") != nullptr;
+    using clk = std::chrono::steady_clock;
+    const auto ta = clk::now();
+    auto ms_since = [&](clk::time_point t) { return std::chrono::duration<double, std::milli>(clk::now() - t).count(); };
     cudaStream_t S = s.stream, T = nullptr;
     MHW_CK(cudaStreamCreateWithFlags(&T, cudaStreamNonBlocking));
     std::vector<cudaEvent_t> ev(chunks, nullptr);
@@ -1289,6 +1296,7 @@ void session_run_packed(Session& s, uint32_t* h_nodes, uint64_t cap_nodes, uint6
             k_iso_rows<<<grid_for((uint64_t)s.n_iso * s.cfg.K), 256, 0, S>>>(s.iso.p, s.iso_row.p, s.n_iso, s.cfg.K,
                                                                              s.out.p, s.stride, s.lens.p);
         MHW_CK(cudaEventRecord(s.ev0, S));
+        const double t_setup = ms_since(ta);
         dispatch(s.model.dev.kind, [&](auto kc) {
             constexpr int KIND = decltype(kc)::value;
             if constexpr (second_order(KIND)) {
@@ -1334,6 +1342,7 @@ void session_run_packed(Session& s, uint32_t* h_nodes, uint64_t cap_nodes, uint6
                 MHW_CK(cudaMemcpyAsync(h_nodes + H, packed.p + rc[c] * rowcap, tot * 4, cudaMemcpyDeviceToHost, T));
             H += tot;
         }
+        const double t_issued = ms_since(ta);
         // global row offsets (one scan over all lengths) and the counters
         k_len64<<<grid_for(s.rows + 1), 256, 0, S>>>(s.lens.p, s.rows, len64.p);
         size_t b = scan_bytes;
@@ -1345,6 +1354,11 @@ void session_run_packed(Session& s, uint32_t* h_nodes, uint64_t cap_nodes, uint6
         mhw_walk_stats st{};
         session_stats(s, st);
         if (stats) *stats = st;
+        if (trace)
+            std::fprintf(stderr,
+                         "[mhw] run_packed: %d chunks, setup %.2f ms, last copy issued %.2f ms, done %.2f ms, "
+                         "device walk+pack %.2f ms\n",
+                         chunks, t_setup, t_issued, ms_since(ta), st.walk_seconds * 1e3);
     } catch (...) {
         cudaStreamSynchronize(S);
         if (T) cudaStreamSynchronize(T);

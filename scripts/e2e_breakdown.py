@@ -54,5 +54,7 @@ for it in range(3):
     t3 = time.perf_counter()
     lib.mhw_graph_free(h)
     t4 = time.perf_counter()
+    if rc or rc2:
+        print("error:", lib.mhw_last_error().decode(), flush=True)
     print(f"upload {1e3*(t1-t0):.1f} ms  packed {1e3*(t2-t1):.1f} ms (rc {rc})  padded {1e3*(t3-t2):.1f} ms "
           f"(rc {rc2})  free {1e3*(t4-t3):.1f} ms  walk {st.walk_seconds*1e3:.1f} ms", flush=True)
