@@ -24,40 +24,48 @@ void throw_cuda(cudaError_t e, const char* what, const char* file, int line) {
     throw Error(code, msg);
 }
 
-// ------------------------------------------------------- device block cache
+// ------------------------------------------------------- device allocation
+// Large buffers come from the device's stream-ordered memory pool with an
+// unbounded release threshold: a session's multi-GB buffers are reallocated
+// on every generate_walks call, and the pool sub-allocates freed memory for
+// any later size (cudaMalloc/cudaFree of such blocks cost milliseconds each
+// and cudaFree synchronises the device). Allocation and free are ordered on
+// the legacy stream and completed before returning, so a block is usable on
+// every stream; a free first waits for in-flight work that may still read it.
 namespace {
-constexpr size_t kCacheMin = 32ull << 20;
-constexpr size_t kCacheGrain = 2ull << 20;
-struct CachedBlock {
-    int device;
-    size_t cap;
-    void* p;
-};
-std::mutex g_cache_mu;
-std::vector<CachedBlock> g_cache;
+constexpr size_t kPoolMin = 1ull << 20;
+std::mutex g_pool_mu;
+bool g_pool_ready[64] = {};
+
+void pool_setup(int dev) {
+    std::lock_guard<std::mutex> lk(g_pool_mu);
+    if (dev < 0 || dev >= 64 || g_pool_ready[dev]) return;
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        uint64_t keep = UINT64_MAX;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+    g_pool_ready[dev] = true;
+}
 }  // namespace
 
 void* dev_alloc(size_t bytes, size_t* cap) {
     int dev = 0;
     cudaGetDevice(&dev);
-    if (bytes >= kCacheMin) {
-        bytes = (bytes + kCacheGrain - 1) / kCacheGrain * kCacheGrain;
-        std::lock_guard<std::mutex> lk(g_cache_mu);
-        size_t best = SIZE_MAX;
-        for (size_t i = 0; i < g_cache.size(); ++i) {
-            const auto& b = g_cache[i];
-            if (b.device == dev && b.cap >= bytes && b.cap <= bytes + bytes / 4 + kCacheGrain &&
-                (best == SIZE_MAX || b.cap < g_cache[best].cap))
-                best = i;
-        }
-        if (best != SIZE_MAX) {
-            void* p = g_cache[best].p;
-            *cap = g_cache[best].cap;
-            g_cache.erase(g_cache.begin() + best);
-            return p;
-        }
-    }
     void* p = nullptr;
+    *cap = bytes;
+    if (bytes >= kPoolMin) {
+        pool_setup(dev);
+        cudaError_t e = cudaMallocAsync(&p, bytes, 0);
+        if (e == cudaErrorMemoryAllocation) {
+            cudaGetLastError();
+            dev_trim();
+            e = cudaMallocAsync(&p, bytes, 0);
+        }
+        if (e != cudaSuccess) throw_cuda(e, "cudaMallocAsync", __FILE__, __LINE__);
+        MHW_CK(cudaStreamSynchronize(0));
+        return p;
+    }
     cudaError_t e = cudaMalloc(&p, bytes);
     if (e == cudaErrorMemoryAllocation) {
         cudaGetLastError();
@@ -65,37 +73,46 @@ void* dev_alloc(size_t bytes, size_t* cap) {
         e = cudaMalloc(&p, bytes);
     }
     if (e != cudaSuccess) throw_cuda(e, "cudaMalloc", __FILE__, __LINE__);
-    *cap = bytes;
     return p;
 }
 
 void dev_free(void* p, size_t cap) {
     if (!p) return;
-    if (cap < kCacheMin) {
+    if (cap < kPoolMin) {
         cudaFree(p);
         return;
     }
     // the block may still be read by in-flight work on any stream
     cudaDeviceSynchronize();
-    int dev = 0;
-    cudaGetDevice(&dev);
-    std::lock_guard<std::mutex> lk(g_cache_mu);
-    g_cache.push_back({dev, cap, p});
+    cudaFreeAsync(p, 0);
+    cudaStreamSynchronize(0);
 }
 
+// Returns the pools' unused memory to the device.
 void dev_trim() {
-    std::vector<CachedBlock> all;
-    {
-        std::lock_guard<std::mutex> lk(g_cache_mu);
-        all.swap(g_cache);
-    }
-    int prev = 0;
+    int prev = 0, n = 0;
     cudaGetDevice(&prev);
-    for (const auto& b : all) {
-        cudaSetDevice(b.device);
-        cudaFree(b.p);
+    cudaGetDeviceCount(&n);
+    for (int d = 0; d < n && d < 64; ++d) {
+        if (!g_pool_ready[d]) continue;
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, d) != cudaSuccess) continue;
+        cudaSetDevice(d);
+        cudaDeviceSynchronize();
+        cudaMemPoolTrimTo(pool, 0);
     }
     cudaSetDevice(prev);
+}
+
+size_t dev_cached_bytes() {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) != cudaSuccess) return 0;
+    uint64_t reserved = 0, used = 0;
+    cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &reserved);
+    cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used);
+    return reserved > used ? (size_t)(reserved - used) : 0;
 }
 
 DevGraph Graph::view() const {

@@ -36,6 +36,7 @@ inline void invalid(const std::string& msg) { throw Error(MHW_ERR_INVALID, msg);
 void* dev_alloc(size_t bytes, size_t* cap);
 void dev_free(void* p, size_t cap);
 void dev_trim();
+size_t dev_cached_bytes();
 
 // RAII device buffer on the current device.
 template <class T>

@@ -1354,18 +1354,27 @@ void session_run_packed(Session& s, uint32_t* h_nodes, uint64_t cap_nodes, uint6
         mhw_walk_stats st{};
         session_stats(s, st);
         if (stats) *stats = st;
+        const double t_done = ms_since(ta);
+        hold_tot.reset();
+        const double t_freehost = ms_since(ta);
         if (trace)
             std::fprintf(stderr,
                          "[mhw] run_packed: %d chunks, setup %.2f ms, last copy issued %.2f ms, done %.2f ms, "
-                         "device walk+pack %.2f ms\n",
-                         chunks, t_setup, t_issued, ms_since(ta), st.walk_seconds * 1e3);
+                         "freehost %.2f ms, device walk+pack %.2f ms\n",
+                         chunks, t_setup, t_issued, t_done, t_freehost, st.walk_seconds * 1e3);
     } catch (...) {
         cudaStreamSynchronize(S);
         if (T) cudaStreamSynchronize(T);
         cleanup();
         throw;
     }
-    cleanup();
+    if (trace) {
+        const double t0 = ms_since(ta);
+        cleanup();
+        std::fprintf(stderr, "[mhw] run_packed: locals freed at %.2f ms, cleanup %.2f ms\n", t0, ms_since(ta) - t0);
+    } else {
+        cleanup();
+    }
 }
 
 // ------------------------------------------------------------ parity API

@@ -40,7 +40,7 @@ out = torch.empty(cap, dtype=torch.int32).pin_memory()
 offs = torch.empty(rows.value + 1, dtype=torch.int64).pin_memory()
 pad = torch.empty(rows.value * stride.value, dtype=torch.int32).pin_memory()
 lens = torch.empty(rows.value, dtype=torch.int32).pin_memory()
-for it in range(3):
+for it in range(int(sys.argv[2]) if len(sys.argv) > 2 else 3):
     t0 = time.perf_counter()
     h = C.c_void_p()
     lib.mhw_graph_upload(C.byref(view), 0, C.byref(h))
