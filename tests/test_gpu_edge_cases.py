@@ -59,10 +59,12 @@ def test_asymmetric_adjacency_raises_like_update_state(mhw):
     g = O.make_graph(3, [(0, 1, 1.0), (1, 2, 1.0), (2, 0, 1.0)], symmetric=True)
     dg = device_graph(g)
     assert not dg.info()["verified_symmetric"]
-    for threads in (1, 8):
-        with pytest.raises(mhw.ValidationError, match="asymmetric adjacency: no back edge"):
-            mhw.generate_walks(dg, walk_model(model_desc(O.NODE2VEC, g)),
-                               mhw.WalkConfig(walks_per_node=1, walk_length=5, threads=threads))
+    O.assign_random_types(g, 2, O.XoRng(1))
+    for kind in (O.NODE2VEC, O.EDGE2VEC, O.FAIRWALK):
+        for threads in (1, 8):
+            with pytest.raises(mhw.ValidationError, match="asymmetric adjacency: no back edge"):
+                mhw.generate_walks(device_graph(g), walk_model(model_desc(kind, g)),
+                                   mhw.WalkConfig(walks_per_node=1, walk_length=5, threads=threads))
 
 
 def test_dead_end_state_terminates_early(mhw, oracle):

@@ -328,6 +328,27 @@ def test_throughput_transitions_pass_chain_chi_square(mhw, oracle, kind):
     assert ok_c, "control: " + msg_c
 
 
+@pytest.mark.parametrize("kind", [O.NODE2VEC, O.EDGE2VEC, O.FAIRWALK])
+def test_lazy_colocated_chains_pass_chain_chi_square(mhw, oracle, kind):
+    """Second-order throughput walks with lazy slot init (init_mode 1): the
+    colocated chain words start EMPTY and are initialised on first visit with
+    the slot-keyed draws; explicit edge types for edge2vec."""
+    g = typed_random_graph(500 + kind, 40, 4.0, weighted=True, types=2)
+    r = np.random.default_rng(kind)
+    pairs = {}
+    for v in range(g.n):
+        for u in g.neighbors_of(v):
+            pairs.setdefault((min(v, int(u)), max(v, int(u))), int(r.integers(0, 3)))
+    g.etype = np.array([pairs[(min(v, int(u)), max(v, int(u)))] for v in range(g.n) for u in g.neighbors_of(v)],
+                       dtype=np.uint16)
+    g.n_etypes = 3
+    md = model_desc(kind, g, p=0.5, q=2.0, M=r.uniform(0.5, 2.0, (3, 3)))
+    cfg = O.WalkCfg(K=400, L=80, seed=78, init_kind=O.INIT_BURN_IN, burn_in_steps=3)
+    c = mhw.generate_walks(device_graph(g), walk_model(md), walk_config(cfg, threads=8, init_mode=1))
+    ok, msg = gate(audit(g, oracle, md, c.rows, c.lengths, min_visits=5000))
+    assert ok, msg
+
+
 @pytest.mark.parametrize("rep", [8, 1, 0])
 def test_hub_replicas_pass_chain_chi_square(mhw, oracle, rep):
     """Deepwalk on a hub-heavy graph with replicated hub chains (8, every
