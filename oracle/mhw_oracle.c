@@ -324,6 +324,33 @@ uint32_t og_pair_etype(uint64_t seed, uint32_t lo, uint32_t hi, uint32_t n_types
     return draw_index(&d, n_types);
 }
 
+void og_pair_weights(uint64_t seed, uint64_t n, const uint32_t* lo, const uint32_t* hi, float wlo, float whi,
+                     float* out) {
+    for (uint64_t i = 0; i < n; ++i) out[i] = og_pair_weight(seed, lo[i], hi[i], wlo, whi);
+}
+
+void og_pair_etypes(uint64_t seed, uint64_t n, const uint32_t* lo, const uint32_t* hi, uint32_t n_types,
+                    uint16_t* out) {
+    for (uint64_t i = 0; i < n; ++i) out[i] = (uint16_t)og_pair_etype(seed, lo[i], hi[i], n_types);
+}
+
+/* graph_checksum (tools/mhwalk.cpp:107-122): FNV-1a over offsets, neighbour
+ * ids and the f64 bits of the weights (1.0 per arc when w is NULL). */
+uint64_t og_graph_checksum(uint32_t n, const uint64_t* offsets, const uint32_t* nbr, const double* w) {
+    uint64_t h = 0xcbf29ce484222325ULL;
+    const uint64_t m = offsets[n];
+    for (uint64_t i = 0; i <= n; ++i) { h ^= offsets[i]; h *= 0x100000001b3ULL; }
+    for (uint64_t i = 0; i < m; ++i) { h ^= nbr[i]; h *= 0x100000001b3ULL; }
+    for (uint64_t i = 0; i < m; ++i) {
+        const double x = w ? w[i] : 1.0;
+        uint64_t bits;
+        memcpy(&bits, &x, sizeof bits);
+        h ^= bits;
+        h *= 0x100000001b3ULL;
+    }
+    return h;
+}
+
 /* Heterogeneous A/P/V graph (BASELINE cfg3): types contiguous by id
  * (A = [0,nA), P = [nA,nA+nP), V = rest). A node a draws Poisson(8) (Knuth
  * product method on Philox units of block (a, j)) P targets uniformly; each P

@@ -111,6 +111,12 @@ int og_rmat_pairs(uint32_t scale, uint32_t edge_factor, double a, double b, doub
                   uint64_t seed, uint64_t* n_pairs, uint32_t** lo, uint32_t** hi);
 float og_pair_weight(uint64_t seed, uint32_t lo, uint32_t hi, float wlo, float whi);
 uint32_t og_pair_etype(uint64_t seed, uint32_t lo, uint32_t hi, uint32_t n_types);
+void og_pair_weights(uint64_t seed, uint64_t n, const uint32_t* lo, const uint32_t* hi, float wlo, float whi,
+                     float* out);
+void og_pair_etypes(uint64_t seed, uint64_t n, const uint32_t* lo, const uint32_t* hi, uint32_t n_types,
+                    uint16_t* out);
+/* graph_checksum of tools/mhwalk.cpp:107-122 (FNV-1a; w NULL = all 1.0) */
+uint64_t og_graph_checksum(uint32_t n, const uint64_t* offsets, const uint32_t* nbr, const double* w);
 int og_hetero_pairs(uint32_t n_nodes, uint64_t seed, uint32_t* nA, uint32_t* nP,
                     uint64_t* n_pairs, uint32_t** lo, uint32_t** hi);
 void og_free(void* p);

@@ -35,6 +35,7 @@ _u16p = C.POINTER(C.c_uint16)
 _u32p = C.POINTER(C.c_uint32)
 _u64p = C.POINTER(C.c_uint64)
 _dp = C.POINTER(C.c_double)
+_fp = C.POINTER(C.c_float)
 
 
 def _ptr(a, t):
@@ -174,6 +175,10 @@ class Oracle:
         L.og_pair_weight.restype = C.c_float
         L.og_pair_etype.argtypes = [C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint32]
         L.og_pair_etype.restype = C.c_uint32
+        L.og_pair_weights.argtypes = [C.c_uint64, C.c_uint64, _u32p, _u32p, C.c_float, C.c_float, _fp]
+        L.og_pair_etypes.argtypes = [C.c_uint64, C.c_uint64, _u32p, _u32p, C.c_uint32, _u16p]
+        L.og_graph_checksum.argtypes = [C.c_uint32, _u64p, _u32p, _dp]
+        L.og_graph_checksum.restype = C.c_uint64
         L.og_free.argtypes = [C.c_void_p]
         L.og_model_bind.argtypes = [C.POINTER(_OgGraph), C.POINTER(_OgModel), C.c_char_p, C.c_size_t]
         L.og_decide.argtypes = [C.POINTER(_OgGraph), C.POINTER(_OgModel), C.c_uint64, _u32p, _u32p,
@@ -250,12 +255,25 @@ class Oracle:
         return lo, hi, nA.value, nP.value
 
     def pair_weights(self, seed, lo, hi, wlo, whi):
-        f = self.lib.og_pair_weight
-        return np.array([f(seed, int(a), int(b), wlo, whi) for a, b in zip(lo, hi)], dtype=np.float32)
+        lo = np.ascontiguousarray(lo, dtype=np.uint32)
+        hi = np.ascontiguousarray(hi, dtype=np.uint32)
+        out = np.zeros(len(lo), dtype=np.float32)
+        self.lib.og_pair_weights(seed, len(lo), _ptr(lo, _u32p), _ptr(hi, _u32p), wlo, whi, _ptr(out, _fp))
+        return out
 
     def pair_etypes(self, seed, lo, hi, n_types):
-        f = self.lib.og_pair_etype
-        return np.array([f(seed, int(a), int(b), n_types) for a, b in zip(lo, hi)], dtype=np.uint16)
+        lo = np.ascontiguousarray(lo, dtype=np.uint32)
+        hi = np.ascontiguousarray(hi, dtype=np.uint32)
+        out = np.zeros(len(lo), dtype=np.uint16)
+        self.lib.og_pair_etypes(seed, len(lo), _ptr(lo, _u32p), _ptr(hi, _u32p), n_types, _ptr(out, _u16p))
+        return out
+
+    def graph_checksum(self, offsets, nbr, w=None):
+        """graph_checksum of tools/mhwalk.cpp:107-122 (FNV-1a)."""
+        off = np.ascontiguousarray(offsets, dtype=np.uint64)
+        nb = np.ascontiguousarray(nbr, dtype=np.uint32)
+        wa = None if w is None else np.ascontiguousarray(w, dtype=np.float64)
+        return int(self.lib.og_graph_checksum(len(off) - 1, _ptr(off, _u64p), _ptr(nb, _u32p), _ptr(wa, _dp)))
 
     # -------------------------------------------------------------- models
     def bind(self, g: HostGraph, md: ModelDesc):
