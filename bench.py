@@ -107,6 +107,14 @@ def make_model(cfg):
                          type_matrix=type_matrix(cfg) if cfg["model"] == "edge2vec" else None)
 
 
+def eager_at_n1(cfg, g):
+    """Would one GPU initialise every slot eagerly (session_create's rule:
+    walker steps >= 8 x slots)? Then N ranks share that work instead."""
+    off = g.download()["offsets"]
+    walkers = int(np.count_nonzero(np.diff(off))) * cfg["K"]
+    return walkers * cfg["L"] >= 8 * int(off[-1])
+
+
 def make_config(cfg, node_begin=0, node_end=0):
     import paper_2010_04895_b200 as mhw
     return mhw.WalkConfig(walks_per_node=cfg["K"], walk_length=cfg["L"], threads=8, seed=WALK_SEED,
@@ -292,6 +300,14 @@ def run_mine(args, cfg):
     model = make_model(cfg)
     cuts = mhw.partition_nodes(g, model, world)
     wcfg = make_config(cfg, int(cuts[rank]), int(cuts[rank + 1]))
+    # Multi-GPU, second-order models with an eagerly initialised chain table
+    # (walks touch most slots): the initial table is a pure function of the
+    # slot, so each rank initialises 1/N of the slots and the words are
+    # all-gathered (the walk itself has no exchange).
+    shard_init = (world > 1 and cfg["model"] in ("node2vec", "edge2vec", "fairwalk")
+                  and cfg.get("sampler", "mh") == "mh" and eager_at_n1(cfg, g))
+    if shard_init:
+        wcfg.init_mode = 2
     sess = mhw.Session(g, model, wcfg)
     t_setup = time.time() - t0
     info = g.info()
@@ -307,8 +323,30 @@ def run_mine(args, cfg):
             dist.barrier()
         torch.cuda.synchronize(dev)
 
-    for _ in range(args.warmup):
+    per = 0
+    if shard_init:
+        S = sess.chain_size()
+        per = (S + world - 1) // world
+        c_dev = "cpu" if host_coll else dev
+        shard = torch.empty(per, dtype=torch.int32, device=dev)
+        full = torch.empty(per * world, dtype=torch.int32, device=dev)
+        lo, hi = min(S, rank * per), min(S, (rank + 1) * per)
+
+    def one_run():
+        if shard_init:
+            sess.init_chain(lo, hi, shard.data_ptr(), stream.cuda_stream)
+            if host_coll:
+                parts = [torch.empty(per, dtype=torch.int32) for _ in range(world)]
+                dist.all_gather(parts, shard.cpu())
+                full.copy_(torch.cat(parts).to(dev))
+            else:
+                dist.all_gather_into_tensor(full, shard)
+            sess.load_chain(full.data_ptr(), stream.cuda_stream)
         sess.run(stream.cuda_stream)
+        return sess.launches() + (2 if shard_init else 0)
+
+    for _ in range(args.warmup):
+        one_run()
     torch.cuda.synchronize(dev)
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     steps_total = 0
@@ -318,9 +356,9 @@ def run_mine(args, cfg):
         for i in range(args.steps):
             flush.zero_()
             ev[i][0].record(stream)
-            sess.run(stream.cuda_stream)
+            n_launch = one_run()
             ev[i][1].record(stream)
-            launches += sess.launches()
+            launches += n_launch
         barrier()
     ms = [a.elapsed_time(b) for a, b in ev]
     st = sess.stats()   # counters of the last run (identical work every run)
@@ -369,7 +407,8 @@ def run_mine(args, cfg):
                        "sampler": cfg.get("sampler", "mh"), "rejection_trials": st.rejection_trials,
                        "seed": SEED, "walk_seed": WALK_SEED,
                        "l2": "explicit 256 MB L2 flush between timed steps (also inputs > L2)",
-                       "parallelism": f"walker ranges x{world}, CSR replicated"},
+                       "parallelism": f"walker ranges x{world}, CSR replicated"
+                                      + (", chain init sharded + all-gather" if shard_init else "")},
             "roofline": roof, "clocks": clk.summary(), "gpu_launches": launches_job,
             "setup_seconds": t_setup,
         }

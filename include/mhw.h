@@ -301,6 +301,18 @@ MHW_API mhw_status mhw_session_download(mhw_session* s, uint32_t* h_nodes, uint3
 MHW_API mhw_status mhw_session_write_corpus(mhw_session* s, const char* path);
 /* Number of kernels the last mhw_session_run enqueued. */
 MHW_API uint32_t mhw_session_launches(const mhw_session* s);
+/* Sharded chain initialisation (second-order models, multi-GPU): the initial
+ * chain table is a pure function of (graph, model, init strategy, seed, slot)
+ * (slot-keyed init draws, mh_init samplers.cpp:37-83), so ranks can each
+ * initialise a slot range and all-gather the words instead of every rank
+ * initialising every slot. chain_size = slots (arcs); init_chain writes the
+ * initial words of slots [begin, end) to d_words (device, end - begin
+ * entries) on `stream`; load_chain installs a full table (chain_size words)
+ * for the NEXT mhw_session_run, which then skips its reset and eager init. */
+MHW_API mhw_status mhw_session_chain_size(const mhw_session* s, uint64_t* words);
+MHW_API mhw_status mhw_session_init_chain(mhw_session* s, uint64_t begin, uint64_t end, uint32_t* d_words,
+                                          void* stream);
+MHW_API mhw_status mhw_session_load_chain(mhw_session* s, const uint32_t* d_words, void* stream);
 MHW_API void mhw_session_free(mhw_session* s);
 
 /* ---- parity entry points ---------------------------------------------- */

@@ -93,6 +93,9 @@ SIGNATURES = {
     "mhw_session_buffers": (C.c_int32, [_P, _PP, _PP, C.POINTER(C.c_uint64), C.POINTER(C.c_uint32)]),
     "mhw_session_download": (C.c_int32, [_P, _P, _P, _P]),
     "mhw_session_launches": (C.c_uint32, [_P]),
+    "mhw_session_chain_size": (C.c_int32, [_P, C.POINTER(C.c_uint64)]),
+    "mhw_session_init_chain": (C.c_int32, [_P, C.c_uint64, C.c_uint64, _P, _P]),
+    "mhw_session_load_chain": (C.c_int32, [_P, _P, _P]),
     "mhw_session_free": (None, [_P]),
     "mhw_decide": (C.c_int32, [_P, C.POINTER(ModelDescC), C.c_uint64, _P, _P, _P, _P, _P, _P, _P, _P]),
     "mhw_alias_tables": (C.c_int32, [_P, _P, _P]),

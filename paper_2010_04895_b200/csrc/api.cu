@@ -580,6 +580,30 @@ mhw_status mhw_session_download(mhw_session* s, uint32_t* h_nodes, uint32_t* h_l
 
 uint32_t mhw_session_launches(const mhw_session* s) { return s ? s->launches : 0; }
 
+mhw_status mhw_session_chain_size(const mhw_session* s, uint64_t* words) {
+    return guard([&] {
+        need(s, "session");
+        need(words, "words");
+        *words = mhw::second_order(s->model.dev.kind) ? s->g->m : 0;
+    });
+}
+
+mhw_status mhw_session_init_chain(mhw_session* s, uint64_t begin, uint64_t end, uint32_t* d_words, void* stream) {
+    return guard([&] {
+        need(s, "session");
+        if (end > begin) need(d_words, "d_words");
+        mhw::session_init_chain(*s, begin, end, d_words, static_cast<cudaStream_t>(stream));
+    });
+}
+
+mhw_status mhw_session_load_chain(mhw_session* s, const uint32_t* d_words, void* stream) {
+    return guard([&] {
+        need(s, "session");
+        need(d_words, "d_words");
+        mhw::session_load_chain(*s, d_words, static_cast<cudaStream_t>(stream));
+    });
+}
+
 void mhw_session_free(mhw_session* s) {
     if (!s) return;
     int dev = s->g ? s->g->device : 0;

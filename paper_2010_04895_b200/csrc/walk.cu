@@ -356,6 +356,42 @@ __global__ void __launch_bounds__(256) k_init_all(RunParams P) {
     if (inits) atomicAdd(&P.ctr[3], inits);
 }
 
+// Initial chain words of slots [b, e) (sharded init): k_init_all's work for
+// a slot range, written contiguously.
+template <int KIND>
+__global__ void __launch_bounds__(256) k_init_range(RunParams P, uint64_t b, uint64_t e, uint32_t* __restrict__ out) {
+    const DevGraph& g = P.g;
+    for (uint64_t a = b + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; a < e;
+         a += (uint64_t)gridDim.x * blockDim.x) {
+        uint32_t lo = 0, hi = g.n;
+        while (hi - lo > 1) {
+            const uint32_t mid = (lo + hi) >> 1;
+            if ((uint64_t)__ldg(&g.nodes[mid].off) <= a) lo = mid;
+            else hi = mid;
+        }
+        const NodeRec r = load_node(g, lo);
+        const SCtx c = make_ctx<KIND>(g, P.m, lo, (uint32_t)(a - (uint64_t)r.off));
+        out[a - b] = init_slot<KIND>(g, P.m, P.cfg, c, a);
+    }
+}
+
+// Installs a full table of slot words: colocated words go to the record of
+// the forward arc s->v of slot (v, affix), s = N(v)[affix].
+__global__ void k_load_chain(DevGraph g, const uint32_t* __restrict__ w, uint4* __restrict__ ac, uint32_t rs,
+                             uint32_t* __restrict__ chain) {
+    for (uint64_t a = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; a < g.m;
+         a += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t e = __ldg(w + a);
+        if (ac) {
+            const uint32_t s = load_id(g, a);
+            const uint32_t sv = __ldg(g.rev + a);
+            if (sv != kNoBack) reinterpret_cast<uint32_t*>(ac + rs * ((uint64_t)load_node(g, s).off + sv))[3] = e;
+        } else {
+            chain[a] = e;
+        }
+    }
+}
+
 // Session arc records (walk.h ArcRec): word 0 = {id u, deg(u) | allpos << 31,
 // off(u), chain word (second order) }, typed models add word 1 = {fp32
 // weight, type(u) | edge_type(arc) << 16, 0, 0}. Warp per source node (its
@@ -1106,9 +1142,11 @@ void session_run(Session& s, cudaStream_t user) {
     cudaStream_t st = user ? user : s.stream;
     const RunParams P = s.params();
     s.launches = 0;
-    MHW_CK(cudaMemsetAsync(s.chain.p, 0xFF, s.chain.bytes(), st));
+    const bool preloaded = s.chain_loaded;  // mhw_session_load_chain: table already initialised
+    s.chain_loaded = false;
+    if (!preloaded) MHW_CK(cudaMemsetAsync(s.chain.p, 0xFF, s.chain.bytes(), st));
     MHW_CK(cudaMemsetAsync(s.ctr.p, 0, s.ctr.bytes(), st));
-    if (s.ac.n && second_order(s.model.dev.kind) && (!s.eager_init || !s.g->verified_sym)) {
+    if (!preloaded && s.ac.n && second_order(s.model.dev.kind) && (!s.eager_init || !s.g->verified_sym)) {
         k_ac_reset<<<grid_for(s.g->m), 256, 0, st>>>(s.ac.p, s.g->m, s.rec_words);
         ++s.launches;
     }
@@ -1157,7 +1195,7 @@ void session_run(Session& s, cudaStream_t user) {
             dispatch(s.model.dev.kind, [&](auto kc) {
                 constexpr int KIND = decltype(kc)::value;
                 if constexpr (second_order(KIND)) {
-                    if (s.eager_init) {
+                    if (s.eager_init && !preloaded) {
                         k_init_all<KIND><<<grid_for(s.g->m), 256, 0, st>>>(P);
                         ++s.launches;
                     }
@@ -1172,6 +1210,35 @@ void session_run(Session& s, cudaStream_t user) {
         MHW_CK(cudaGetLastError());
     }
     MHW_CK(cudaEventRecord(s.ev1, st));
+}
+
+void session_init_chain(Session& s, uint64_t begin, uint64_t end, uint32_t* d_words, cudaStream_t user) {
+    DeviceGuard dg(s.g->device);
+    if (!second_order(s.model.dev.kind) || s.ex || s.wc.schedule == MHW_SCHEDULE_DETERMINISTIC)
+        invalid("chain preloading applies to second-order models on the throughput schedule");
+    if (begin > end || end > s.g->m) invalid("slot range out of bounds");
+    if (begin == end) return;
+    cudaStream_t st = user ? user : s.stream;
+    const RunParams P = s.params();
+    dispatch(s.model.dev.kind, [&](auto kc) {
+        constexpr int KIND = decltype(kc)::value;
+        if constexpr (second_order(KIND))
+            k_init_range<KIND><<<grid_for(end - begin), 256, 0, st>>>(P, begin, end, d_words);
+    });
+    MHW_CK(cudaGetLastError());
+}
+
+void session_load_chain(Session& s, const uint32_t* d_words, cudaStream_t user) {
+    DeviceGuard dg(s.g->device);
+    if (!second_order(s.model.dev.kind) || s.ex || s.wc.schedule == MHW_SCHEDULE_DETERMINISTIC)
+        invalid("chain preloading applies to second-order models on the throughput schedule");
+    cudaStream_t st = user ? user : s.stream;
+    if (s.g->m) {
+        k_load_chain<<<grid_for(s.g->m), 256, 0, st>>>(s.g->view(), d_words, s.ac.n ? s.ac.p : nullptr,
+                                                         s.rec_words, s.chain.p);
+        MHW_CK(cudaGetLastError());
+    }
+    s.chain_loaded = true;
 }
 
 void session_stats(Session& s, mhw_walk_stats& out) {

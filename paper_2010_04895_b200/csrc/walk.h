@@ -65,6 +65,7 @@ struct Session {
     int sort_bits = 1;
     int grid = 0;
     bool eager_init = false;
+    bool chain_loaded = false;  // mhw_session_load_chain installed the initial table
     bool use_ar = false;     // arc-record walk kernel variant
     int minb = 1;
     uint32_t launches = 0;
@@ -81,6 +82,8 @@ struct Session {
 uint64_t k_slots(int kind, const Graph& g);
 void session_create(Session& s, Graph& g, const mhw_model_desc& md, const mhw_walk_config& wc);
 void session_run(Session& s, cudaStream_t stream);
+void session_init_chain(Session& s, uint64_t begin, uint64_t end, uint32_t* d_words, cudaStream_t stream);
+void session_load_chain(Session& s, const uint32_t* d_words, cudaStream_t stream);
 void session_stats(Session& s, mhw_walk_stats& out);
 void session_download(Session& s, uint32_t* nodes, uint32_t* lens, cudaStream_t stream);
 void session_write_corpus(Session& s, const char* path, const mhw_walk_stats& st);

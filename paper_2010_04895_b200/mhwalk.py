@@ -523,6 +523,21 @@ class Session:
     def launches(self) -> int:
         return L.lib().mhw_session_launches(self._h)
 
+    # sharded chain initialisation (multi-GPU): see include/mhw.h
+    def chain_size(self) -> int:
+        n = C.c_uint64()
+        _check(L.lib().mhw_session_chain_size(self._h, C.byref(n)))
+        return n.value
+
+    def init_chain(self, begin: int, end: int, d_words: int, stream: int | None = None):
+        """Initial words of slots [begin, end) into device memory d_words."""
+        _check(L.lib().mhw_session_init_chain(self._h, begin, end, C.c_void_p(d_words),
+                                              C.c_void_p(stream) if stream else None))
+
+    def load_chain(self, d_words: int, stream: int | None = None):
+        """Installs a full initial table (chain_size words) for the next run."""
+        _check(L.lib().mhw_session_load_chain(self._h, C.c_void_p(d_words), C.c_void_p(stream) if stream else None))
+
     def download(self, nodes=None, lengths=None, stream: int | None = None):
         if nodes is None:
             nodes = np.zeros((self.rows, self.stride), dtype=np.uint32)

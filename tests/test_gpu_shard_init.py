@@ -1,0 +1,78 @@
+"""Sharded chain initialisation (mhw_session_init_chain / _load_chain), the
+multi-GPU exchange of bench.py: the initial chain table is a pure function of
+(graph, model, init strategy, seed, slot), so ranks initialise slot ranges and
+all-gather the words. The words equal the slot-keyed mh_init of the oracle
+(samplers.cpp:37-83 under the engine's Philox layout), a table assembled from
+shards equals one initialised whole, and a run on a preloaded table skips its
+own initialisation and still passes the chain chi-square gate."""
+import numpy as np
+import pytest
+import torch
+
+from oracle import oracle as O
+from tests.helpers import device_graph, model_desc, typed_random_graph, walk_config, walk_model
+from tests.stats import audit, gate
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def mhw():
+    import paper_2010_04895_b200 as m
+    assert m.device_count() > 0
+    return m
+
+
+def _states(g):
+    deg = np.diff(g.offsets).astype(np.int64)
+    pos = np.repeat(np.arange(g.n, dtype=np.uint32), deg)
+    aff = (np.arange(g.m, dtype=np.int64) - np.repeat(g.offsets[:-1].astype(np.int64), deg)).astype(np.uint32)
+    return pos, aff
+
+
+@pytest.mark.parametrize("init", [O.INIT_RANDOM, O.INIT_HIGH_WEIGHT, O.INIT_BURN_IN])
+@pytest.mark.parametrize("kind", [O.NODE2VEC, O.EDGE2VEC, O.FAIRWALK])
+def test_sharded_init_words_equal_slot_init(mhw, oracle, kind, init):
+    g = typed_random_graph(700 + kind, 120, 6.0, weighted=True, types=2)
+    md = model_desc(kind, g, p=0.3, q=3.0, M=np.random.default_rng(kind).uniform(0.5, 2.0, (4, 4)))
+    cfg = O.WalkCfg(K=2, L=10, seed=19, init_kind=init, burn_in_steps=6, hw_sample_size=4)
+    s = mhw.Session(device_graph(g), walk_model(md), walk_config(cfg, threads=8, init_mode=2))
+    S = s.chain_size()
+    assert S == g.m
+    words = torch.empty(S, dtype=torch.int32, device="cuda")
+    cuts = [0, S // 3, (2 * S) // 3, S]  # three ragged shards
+    for b, e in zip(cuts[:-1], cuts[1:]):
+        s.init_chain(b, e, words.data_ptr() + 4 * b)
+    torch.cuda.synchronize()
+    raw = words.cpu().numpy().view(np.uint32)
+    # chain words carry the Last index and its cached alpha class (bits 30-31);
+    # init_states reports the index (sentinels unchanged)
+    got = np.where(raw >= 0xFFFFFFFD, raw, raw & 0x3FFFFFFF)
+    pos, aff = _states(g)
+    ref = mhw.init_states(device_graph(g), walk_model(md), walk_config(cfg, threads=8), pos, aff)
+    assert np.array_equal(got, ref)
+    for a in np.random.default_rng(kind + init).choice(g.m, 40, replace=False):
+        o = oracle.init_philox(g, md, cfg, int(pos[a]), int(aff[a]), int(a))
+        assert got[a] == (0xFFFFFFFE if o is None else o), a
+
+
+@pytest.mark.parametrize("kind", [O.NODE2VEC, O.FAIRWALK])
+def test_preloaded_chain_run_passes_chi_square(mhw, oracle, kind):
+    g = typed_random_graph(300 + kind, 40, 4.0, weighted=True, types=2)
+    md = model_desc(kind, g, p=0.5, q=2.0)
+    cfg = O.WalkCfg(K=400, L=80, seed=77, init_kind=O.INIT_BURN_IN, burn_in_steps=5)
+    s = mhw.Session(device_graph(g), walk_model(md), walk_config(cfg, threads=8, init_mode=2))
+    words = torch.empty(s.chain_size(), dtype=torch.int32, device="cuda")
+    half = s.chain_size() // 2
+    s.init_chain(0, half, words.data_ptr())
+    s.init_chain(half, s.chain_size(), words.data_ptr() + 4 * half)
+    s.load_chain(words.data_ptr())
+    s.run()
+    st = s.stats()
+    assert st.slot_inits == 0  # no eager or lazy init in the run itself
+    rows, lens = s.download()
+    ok, msg = gate(audit(g, oracle, md, rows, lens, min_visits=5000))
+    assert ok, msg
+    # the next run without a preload initialises on its own again
+    s.run()
+    assert s.stats().slot_inits == g.m
