@@ -128,6 +128,8 @@ DevGraph Graph::view() const {
     d.tcount = tcount.n ? tcount.p : nullptr;
     d.htab = htab.n ? htab.p : nullptr;
     d.arc = arc.n ? arc.p : nullptr;
+    d.bloom = bloom.n ? bloom.p : nullptr;
+    d.bloom_blocks = bloom_blocks;
     d.n_ntypes = n_ntypes;
     d.n_etypes = n_etypes;
     d.verified_sym = verified_sym ? 1 : 0;
@@ -136,7 +138,7 @@ DevGraph Graph::view() const {
 
 uint64_t Graph::device_bytes() const {
     return nodes.bytes() + ids.bytes() + w.bytes() + ntype.bytes() + etype.bytes() + rev.bytes() +
-           wtotal.bytes() + tcount.bytes() + htab.bytes() + arc.bytes();
+           wtotal.bytes() + tcount.bytes() + htab.bytes() + arc.bytes() + bloom.bytes();
 }
 
 namespace {
@@ -340,6 +342,27 @@ __global__ void k_tcount(DevGraph g, uint32_t* __restrict__ tc) {
         for (uint32_t i = lane; i < r.deg; i += 32) {
             const uint16_t t = load_node(g, load_id(g, r.off + i)).type;
             atomicAdd(tc + v * T + t, 1u);
+        }
+    }
+}
+
+// Edge Bloom filter: warp per node v, every arc v -> u sets the 4 bits of
+// the unordered key {v, u} (a symmetric pair sets them twice; an asymmetric
+// graph stays exact: any arc s -> x makes {s, x} a hit).
+__global__ void k_bloom_build(DevGraph g, uint32_t* __restrict__ bloom, uint32_t blocks) {
+    const unsigned lane = threadIdx.x & 31;
+    const uint64_t wid = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    for (uint64_t v = wid; v < g.n; v += nw) {
+        const NodeRec r = load_node(g, (uint32_t)v);
+        for (uint32_t i = lane; i < r.deg; i += 32) {
+            const uint32_t u = load_id(g, r.off + i);
+            const uint64_t x = bloom_key((uint32_t)v, u);
+            uint32_t* blk = bloom + 8 * (uint64_t)bloom_block(x, blocks);
+            for (int k = 0; k < 4; ++k) {
+                const uint32_t bit = (uint32_t)(x >> (8 * k)) & 255u;
+                atomicOr(blk + (bit >> 5), 1u << (bit & 31));
+            }
         }
     }
 }
@@ -1004,6 +1027,32 @@ void graph_ensure_hash(Graph& g) {
     g.htab.alloc(8 * buckets);
     MHW_CK(cudaMemsetAsync(g.htab.p, 0xFF, g.htab.bytes(), g.stream));
     k_hash_build<<<grid_for(g.m), kBlock, 0, g.stream>>>(g.view(), g.htab.p);
+    MHW_CK(cudaGetLastError());
+    MHW_CK(cudaStreamSynchronize(g.stream));
+}
+
+// Edge Bloom filter for the alpha test: 4 bits per arc (8 per undirected
+// edge, ~2.4% false positives), built only when it stays small enough to
+// live in L2 (MHW_BLOOM_MB, default 64 MB; MHW_BLOOM_BITS overrides the
+// density). Measured on cfg2: 4 bits/arc 41.2 ms, 8 bits 43.2, 16 bits
+// 46.5, none 48.8 -- L2 residency beats a lower false-positive rate.
+// MHW_BLOOM=0 disables it.
+void graph_ensure_bloom(Graph& g) {
+    if (g.bloom.n || !g.m) return;
+    const char* off = std::getenv("MHW_BLOOM");
+    if (off && off[0] == '0') return;
+    const char* mb = std::getenv("MHW_BLOOM_MB");
+    const uint64_t budget = (uint64_t)(mb ? std::atoll(mb) : 64) << 20;
+    const char* bits = std::getenv("MHW_BLOOM_BITS");
+    const uint64_t bytes = g.m * (uint64_t)(bits ? std::atoi(bits) : 4) / 8;  // bits per arc
+    if (bytes > budget || bytes < 32) return;
+    const uint64_t blocks = (bytes + 31) / 32;
+    if (blocks >= (1ull << 32)) return;
+    DeviceGuard dg(g.device);
+    g.bloom.alloc(8 * blocks);
+    g.bloom_blocks = (uint32_t)blocks;
+    MHW_CK(cudaMemsetAsync(g.bloom.p, 0, g.bloom.bytes(), g.stream));
+    k_bloom_build<<<grid_for(g.n * 32ull), kBlock, 0, g.stream>>>(g.view(), g.bloom.p, g.bloom_blocks);
     MHW_CK(cudaGetLastError());
     MHW_CK(cudaStreamSynchronize(g.stream));
 }

@@ -65,6 +65,8 @@ struct DevGraph {
     const uint32_t* __restrict__ tcount;  // fairwalk type counts, n * n_ntypes
     const uint32_t* __restrict__ htab;    // adjacency hash sets (nullptr: not built)
     const uint4* __restrict__ arc;        // arc records (nullptr: not built)
+    const uint32_t* __restrict__ bloom;   // edge Bloom filter, 8 words per block (nullptr: not built)
+    uint32_t bloom_blocks;
     uint16_t n_ntypes;
     uint16_t n_etypes;
     int verified_sym;                     // every arc has its back arc
@@ -108,6 +110,38 @@ __host__ __device__ __forceinline__ uint32_t hash_bucket(uint32_t key, uint32_t 
     h *= 0xC2B2AE35u;
     h ^= h >> 16;
     return (uint32_t)(((uint64_t)h * nb) >> 32);
+}
+
+// ------------------------------------------------------ edge Bloom filter
+// Blocked Bloom filter over undirected edges {a, b}: one 32-byte block per
+// key (one sector, L2-resident when it fits), 4 bits set inside it. A miss
+// proves non-adjacency exactly; a hit falls through to the exact test.
+__host__ __device__ __forceinline__ uint64_t bloom_key(uint32_t a, uint32_t b) {
+    uint64_t x = a < b ? (((uint64_t)a << 32) | b) : (((uint64_t)b << 32) | a);
+    x ^= x >> 33;
+    x *= 0xff51afd7ed558ccdull;
+    x ^= x >> 33;
+    x *= 0xc4ceb9fe1a85ec53ull;
+    x ^= x >> 33;
+    return x;
+}
+
+__host__ __device__ __forceinline__ uint32_t bloom_block(uint64_t x, uint32_t blocks) {
+    return (uint32_t)(((x >> 32) * (uint64_t)blocks) >> 32);
+}
+
+__device__ __forceinline__ bool bloom_maybe(const DevGraph& g, uint32_t a, uint32_t b) {
+    const uint64_t x = bloom_key(a, b);
+    const uint4* blk = reinterpret_cast<const uint4*>(g.bloom) + 2 * (uint64_t)bloom_block(x, g.bloom_blocks);
+    const uint4 lo = __ldg(blk), hi = __ldg(blk + 1);
+    const uint32_t w[8] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};
+    bool all = true;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const uint32_t bit = (uint32_t)(x >> (8 * k)) & 255u;
+        all &= (w[bit >> 5] >> (bit & 31)) & 1u;
+    }
+    return all;
 }
 
 __device__ __forceinline__ bool hash_contains(const uint32_t* __restrict__ tab, long long off, uint32_t v,
@@ -346,6 +380,9 @@ __device__ __forceinline__ uint32_t alpha_class(const DevGraph& g, const DevMode
                                                 uint32_t u, const NodeRec* urec) {
     if (m.alpha_trivial) return 1;
     if (u == c.s) return 0;
+    // the L2-resident edge filter settles most non-adjacent pairs without a
+    // DRAM access
+    if (g.bloom && !bloom_maybe(g, c.s, u)) return 2;
     // s's own hash set needs nothing about u: probe it without waiting for
     // the candidate's node record (shorter dependency chain per step).
     if (g.htab && c.deg_s >= kHashMinDeg) return hash_contains(g.htab, c.off_s, c.s, c.deg_s, u) ? 1u : 2u;

@@ -909,7 +909,10 @@ void model_bind(Model& mb, Graph& g, const mhw_model_desc& d) {
     if (second_order(k)) {
         graph_ensure_rev(g);
         graph_ensure_wtotal(g);
-        if (!m.alpha_trivial) graph_ensure_hash(g);
+        if (!m.alpha_trivial) {
+            graph_ensure_hash(g);
+            graph_ensure_bloom(g);
+        }
     }
     if (k == FAIRWALK) graph_ensure_tcount(g);
 }
@@ -1079,6 +1082,19 @@ void session_create(Session& s, Graph& g, const mhw_model_desc& md, const mhw_wa
         const bool dense = (double)s.n_items * s.cfg.L >= 8.0 * (double)s.slots;
         s.eager_init = second_order(m.kind) && (wc.init_mode == 2 || (wc.init_mode == 0 && dense));
         s.minb = walk_minb(m.kind);
+        // pin a small edge filter in L2 (cfg2: 16 MB, +3%; a 64 MB window
+        // starves the rest of the working set: cfg4 -30%)
+        if (g.bloom.n && g.bloom.bytes() <= (24ull << 20)) {
+            int dev = 0, max_persist = 0;
+            MHW_CK(cudaGetDevice(&dev));
+            MHW_CK(cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, dev));
+            size_t cur = 0;
+            MHW_CK(cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize));
+            if ((size_t)max_persist >= g.bloom.bytes()) {
+                if (cur < g.bloom.bytes()) MHW_CK(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, g.bloom.bytes()));
+                s.l2_pin = true;
+            }
+        }
         // arc records (after the session buffers, so the memory check sees them)
         const char* ar_env = std::getenv("MHW_ARC_RECORDS");
         const bool want_ar = !(ar_env && ar_env[0] == '0');
@@ -1113,6 +1129,18 @@ void session_create(Session& s, Graph& g, const mhw_model_desc& md, const mhw_wa
     MHW_CK(cudaStreamSynchronize(st));
 }
 
+// Persisting L2 access window over [p, p + bytes) on stream st (bytes 0
+// clears it). The device's persisting set-aside is raised once to fit.
+static void l2_window(cudaStream_t st, void* p, size_t bytes) {
+    cudaStreamAttrValue attr{};
+    attr.accessPolicyWindow.base_ptr = p;
+    attr.accessPolicyWindow.num_bytes = bytes;
+    attr.accessPolicyWindow.hitRatio = bytes ? 1.0f : 0.0f;
+    attr.accessPolicyWindow.hitProp = bytes ? cudaAccessPropertyPersisting : cudaAccessPropertyNormal;
+    attr.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+    MHW_CK(cudaStreamSetAttribute(st, cudaStreamAttributeAccessPolicyWindow, &attr));
+}
+
 uint64_t k_slots(int kind, const Graph& g) {
     if (kind == DEEPWALK) return g.n;
     if (kind == METAPATH2VEC) return (uint64_t)g.n * g.n_ntypes;
@@ -1142,6 +1170,10 @@ void session_run(Session& s, cudaStream_t user) {
     cudaStream_t st = user ? user : s.stream;
     const RunParams P = s.params();
     s.launches = 0;
+    // A small edge filter is pinned in L2 for the walk (persisting access
+    // window on the launch stream, cleared again after the launches).
+    const bool pin = s.l2_pin && s.g->bloom.n;
+    if (pin) l2_window(st, s.g->bloom.p, s.g->bloom.bytes());
     const bool preloaded = s.chain_loaded;  // mhw_session_load_chain: table already initialised
     s.chain_loaded = false;
     if (!preloaded) MHW_CK(cudaMemsetAsync(s.chain.p, 0xFF, s.chain.bytes(), st));
@@ -1209,6 +1241,7 @@ void session_run(Session& s, cudaStream_t user) {
         }
         MHW_CK(cudaGetLastError());
     }
+    if (pin) l2_window(st, nullptr, 0);
     MHW_CK(cudaEventRecord(s.ev1, st));
 }
 
@@ -1307,6 +1340,21 @@ void session_download_packed(Session& s, uint32_t* h_nodes, uint64_t cap_nodes, 
 // are contiguous); chunk c is walked, packed on the device and copied to the
 // host on a second stream while chunk c+1 walks. Every chunk shares the chain
 // table (same sampler state as one launch; only the interleaving differs).
+// Pinned per-chunk totals for session_run_packed: one process-wide buffer
+// per host thread, grown on demand and never freed (cudaFreeHost can stall a
+// call for 100+ ms).
+static uint64_t* pinned_scratch(size_t n) {
+    thread_local uint64_t* buf = nullptr;
+    thread_local size_t cap = 0;
+    if (n > cap) {
+        uint64_t* p = nullptr;
+        MHW_CK(cudaMallocHost(&p, std::max<size_t>(n, 64) * sizeof(uint64_t)));
+        buf = p;  // the previous (smaller) buffer is kept: it may still be in use by an unfinished caller
+        cap = std::max<size_t>(n, 64);
+    }
+    return buf;
+}
+
 void session_run_packed(Session& s, uint32_t* h_nodes, uint64_t cap_nodes, uint64_t* h_offsets,
                         uint64_t cap_rows, int chunks, mhw_walk_stats* stats) {
     DeviceGuard dg(s.g->device);
@@ -1347,9 +1395,7 @@ void session_run_packed(Session& s, uint32_t* h_nodes, uint64_t cap_nodes, uint6
         DBuf<uint32_t> packed(std::max<uint64_t>(s.rows * rowcap, 1));
         DBuf<uint64_t> len64(s.rows + 1), goff(s.rows + 1);
         std::vector<DBuf<uint64_t>> offc(chunks);
-        uint64_t* h_tot = nullptr;
-        MHW_CK(cudaMallocHost(&h_tot, chunks * sizeof(uint64_t)));
-        std::unique_ptr<uint64_t, decltype(&cudaFreeHost)> hold_tot(h_tot, cudaFreeHost);
+        uint64_t* h_tot = pinned_scratch(chunks);
         size_t scan_bytes = 0;
         MHW_CK(cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, len64.p, goff.p, (int64_t)s.rows + 1, S));
         DBuf<uint8_t> scan_tmp(std::max<size_t>(scan_bytes, 1));
@@ -1362,6 +1408,8 @@ void session_run_packed(Session& s, uint32_t* h_nodes, uint64_t cap_nodes, uint6
         if (s.n_iso)
             k_iso_rows<<<grid_for((uint64_t)s.n_iso * s.cfg.K), 256, 0, S>>>(s.iso.p, s.iso_row.p, s.n_iso, s.cfg.K,
                                                                              s.out.p, s.stride, s.lens.p);
+        const bool pin = s.l2_pin && s.g->bloom.n;
+        if (pin) l2_window(S, s.g->bloom.p, s.g->bloom.bytes());
         MHW_CK(cudaEventRecord(s.ev0, S));
         const double t_setup = ms_since(ta);
         dispatch(s.model.dev.kind, [&](auto kc) {
@@ -1396,6 +1444,7 @@ void session_run_packed(Session& s, uint32_t* h_nodes, uint64_t cap_nodes, uint6
             MHW_CK(cudaMemcpyAsync(h_tot + c, offc[c].p + nr, 8, cudaMemcpyDeviceToHost, S));
             MHW_CK(cudaEventRecord(ev[c], S));
         }
+        if (pin) l2_window(S, nullptr, 0);
         MHW_CK(cudaEventRecord(s.ev1, S));
         MHW_CK(cudaGetLastError());
         // copy chunk c while later chunks walk
@@ -1421,14 +1470,11 @@ void session_run_packed(Session& s, uint32_t* h_nodes, uint64_t cap_nodes, uint6
         mhw_walk_stats st{};
         session_stats(s, st);
         if (stats) *stats = st;
-        const double t_done = ms_since(ta);
-        hold_tot.reset();
-        const double t_freehost = ms_since(ta);
         if (trace)
             std::fprintf(stderr,
                          "[mhw] run_packed: %d chunks, setup %.2f ms, last copy issued %.2f ms, done %.2f ms, "
-                         "freehost %.2f ms, device walk+pack %.2f ms\n",
-                         chunks, t_setup, t_issued, t_done, t_freehost, st.walk_seconds * 1e3);
+                         "device walk+pack %.2f ms\n",
+                         chunks, t_setup, t_issued, ms_since(ta), st.walk_seconds * 1e3);
     } catch (...) {
         cudaStreamSynchronize(S);
         if (T) cudaStreamSynchronize(T);

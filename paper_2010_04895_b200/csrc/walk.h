@@ -66,6 +66,7 @@ struct Session {
     int grid = 0;
     bool eager_init = false;
     bool chain_loaded = false;  // mhw_session_load_chain installed the initial table
+    bool l2_pin = false;        // persisting L2 window over the edge filter during runs
     bool use_ar = false;     // arc-record walk kernel variant
     int minb = 1;
     uint32_t launches = 0;

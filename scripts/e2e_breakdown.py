@@ -49,8 +49,10 @@ for it in range(int(sys.argv[2]) if len(sys.argv) > 2 else 3):
     rc = lib.mhw_generate_walks_packed(h, C.byref(md), C.byref(c), C.c_void_p(out.data_ptr()), cap,
                                        C.c_void_p(offs.data_ptr()), rows.value + 1, C.byref(st))
     t2 = time.perf_counter()
-    rc2 = lib.mhw_generate_walks_into(h, C.byref(md), C.byref(c), C.c_void_p(pad.data_ptr()),
-                                      C.c_void_p(lens.data_ptr()), rows.value, C.byref(st))
+    rc2 = 0
+    if len(sys.argv) <= 3 or sys.argv[3] != "packed":
+        rc2 = lib.mhw_generate_walks_into(h, C.byref(md), C.byref(c), C.c_void_p(pad.data_ptr()),
+                                          C.c_void_p(lens.data_ptr()), rows.value, C.byref(st))
     t3 = time.perf_counter()
     lib.mhw_graph_free(h)
     t4 = time.perf_counter()
