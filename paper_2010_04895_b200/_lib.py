@@ -7,7 +7,8 @@ import ctypes as C
 import os
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG, "libmhw.so")
+# MHW_LIB: an alternative build of the same library (A/B experiments)
+LIB_PATH = os.environ.get("MHW_LIB") or os.path.join(PKG, "libmhw.so")
 
 
 class GraphView(C.Structure):

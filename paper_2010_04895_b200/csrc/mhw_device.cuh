@@ -134,12 +134,16 @@ __device__ __forceinline__ bool bloom_maybe(const DevGraph& g, uint32_t a, uint3
     const uint64_t x = bloom_key(a, b);
     const uint4* blk = reinterpret_cast<const uint4*>(g.bloom) + 2 * (uint64_t)bloom_block(x, g.bloom_blocks);
     const uint4 lo = __ldg(blk), hi = __ldg(blk + 1);
-    const uint32_t w[8] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};
+    // 256-bit block as four 64-bit words, selected without a local array
+    const uint64_t q0 = ((uint64_t)lo.y << 32) | lo.x, q1 = ((uint64_t)lo.w << 32) | lo.z;
+    const uint64_t q2 = ((uint64_t)hi.y << 32) | hi.x, q3 = ((uint64_t)hi.w << 32) | hi.z;
     bool all = true;
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
         const uint32_t bit = (uint32_t)(x >> (8 * k)) & 255u;
-        all &= (w[bit >> 5] >> (bit & 31)) & 1u;
+        const uint32_t j = bit >> 6;
+        const uint64_t q = j == 0 ? q0 : (j == 1 ? q1 : (j == 2 ? q2 : q3));
+        all &= ((q >> (bit & 63)) & 1ull) != 0;
     }
     return all;
 }
