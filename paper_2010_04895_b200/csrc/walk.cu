@@ -362,7 +362,7 @@ __global__ void __launch_bounds__(256, 8) k_init_all(RunParams P) {
 // Initial chain words of slots [b, e) (sharded init): k_init_all's work for
 // a slot range, written contiguously.
 template <int KIND>
-__global__ void __launch_bounds__(256) k_init_range(RunParams P, uint64_t b, uint64_t e, uint32_t* __restrict__ out) {
+__global__ void __launch_bounds__(256, 8) k_init_range(RunParams P, uint64_t b, uint64_t e, uint32_t* __restrict__ out) {
     const DevGraph& g = P.g;
     for (uint64_t a = b + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; a < e;
          a += (uint64_t)gridDim.x * blockDim.x) {
