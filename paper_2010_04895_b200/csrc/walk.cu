@@ -326,11 +326,12 @@ __global__ void __launch_bounds__(kWalkBlock) __maxnreg__(REGS) k_walk(RunParams
 // Eager chain-table initialisation of every arc-keyed slot (second-order
 // models). Result-identical to the lazy path (init randomness is keyed by the
 // slot), but runs with full warps and neighbouring threads share the node v.
-// 8 blocks/SM (32 registers, a few spills): the slots are independent
-// random-gather chains, and occupancy wins (cfg2: 64 regs 40.1 ms step,
-// 40 regs 39.6, 32 regs 39.1).
+// node2vec at 8 blocks/SM (32 registers, a few spills): the slots are
+// independent random-gather chains, and occupancy wins (cfg2: 64 regs
+// 40.1 ms step, 40 regs 39.6, 32 regs 39.1); the typed models spill more at
+// 32 registers and keep 4 blocks/SM (cfg3b 112 vs 117 ms).
 template <int KIND>
-__global__ void __launch_bounds__(256, 8) k_init_all(RunParams P) {
+__global__ void __launch_bounds__(256, KIND == NODE2VEC ? 8 : 4) k_init_all(RunParams P) {
     const DevGraph& g = P.g;
     unsigned long long inits = 0;
     for (uint64_t a = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; a < g.m;
@@ -362,7 +363,7 @@ __global__ void __launch_bounds__(256, 8) k_init_all(RunParams P) {
 // Initial chain words of slots [b, e) (sharded init): k_init_all's work for
 // a slot range, written contiguously.
 template <int KIND>
-__global__ void __launch_bounds__(256, 8) k_init_range(RunParams P, uint64_t b, uint64_t e, uint32_t* __restrict__ out) {
+__global__ void __launch_bounds__(256, KIND == NODE2VEC ? 8 : 4) k_init_range(RunParams P, uint64_t b, uint64_t e, uint32_t* __restrict__ out) {
     const DevGraph& g = P.g;
     for (uint64_t a = b + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; a < e;
          a += (uint64_t)gridDim.x * blockDim.x) {
