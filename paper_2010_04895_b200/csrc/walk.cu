@@ -61,14 +61,23 @@ __device__ __noinline__ uint32_t init_slot_ool(const DevGraph g, const DevModel 
 // word is the chain word of the state entered through that arc (colocated
 // chains: the word a step locks sits in the sector the previous step loaded
 // as its candidate record, so the lock is an L2 hit).
-template <int KIND, int REGS, bool LAZY, bool AR>
+// AR = 2 (node2vec, small node tables): narrow 8-byte records {u, chain
+// word}; the candidate's degree and offset come from its L2-resident node
+// record, so the record array the walk gathers from is half as large.
+template <int KIND, int REGS, bool LAZY, int AR>
 __global__ void __launch_bounds__(kWalkBlock) __maxnreg__(REGS) k_walk(RunParams P) {
     const DevGraph& g = P.g;
     constexpr bool TYPED = AR && needs_utype<KIND>();
     constexpr bool CC = AR && second_order(KIND);
-    constexpr uint32_t RS = TYPED ? 2u : 1u;  // uint4 words per record
+    constexpr bool NARROW = AR == 2;
+    constexpr uint32_t RS = TYPED ? 2u : 1u;  // uint4 words per record (wide layouts)
     const uint4* const arcs = (AR && KIND != DEEPWALK) ? P.ac : g.arc;
     auto load_rec = [&](uint64_t arc, uint4& b) {
+        if constexpr (NARROW) {
+            const uint2 x = __ldg(reinterpret_cast<const uint2*>(P.ac) + arc);
+            const NodeRec r = load_node(g, x.x);
+            return make_uint4(x.x, r.deg | ((r.flags & NF_ALLPOS) ? 0x80000000u : 0u), (uint32_t)r.off, x.y);
+        }
         if (TYPED) b = __ldg(arcs + RS * arc + 1);
         return __ldg(arcs + RS * arc);
     };
@@ -155,7 +164,9 @@ __global__ void __launch_bounds__(kWalkBlock) __maxnreg__(REGS) k_walk(RunParams
                 // (its timing cannot depend on the proposal); the candidate
                 // evaluation overlaps its latency, and the chain state it
                 // returns is only consumed by the decision.
-                uint32_t* const cw = CC ? reinterpret_cast<uint32_t*>(P.ac + RS * loc) + 3 : P.chain + slot;
+                uint32_t* const cw = !CC ? P.chain + slot
+                                         : (NARROW ? reinterpret_cast<uint32_t*>(P.ac) + 2 * loc + 1
+                                                   : reinterpret_cast<uint32_t*>(P.ac + RS * loc) + 3);
                 uint32_t e = atomicExch(cw, kLocked);
                 const uint32_t cand = d.index(c.deg);
                 const double u = d.unit();
@@ -349,9 +360,9 @@ __global__ void __launch_bounds__(256, KIND == NODE2VEC ? 8 : 4) k_init_all(RunP
         const uint32_t e = init_slot<KIND>(g, P.m, P.cfg, c, a);
         if (P.ac) {
             // colocated: the word lives in the record of the forward arc s->v
-            constexpr uint32_t RS = needs_utype<KIND>() ? 2u : 1u;
             const uint32_t sv = __ldg(g.rev + a);  // index of v in N(s)
-            if (sv != kNoBack) reinterpret_cast<uint32_t*>(P.ac + RS * (c.off_s + sv))[3] = e;
+            if (sv != kNoBack)
+                reinterpret_cast<uint32_t*>(P.ac)[((uint64_t)c.off_s + sv) * P.rec_u32 + (P.rec_u32 == 2 ? 1 : 3)] = e;
         } else {
             P.chain[a] = e;
         }
@@ -381,7 +392,7 @@ __global__ void __launch_bounds__(256, KIND == NODE2VEC ? 8 : 4) k_init_range(Ru
 
 // Installs a full table of slot words: colocated words go to the record of
 // the forward arc s->v of slot (v, affix), s = N(v)[affix].
-__global__ void k_load_chain(DevGraph g, const uint32_t* __restrict__ w, uint4* __restrict__ ac, uint32_t rs,
+__global__ void k_load_chain(DevGraph g, const uint32_t* __restrict__ w, uint32_t* __restrict__ ac, uint32_t rw,
                              uint32_t* __restrict__ chain) {
     for (uint64_t a = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; a < g.m;
          a += (uint64_t)gridDim.x * blockDim.x) {
@@ -389,7 +400,7 @@ __global__ void k_load_chain(DevGraph g, const uint32_t* __restrict__ w, uint4* 
         if (ac) {
             const uint32_t s = load_id(g, a);
             const uint32_t sv = __ldg(g.rev + a);
-            if (sv != kNoBack) reinterpret_cast<uint32_t*>(ac + rs * ((uint64_t)load_node(g, s).off + sv))[3] = e;
+            if (sv != kNoBack) ac[((uint64_t)load_node(g, s).off + sv) * rw + (rw == 2 ? 1 : 3)] = e;
         } else {
             chain[a] = e;
         }
@@ -400,8 +411,10 @@ __global__ void k_load_chain(DevGraph g, const uint32_t* __restrict__ w, uint4* 
 // off(u), chain word (second order) }, typed models add word 1 = {fp32
 // weight, type(u) | edge_type(arc) << 16, 0, 0}. Warp per source node (its
 // type gives the computed edge type, graph.hpp:47-50). k_ac_reset empties the
-// chain words before a lazy run.
-__global__ void k_arc_chain(DevGraph g, uint4* __restrict__ out, uint32_t rs) {
+// chain words before a lazy run. rw = u32 words per record (2: narrow {u,
+// chain word} records of node2vec).
+__global__ void k_arc_chain(DevGraph g, uint4* __restrict__ out, uint32_t rw) {
+    const uint32_t rs = rw / 4;
     const unsigned lane = threadIdx.x & 31;
     const uint64_t wid = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
@@ -410,6 +423,10 @@ __global__ void k_arc_chain(DevGraph g, uint4* __restrict__ out, uint32_t rs) {
         for (uint32_t i = lane; i < rv.deg; i += 32) {
             const uint64_t a = (uint64_t)rv.off + i;
             const uint32_t u = load_id(g, a);
+            if (rw == 2) {
+                reinterpret_cast<uint2*>(out)[a] = make_uint2(u, kEmpty);
+                continue;
+            }
             const NodeRec r = load_node(g, u);
             out[rs * a] = make_uint4(u, r.deg | ((r.flags & NF_ALLPOS) ? 0x80000000u : 0u), (uint32_t)r.off, kEmpty);
             if (rs == 2) {
@@ -421,9 +438,10 @@ __global__ void k_arc_chain(DevGraph g, uint4* __restrict__ out, uint32_t rs) {
     }
 }
 
-__global__ void k_ac_reset(uint4* __restrict__ ac, uint64_t m, uint32_t rs) {
+__global__ void k_ac_reset(uint32_t* __restrict__ ac, uint64_t m, uint32_t rw) {
+    const uint32_t co = rw == 2 ? 1 : 3;
     for (uint64_t a = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; a < m; a += (uint64_t)gridDim.x * blockDim.x)
-        reinterpret_cast<uint32_t*>(ac + rs * a)[3] = kEmpty;
+        ac[a * rw + co] = kEmpty;
 }
 
 // Packed corpus: widen lengths for the 64-bit offset scan, then one warp per
@@ -809,9 +827,10 @@ int walk_minb(int kind) {
     return v == 64 ? 64 : (v == 80 ? 80 : 255);
 }
 
-// Calls f(REGS, LAZY, AR) with the compile-time variant of the session.
+// Calls f(REGS, LAZY, AR) with the compile-time variant of the session
+// (ar: 0 none, 1 records, 2 narrow node2vec records).
 template <int KIND, class F>
-void with_variant(int regs, bool lazy, bool ar, F&& f) {
+void with_variant(int regs, bool lazy, int ar, F&& f) {
     using T = std::true_type;
     using N = std::false_type;
     auto by_regs = [&](auto lz, auto a) {
@@ -819,18 +838,21 @@ void with_variant(int regs, bool lazy, bool ar, F&& f) {
         else if (regs == 64) f(std::integral_constant<int, 64>{}, lz, a);
         else f(std::integral_constant<int, 255>{}, lz, a);
     };
-    {
-        if (ar) {
-            if (lazy) by_regs(T{}, T{});
-            else by_regs(N{}, T{});
-            return;
+    auto by_ar = [&](auto lz) {
+        if constexpr (KIND == NODE2VEC) {
+            if (ar == 2) {
+                by_regs(lz, std::integral_constant<int, 2>{});
+                return;
+            }
         }
-    }
-    if (lazy) by_regs(T{}, N{});
-    else by_regs(N{}, N{});
+        if (ar) by_regs(lz, std::integral_constant<int, 1>{});
+        else by_regs(lz, std::integral_constant<int, 0>{});
+    };
+    if (lazy) by_ar(T{});
+    else by_ar(N{});
 }
 
-template <int KIND, int REGS, bool LAZY, bool AR>
+template <int KIND, int REGS, bool LAZY, int AR>
 int walk_grid() {
     int per_sm = 0;
     MHW_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_walk<KIND, REGS, LAZY, AR>, kWalkBlock, 0));
@@ -1105,8 +1127,12 @@ void session_create(Session& s, Graph& g, const mhw_model_desc& md, const mhw_wa
         if (want_ar && m.kind != DEEPWALK && g.m && g.m < (1ull << 32)) {
             // session arc records (typed models: 32 B with weight and types);
             // second-order models keep their chain words in them
-            s.rec_words = typed_kind(m.kind) ? 2 : 1;
-            const uint64_t need = 16ull * s.rec_words * g.m;
+            // node2vec: narrow 8-byte records when the node table (16 B per
+            // node) is small enough to stay in L2 (MHW_NARROW=0/1 forces)
+            const char* nw = std::getenv("MHW_NARROW");
+            const bool narrow = m.kind == NODE2VEC && (nw ? nw[0] == '1' : 16ull * g.n <= (32ull << 20));
+            s.rec_u32 = typed_kind(m.kind) ? 8 : (narrow ? 2 : 4);
+            const uint64_t need = 4ull * s.rec_u32 * g.m;
             size_t free_b = 0, total_b = 0;
             MHW_CK(cudaMemGetInfo(&free_b, &total_b));
             if (free_b < need + (2ull << 30)) {
@@ -1114,8 +1140,8 @@ void session_create(Session& s, Graph& g, const mhw_model_desc& md, const mhw_wa
                 MHW_CK(cudaMemGetInfo(&free_b, &total_b));
             }
             if (free_b >= need + (2ull << 30)) {
-                s.ac.alloc(g.m * s.rec_words);
-                k_arc_chain<<<grid_for(g.n * 32ull), 256, 0, st>>>(g.view(), s.ac.p, s.rec_words);
+                s.ac.alloc((g.m * s.rec_u32 + 3) / 4);
+                k_arc_chain<<<grid_for(g.n * 32ull), 256, 0, st>>>(g.view(), s.ac.p, s.rec_u32);
                 MHW_CK(cudaGetLastError());
                 s.use_ar = true;
             }
@@ -1125,7 +1151,7 @@ void session_create(Session& s, Graph& g, const mhw_model_desc& md, const mhw_wa
         if (want_ar && m.kind == DEEPWALK) s.use_ar = graph_ensure_arcrec(g, ARC_AUX_WEIGHT);
         dispatch(m.kind, [&](auto kc) {
             constexpr int KIND = decltype(kc)::value;
-            with_variant<KIND>(s.minb, !s.eager_init, s.use_ar, [&](auto rg, auto lz, auto ar) {
+            with_variant<KIND>(s.minb, !s.eager_init, s.ar_mode(), [&](auto rg, auto lz, auto ar) {
                 s.grid = walk_grid<KIND, decltype(rg)::value, decltype(lz)::value, decltype(ar)::value>();
             });
         });
@@ -1162,6 +1188,7 @@ RunParams Session::params() const {
     P.n_items = n_items;
     P.chain = chain.p;
     P.ac = ac.n ? ac.p : nullptr;
+    P.rec_u32 = rec_u32;
     P.out = out.p;
     P.stride = stride;
     P.lens = lens.p;
@@ -1183,7 +1210,7 @@ void session_run(Session& s, cudaStream_t user) {
     if (!preloaded) MHW_CK(cudaMemsetAsync(s.chain.p, 0xFF, s.chain.bytes(), st));
     MHW_CK(cudaMemsetAsync(s.ctr.p, 0, s.ctr.bytes(), st));
     if (!preloaded && s.ac.n && second_order(s.model.dev.kind) && (!s.eager_init || !s.g->verified_sym)) {
-        k_ac_reset<<<grid_for(s.g->m), 256, 0, st>>>(s.ac.p, s.g->m, s.rec_words);
+        k_ac_reset<<<grid_for(s.g->m), 256, 0, st>>>(reinterpret_cast<uint32_t*>(s.ac.p), s.g->m, s.rec_u32);
         ++s.launches;
     }
     if (s.n_iso) {
@@ -1236,7 +1263,7 @@ void session_run(Session& s, cudaStream_t user) {
                         ++s.launches;
                     }
                 }
-                with_variant<KIND>(s.minb, !s.eager_init, s.use_ar, [&](auto rg, auto lz, auto ar) {
+                with_variant<KIND>(s.minb, !s.eager_init, s.ar_mode(), [&](auto rg, auto lz, auto ar) {
                     k_walk<KIND, decltype(rg)::value, decltype(lz)::value, decltype(ar)::value>
                         <<<s.grid, kWalkBlock, 0, st>>>(P);
                 });
@@ -1271,8 +1298,8 @@ void session_load_chain(Session& s, const uint32_t* d_words, cudaStream_t user) 
         invalid("chain preloading applies to second-order models on the throughput schedule");
     cudaStream_t st = user ? user : s.stream;
     if (s.g->m) {
-        k_load_chain<<<grid_for(s.g->m), 256, 0, st>>>(s.g->view(), d_words, s.ac.n ? s.ac.p : nullptr,
-                                                         s.rec_words, s.chain.p);
+        k_load_chain<<<grid_for(s.g->m), 256, 0, st>>>(
+            s.g->view(), d_words, s.ac.n ? reinterpret_cast<uint32_t*>(s.ac.p) : nullptr, s.rec_u32, s.chain.p);
         MHW_CK(cudaGetLastError());
     }
     s.chain_loaded = true;
@@ -1408,7 +1435,7 @@ void session_run_packed(Session& s, uint32_t* h_nodes, uint64_t cap_nodes, uint6
         MHW_CK(cudaMemsetAsync(s.chain.p, 0xFF, s.chain.bytes(), S));
         MHW_CK(cudaMemsetAsync(s.ctr.p, 0, s.ctr.bytes(), S));
         if (s.ac.n && second_order(s.model.dev.kind) && (!s.eager_init || !s.g->verified_sym))
-            k_ac_reset<<<grid_for(s.g->m), 256, 0, S>>>(s.ac.p, s.g->m, s.rec_words);
+            k_ac_reset<<<grid_for(s.g->m), 256, 0, S>>>(reinterpret_cast<uint32_t*>(s.ac.p), s.g->m, s.rec_u32);
         if (s.n_iso)
             k_iso_rows<<<grid_for((uint64_t)s.n_iso * s.cfg.K), 256, 0, S>>>(s.iso.p, s.iso_row.p, s.n_iso, s.cfg.K,
                                                                              s.out.p, s.stride, s.lens.p);
@@ -1431,7 +1458,7 @@ void session_run_packed(Session& s, uint32_t* h_nodes, uint64_t cap_nodes, uint6
             MHW_CK(cudaMemsetAsync(s.ctr.p, 0, sizeof(unsigned long long), S));  // work counter
             dispatch(s.model.dev.kind, [&](auto kc) {
                 constexpr int KIND = decltype(kc)::value;
-                with_variant<KIND>(s.minb, !s.eager_init, s.use_ar, [&](auto rg, auto lz, auto ar) {
+                with_variant<KIND>(s.minb, !s.eager_init, s.ar_mode(), [&](auto rg, auto lz, auto ar) {
                     k_walk<KIND, decltype(rg)::value, decltype(lz)::value, decltype(ar)::value>
                         <<<s.grid, kWalkBlock, 0, S>>>(Pc);
                 });

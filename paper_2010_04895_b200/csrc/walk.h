@@ -17,6 +17,7 @@ struct RunParams {
     uint32_t n_act;
     uint64_t n_items;         // n_act * K walkers
     uint32_t* chain;          // one packed Last word per state slot
+    uint32_t rec_u32;         // u32 words per session arc record: 4 (16 B), 8 (typed 32 B), 2 (narrow 8 B)
     uint4* ac;                // node2vec throughput: arc records whose .w is the chain
                               // word of the state entered through that arc (else null)
     uint32_t* out;            // rows x stride walk buffer
@@ -54,7 +55,7 @@ struct Session {
     uint32_t stride = 0;
     DBuf<uint32_t> chain, out, lens, rep_group;
     DBuf<uint4> ac;          // session arc records (+ colocated chain words, second order)
-    uint32_t rec_words = 1;  // uint4 words per record: 2 for typed models
+    uint32_t rec_u32 = 4;    // u32 words per record: 4, 8 (typed models), 2 (narrow node2vec records)
     std::unique_ptr<ExactState> ex;  // alias / direct / rejection baselines (exact.cu)
     DBuf<unsigned long long> ctr;
     // deterministic schedule scratch
@@ -78,6 +79,7 @@ struct Session {
     Session& operator=(const Session&) = delete;
     ~Session();
     RunParams params() const;
+    int ar_mode() const { return use_ar ? (rec_u32 == 2 ? 2 : 1) : 0; }
 };
 
 uint64_t k_slots(int kind, const Graph& g);

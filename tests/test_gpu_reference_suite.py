@@ -328,6 +328,22 @@ def test_throughput_transitions_pass_chain_chi_square(mhw, oracle, kind):
     assert ok_c, "control: " + msg_c
 
 
+@pytest.mark.parametrize("narrow", ["0", "1"])
+def test_node2vec_record_layouts_pass_chain_chi_square(mhw, oracle, narrow, monkeypatch):
+    """node2vec session records: 16-byte {u, deg, off, chain word} and the
+    narrow 8-byte {u, chain word} layout (node record from L2), eager and
+    lazy slot init."""
+    monkeypatch.setenv("MHW_NARROW", narrow)
+    g = typed_random_graph(901, 40, 4.0, weighted=False, types=2)
+    md = model_desc(O.NODE2VEC, g, p=0.25, q=4.0)
+    for init_mode in (1, 2):
+        cfg = O.WalkCfg(K=400, L=80, seed=79 + init_mode, init_kind=O.INIT_BURN_IN, burn_in_steps=4)
+        c = mhw.generate_walks(device_graph(g, weighted=False), walk_model(md),
+                               walk_config(cfg, threads=8, init_mode=init_mode))
+        ok, msg = gate(audit(g, oracle, md, c.rows, c.lengths, min_visits=5000))
+        assert ok, msg
+
+
 @pytest.mark.parametrize("kind", [O.NODE2VEC, O.EDGE2VEC, O.FAIRWALK])
 def test_lazy_colocated_chains_pass_chain_chi_square(mhw, oracle, kind):
     """Second-order throughput walks with lazy slot init (init_mode 1): the
