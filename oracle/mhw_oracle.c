@@ -583,6 +583,19 @@ int og_alias_build(uint32_t n, const double* w, double* prob, uint32_t* alias) {
     return OG_OK;
 }
 
+/* Per-node static alias tables over a CSR (engine.cpp:136-146 builds one per
+ * node); nodes without positive weight get prob 0 / alias i like the device
+ * dump (mhw_alias_tables). */
+void og_alias_tables(uint32_t n, const uint64_t* offsets, const double* w, double* prob, uint32_t* alias) {
+    for (uint32_t v = 0; v < n; ++v) {
+        const uint64_t a = offsets[v], b = offsets[v + 1];
+        if (a == b) continue;
+        if (og_alias_build((uint32_t)(b - a), w + a, prob + a, alias + a) != OG_OK) {
+            for (uint64_t i = a; i < b; ++i) { prob[i] = 0.0; alias[i] = (uint32_t)(i - a); }
+        }
+    }
+}
+
 /* direct_sample with the unit supplied, samplers.cpp:133-146 */
 uint32_t og_direct_sample_u(uint32_t n, const double* w, double u) {
     double total = 0.0;

@@ -134,6 +134,8 @@ void og_decide(const og_graph* g, const og_model* m, uint64_t count, const uint3
 /* ----------------------------------------------------------- samplers */
 /* alias_build (samplers.cpp:95-131). returns 0 ok, 2 invalid. */
 int og_alias_build(uint32_t n, const double* w, double* prob, uint32_t* alias);
+/* per-node alias tables of a CSR (nodes without positive weight: prob 0, alias i) */
+void og_alias_tables(uint32_t n, const uint64_t* offsets, const double* w, double* prob, uint32_t* alias);
 /* direct_sample given u (samplers.cpp:133-146) */
 uint32_t og_direct_sample_u(uint32_t n, const double* w, double u);
 /* Per-slot init under the philox layout: returns 1 and *last on success, 0 dead end. */

@@ -179,6 +179,7 @@ class Oracle:
         L.og_pair_etypes.argtypes = [C.c_uint64, C.c_uint64, _u32p, _u32p, C.c_uint32, _u16p]
         L.og_graph_checksum.argtypes = [C.c_uint32, _u64p, _u32p, _dp]
         L.og_graph_checksum.restype = C.c_uint64
+        L.og_alias_tables.argtypes = [C.c_uint32, _u64p, _dp, _dp, _u32p]
         L.og_free.argtypes = [C.c_void_p]
         L.og_model_bind.argtypes = [C.POINTER(_OgGraph), C.POINTER(_OgModel), C.c_char_p, C.c_size_t]
         L.og_decide.argtypes = [C.POINTER(_OgGraph), C.POINTER(_OgModel), C.c_uint64, _u32p, _u32p,
@@ -318,6 +319,15 @@ class Oracle:
         rc = self.lib.og_alias_build(len(w), _ptr(w, _dp), _ptr(prob, _dp), _ptr(alias, _u32p))
         if rc:
             raise OracleError(rc, "alias_build: no positive weight")
+        return prob, alias
+
+    def alias_tables(self, offsets, w):
+        """Static alias tables of every node (engine.cpp:136-146), CSR order."""
+        off = np.ascontiguousarray(offsets, dtype=np.uint64)
+        wa = np.ascontiguousarray(w, dtype=np.float64)
+        prob = np.zeros(len(wa))
+        alias = np.zeros(len(wa), dtype=np.uint32)
+        self.lib.og_alias_tables(len(off) - 1, _ptr(off, _u64p), _ptr(wa, _dp), _ptr(prob, _dp), _ptr(alias, _u32p))
         return prob, alias
 
     def _cfg(self, cfg: WalkCfg, rng, order):
