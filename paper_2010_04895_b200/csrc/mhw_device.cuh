@@ -576,15 +576,17 @@ __device__ bool random_positive(const DevGraph& g, const DevModel& m, const SCtx
 // mh_init (samplers.cpp:37-83) with slot-keyed Philox blocks: random -> block
 // 0; high_weight probes -> blocks 0..hw-1, fallback -> block hw; burn_in ->
 // block 0 pick, blocks 1..k transitions. Returns the packed entry or kDead.
+// w_out (optional) receives w'(Last) of the returned entry.
 template <int KIND>
 __device__ uint32_t init_slot(const DevGraph& g, const DevModel& m, const DevCfg& cfg, const SCtx& c,
-                              uint64_t slot) {
+                              uint64_t slot, double* w_out = nullptr) {
     if (c.deg == 0) return kDead;
     const uint2 key = philox_key(cfg.seed, DOM_INIT);
     uint32_t last, cls;
     double wl;
     if (cfg.init_kind == INIT_RANDOM) {
         if (!random_positive<KIND>(g, m, c, key, slot, 0, &last, &cls, &wl)) return kDead;
+        if (w_out) *w_out = wl;
         return pack_entry(last, cls);
     }
     if (cfg.init_kind == INIT_HIGH_WEIGHT) {
@@ -620,9 +622,11 @@ __device__ uint32_t init_slot(const DevGraph& g, const DevModel& m, const DevCfg
             }
             if (!found) {
                 if (!random_positive<KIND>(g, m, c, key, slot, cfg.hw, &last, &cls, &wl)) return kDead;
+                if (w_out) *w_out = wl;
                 return pack_entry(last, cls);
             }
         }
+        if (w_out) *w_out = best_w;
         return found ? pack_entry(best, best_cls) : kDead;
     }
     // burn-in
@@ -639,6 +643,7 @@ __device__ uint32_t init_slot(const DevGraph& g, const DevModel& m, const DevCfg
             wl = wc;
         }
     }
+    if (w_out) *w_out = wl;
     return pack_entry(last, cls);
 }
 

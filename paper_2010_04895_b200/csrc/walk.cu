@@ -36,8 +36,26 @@ constexpr uint32_t kDeadMark = 0xFFFFFFFEu;
 // Releases a chain slot taken with atomicExch(kLocked). The lock protects
 // only the chain word itself, so a relaxed GPU-scope store suffices (no
 // other data is published; a release store would add a full fence).
+// u32 index of the chain word inside a session record of rw words.
+__host__ __device__ __forceinline__ uint32_t chain_word_off(uint32_t rw) { return rw == 2 ? 1 : (rw == 8 ? 5 : 3); }
+
 __device__ __forceinline__ void chain_release(uint32_t* p, uint32_t v) {
     asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// 16-byte atomic exchange (sm_90+): a typed record's chain word travels with
+// the cached w'(Last) in one access, so both are always read and written
+// together.
+__device__ __forceinline__ uint4 atom_exch128(uint4* p, uint4 v) {
+    const unsigned long long lo = ((unsigned long long)v.y << 32) | v.x, hi = ((unsigned long long)v.w << 32) | v.z;
+    unsigned long long rlo, rhi;
+    asm volatile(
+        "{\n\t.reg .b128 d, b;\n\tmov.b128 b, {%2, %3};\n\tatom.global.exch.b128 d, [%4], b;\n\t"
+        "mov.b128 {%0, %1}, d;\n\t}"
+        : "=l"(rlo), "=l"(rhi)
+        : "l"(lo), "l"(hi), "l"(p)
+        : "memory");
+    return make_uint4((uint32_t)rlo, (uint32_t)(rlo >> 32), (uint32_t)rhi, (uint32_t)(rhi >> 32));
 }
 
 __device__ __forceinline__ void fail_back_edge(unsigned long long* ctr, uint32_t from, uint32_t to) {
@@ -70,6 +88,11 @@ __global__ void __launch_bounds__(kWalkBlock) __maxnreg__(REGS) k_walk(RunParams
     constexpr bool TYPED = AR && needs_utype<KIND>();
     constexpr bool CC = AR && second_order(KIND);
     constexpr bool NARROW = AR == 2;
+    // typed second-order records carry w'(Last) next to the chain word
+    // (word 1 = {type | etype << 16, chain word, w'(Last) as f64}), taken and
+    // released with one 16-byte exchange: the decision needs no load of the
+    // Last's record, which is fetched only when the walker moves to it
+    constexpr bool WLC = TYPED && CC;
     constexpr uint32_t RS = TYPED ? 2u : 1u;  // uint4 words per record (wide layouts)
     const uint4* const arcs = (AR && KIND != DEEPWALK) ? P.ac : g.arc;
     auto load_rec = [&](uint64_t arc, uint4& b) {
@@ -83,7 +106,7 @@ __global__ void __launch_bounds__(kWalkBlock) __maxnreg__(REGS) k_walk(RunParams
     };
     auto rec_node = [&](const uint4& a, const uint4& b) {
         NodeRec r = arc_node(a);
-        if (TYPED) r.type = (uint16_t)(b.y & 0xFFFFu);
+        if (TYPED) r.type = (uint16_t)(b.x & 0xFFFFu);
         return r;
     };
     const uint2 wkey = philox_key(P.cfg.seed, DOM_WALK);
@@ -123,6 +146,7 @@ __global__ void __launch_bounds__(kWalkBlock) __maxnreg__(REGS) k_walk(RunParams
         uint32_t affix = 0;
         uint64_t slot = 0;
         uint64_t loc = 0;  // CC: forward arc s->v holding the chain word of state (s, v)
+        uint32_t tx = 0;   // WLC: static type word of record loc (rewritten by every exchange)
         if (KIND == METAPATH2VEC) c.req = P.m.metapath[metapath_next(P.m, 0)];
         if (!second_order(KIND)) slot = slot_of<KIND>(P.m, P.cfg, c, 0, walker);
         uint32_t len = 1;
@@ -164,10 +188,18 @@ __global__ void __launch_bounds__(kWalkBlock) __maxnreg__(REGS) k_walk(RunParams
                 // (its timing cannot depend on the proposal); the candidate
                 // evaluation overlaps its latency, and the chain state it
                 // returns is only consumed by the decision.
-                uint32_t* const cw = !CC ? P.chain + slot
-                                         : (NARROW ? reinterpret_cast<uint32_t*>(P.ac) + 2 * loc + 1
-                                                   : reinterpret_cast<uint32_t*>(P.ac + RS * loc) + 3);
-                uint32_t e = atomicExch(cw, kLocked);
+                uint32_t* const cw = (!CC || WLC) ? P.chain + slot
+                                                  : (NARROW ? reinterpret_cast<uint32_t*>(P.ac) + 2 * loc + 1
+                                                            : reinterpret_cast<uint32_t*>(P.ac + RS * loc) + 3);
+                uint4* const cb = WLC ? P.ac + 2 * loc + 1 : nullptr;
+                uint4 E = make_uint4(0, 0, 0, 0);
+                uint32_t e;
+                if (WLC) {
+                    E = atom_exch128(cb, make_uint4(tx, kLocked, 0u, 0u));
+                    e = E.y;
+                } else {
+                    e = atomicExch(cw, kLocked);
+                }
                 const uint32_t cand = d.index(c.deg);
                 const double u = d.unit();
                 uint32_t uc;
@@ -192,7 +224,7 @@ __global__ void __launch_bounds__(kWalkBlock) __maxnreg__(REGS) k_walk(RunParams
                     second_order(KIND) ? alpha_class(g, P.m, c, uc, rc_early ? &rc : nullptr) : 0u;
                 double wc;
                 if (AR && KIND == DEEPWALK) wc = (double)__uint_as_float(ac.w);
-                else if (TYPED) wc = wprime_v<KIND>(g, P.m, c, (double)__uint_as_float(bc.x), rc.type, bc.y >> 16, cls_c);
+                else if (TYPED) wc = wprime_v<KIND>(g, P.m, c, (double)__uint_as_float(ac.w), rc.type, bc.x >> 16, cls_c);
                 else wc = wprime<KIND>(g, P.m, c, cand, rc.type, cls_c);
                 if (e == kLocked) {
                     unsigned ns = 32;
@@ -200,14 +232,22 @@ __global__ void __launch_bounds__(kWalkBlock) __maxnreg__(REGS) k_walk(RunParams
                         ++retries;
                         __nanosleep(ns);
                         ns = ns < 512 ? ns * 2 : 512;
-                        e = atomicExch(cw, kLocked);
+                        if (WLC) {
+                            E = atom_exch128(cb, make_uint4(tx, kLocked, 0u, 0u));
+                            e = E.y;
+                        } else {
+                            e = atomicExch(cw, kLocked);
+                        }
                     } while (e == kLocked);
                 }
                 if (e == kEmpty) {
                     if constexpr (LAZY) {
                         // CC: slot id of (s, v) = off(v) + index of s in N(v)
                         if (CC) slot = (uint64_t)c.off + __ldg(g.rev + loc);
-                        e = init_slot<KIND>(g, P.m, P.cfg, c, slot);
+                        double w0 = 0.0;
+                        e = init_slot<KIND>(g, P.m, P.cfg, c, slot, WLC ? &w0 : nullptr);
+                        E.z = (uint32_t)__double2loint(w0);
+                        E.w = (uint32_t)__double2hiint(w0);
                         ++inits;
                     } else {
                         e = kDead;  // unreachable: eager init filled every slot
@@ -215,7 +255,8 @@ __global__ void __launch_bounds__(kWalkBlock) __maxnreg__(REGS) k_walk(RunParams
                     }
                 }
                 if (e == kDead) {
-                    chain_release(cw, kDead);
+                    if (WLC) atom_exch128(cb, make_uint4(tx, kDead, 0u, 0u));
+                    else chain_release(cw, kDead);
                     dead = true;
                     break;
                 }
@@ -225,7 +266,7 @@ __global__ void __launch_bounds__(kWalkBlock) __maxnreg__(REGS) k_walk(RunParams
                 // deepwalk (cheap, L2-resident graphs; measured win). For
                 // node2vec/edge2vec the extra sectors cost more than the
                 // shorter rejection path saves (profiles/, round 1).
-                constexpr bool kSpec = needs_utype<KIND>() || KIND == DEEPWALK;
+                constexpr bool kSpec = !WLC && (needs_utype<KIND>() || KIND == DEEPWALK);
                 uint32_t ul = 0;
                 NodeRec rl{};
                 uint4 al = make_uint4(0, 0, 0, 0), bl = make_uint4(0, 0, 0, 0);
@@ -240,11 +281,17 @@ __global__ void __launch_bounds__(kWalkBlock) __maxnreg__(REGS) k_walk(RunParams
                     }
                 }
                 double wl;
-                if (AR && KIND == DEEPWALK) wl = (double)__uint_as_float(al.w);
-                else if (TYPED) wl = wprime_v<KIND>(g, P.m, c, (double)__uint_as_float(bl.x), rl.type, bl.y >> 16, cls_l);
+                if (WLC) wl = __hiloint2double((int)E.w, (int)E.z);
+                else if (AR && KIND == DEEPWALK) wl = (double)__uint_as_float(al.w);
+                else if (TYPED) wl = wprime_v<KIND>(g, P.m, c, (double)__uint_as_float(al.w), rl.type, bl.x >> 16, cls_l);
                 else wl = wprime<KIND>(g, P.m, c, last, rl.type, cls_l);
                 const bool acc = mh_accept(wc, wl, u) && cand != last;
-                chain_release(cw, acc ? pack_entry(cand, cls_c) : e);
+                if (WLC)
+                    atom_exch128(cb, acc ? make_uint4(tx, pack_entry(cand, cls_c), (uint32_t)__double2loint(wc),
+                                                      (uint32_t)__double2hiint(wc))
+                                         : make_uint4(tx, e, E.z, E.w));
+                else
+                    chain_release(cw, acc ? pack_entry(cand, cls_c) : e);
                 chosen = acc ? cand : last;
                 if constexpr (AR) {
                     const bool take_c = acc || cand == last;
@@ -306,8 +353,9 @@ __global__ void __launch_bounds__(kWalkBlock) __maxnreg__(REGS) k_walk(RunParams
                     break;
                 }
                 if (KIND == EDGE2VEC)
-                    c.in_type = TYPED ? (bn.y >> 16) : edge_type_of(g, c.off + chosen, c.vtype, rn.type);
+                    c.in_type = TYPED ? (bn.x >> 16) : edge_type_of(g, c.off + chosen, c.vtype, rn.type);
                 if (CC) loc = (uint64_t)c.off + chosen;
+                if (WLC) tx = bn.x;
                 c.s = c.v;
                 c.off_s = c.off;
                 c.deg_s = c.deg;
@@ -357,12 +405,19 @@ __global__ void __launch_bounds__(256, KIND == NODE2VEC ? 8 : 4) k_init_all(RunP
         const NodeRec r = load_node(g, lo);
         const uint32_t affix = (uint32_t)(a - (uint64_t)r.off);
         const SCtx c = make_ctx<KIND>(g, P.m, lo, affix);
-        const uint32_t e = init_slot<KIND>(g, P.m, P.cfg, c, a);
+        double wl = 0.0;
+        const uint32_t e = init_slot<KIND>(g, P.m, P.cfg, c, a, &wl);
         if (P.ac) {
             // colocated: the word lives in the record of the forward arc s->v
             const uint32_t sv = __ldg(g.rev + a);  // index of v in N(s)
-            if (sv != kNoBack)
-                reinterpret_cast<uint32_t*>(P.ac)[((uint64_t)c.off_s + sv) * P.rec_u32 + (P.rec_u32 == 2 ? 1 : 3)] = e;
+            if (sv != kNoBack) {
+                uint32_t* w = reinterpret_cast<uint32_t*>(P.ac) + ((uint64_t)c.off_s + sv) * P.rec_u32;
+                w[chain_word_off(P.rec_u32)] = e;
+                if (P.rec_u32 == 8) {  // typed: w'(Last) next to the word
+                    w[6] = (uint32_t)__double2loint(wl);
+                    w[7] = (uint32_t)__double2hiint(wl);
+                }
+            }
         } else {
             P.chain[a] = e;
         }
@@ -391,18 +446,37 @@ __global__ void __launch_bounds__(256, KIND == NODE2VEC ? 8 : 4) k_init_range(Ru
 }
 
 // Installs a full table of slot words: colocated words go to the record of
-// the forward arc s->v of slot (v, affix), s = N(v)[affix].
-__global__ void k_load_chain(DevGraph g, const uint32_t* __restrict__ w, uint32_t* __restrict__ ac, uint32_t rw,
+// the forward arc s->v of slot (v, affix), s = N(v)[affix]; typed records
+// also get w'(Last) of the word's Last (its class is in the word).
+template <int KIND>
+__global__ void k_load_chain(RunParams P, const uint32_t* __restrict__ w, uint32_t* __restrict__ ac, uint32_t rw,
                              uint32_t* __restrict__ chain) {
+    const DevGraph& g = P.g;
     for (uint64_t a = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; a < g.m;
          a += (uint64_t)gridDim.x * blockDim.x) {
         const uint32_t e = __ldg(w + a);
-        if (ac) {
-            const uint32_t s = load_id(g, a);
-            const uint32_t sv = __ldg(g.rev + a);
-            if (sv != kNoBack) ac[((uint64_t)load_node(g, s).off + sv) * rw + (rw == 2 ? 1 : 3)] = e;
-        } else {
+        if (!ac) {
             chain[a] = e;
+            continue;
+        }
+        const uint32_t s = load_id(g, a);
+        const uint32_t sv = __ldg(g.rev + a);
+        if (sv == kNoBack) continue;
+        uint32_t* rec = ac + ((uint64_t)load_node(g, s).off + sv) * rw;
+        rec[chain_word_off(rw)] = e;
+        if (rw == 8 && e < kLocked) {
+            uint32_t lo = 0, hi = g.n;  // owner v of slot a
+            while (hi - lo > 1) {
+                const uint32_t mid = (lo + hi) >> 1;
+                if ((uint64_t)__ldg(&g.nodes[mid].off) <= a) lo = mid;
+                else hi = mid;
+            }
+            const NodeRec r = load_node(g, lo);
+            const SCtx c = make_ctx<KIND>(g, P.m, lo, (uint32_t)(a - (uint64_t)r.off));
+            const uint32_t last = e & kIdxMask;
+            const double wl = wprime<KIND>(g, P.m, c, last, load_node(g, load_id(g, c.off + last)).type, e >> 30);
+            rec[6] = (uint32_t)__double2loint(wl);
+            rec[7] = (uint32_t)__double2hiint(wl);
         }
     }
 }
@@ -412,7 +486,9 @@ __global__ void k_load_chain(DevGraph g, const uint32_t* __restrict__ w, uint32_
 // weight, type(u) | edge_type(arc) << 16, 0, 0}. Warp per source node (its
 // type gives the computed edge type, graph.hpp:47-50). k_ac_reset empties the
 // chain words before a lazy run. rw = u32 words per record (2: narrow {u,
-// chain word} records of node2vec).
+// chain word} records of node2vec). Typed records (rw 8): word 0 = {u,
+// deg | allpos << 31, off, fp32 weight}, word 1 = {type(u) | edge_type << 16,
+// chain word, w'(Last) as f64}.
 __global__ void k_arc_chain(DevGraph g, uint4* __restrict__ out, uint32_t rw) {
     const uint32_t rs = rw / 4;
     const unsigned lane = threadIdx.x & 31;
@@ -428,18 +504,21 @@ __global__ void k_arc_chain(DevGraph g, uint4* __restrict__ out, uint32_t rw) {
                 continue;
             }
             const NodeRec r = load_node(g, u);
-            out[rs * a] = make_uint4(u, r.deg | ((r.flags & NF_ALLPOS) ? 0x80000000u : 0u), (uint32_t)r.off, kEmpty);
+            const uint32_t dw = r.deg | ((r.flags & NF_ALLPOS) ? 0x80000000u : 0u);
             if (rs == 2) {
                 const float w = g.w ? __ldg(g.w + a) : 1.0f;
                 const uint32_t et = edge_type_of(g, a, rv.type, r.type);
-                out[rs * a + 1] = make_uint4(__float_as_uint(w), (uint32_t)r.type | (et << 16), 0u, 0u);
+                out[rs * a] = make_uint4(u, dw, (uint32_t)r.off, __float_as_uint(w));
+                out[rs * a + 1] = make_uint4((uint32_t)r.type | (et << 16), kEmpty, 0u, 0u);
+            } else {
+                out[rs * a] = make_uint4(u, dw, (uint32_t)r.off, kEmpty);
             }
         }
     }
 }
 
 __global__ void k_ac_reset(uint32_t* __restrict__ ac, uint64_t m, uint32_t rw) {
-    const uint32_t co = rw == 2 ? 1 : 3;
+    const uint32_t co = chain_word_off(rw);
     for (uint64_t a = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; a < m; a += (uint64_t)gridDim.x * blockDim.x)
         ac[a * rw + co] = kEmpty;
 }
@@ -1298,8 +1377,13 @@ void session_load_chain(Session& s, const uint32_t* d_words, cudaStream_t user) 
         invalid("chain preloading applies to second-order models on the throughput schedule");
     cudaStream_t st = user ? user : s.stream;
     if (s.g->m) {
-        k_load_chain<<<grid_for(s.g->m), 256, 0, st>>>(
-            s.g->view(), d_words, s.ac.n ? reinterpret_cast<uint32_t*>(s.ac.p) : nullptr, s.rec_u32, s.chain.p);
+        const RunParams P = s.params();
+        dispatch(s.model.dev.kind, [&](auto kc) {
+            constexpr int KIND = decltype(kc)::value;
+            if constexpr (second_order(KIND))
+                k_load_chain<KIND><<<grid_for(s.g->m), 256, 0, st>>>(
+                    P, d_words, s.ac.n ? reinterpret_cast<uint32_t*>(s.ac.p) : nullptr, s.rec_u32, s.chain.p);
+        });
         MHW_CK(cudaGetLastError());
     }
     s.chain_loaded = true;
