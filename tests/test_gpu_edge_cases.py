@@ -137,3 +137,24 @@ def test_walks_write_matches_write_corpus_format(mhw, tmp_path):
     lib.mhw_walks_free(h)
     assert open(p).read() == want
     assert open(p + ".stats.jsonl").read().startswith("{")
+
+
+def test_mega_hub_star(mhw):
+    """A hub of degree 150,000 (past the 65,536-replica cap of the automatic
+    deepwalk layout, with a 4,688-bucket hash set for the alpha test): walks
+    stay valid, full length, and return to the hub every other step."""
+    n = 150_001
+    leaves = np.arange(1, n, dtype=np.int64)
+    off = np.concatenate([[0, n - 1], n - 1 + np.arange(1, n)]).astype(np.int64)
+    nbr = np.concatenate([leaves, np.zeros(n - 1, dtype=np.int64)]).astype(np.int32)
+    w = (1.0 + (np.arange(2 * (n - 1)) % 7)).astype(np.float32)
+    g = mhw.Graph.from_csr(off, nbr, weights=w, symmetric=True)
+    for kind in (mhw.ModelKind.deepwalk, mhw.ModelKind.node2vec):
+        m = mhw.WalkModel(kind=kind, p=0.5, q=2.0)
+        c = mhw.generate_walks(g, m, mhw.WalkConfig(walks_per_node=2, walk_length=12, threads=8, seed=3))
+        assert len(c) == 2 * n and (c.lengths == 13).all()
+        rows = c.rows[:, :13].astype(np.int64)
+        hub_pos = rows[:, 0] == 0
+        # from the hub every step leaves it; from a leaf every step returns
+        assert (rows[hub_pos][:, 1::2] != 0).all() and (rows[hub_pos][:, 2::2] == 0).all()
+        assert (rows[~hub_pos][:, 1::2] == 0).all() and (rows[~hub_pos][:, 2::2] != 0).all()
