@@ -370,15 +370,7 @@ unsigned grid_for(uint64_t work, int block = 256) {
     return (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(g, 148ull * 16));
 }
 
-size_t free_bytes() {
-    size_t f = 0, t = 0;
-    MHW_CK(cudaMemGetInfo(&f, &t));
-    if (f < (4ull << 30)) {
-        dev_trim();
-        MHW_CK(cudaMemGetInfo(&f, &t));
-    }
-    return f;
-}
+size_t free_bytes() { return dev_available_bytes(); }
 
 }  // namespace
 

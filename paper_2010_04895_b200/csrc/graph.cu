@@ -104,6 +104,16 @@ void dev_trim() {
     cudaSetDevice(prev);
 }
 
+// Device memory available to dev_alloc: the driver's free memory plus what
+// the pool holds reserved but unused (cudaMemGetInfo counts that as used;
+// trimming it to make the number look bigger would only make the next
+// allocations map it again).
+size_t dev_available_bytes() {
+    size_t f = 0, t = 0;
+    MHW_CK(cudaMemGetInfo(&f, &t));
+    return f + dev_cached_bytes();
+}
+
 size_t dev_cached_bytes() {
     int dev = 0;
     cudaGetDevice(&dev);
@@ -1062,13 +1072,7 @@ bool graph_ensure_arcrec(Graph& g, int aux) {
     if (!g.m || g.m >= (1ull << 32)) return false;
     DeviceGuard dg(g.device);
     if (aux == ARC_AUX_REV) graph_ensure_rev(g);
-    size_t free_b = 0, total_b = 0;
-    MHW_CK(cudaMemGetInfo(&free_b, &total_b));
-    if (free_b < 16 * g.m + (2ull << 30)) {
-        dev_trim();  // cached blocks count as used
-        MHW_CK(cudaMemGetInfo(&free_b, &total_b));
-    }
-    if (free_b < 16 * g.m + (2ull << 30)) return false;  // keep headroom; the walk works without
+    if (dev_available_bytes() < 16 * g.m + (2ull << 30)) return false;  // keep headroom; the walk works without
     g.arc.alloc(g.m);
     g.arc_aux = aux;
     k_arcrec<<<grid_for(g.m), kBlock, 0, g.stream>>>(g.view(), aux, g.arc.p);

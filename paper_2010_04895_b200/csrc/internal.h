@@ -37,6 +37,7 @@ void* dev_alloc(size_t bytes, size_t* cap);
 void dev_free(void* p, size_t cap);
 void dev_trim();
 size_t dev_cached_bytes();
+size_t dev_available_bytes();  // cudaMemGetInfo free + pool memory reserved but unused
 
 // RAII device buffer on the current device.
 template <class T>

@@ -1038,7 +1038,11 @@ void session_create(Session& s, Graph& g, const mhw_model_desc& md, const mhw_wa
     if (wc.schedule < 0 || wc.schedule > 1) invalid("unknown schedule");
     s.g = &g;
     s.wc = wc;
+    const bool trace = std::getenv("MHW_TRACE") != nullptr;
+    const auto tc0 = std::chrono::steady_clock::now();
+    auto tms = [&] { return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tc0).count(); };
     model_bind(s.model, g, md);
+    const double t_bind = trace ? (cudaDeviceSynchronize(), tms()) : 0.0;
     const DevModel& m = s.model.dev;
     s.cfg.seed = wc.seed;
     s.cfg.K = wc.walks_per_node;
@@ -1212,13 +1216,7 @@ void session_create(Session& s, Graph& g, const mhw_model_desc& md, const mhw_wa
             const bool narrow = m.kind == NODE2VEC && (nw ? nw[0] == '1' : 16ull * g.n <= (32ull << 20));
             s.rec_u32 = typed_kind(m.kind) ? 8 : (narrow ? 2 : 4);
             const uint64_t need = 4ull * s.rec_u32 * g.m;
-            size_t free_b = 0, total_b = 0;
-            MHW_CK(cudaMemGetInfo(&free_b, &total_b));
-            if (free_b < need + (2ull << 30)) {
-                dev_trim();
-                MHW_CK(cudaMemGetInfo(&free_b, &total_b));
-            }
-            if (free_b >= need + (2ull << 30)) {
+            if (dev_available_bytes() >= need + (2ull << 30)) {
                 s.ac.alloc((g.m * s.rec_u32 + 3) / 4);
                 k_arc_chain<<<grid_for(g.n * 32ull), 256, 0, st>>>(g.view(), s.ac.p, s.rec_u32);
                 MHW_CK(cudaGetLastError());
@@ -1236,6 +1234,7 @@ void session_create(Session& s, Graph& g, const mhw_model_desc& md, const mhw_wa
         });
     }
     MHW_CK(cudaStreamSynchronize(st));
+    if (trace) std::fprintf(stderr, "[mhw] session_create: model_bind %.2f ms, total %.2f ms\n", t_bind, tms());
 }
 
 // Persisting L2 access window over [p, p + bytes) on stream st (bytes 0
