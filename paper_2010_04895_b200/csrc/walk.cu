@@ -900,9 +900,13 @@ unsigned grid_for(uint64_t work, int block = 256) {
 // measured in profiles/); MHW_WALK_REGS selects it at session creation.
 // Defaults from the sweep in profiles/: deepwalk 80 (4.84 vs 5.27 ms on cfg1),
 // second-order models uncapped (no spills; 65.7 vs 69-71 ms on cfg2).
-int walk_minb(int kind) {
+int walk_minb(int kind, bool eager) {
     const char* e = std::getenv("MHW_WALK_REGS");
-    const int v = e ? std::atoi(e) : (kind == DEEPWALK ? 80 : 255);
+    // deepwalk: 80; eagerly initialised edge2vec / fairwalk: 80 (84-86 -> 80
+    // registers without spills lifts occupancy from 2 to 3 blocks/SM: cfg3b
+    // 99.5 -> 94.3 ms, cfg4 181 -> 176 ms); the lazy variants would spill
+    const bool cap = kind == DEEPWALK || (eager && (kind == EDGE2VEC || kind == FAIRWALK));
+    const int v = e ? std::atoi(e) : (cap ? 80 : 255);
     return v == 64 ? 64 : (v == 80 ? 80 : 255);
 }
 
@@ -1190,7 +1194,7 @@ void session_create(Session& s, Graph& g, const mhw_model_desc& md, const mhw_wa
         // (identical chain values: init randomness is slot-keyed).
         const bool dense = (double)s.n_items * s.cfg.L >= 8.0 * (double)s.slots;
         s.eager_init = second_order(m.kind) && (wc.init_mode == 2 || (wc.init_mode == 0 && dense));
-        s.minb = walk_minb(m.kind);
+        s.minb = walk_minb(m.kind, s.eager_init);
         // pin a small edge filter in L2 (cfg2: 16 MB, +3%; a 64 MB window
         // starves the rest of the working set: cfg4 -30%)
         if (g.bloom.n && g.bloom.bytes() <= (24ull << 20)) {
