@@ -490,7 +490,7 @@ mhw_status mhw_generate_walks_packed(const mhw_graph* g, const mhw_model_desc* m
         const auto t1 = std::chrono::steady_clock::now();
         if (capacity_rows < s.rows + 1) mhw::invalid("offset buffer too small for the corpus");
         const char* e = std::getenv("MHW_E2E_CHUNKS");
-        const int chunks = e ? std::atoi(e) : 16;
+        const int chunks = e ? std::atoi(e) : 8;
         mhw::session_run_packed(s, h_nodes, capacity_nodes, h_offsets, capacity_rows, chunks, stats);
         if (trace) {
             const auto t2 = std::chrono::steady_clock::now();
