@@ -295,29 +295,32 @@ __global__ void k_arcrec(DevGraph g, int aux, uint4* __restrict__ out) {
 
 // rev[] by sorting: keys (dst << bits | src) of every arc. For a symmetric
 // CSR the k-th arc in (dst, src) order is the reverse of CSR arc k.
-__global__ void k_rev_keys(DevGraph g, int bits, uint64_t* __restrict__ keys, uint32_t* __restrict__ vals) {
+// Keys = destination u of every arc, values = (source v, index within N(v)),
+// in CSR order; a stable sort by u alone then lists each u's in-arcs by
+// increasing v (CSR order is v-major), i.e. in N(u) order for a symmetric
+// CSR -- half the radix passes of sorting (u, v) pairs.
+__global__ void k_rev_keys(DevGraph g, uint32_t* __restrict__ keys, uint64_t* __restrict__ vals) {
     const unsigned lane = threadIdx.x & 31;
     const uint64_t wid = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
     for (uint64_t v = wid; v < g.n; v += nw) {
         const NodeRec r = load_node(g, (uint32_t)v);
         for (uint32_t i = lane; i < r.deg; i += 32) {
-            keys[r.off + i] = ((uint64_t)load_id(g, r.off + i) << bits) | v;
-            vals[r.off + i] = i;  // index of the arc within its source slice
+            keys[r.off + i] = load_id(g, r.off + i);
+            vals[r.off + i] = (v << 32) | i;  // source and index of the arc within its slice
         }
     }
 }
 
-// Sorted position k holds arc (v -> u) with key (u, v): if CSR arc k is
+// Sorted position k holds arc (v -> u) with key u: if CSR arc k is
 // (u -> v) then v sits at index k - off(u) of N(u).
-__global__ void k_rev_scatter(DevGraph g, int bits, const uint64_t* __restrict__ keys,
-                              const uint32_t* __restrict__ vals, uint32_t* __restrict__ rev,
-                              unsigned* __restrict__ mismatch) {
-    const uint64_t mask = (bits >= 64) ? ~0ull : ((1ull << bits) - 1);
+__global__ void k_rev_scatter(DevGraph g, const uint32_t* __restrict__ keys, const uint64_t* __restrict__ vals,
+                              uint32_t* __restrict__ rev, unsigned* __restrict__ mismatch) {
     for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < g.m;
          k += (uint64_t)gridDim.x * blockDim.x) {
-        const uint64_t key = keys[k];
-        const uint32_t u = (uint32_t)(key >> bits), v = (uint32_t)(key & mask);
+        const uint32_t u = keys[k];
+        const uint64_t val = vals[k];
+        const uint32_t v = (uint32_t)(val >> 32);
         const NodeRec ru = load_node(g, u);
         const NodeRec rv = load_node(g, v);
         const bool ok = (uint64_t)ru.off <= k && k < (uint64_t)ru.off + ru.deg && load_id(g, k) == v;
@@ -325,7 +328,7 @@ __global__ void k_rev_scatter(DevGraph g, int bits, const uint64_t* __restrict__
             atomicAdd(mismatch, 1u);
             continue;
         }
-        rev[rv.off + vals[k]] = (uint32_t)(k - (uint64_t)ru.off);
+        rev[rv.off + (uint32_t)val] = (uint32_t)(k - (uint64_t)ru.off);
     }
 }
 
@@ -1004,16 +1007,16 @@ void graph_ensure_rev(Graph& g) {
     unsigned h = 1;
     {
         // one radix sort of (dst, src) keys; valid when the CSR is symmetric
-        DBuf<uint64_t> k1(g.m), k2(g.m);
-        DBuf<uint32_t> v1(g.m), v2(g.m);
+        DBuf<uint32_t> k1(g.m), k2(g.m);
+        DBuf<uint64_t> v1(g.m), v2(g.m);
         DBuf<unsigned> mismatch(1);
         MHW_CK(cudaMemsetAsync(mismatch.p, 0, sizeof(unsigned), st));
-        k_rev_keys<<<grid_for((uint64_t)g.n * 32), kBlock, 0, st>>>(v, bits, k1.p, v1.p);
+        k_rev_keys<<<grid_for((uint64_t)g.n * 32), kBlock, 0, st>>>(v, k1.p, v1.p);
         size_t bytes = 0;
-        MHW_CK(cub::DeviceRadixSort::SortPairs(nullptr, bytes, k1.p, k2.p, v1.p, v2.p, (int64_t)g.m, 0, 2 * bits, st));
+        MHW_CK(cub::DeviceRadixSort::SortPairs(nullptr, bytes, k1.p, k2.p, v1.p, v2.p, (int64_t)g.m, 0, bits, st));
         DBuf<uint8_t> temp(std::max<size_t>(bytes, 1));
-        MHW_CK(cub::DeviceRadixSort::SortPairs(temp.p, bytes, k1.p, k2.p, v1.p, v2.p, (int64_t)g.m, 0, 2 * bits, st));
-        k_rev_scatter<<<grid_for(g.m), kBlock, 0, st>>>(v, bits, k2.p, v2.p, g.rev.p, mismatch.p);
+        MHW_CK(cub::DeviceRadixSort::SortPairs(temp.p, bytes, k1.p, k2.p, v1.p, v2.p, (int64_t)g.m, 0, bits, st));
+        k_rev_scatter<<<grid_for(g.m), kBlock, 0, st>>>(v, k2.p, v2.p, g.rev.p, mismatch.p);
         MHW_CK(cudaGetLastError());
         MHW_CK(cudaMemcpyAsync(&h, mismatch.p, sizeof(h), cudaMemcpyDeviceToHost, st));
         MHW_CK(cudaStreamSynchronize(st));
