@@ -280,15 +280,13 @@ __global__ void k_hash_build(DevGraph g, uint32_t* __restrict__ tab) {
     }
 }
 
-// Thread per arc: arc record {u, deg(u)|allpos<<31, off(u), aux}.
-__global__ void k_arcrec(DevGraph g, int aux, uint4* __restrict__ out) {
+// Thread per arc: arc record {u, deg(u)|allpos<<31, off(u), fp32 w(a)}.
+__global__ void k_arcrec(DevGraph g, uint4* __restrict__ out) {
     for (uint64_t a = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; a < g.m;
          a += (uint64_t)gridDim.x * blockDim.x) {
         const uint32_t u = load_id(g, a);
         const NodeRec r = load_node(g, u);
-        uint32_t x = 0;
-        if (aux == ARC_AUX_REV) x = __ldg(g.rev + a);
-        else x = __float_as_uint(g.w ? __ldg(g.w + a) : 1.0f);
+        const uint32_t x = __float_as_uint(g.w ? __ldg(g.w + a) : 1.0f);
         out[a] = make_uint4(u, r.deg | ((r.flags & NF_ALLPOS) ? 0x80000000u : 0u), (uint32_t)r.off, x);
     }
 }
@@ -711,7 +709,8 @@ void graph_finalize(Graph& g, const int64_t* d_off, const uint16_t* d_ntypes) {
     g.tcount.reset();
     g.htab.reset();
     g.arc.reset();
-    g.arc_aux = 0;
+    g.bloom.reset();
+    g.bloom_blocks = 0;
     g.verified_sym = false;
 }
 
@@ -960,7 +959,6 @@ void graph_replicate(const Graph& s, Graph& d, int device) {
     copy_buf(s.tcount, s.device, d.tcount, device, d.stream);
     copy_buf(s.htab, s.device, d.htab, device, d.stream);
     copy_buf(s.arc, s.device, d.arc, device, d.stream);
-    d.arc_aux = s.arc_aux;
     MHW_CK(cudaStreamSynchronize(d.stream));
     d.n = s.n;
     d.m = s.m;
@@ -1070,15 +1068,13 @@ void graph_ensure_bloom(Graph& g) {
     MHW_CK(cudaStreamSynchronize(g.stream));
 }
 
-bool graph_ensure_arcrec(Graph& g, int aux) {
-    if (g.arc.n && g.arc_aux == aux) return true;
+bool graph_ensure_arcrec(Graph& g) {
+    if (g.arc.n) return true;
     if (!g.m || g.m >= (1ull << 32)) return false;
     DeviceGuard dg(g.device);
-    if (aux == ARC_AUX_REV) graph_ensure_rev(g);
     if (dev_available_bytes() < 16 * g.m + (2ull << 30)) return false;  // keep headroom; the walk works without
     g.arc.alloc(g.m);
-    g.arc_aux = aux;
-    k_arcrec<<<grid_for(g.m), kBlock, 0, g.stream>>>(g.view(), aux, g.arc.p);
+    k_arcrec<<<grid_for(g.m), kBlock, 0, g.stream>>>(g.view(), g.arc.p);
     MHW_CK(cudaGetLastError());
     MHW_CK(cudaStreamSynchronize(g.stream));
     return true;

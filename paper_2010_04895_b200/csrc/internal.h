@@ -109,7 +109,6 @@ struct Graph {
     DBuf<uint32_t> bloom;    // edge Bloom filter (second-order alpha), lazily built
     uint32_t bloom_blocks = 0;
     DBuf<uint4> arc;         // arc records, lazily built (m < 2^32)
-    int arc_aux = 0;         // ARC_AUX_REV / ARC_AUX_WEIGHT
     uint16_t n_ntypes = 0, n_etypes = 0;
     bool symmetric = false;
     bool verified_sym = false;
@@ -142,7 +141,7 @@ void graph_ensure_wtotal(Graph& g);
 void graph_ensure_tcount(Graph& g);
 void graph_ensure_hash(Graph& g);
 void graph_ensure_bloom(Graph& g);
-bool graph_ensure_arcrec(Graph& g, int aux);
+bool graph_ensure_arcrec(Graph& g);  // deepwalk arc records (fp32 weight aux)
 void graph_alias_tables(Graph& g, double* prob, uint32_t* alias);
 // Same tables left on the device (prob, alias: m entries each).
 void graph_alias_device(Graph& g, double* prob, uint32_t* alias);

@@ -74,11 +74,9 @@ struct DevGraph {
 
 // ------------------------------------------------------------ arc records
 // For graphs with < 2^32 arcs, arc a = (v -> u) has a 16-byte record
-// {u, deg(u) | NF_ALLPOS(u) << 31, off(u), aux} with aux = rev[a] (index of v
-// in N(u), second-order models) or the fp32 weight bits of a (first-order):
-// one load yields everything the next walker state needs.
-constexpr int ARC_AUX_REV = 1;
-constexpr int ARC_AUX_WEIGHT = 2;
+// {u, deg(u) | NF_ALLPOS(u) << 31, off(u), fp32 w(a)} (graph records, used by
+// deepwalk; the other models use per-session records, walk.cu): one load
+// yields everything the next walker state needs.
 
 __device__ __forceinline__ NodeRec arc_node(uint4 a) {
     NodeRec r;

@@ -1229,7 +1229,7 @@ void session_create(Session& s, Graph& g, const mhw_model_desc& md, const mhw_wa
         }
         if (!s.ac.n || !second_order(m.kind)) s.chain.alloc(std::max<uint64_t>(s.slots, 1));
         else s.chain.alloc(1);
-        if (want_ar && m.kind == DEEPWALK) s.use_ar = graph_ensure_arcrec(g, ARC_AUX_WEIGHT);
+        if (want_ar && m.kind == DEEPWALK) s.use_ar = graph_ensure_arcrec(g);
         dispatch(m.kind, [&](auto kc) {
             constexpr int KIND = decltype(kc)::value;
             with_variant<KIND>(s.minb, !s.eager_init, s.ar_mode(), [&](auto rg, auto lz, auto ar) {
