@@ -457,12 +457,7 @@ mhw_status mhw_walk_rows(const mhw_graph* g, const mhw_model_desc* model, const 
         need(g, "graph");
         need(model, "model");
         need(config, "config");
-        auto* gg = const_cast<mhw_graph*>(g);
-        mhw::DeviceGuard dg(gg->device);
-        mhw_session s;
-        mhw::session_create(s, *gg, *model, *config);
-        if (rows) *rows = s.rows;
-        if (stride) *stride = s.stride;
+        mhw::walk_rows(*const_cast<mhw_graph*>(g), *model, *config, rows, stride);
     });
 }
 

@@ -1358,6 +1358,39 @@ void session_run(Session& s, cudaStream_t user) {
     MHW_CK(cudaEventRecord(s.ev1, st));
 }
 
+// Corpus rows of a generate_walks call (valid starts in the node range x
+// K) and the padded row stride, without building a session.
+void walk_rows(Graph& g, const mhw_model_desc& md, const mhw_walk_config& wc, uint64_t* rows, uint32_t* stride) {
+    DeviceGuard dg(g.device);
+    if (wc.walks_per_node == 0 || wc.walk_length == 0)
+        invalid("walks_per_node, walk_length and threads must be positive");
+    Model mb;
+    model_bind(mb, g, md);
+    const uint32_t b = wc.node_begin, e = wc.node_end ? wc.node_end : g.n;
+    if (e > g.n || b > e) invalid("node range out of bounds");
+    uint64_t n_valid = 0;
+    if (e > b) {
+        cudaStream_t st = g.stream;
+        const uint32_t span = e - b;
+        DBuf<uint8_t> valid(span), act(span), iso(span);
+        DBuf<uint32_t> rank(span);
+        k_classify<<<grid_for(span), 256, 0, st>>>(g.view(), mb.dev, b, e, valid.p, act.p, iso.p);
+        MHW_CK(cudaGetLastError());
+        size_t bytes = 0;
+        MHW_CK(cub::DeviceScan::ExclusiveSum(nullptr, bytes, valid.p, rank.p, (int64_t)span, st));
+        DBuf<uint8_t> temp(std::max<size_t>(bytes, 1));
+        MHW_CK(cub::DeviceScan::ExclusiveSum(temp.p, bytes, valid.p, rank.p, (int64_t)span, st));
+        uint32_t last_rank = 0;
+        uint8_t last_valid = 0;
+        MHW_CK(cudaMemcpyAsync(&last_rank, rank.p + span - 1, 4, cudaMemcpyDeviceToHost, st));
+        MHW_CK(cudaMemcpyAsync(&last_valid, valid.p + span - 1, 1, cudaMemcpyDeviceToHost, st));
+        MHW_CK(cudaStreamSynchronize(st));
+        n_valid = (uint64_t)last_rank + last_valid;
+    }
+    if (rows) *rows = n_valid * wc.walks_per_node;
+    if (stride) *stride = (wc.walk_length + 1 + 3) & ~3u;
+}
+
 void session_init_chain(Session& s, uint64_t begin, uint64_t end, uint32_t* d_words, cudaStream_t user) {
     DeviceGuard dg(s.g->device);
     if (!second_order(s.model.dev.kind) || s.ex || s.wc.schedule == MHW_SCHEDULE_DETERMINISTIC)
@@ -1491,14 +1524,16 @@ void session_run_packed(Session& s, uint32_t* h_nodes, uint64_t cap_nodes, uint6
     auto ms_since = [&](clk::time_point t) { return std::chrono::duration<double, std::milli>(clk::now() - t).count(); };
     cudaStream_t S = s.stream, T = nullptr;
     MHW_CK(cudaStreamCreateWithFlags(&T, cudaStreamNonBlocking));
-    std::vector<cudaEvent_t> ev(chunks, nullptr);
+    std::vector<cudaEvent_t> ev(chunks, nullptr), cdone(chunks, nullptr);
     auto cleanup = [&] {
-        for (auto& e : ev)
-            if (e) cudaEventDestroy(e);
+        for (auto* v : {&ev, &cdone})
+            for (auto& e : *v)
+                if (e) cudaEventDestroy(e);
         if (T) cudaStreamDestroy(T);
     };
     try {
-        for (auto& e : ev) MHW_CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        for (auto* v : {&ev, &cdone})
+            for (auto& e : *v) MHW_CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
         // chunk boundaries over the active-node list and their first rows
         std::vector<uint32_t> jc(chunks + 1);
         std::vector<uint64_t> rc(chunks + 1);
@@ -1510,7 +1545,10 @@ void session_run_packed(Session& s, uint32_t* h_nodes, uint64_t cap_nodes, uint6
         uint64_t max_rows = 0;
         for (int c = 0; c < chunks; ++c) max_rows = std::max(max_rows, rc[c + 1] - rc[c]);
         const uint64_t rowcap = (uint64_t)s.cfg.L + 1;
-        DBuf<uint32_t> packed(std::max<uint64_t>(s.rows * rowcap, 1));
+        // two staging buffers of one chunk each: chunk c packs into buffer
+        // c & 1 once the copy of chunk c - 2 out of it has finished
+        DBuf<uint32_t> stage0(std::max<uint64_t>(max_rows * rowcap, 1)), stage1(std::max<uint64_t>(max_rows * rowcap, 1));
+        uint32_t* const stage[2] = {stage0.p, stage1.p};
         DBuf<uint64_t> len64(s.rows + 1), goff(s.rows + 1);
         std::vector<DBuf<uint64_t>> offc(chunks);
         uint64_t* h_tot = pinned_scratch(chunks);
@@ -1536,6 +1574,16 @@ void session_run_packed(Session& s, uint32_t* h_nodes, uint64_t cap_nodes, uint6
                 if (s.eager_init) k_init_all<KIND><<<grid_for(s.g->m), 256, 0, S>>>(P);
             }
         });
+        uint64_t H = 0;
+        auto issue_copy = [&](int c) {
+            MHW_CK(cudaEventSynchronize(ev[c]));
+            const uint64_t tot = h_tot[c];
+            if (H + tot > cap_nodes) invalid("node buffer too small for the corpus");
+            MHW_CK(cudaStreamWaitEvent(T, ev[c], 0));
+            if (tot) MHW_CK(cudaMemcpyAsync(h_nodes + H, stage[c & 1], tot * 4, cudaMemcpyDeviceToHost, T));
+            MHW_CK(cudaEventRecord(cdone[c], T));
+            H += tot;
+        };
         for (int c = 0; c < chunks; ++c) {
             RunParams Pc = P;
             Pc.act = s.act.p + jc[c];
@@ -1550,32 +1598,25 @@ void session_run_packed(Session& s, uint32_t* h_nodes, uint64_t cap_nodes, uint6
                         <<<s.grid, kWalkBlock, 0, S>>>(Pc);
                 });
             });
-            // pack rows [rc[c], rc[c+1]) into packed + rc[c] * (L+1)
+            // pack rows [rc[c], rc[c+1]) into staging buffer c & 1
             const uint64_t nr = rc[c + 1] - rc[c];
             offc[c].alloc(nr + 1);
             k_len64<<<grid_for(nr + 1), 256, 0, S>>>(s.lens.p + rc[c], nr, len64.p + rc[c]);
             size_t b = scan_bytes;
             MHW_CK(cub::DeviceScan::ExclusiveSum(scan_tmp.p, b, len64.p + rc[c], offc[c].p, (int64_t)nr + 1, S));
+            if (c >= 2) MHW_CK(cudaStreamWaitEvent(S, cdone[c - 2], 0));
             if (nr)
                 k_pack<<<grid_for(nr * 32), 256, 0, S>>>(s.out.p + rc[c] * s.stride, s.stride, offc[c].p, nr,
-                                                        packed.p + rc[c] * rowcap);
+                                                        stage[c & 1]);
             MHW_CK(cudaMemcpyAsync(h_tot + c, offc[c].p + nr, 8, cudaMemcpyDeviceToHost, S));
             MHW_CK(cudaEventRecord(ev[c], S));
+            // copy chunk c - 1 while chunk c walks
+            if (c >= 1) issue_copy(c - 1);
         }
         if (pin) l2_window(S, nullptr, 0);
         MHW_CK(cudaEventRecord(s.ev1, S));
         MHW_CK(cudaGetLastError());
-        // copy chunk c while later chunks walk
-        uint64_t H = 0;
-        for (int c = 0; c < chunks; ++c) {
-            MHW_CK(cudaEventSynchronize(ev[c]));
-            const uint64_t tot = h_tot[c];
-            if (H + tot > cap_nodes) invalid("node buffer too small for the corpus");
-            MHW_CK(cudaStreamWaitEvent(T, ev[c], 0));
-            if (tot)
-                MHW_CK(cudaMemcpyAsync(h_nodes + H, packed.p + rc[c] * rowcap, tot * 4, cudaMemcpyDeviceToHost, T));
-            H += tot;
-        }
+        issue_copy(chunks - 1);
         const double t_issued = ms_since(ta);
         // global row offsets (one scan over all lengths) and the counters
         k_len64<<<grid_for(s.rows + 1), 256, 0, S>>>(s.lens.p, s.rows, len64.p);

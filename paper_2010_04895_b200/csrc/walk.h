@@ -85,6 +85,7 @@ struct Session {
 uint64_t k_slots(int kind, const Graph& g);
 void session_create(Session& s, Graph& g, const mhw_model_desc& md, const mhw_walk_config& wc);
 void session_run(Session& s, cudaStream_t stream);
+void walk_rows(Graph& g, const mhw_model_desc& md, const mhw_walk_config& wc, uint64_t* rows, uint32_t* stride);
 void session_init_chain(Session& s, uint64_t begin, uint64_t end, uint32_t* d_words, cudaStream_t stream);
 void session_load_chain(Session& s, const uint32_t* d_words, cudaStream_t stream);
 void session_stats(Session& s, mhw_walk_stats& out);

@@ -158,3 +158,25 @@ def test_mega_hub_star(mhw):
         # from the hub every step leaves it; from a leaf every step returns
         assert (rows[hub_pos][:, 1::2] != 0).all() and (rows[hub_pos][:, 2::2] == 0).all()
         assert (rows[~hub_pos][:, 1::2] == 0).all() and (rows[~hub_pos][:, 2::2] != 0).all()
+
+
+def test_walk_rows_matches_corpus(mhw):
+    """mhw_walk_rows sizes the caller's buffers without building a session:
+    valid starts (metapath2vec: type == metapath[0]) in the node range x K."""
+    import ctypes as C
+
+    from paper_2010_04895_b200 import _lib as L
+    rng = O.XoRng(44)
+    g = O.random_graph(90, 4.0, True, rng, ensure_connected=False)
+    O.assign_random_types(g, 2, rng)
+    dg = device_graph(g)
+    for kind in (O.DEEPWALK, O.METAPATH2VEC, O.NODE2VEC):
+        m = walk_model(model_desc(kind, g))
+        for b, e in ((0, 0), (10, 70)):
+            cfg = mhw.WalkConfig(walks_per_node=3, walk_length=9, threads=8, seed=1, node_begin=b, node_end=e)
+            d, keep = m._desc()
+            c = cfg._c()
+            rows, stride = C.c_uint64(), C.c_uint32()
+            assert L.lib().mhw_walk_rows(dg.handle, C.byref(d), C.byref(c), C.byref(rows), C.byref(stride)) == 0
+            corpus = mhw.generate_walks(dg, m, cfg)
+            assert rows.value == len(corpus) and stride.value == 12
