@@ -125,14 +125,51 @@ def make_config(cfg, node_begin=0, node_end=0):
 
 
 class Clocks:
-    """nvidia-smi sampling during the timed region."""
+    """SM clock + throttle-reason sampling during the timed region.
+
+    NVML from a host thread every 2 ms (a cfg1 timed region is ~10 ms, far
+    shorter than nvidia-smi's 200 ms loop); nvidia-smi -lms is the fallback
+    when pynvml is missing. The device is the physical index (one visible GPU)."""
 
     def __init__(self, device):
         self.device = device
         self.proc = None
+        self.nvml = None
+        self.rows = []
         self.path = os.path.join(ROOT, "gpurun_out", f"clocks_{os.getpid()}.csv")
 
+    def _nvml_loop(self, h, N):
+        bits = [("hw_slowdown", N.nvmlClocksEventReasonHwSlowdown),
+                ("hw_thermal_slowdown", N.nvmlClocksEventReasonHwThermalSlowdown),
+                ("sw_thermal_slowdown", N.nvmlClocksEventReasonSwThermalSlowdown),
+                ("sw_power_cap", N.nvmlClocksEventReasonSwPowerCap)]
+        mx = N.nvmlDeviceGetMaxClockInfo(h, N.NVML_CLOCK_SM)
+        while not self.stop.is_set():
+            try:
+                sm = N.nvmlDeviceGetClockInfo(h, N.NVML_CLOCK_SM)
+                r = N.nvmlDeviceGetCurrentClocksEventReasons(h)
+                self.rows.append((sm, mx, [n for n, b in bits if r & b]))
+            except Exception:
+                pass
+            self.stop.wait(0.002)
+
     def __enter__(self):
+        try:
+            import threading
+            import pynvml as N
+            N.nvmlInit()
+            vis = os.environ.get("CUDA_VISIBLE_DEVICES", "")
+            idx = int(vis.split(",")[self.device]) if vis and vis.split(",")[0].isdigit() else self.device
+            h = N.nvmlDeviceGetHandleByIndex(idx)
+            self.stop = threading.Event()
+            self.nvml = threading.Thread(target=self._nvml_loop, args=(h, N), daemon=True)
+            self.nvml.start()
+            return self
+        except Exception:
+            self.nvml = None
+        return self._enter_smi()
+
+    def _enter_smi(self):
         os.makedirs(os.path.dirname(self.path), exist_ok=True)
         q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
@@ -147,6 +184,9 @@ class Clocks:
         return self
 
     def __exit__(self, *a):
+        if self.nvml:
+            self.stop.set()
+            self.nvml.join(timeout=5)
         if self.proc:
             self.proc.terminate()
             try:
@@ -156,6 +196,12 @@ class Clocks:
             self.f.close()
 
     def summary(self):
+        if self.nvml:
+            if not self.rows:
+                return None
+            reasons = sorted({n for _, _, rs in self.rows for n in rs})
+            return {"sm_mhz": float(np.median([r[0] for r in self.rows])), "sm_max_mhz": float(self.rows[0][1]),
+                    "reasons": reasons, "samples": len(self.rows), "source": "nvml 2 ms"}
         try:
             rows = [r.split(",") for r in open(self.path).read().strip().splitlines()]
         except Exception:

@@ -72,6 +72,16 @@ struct DevGraph {
     int verified_sym;                     // every arc has its back arc
 };
 
+// One 32-byte sector in one request: sm_100's 256-bit vector load
+// (LDG.E.ENL2.256). Two 16-byte __ldg of the same sector are two L1 lookups
+// and, on a miss, two L2 requests; the L2-resident probes (edge filter, hash
+// buckets) are request-rate bound.
+__device__ __forceinline__ void ldg256(const void* p, uint4& lo, uint4& hi) {
+    asm("ld.global.nc.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(lo.x), "=r"(lo.y), "=r"(lo.z), "=r"(lo.w), "=r"(hi.x), "=r"(hi.y), "=r"(hi.z), "=r"(hi.w)
+                 : "l"(p));
+}
+
 // ------------------------------------------------------------ arc records
 // For graphs with < 2^32 arcs, arc a = (v -> u) has a 16-byte record
 // {u, deg(u) | NF_ALLPOS(u) << 31, off(u), fp32 w(a)} (graph records, used by
@@ -131,7 +141,8 @@ __host__ __device__ __forceinline__ uint32_t bloom_block(uint64_t x, uint32_t bl
 __device__ __forceinline__ bool bloom_maybe(const DevGraph& g, uint32_t a, uint32_t b) {
     const uint64_t x = bloom_key(a, b);
     const uint4* blk = reinterpret_cast<const uint4*>(g.bloom) + 2 * (uint64_t)bloom_block(x, g.bloom_blocks);
-    const uint4 lo = __ldg(blk), hi = __ldg(blk + 1);
+    uint4 lo, hi;
+    ldg256(blk, lo, hi);
     // 256-bit block as four 64-bit words, selected without a local array
     const uint64_t q0 = ((uint64_t)lo.y << 32) | lo.x, q1 = ((uint64_t)lo.w << 32) | lo.z;
     const uint64_t q2 = ((uint64_t)hi.y << 32) | hi.x, q3 = ((uint64_t)hi.w << 32) | hi.z;
@@ -152,7 +163,8 @@ __device__ __forceinline__ bool hash_contains(const uint32_t* __restrict__ tab, 
     const uint4* base = reinterpret_cast<const uint4*>(tab) + 2 * hash_base(off, v);
     uint32_t b = hash_bucket(key, nb);
     for (;;) {
-        const uint4 x = __ldg(base + 2 * b), y = __ldg(base + 2 * b + 1);
+        uint4 x, y;
+        ldg256(base + 2 * b, x, y);
         if (x.x == key || x.y == key || x.z == key || x.w == key || y.x == key || y.y == key || y.z == key ||
             y.w == key)
             return true;

@@ -101,7 +101,11 @@ __global__ void __launch_bounds__(kWalkBlock) __maxnreg__(REGS) k_walk(RunParams
             const NodeRec r = load_node(g, x.x);
             return make_uint4(x.x, r.deg | ((r.flags & NF_ALLPOS) ? 0x80000000u : 0u), (uint32_t)r.off, x.y);
         }
-        if (TYPED) b = __ldg(arcs + RS * arc + 1);
+        if constexpr (TYPED) {
+            uint4 a;
+            ldg256(arcs + RS * arc, a, b);  // the whole 32-byte record in one request
+            return a;
+        }
         return __ldg(arcs + RS * arc);
     };
     auto rec_node = [&](const uint4& a, const uint4& b) {
