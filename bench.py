@@ -107,12 +107,16 @@ def make_model(cfg):
                          type_matrix=type_matrix(cfg) if cfg["model"] == "edge2vec" else None)
 
 
-def eager_at_n1(cfg, g):
-    """Would one GPU initialise every slot eagerly (session_create's rule:
-    walker steps >= 8 x slots)? Then N ranks share that work instead."""
+def shard_init_pays(cfg, g):
+    """Do the walks touch most arc-keyed slots (walker steps >= 2 x slots)?
+    Then N ranks share one initialisation (each inits 1/N of the records,
+    all-gather, coalesced install) instead of each rank initialising, eagerly
+    or lazily, most of the table itself. cfg5 (steps = 5 x slots, lazy at N=1,
+    every slot touched): 8 shards 205 -> 154 ms per rank
+    (profiles/shard_scaling_r01.md)."""
     off = g.download()["offsets"]
     walkers = int(np.count_nonzero(np.diff(off))) * cfg["K"]
-    return walkers * cfg["L"] >= 8 * int(off[-1])
+    return walkers * cfg["L"] >= 2 * int(off[-1])
 
 
 def make_config(cfg, node_begin=0, node_end=0):
@@ -121,7 +125,8 @@ def make_config(cfg, node_begin=0, node_end=0):
                           init=mhw.InitStrategy(mhw.InitKind[cfg["init"]], cfg.get("burn_in", 100), 32),
                           schedule=mhw.Schedule.throughput, node_begin=node_begin, node_end=node_end,
                           chain_replica_degree=int(os.environ.get("MHW_REP_DEG", "0")),
-                          sampler_kind=mhw.SamplerKind[cfg.get("sampler", "mh")])
+                          sampler_kind=mhw.SamplerKind[cfg.get("sampler", "mh")],
+                          init_mode=int(os.environ.get("MHW_INIT_MODE", "0")))
 
 
 class Clocks:
@@ -346,12 +351,12 @@ def run_mine(args, cfg):
     model = make_model(cfg)
     cuts = mhw.partition_nodes(g, model, world)
     wcfg = make_config(cfg, int(cuts[rank]), int(cuts[rank + 1]))
-    # Multi-GPU, second-order models with an eagerly initialised chain table
-    # (walks touch most slots): the initial table is a pure function of the
-    # slot, so each rank initialises 1/N of the slots and the words are
-    # all-gathered (the walk itself has no exchange).
+    # Multi-GPU, second-order models whose walks touch most slots: the initial
+    # table is a pure function of the slot, so each rank initialises 1/N of
+    # the records (record order: the install is a coalesced strided copy) and
+    # the words are all-gathered (the walk itself has no exchange).
     shard_init = (world > 1 and cfg["model"] in ("node2vec", "edge2vec", "fairwalk")
-                  and cfg.get("sampler", "mh") == "mh" and eager_at_n1(cfg, g))
+                  and cfg.get("sampler", "mh") == "mh" and shard_init_pays(cfg, g))
     if shard_init:
         wcfg.init_mode = 2
     sess = mhw.Session(g, model, wcfg)
@@ -372,22 +377,22 @@ def run_mine(args, cfg):
     per = 0
     if shard_init:
         S = sess.chain_size()
+        W = sess.record_width()  # u32 words per record entry (3: typed records carry w'(Last))
         per = (S + world - 1) // world
-        c_dev = "cpu" if host_coll else dev
-        shard = torch.empty(per, dtype=torch.int32, device=dev)
-        full = torch.empty(per * world, dtype=torch.int32, device=dev)
+        shard = torch.empty(per * W, dtype=torch.int32, device=dev)
+        full = torch.empty(per * world * W, dtype=torch.int32, device=dev)
         lo, hi = min(S, rank * per), min(S, (rank + 1) * per)
 
     def one_run():
         if shard_init:
-            sess.init_chain(lo, hi, shard.data_ptr(), stream.cuda_stream)
+            sess.init_records(lo, hi, shard.data_ptr(), stream.cuda_stream)
             if host_coll:
-                parts = [torch.empty(per, dtype=torch.int32) for _ in range(world)]
+                parts = [torch.empty(per * W, dtype=torch.int32) for _ in range(world)]
                 dist.all_gather(parts, shard.cpu())
                 full.copy_(torch.cat(parts).to(dev))
             else:
                 dist.all_gather_into_tensor(full, shard)
-            sess.load_chain(full.data_ptr(), stream.cuda_stream)
+            sess.load_records(full.data_ptr(), stream.cuda_stream)
         sess.run(stream.cuda_stream)
         return sess.launches() + (2 if shard_init else 0)
 

@@ -313,6 +313,20 @@ MHW_API mhw_status mhw_session_chain_size(const mhw_session* s, uint64_t* words)
 MHW_API mhw_status mhw_session_init_chain(mhw_session* s, uint64_t begin, uint64_t end, uint32_t* d_words,
                                           void* stream);
 MHW_API mhw_status mhw_session_load_chain(mhw_session* s, const uint32_t* d_words, void* stream);
+/* The same table in RECORD order: word i belongs to arc i = (s -> v), i.e.
+ * to state (s, v), slot off(v) + index of s in N(v). Sessions keep each
+ * second-order chain word in the record of the arc that enters its state, so
+ * a record-order table installs with one coalesced strided copy
+ * (load_records) instead of a random scatter (load_chain); ranks all-gather
+ * contiguous record ranges exactly as with init_chain. Entry i of
+ * init_records holds word (off(v) + rev(i)) of init_chain; an entry is
+ * record_width u32 words: 1, or 3 for edge2vec / fairwalk sessions, whose
+ * records cache w'(Last) beside the word ({word, w'(Last) as f64 lo, hi}),
+ * so the install computes nothing. d_words holds (end - begin) * width words. */
+MHW_API mhw_status mhw_session_record_width(const mhw_session* s, uint32_t* width);
+MHW_API mhw_status mhw_session_init_records(mhw_session* s, uint64_t begin, uint64_t end, uint32_t* d_words,
+                                            void* stream);
+MHW_API mhw_status mhw_session_load_records(mhw_session* s, const uint32_t* d_words, void* stream);
 MHW_API void mhw_session_free(mhw_session* s);
 
 /* ---- parity entry points ---------------------------------------------- */

@@ -599,6 +599,30 @@ mhw_status mhw_session_load_chain(mhw_session* s, const uint32_t* d_words, void*
     });
 }
 
+mhw_status mhw_session_init_records(mhw_session* s, uint64_t begin, uint64_t end, uint32_t* d_words, void* stream) {
+    return guard([&] {
+        need(s, "session");
+        if (end > begin) need(d_words, "d_words");
+        mhw::session_init_chain(*s, begin, end, d_words, static_cast<cudaStream_t>(stream), true);
+    });
+}
+
+mhw_status mhw_session_record_width(const mhw_session* s, uint32_t* width) {
+    return guard([&] {
+        need(s, "session");
+        need(width, "width");
+        *width = mhw::session_record_width(*s);
+    });
+}
+
+mhw_status mhw_session_load_records(mhw_session* s, const uint32_t* d_words, void* stream) {
+    return guard([&] {
+        need(s, "session");
+        need(d_words, "d_words");
+        mhw::session_load_chain(*s, d_words, static_cast<cudaStream_t>(stream), true);
+    });
+}
+
 void mhw_session_free(mhw_session* s) {
     if (!s) return;
     int dev = s->g ? s->g->device : 0;

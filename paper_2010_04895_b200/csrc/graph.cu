@@ -135,6 +135,7 @@ DevGraph Graph::view() const {
     d.etype = etype.n ? etype.p : nullptr;
     d.rev = rev.n ? rev.p : nullptr;
     d.wtotal = wtotal.n ? wtotal.p : nullptr;
+    d.wblk = wblk.n ? wblk.p : nullptr;
     d.tcount = tcount.n ? tcount.p : nullptr;
     d.htab = htab.n ? htab.p : nullptr;
     d.arc = arc.n ? arc.p : nullptr;
@@ -148,7 +149,7 @@ DevGraph Graph::view() const {
 
 uint64_t Graph::device_bytes() const {
     return nodes.bytes() + ids.bytes() + w.bytes() + ntype.bytes() + etype.bytes() + rev.bytes() +
-           wtotal.bytes() + tcount.bytes() + htab.bytes() + arc.bytes() + bloom.bytes();
+           wtotal.bytes() + wblk.bytes() + tcount.bytes() + htab.bytes() + arc.bytes() + bloom.bytes();
 }
 
 namespace {
@@ -339,6 +340,64 @@ __global__ void k_wtotal(DevGraph g, double* __restrict__ out) {
         double t = 0.0;
         for (uint32_t i = 0; i < r.deg; ++i) t = __dadd_rn(t, (double)g.w[r.off + i]);
         out[v] = t;
+    }
+}
+
+// Warp per node of degree >= kBootBlkMin: exact block prefix sums for the
+// weighted bootstrap (bootstrap_pick). direct_sample subtracts the weights
+// one by one from r = u * total (samplers.cpp:136-145). With weights >= 0
+// that are all multiples of 2^e (e = the smallest fp32 ulp exponent in the
+// slice) and total < 2^(53 + e), every remainder the scan keeps is exact
+// (r - P_i, P_i the exact prefix), and the first negative one has the right
+// sign; so block prefixes (exact in any summation order) locate the crossing
+// block and the scan resumes there with identical arithmetic. Slices without
+// that guarantee get NaN in their first entry and keep the full scan.
+__global__ void k_wblk(DevGraph g, double* __restrict__ out) {
+    const unsigned lane = threadIdx.x & 31;
+    const uint64_t wid = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    for (uint64_t v = wid; v < g.n; v += nw) {
+        const NodeRec r = load_node(g, (uint32_t)v);
+        if (r.deg < kBootBlkMin) continue;
+        const float* w = g.w + r.off;
+        int emin = 1 << 20;
+        double tot = 0.0;
+        for (uint32_t i = lane; i < r.deg; i += 32) {
+            const float x = w[i];
+            if (x > 0.0f) {
+                const int ex = x >= 1.17549435e-38f ? ((__float_as_int(x) >> 23) & 0xFF) - 127 - 23 : -149;
+                emin = min(emin, ex);
+            }
+            tot += (double)x;
+        }
+        for (int o = 16; o; o >>= 1) {
+            emin = min(emin, __shfl_xor_sync(0xFFFFFFFFu, emin, o));
+            tot += __shfl_xor_sync(0xFFFFFFFFu, tot, o);
+        }
+        double* P = out + wblk_base(r.off, (uint32_t)v);
+        const uint32_t nb = (r.deg + 31) >> 5;
+        // emin == 1 << 20: all weights zero (total 0, the bootstrap is a dead end)
+        const bool exact = emin < (1 << 20) && emin + 53 < 1000 && tot < ldexp(1.0, emin + 53);
+        if (!exact) {
+            if (lane == 0) P[0] = __longlong_as_double(0x7FF8000000000000ll);
+            continue;
+        }
+        double carry = 0.0;
+        for (uint32_t b0 = 0; b0 < nb; b0 += 32) {
+            const uint32_t b = b0 + lane;
+            double x = 0.0;
+            if (b < nb) {
+                const uint32_t e = min(r.deg, 32 * b + 32);
+                for (uint32_t i = 32 * b; i < e; ++i) x += (double)w[i];
+            }
+            for (int o = 1; o < 32; o <<= 1) {  // inclusive scan over the 32 blocks
+                const double y = __shfl_up_sync(0xFFFFFFFFu, x, o);
+                if (lane >= (unsigned)o) x += y;
+            }
+            x += carry;
+            if (b < nb) P[b] = x;
+            carry = __shfl_sync(0xFFFFFFFFu, x, 31);
+        }
     }
 }
 
@@ -706,6 +765,7 @@ void graph_finalize(Graph& g, const int64_t* d_off, const uint16_t* d_ntypes) {
     g.isolated = h[2];
     g.rev.reset();
     g.wtotal.reset();
+    g.wblk.reset();
     g.tcount.reset();
     g.htab.reset();
     g.arc.reset();
@@ -956,6 +1016,7 @@ void graph_replicate(const Graph& s, Graph& d, int device) {
     copy_buf(s.etype, s.device, d.etype, device, d.stream);
     copy_buf(s.rev, s.device, d.rev, device, d.stream);
     copy_buf(s.wtotal, s.device, d.wtotal, device, d.stream);
+    copy_buf(s.wblk, s.device, d.wblk, device, d.stream);
     copy_buf(s.tcount, s.device, d.tcount, device, d.stream);
     copy_buf(s.htab, s.device, d.htab, device, d.stream);
     copy_buf(s.arc, s.device, d.arc, device, d.stream);
@@ -1086,6 +1147,11 @@ void graph_ensure_wtotal(Graph& g) {
     g.wtotal.alloc(g.n);
     k_wtotal<<<grid_for(g.n, 64), 64, 0, g.stream>>>(g.view(), g.wtotal.p);
     MHW_CK(cudaGetLastError());
+    if (g.max_deg >= kBootBlkMin) {
+        g.wblk.alloc((g.m >> 5) + g.n + 1);
+        k_wblk<<<grid_for((uint64_t)g.n * 32), 256, 0, g.stream>>>(g.view(), g.wblk.p);
+        MHW_CK(cudaGetLastError());
+    }
     MHW_CK(cudaStreamSynchronize(g.stream));
 }
 

@@ -104,6 +104,7 @@ struct Graph {
     DBuf<uint16_t> etype;    // empty: derived
     DBuf<uint32_t> rev;      // lazily built
     DBuf<double> wtotal;     // lazily built
+    DBuf<double> wblk;       // bootstrap block prefix sums, built with wtotal
     DBuf<uint32_t> tcount;   // lazily built
     DBuf<uint32_t> htab;     // adjacency hash sets, lazily built
     DBuf<uint32_t> bloom;    // edge Bloom filter (second-order alpha), lazily built

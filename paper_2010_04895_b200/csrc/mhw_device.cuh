@@ -62,6 +62,7 @@ struct DevGraph {
     const uint16_t* __restrict__ etype;   // nullptr: derived from node types
     const uint32_t* __restrict__ rev;     // index of v in N(u) for arc v->u
     const double* __restrict__ wtotal;    // sequential fp64 slice sums
+    const double* __restrict__ wblk;      // exact block prefix sums for the bootstrap (nullptr: not built)
     const uint32_t* __restrict__ tcount;  // fairwalk type counts, n * n_ntypes
     const uint32_t* __restrict__ htab;    // adjacency hash sets (nullptr: not built)
     const uint4* __restrict__ arc;        // arc records (nullptr: not built)
@@ -657,6 +658,13 @@ __device__ uint32_t init_slot(const DevGraph& g, const DevModel& m, const DevCfg
     return pack_entry(last, cls);
 }
 
+// Block prefix sums of the weighted bootstrap: node v's blocks of 32 arcs
+// start at entry (off >> 5) + v (disjoint across nodes, as hash_base).
+constexpr uint32_t kBootBlkMin = 64;
+__host__ __device__ __forceinline__ uint64_t wblk_base(long long off, uint32_t v) {
+    return ((uint64_t)off >> 5) + v;
+}
+
 // Bootstrap step of a second-order walk: direct_sample over static weights
 // (engine.cpp:81-83, samplers.cpp:133-146). Unweighted: min(floor(u*deg),
 // deg-1), which is what the sequential r -= 1.0 loop returns exactly.
@@ -670,7 +678,33 @@ __device__ __forceinline__ bool bootstrap_pick(const DevGraph& g, const SCtx& c,
     if (!(total > 0)) return false;
     double r = __dmul_rn(u, total);
     const float* w = g.w + c.off;
-    for (uint32_t i = 0; i < c.deg; ++i) {
+    uint32_t i0 = 0;
+    if (g.wblk && c.deg >= kBootBlkMin) {
+        // Exact block prefix sums (built only where every subtraction of the
+        // sequential scan is exact, see k_wblk): r - P[b-1] is then exactly
+        // the remainder the reference holds after 32b subtractions, so the
+        // scan can start at the block where the remainder turns negative.
+        const double* P = g.wblk + wblk_base(c.off, c.v);
+        if (__ldg(P) == __ldg(P)) {  // NaN marks a slice without the exactness guarantee
+            uint32_t lo = 0, len = (c.deg + 31) >> 5;
+            while (len > 0) {  // first block whose end prefix exceeds r
+                const uint32_t half = len >> 1;
+                if (__ldg(P + lo + half) <= r) {
+                    lo += half + 1;
+                    len -= half + 1;
+                } else {
+                    len = half;
+                }
+            }
+            if (lo == (c.deg + 31) >> 5) {
+                i0 = c.deg;  // r >= total: no crossing, fallback below
+            } else {
+                if (lo) r = __dsub_rn(r, __ldg(P + lo - 1));
+                i0 = 32 * lo;
+            }
+        }
+    }
+    for (uint32_t i = i0; i < c.deg; ++i) {
         r = __dsub_rn(r, (double)__ldg(w + i));
         if (r < 0) {
             *out = i;

@@ -449,6 +449,74 @@ __global__ void __launch_bounds__(256, KIND == NODE2VEC ? 8 : 4) k_init_range(Ru
     }
 }
 
+// Initial chain words in RECORD order (sharded init of colocated chains):
+// record a = forward arc s->v holds the word of state (s, v), whose slot is
+// off(v) + rev[a] (index of s in N(v)) -- the same slot-keyed init as
+// k_init_range, permuted so that the install (k_load_rec) is a coalesced
+// strided copy instead of a random scatter. out == nullptr: write straight
+// into the session records (eager init in record order).
+template <int KIND>
+__global__ void __launch_bounds__(256, KIND == NODE2VEC ? 8 : 4) k_init_rec(RunParams P, uint64_t b, uint64_t e, uint32_t* __restrict__ out) {
+    const DevGraph& g = P.g;
+    unsigned long long inits = 0;
+    for (uint64_t a = b + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; a < e;
+         a += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t v = load_id(g, a);
+        const uint32_t affix = __ldg(g.rev + a);
+        uint32_t w = kEmpty;  // no back arc: no state (s, v) can ever use this record
+        double wl = 0.0;
+        if (affix != kNoBack) {
+            const SCtx c = make_ctx<KIND>(g, P.m, v, affix);
+            w = init_slot<KIND>(g, P.m, P.cfg, c, (uint64_t)c.off + affix, &wl);
+            ++inits;
+        }
+        if (out) {
+            if (P.ac && P.rec_u32 == 8) {  // typed records: the word and w'(Last) travel together
+                uint32_t* o = out + 3 * (a - b);
+                o[0] = w;
+                o[1] = (uint32_t)__double2loint(wl);
+                o[2] = (uint32_t)__double2hiint(wl);
+            } else {
+                out[a - b] = w;
+            }
+        } else {
+            uint32_t* r = reinterpret_cast<uint32_t*>(P.ac) + a * P.rec_u32;
+            r[chain_word_off(P.rec_u32)] = w;
+            if (P.rec_u32 == 8) {
+                r[6] = (uint32_t)__double2loint(wl);
+                r[7] = (uint32_t)__double2hiint(wl);
+            }
+        }
+    }
+    if (!out && inits) atomicAdd(&P.ctr[3], inits);
+}
+
+// Installs a record-order table (k_init_rec words): one strided write per
+// record; typed records take {word, w'(Last)} (3 words per record). Without
+// session records the words go to their slots (chain table in slot order).
+__global__ void k_load_rec(RunParams P, const uint32_t* __restrict__ w, uint32_t* __restrict__ ac, uint32_t rw,
+                           uint32_t* __restrict__ chain) {
+    const DevGraph& g = P.g;
+    for (uint64_t a = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; a < g.m;
+         a += (uint64_t)gridDim.x * blockDim.x) {
+        if (ac && rw == 8) {
+            uint32_t* rec = ac + a * rw;
+            rec[5] = __ldg(w + 3 * a);
+            rec[6] = __ldg(w + 3 * a + 1);
+            rec[7] = __ldg(w + 3 * a + 2);
+            continue;
+        }
+        const uint32_t e = __ldg(w + a);
+        if (ac) {
+            ac[a * rw + chain_word_off(rw)] = e;
+            continue;
+        }
+        const uint32_t affix = __ldg(g.rev + a);
+        if (affix == kNoBack) continue;
+        chain[(uint64_t)load_node(g, load_id(g, a)).off + affix] = e;
+    }
+}
+
 // Installs a full table of slot words: colocated words go to the record of
 // the forward arc s->v of slot (v, affix), s = N(v)[affix]; typed records
 // also get w'(Last) of the word's Last (its class is in the word).
@@ -1282,6 +1350,21 @@ RunParams Session::params() const {
     return P;
 }
 
+// Eager init of every arc-keyed slot: slot order (k_init_all: a warp's
+// threads share v, so the burn-in candidates of N(v) are local; the words
+// scatter into the records) or record order (k_init_rec: coalesced writes,
+// scattered N(v) reads). MHW_INIT_ORDER=rec|slot; default slot.
+template <int KIND>
+static void launch_init_all(const Session& s, const RunParams& P, cudaStream_t st) {
+    static const int rec = [] {
+        const char* e = std::getenv("MHW_INIT_ORDER");
+        return e && e[0] == 'r' ? 1 : 0;
+    }();
+    if (rec && s.ac.n) k_init_rec<KIND><<<grid_for(s.g->m), 256, 0, st>>>(P, 0, s.g->m, nullptr);
+    else k_init_all<KIND><<<grid_for(s.g->m), 256, 0, st>>>(P);
+    MHW_CK(cudaGetLastError());
+}
+
 void session_run(Session& s, cudaStream_t user) {
     DeviceGuard dg(s.g->device);
     cudaStream_t st = user ? user : s.stream;
@@ -1345,7 +1428,7 @@ void session_run(Session& s, cudaStream_t user) {
                 constexpr int KIND = decltype(kc)::value;
                 if constexpr (second_order(KIND)) {
                     if (s.eager_init && !preloaded) {
-                        k_init_all<KIND><<<grid_for(s.g->m), 256, 0, st>>>(P);
+                        launch_init_all<KIND>(s, P, st);
                         ++s.launches;
                     }
                 }
@@ -1395,7 +1478,8 @@ void walk_rows(Graph& g, const mhw_model_desc& md, const mhw_walk_config& wc, ui
     if (stride) *stride = (wc.walk_length + 1 + 3) & ~3u;
 }
 
-void session_init_chain(Session& s, uint64_t begin, uint64_t end, uint32_t* d_words, cudaStream_t user) {
+void session_init_chain(Session& s, uint64_t begin, uint64_t end, uint32_t* d_words, cudaStream_t user,
+                        bool rec_order) {
     DeviceGuard dg(s.g->device);
     if (!second_order(s.model.dev.kind) || s.ex || s.wc.schedule == MHW_SCHEDULE_DETERMINISTIC)
         invalid("chain preloading applies to second-order models on the throughput schedule");
@@ -1405,13 +1489,15 @@ void session_init_chain(Session& s, uint64_t begin, uint64_t end, uint32_t* d_wo
     const RunParams P = s.params();
     dispatch(s.model.dev.kind, [&](auto kc) {
         constexpr int KIND = decltype(kc)::value;
-        if constexpr (second_order(KIND))
-            k_init_range<KIND><<<grid_for(end - begin), 256, 0, st>>>(P, begin, end, d_words);
+        if constexpr (second_order(KIND)) {
+            if (rec_order) k_init_rec<KIND><<<grid_for(end - begin), 256, 0, st>>>(P, begin, end, d_words);
+            else k_init_range<KIND><<<grid_for(end - begin), 256, 0, st>>>(P, begin, end, d_words);
+        }
     });
     MHW_CK(cudaGetLastError());
 }
 
-void session_load_chain(Session& s, const uint32_t* d_words, cudaStream_t user) {
+void session_load_chain(Session& s, const uint32_t* d_words, cudaStream_t user, bool rec_order) {
     DeviceGuard dg(s.g->device);
     if (!second_order(s.model.dev.kind) || s.ex || s.wc.schedule == MHW_SCHEDULE_DETERMINISTIC)
         invalid("chain preloading applies to second-order models on the throughput schedule");
@@ -1420,14 +1506,18 @@ void session_load_chain(Session& s, const uint32_t* d_words, cudaStream_t user) 
         const RunParams P = s.params();
         dispatch(s.model.dev.kind, [&](auto kc) {
             constexpr int KIND = decltype(kc)::value;
-            if constexpr (second_order(KIND))
-                k_load_chain<KIND><<<grid_for(s.g->m), 256, 0, st>>>(
-                    P, d_words, s.ac.n ? reinterpret_cast<uint32_t*>(s.ac.p) : nullptr, s.rec_u32, s.chain.p);
+            uint32_t* const ac = s.ac.n ? reinterpret_cast<uint32_t*>(s.ac.p) : nullptr;
+            if constexpr (second_order(KIND)) {
+                if (rec_order) k_load_rec<<<grid_for(s.g->m), 256, 0, st>>>(P, d_words, ac, s.rec_u32, s.chain.p);
+                else k_load_chain<KIND><<<grid_for(s.g->m), 256, 0, st>>>(P, d_words, ac, s.rec_u32, s.chain.p);
+            }
         });
         MHW_CK(cudaGetLastError());
     }
     s.chain_loaded = true;
 }
+
+uint32_t session_record_width(const Session& s) { return (s.ac.n && s.rec_u32 == 8) ? 3u : 1u; }
 
 void session_stats(Session& s, mhw_walk_stats& out) {
     DeviceGuard dg(s.g->device);
@@ -1575,7 +1665,7 @@ void session_run_packed(Session& s, uint32_t* h_nodes, uint64_t cap_nodes, uint6
         dispatch(s.model.dev.kind, [&](auto kc) {
             constexpr int KIND = decltype(kc)::value;
             if constexpr (second_order(KIND)) {
-                if (s.eager_init) k_init_all<KIND><<<grid_for(s.g->m), 256, 0, S>>>(P);
+                if (s.eager_init) launch_init_all<KIND>(s, P, S);
             }
         });
         uint64_t H = 0;

@@ -86,8 +86,11 @@ uint64_t k_slots(int kind, const Graph& g);
 void session_create(Session& s, Graph& g, const mhw_model_desc& md, const mhw_walk_config& wc);
 void session_run(Session& s, cudaStream_t stream);
 void walk_rows(Graph& g, const mhw_model_desc& md, const mhw_walk_config& wc, uint64_t* rows, uint32_t* stride);
-void session_init_chain(Session& s, uint64_t begin, uint64_t end, uint32_t* d_words, cudaStream_t stream);
-void session_load_chain(Session& s, const uint32_t* d_words, cudaStream_t stream);
+void session_init_chain(Session& s, uint64_t begin, uint64_t end, uint32_t* d_words, cudaStream_t stream,
+                        bool rec_order = false);
+void session_load_chain(Session& s, const uint32_t* d_words, cudaStream_t stream, bool rec_order = false);
+// u32 words per record of a record-order table (3: typed records carry w'(Last)).
+uint32_t session_record_width(const Session& s);
 void session_stats(Session& s, mhw_walk_stats& out);
 void session_download(Session& s, uint32_t* nodes, uint32_t* lens, cudaStream_t stream);
 void session_write_corpus(Session& s, const char* path, const mhw_walk_stats& st);

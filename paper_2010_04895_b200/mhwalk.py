@@ -538,6 +538,22 @@ class Session:
         """Installs a full initial table (chain_size words) for the next run."""
         _check(L.lib().mhw_session_load_chain(self._h, C.c_void_p(d_words), C.c_void_p(stream) if stream else None))
 
+    def init_records(self, begin: int, end: int, d_words: int, stream: int | None = None):
+        """Initial words of records (arcs) [begin, end): the chain table in the
+        order the session stores it (coalesced install by load_records)."""
+        _check(L.lib().mhw_session_init_records(self._h, begin, end, C.c_void_p(d_words),
+                                                C.c_void_p(stream) if stream else None))
+
+    def record_width(self) -> int:
+        """u32 words per entry of a record-order table (3 for typed records)."""
+        w = C.c_uint32()
+        _check(L.lib().mhw_session_record_width(self._h, C.byref(w)))
+        return w.value
+
+    def load_records(self, d_words: int, stream: int | None = None):
+        """Installs a full record-order table for the next run."""
+        _check(L.lib().mhw_session_load_records(self._h, C.c_void_p(d_words), C.c_void_p(stream) if stream else None))
+
     def download(self, nodes=None, lengths=None, stream: int | None = None):
         if nodes is None:
             nodes = np.zeros((self.rows, self.stride), dtype=np.uint32)

@@ -76,3 +76,56 @@ def test_preloaded_chain_run_passes_chi_square(mhw, oracle, kind):
     # the next run without a preload initialises on its own again
     s.run()
     assert s.stats().slot_inits == g.m
+
+
+@pytest.mark.parametrize("init", [O.INIT_RANDOM, O.INIT_BURN_IN])
+@pytest.mark.parametrize("kind", [O.NODE2VEC, O.EDGE2VEC, O.FAIRWALK])
+def test_record_order_words_are_slot_words_permuted(mhw, oracle, kind, init):
+    """init_records word i (arc i = s -> v) == init_chain word off(v) + index of s in N(v)."""
+    g = typed_random_graph(900 + kind, 150, 6.0, weighted=True, types=2)
+    md = model_desc(kind, g, p=0.3, q=3.0, M=np.random.default_rng(kind).uniform(0.5, 2.0, (4, 4)))
+    cfg = O.WalkCfg(K=2, L=10, seed=23, init_kind=init, burn_in_steps=6)
+    s = mhw.Session(device_graph(g), walk_model(md), walk_config(cfg, threads=8, init_mode=2))
+    S = s.chain_size()
+    W = s.record_width()
+    assert W == (1 if kind == O.NODE2VEC else 3)
+    slot = torch.empty(S, dtype=torch.int32, device="cuda")
+    rec = torch.empty(S * W, dtype=torch.int32, device="cuda")
+    s.init_chain(0, S, slot.data_ptr())
+    cuts = [0, S // 4, S // 2 + 3, S]  # ragged record shards
+    for b, e in zip(cuts[:-1], cuts[1:]):
+        s.init_records(b, e, rec.data_ptr() + 4 * W * b)
+    torch.cuda.synchronize()
+    sw = slot.cpu().numpy().view(np.uint32)
+    full = rec.cpu().numpy().view(np.uint32).reshape(S, W)
+    rw = full[:, 0]
+    if W == 3:  # w'(Last) of every live word: positive and finite
+        wl = full[:, 1:].copy().view(np.float64)[:, 0]
+        live = rw < 0xFFFFFFFD
+        assert np.all(np.isfinite(wl[live])) and np.all(wl[live] > 0)
+    off = g.offsets.astype(np.int64)
+    src = np.repeat(np.arange(g.n), np.diff(off))
+    for a in range(g.m):
+        v = int(g.nbr[a])
+        sl = off[v:v + 2]
+        idx = int(np.searchsorted(g.nbr[sl[0]:sl[1]], src[a]))
+        assert rw[a] == sw[sl[0] + idx], a
+
+
+@pytest.mark.parametrize("kind", [O.NODE2VEC, O.EDGE2VEC, O.FAIRWALK])
+def test_record_order_preload_run_passes_chi_square(mhw, oracle, kind):
+    g = typed_random_graph(500 + kind, 40, 4.0, weighted=True, types=2)
+    md = model_desc(kind, g, p=0.5, q=2.0, M=np.random.default_rng(kind).uniform(0.5, 2.0, (4, 4)))
+    cfg = O.WalkCfg(K=400, L=80, seed=78, init_kind=O.INIT_BURN_IN, burn_in_steps=5)
+    s = mhw.Session(device_graph(g), walk_model(md), walk_config(cfg, threads=8, init_mode=2))
+    W = s.record_width()
+    words = torch.empty(s.chain_size() * W, dtype=torch.int32, device="cuda")
+    third = s.chain_size() // 3
+    s.init_records(0, third, words.data_ptr())
+    s.init_records(third, s.chain_size(), words.data_ptr() + 4 * W * third)
+    s.load_records(words.data_ptr())
+    s.run()
+    assert s.stats().slot_inits == 0
+    rows, lens = s.download()
+    ok, msg = gate(audit(g, oracle, md, rows, lens, min_visits=5000))
+    assert ok, msg
