@@ -144,16 +144,18 @@ __device__ __forceinline__ bool bloom_maybe(const DevGraph& g, uint32_t a, uint3
     const uint4* blk = reinterpret_cast<const uint4*>(g.bloom) + 2 * (uint64_t)bloom_block(x, g.bloom_blocks);
     uint4 lo, hi;
     ldg256(blk, lo, hi);
-    // 256-bit block as four 64-bit words, selected without a local array
-    const uint64_t q0 = ((uint64_t)lo.y << 32) | lo.x, q1 = ((uint64_t)lo.w << 32) | lo.z;
-    const uint64_t q2 = ((uint64_t)hi.y << 32) | hi.x, q3 = ((uint64_t)hi.w << 32) | hi.z;
+    // 256-bit block as eight 32-bit words, selected by predicated moves (no
+    // branches, no local array)
     bool all = true;
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
         const uint32_t bit = (uint32_t)(x >> (8 * k)) & 255u;
-        const uint32_t j = bit >> 6;
-        const uint64_t q = j == 0 ? q0 : (j == 1 ? q1 : (j == 2 ? q2 : q3));
-        all &= ((q >> (bit & 63)) & 1ull) != 0;
+        const uint32_t j = bit >> 5;
+        const uint32_t a = (j & 1) ? lo.y : lo.x, b = (j & 1) ? lo.w : lo.z;
+        const uint32_t c = (j & 1) ? hi.y : hi.x, d = (j & 1) ? hi.w : hi.z;
+        const uint32_t e = (j & 2) ? b : a, f = (j & 2) ? d : c;
+        const uint32_t q = (j & 4) ? f : e;
+        all &= ((q >> (bit & 31)) & 1u) != 0;
     }
     return all;
 }
@@ -391,13 +393,15 @@ __device__ __forceinline__ uint32_t edge_type_of(const DevGraph& g, long long ar
 // alpha class of candidate u under state c: 0 return (u == s), 1 adjacent to
 // s, 2 otherwise (models.cpp:76-80). urec: the candidate's record if already
 // loaded (lets a verified-symmetric graph search the shorter slice).
+// bloom: the edge-filter result if the caller probed it already (1 maybe
+// adjacent, 0 not), -1 to probe here.
 __device__ __forceinline__ uint32_t alpha_class(const DevGraph& g, const DevModel& m, const SCtx& c,
-                                                uint32_t u, const NodeRec* urec) {
+                                                uint32_t u, const NodeRec* urec, int bloom = -1) {
     if (m.alpha_trivial) return 1;
     if (u == c.s) return 0;
     // the L2-resident edge filter settles most non-adjacent pairs without a
     // DRAM access
-    if (g.bloom && !bloom_maybe(g, c.s, u)) return 2;
+    if (g.bloom && !(bloom >= 0 ? bloom != 0 : bloom_maybe(g, c.s, u))) return 2;
     // s's own hash set needs nothing about u: probe it without waiting for
     // the candidate's node record (shorter dependency chain per step).
     if (g.htab && c.deg_s >= kHashMinDeg) return hash_contains(g.htab, c.off_s, c.s, c.deg_s, u) ? 1u : 2u;

@@ -210,7 +210,23 @@ __global__ void __launch_bounds__(kWalkBlock) __maxnreg__(REGS) k_walk(RunParams
                 uint4 ac = make_uint4(0, 0, 0, 0), bc = make_uint4(0, 0, 0, 0);
                 NodeRec rc{};
                 bool rc_early;
-                if constexpr (AR) {
+                int pre_bloom = -1;
+                if constexpr (NARROW) {
+                    // The edge-filter probe needs only the candidate id: it is
+                    // computed and issued before the candidate's node record is
+                    // consumed, so the two L2 accesses overlap instead of
+                    // running back to back.
+                    const uint2 x = __ldg(reinterpret_cast<const uint2*>(P.ac) + c.off + cand);
+                    uc = x.x;
+                    const int4 nraw = __ldg(reinterpret_cast<const int4*>(g.nodes) + uc);  // issued first
+                    if (g.bloom && !P.m.alpha_trivial && uc != c.s) pre_bloom = bloom_maybe(g, c.s, uc) ? 1 : 0;
+                    rc.off = ((long long)(uint32_t)nraw.y << 32) | (uint32_t)nraw.x;
+                    rc.deg = (uint32_t)nraw.z;
+                    rc.type = (uint16_t)((uint32_t)nraw.w & 0xFFFFu);
+                    rc.flags = (uint16_t)((uint32_t)nraw.w >> 16);
+                    ac = make_uint4(uc, rc.deg | ((rc.flags & NF_ALLPOS) ? 0x80000000u : 0u), (uint32_t)rc.off, x.y);
+                    rc_early = true;
+                } else if constexpr (AR) {
                     ac = load_rec(c.off + cand, bc);
                     uc = ac.x;
                     rc = rec_node(ac, bc);
@@ -225,7 +241,7 @@ __global__ void __launch_bounds__(kWalkBlock) __maxnreg__(REGS) k_walk(RunParams
                     if (rc_early) rc = load_node(g, uc);
                 }
                 const uint32_t cls_c =
-                    second_order(KIND) ? alpha_class(g, P.m, c, uc, rc_early ? &rc : nullptr) : 0u;
+                    second_order(KIND) ? alpha_class(g, P.m, c, uc, rc_early ? &rc : nullptr, pre_bloom) : 0u;
                 double wc;
                 if (AR && KIND == DEEPWALK) wc = (double)__uint_as_float(ac.w);
                 else if (TYPED) wc = wprime_v<KIND>(g, P.m, c, (double)__uint_as_float(ac.w), rc.type, bc.x >> 16, cls_c);
