@@ -394,9 +394,13 @@ __device__ __forceinline__ uint32_t edge_type_of(const DevGraph& g, long long ar
 // s, 2 otherwise (models.cpp:76-80). urec: the candidate's record if already
 // loaded (lets a verified-symmetric graph search the shorter slice).
 // bloom: the edge-filter result if the caller probed it already (1 maybe
-// adjacent, 0 not), -1 to probe here.
+// adjacent, 0 not), -1 to probe here. load_urec: without urec, fetch the
+// candidate's record here when (and only when) the shorter-slice choice needs
+// it -- callers keep a single call site, so lanes that need the record and
+// lanes that do not stay converged through the filter probe.
 __device__ __forceinline__ uint32_t alpha_class(const DevGraph& g, const DevModel& m, const SCtx& c,
-                                                uint32_t u, const NodeRec* urec, int bloom = -1) {
+                                                uint32_t u, const NodeRec* urec, int bloom = -1,
+                                                bool load_urec = false) {
     if (m.alpha_trivial) return 1;
     if (u == c.s) return 0;
     // the L2-resident edge filter settles most non-adjacent pairs without a
@@ -412,11 +416,12 @@ __device__ __forceinline__ uint32_t alpha_class(const DevGraph& g, const DevMode
     long long off_a = c.off_s;
     uint32_t node_b = 0, deg_b = 0, key_b = 0;           // longer slice
     long long off_b = 0;
-    const bool both = g.verified_sym && urec;
+    const bool both = g.verified_sym && (urec || load_urec);
     if (both) {
+        const NodeRec ur = urec ? *urec : load_node(g, u);
         node_b = u;
-        off_b = urec->off;
-        deg_b = urec->deg;
+        off_b = ur.off;
+        deg_b = ur.deg;
         key_b = c.s;
         if (deg_b < deg_a) {
             uint32_t t = node_a; node_a = node_b; node_b = t;
@@ -483,12 +488,12 @@ __device__ __forceinline__ double eval_index(const DevGraph& g, const DevModel& 
     if (KIND != DEEPWALK) {
         const uint32_t u = load_id(g, c.off + i);
         if (second_order(KIND) && !c.boot && !m.alpha_trivial) {
-            if (needs_utype<KIND>() || (needs_urec_for_alpha(g, c) && u != c.s)) {
+            if (needs_utype<KIND>()) {
                 const NodeRec r = load_node(g, u);
                 utype = r.type;
                 cls = alpha_class(g, m, c, u, &r);
             } else {
-                cls = alpha_class(g, m, c, u, nullptr);
+                cls = alpha_class(g, m, c, u, nullptr, -1, true);
             }
         } else {
             if (needs_utype<KIND>()) utype = load_node(g, u).type;
