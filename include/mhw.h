@@ -111,11 +111,14 @@ typedef struct mhw_walk_config {
     int32_t schedule;          /* mhw_schedule */
     uint32_t node_begin;
     uint32_t node_end;
-    /* Node-keyed models (deepwalk, metapath2vec): nodes of degree d >= D get
-     * 2^(floor(log2(d/D))+1) (at most 65536) independent chains per state,
-     * picked by walker id. 0 = auto (metapath2vec: D = 128; deepwalk: the
-     * smallest power-of-two D whose replica region is <= 8M chain words);
-     * 0xFFFFFFFF = one chain per state exactly as SamplerManager. */
+    /* Node-keyed models (deepwalk, metapath2vec): nodes of visit weight
+     * d >= D get 2^(floor(log2(d/D))+1) (at most 65536) independent chains
+     * per state, picked by walker id. The weight is the degree (deepwalk) or
+     * floor(deg * F[type]) (metapath2vec; F_t = share of the metapath's
+     * steady cycle at type t * arcs / arcs incident to type t). 0 = auto
+     * (metapath2vec: D = 32; deepwalk: the smallest power-of-two D whose
+     * replica region is <= 8M chain words); 0xFFFFFFFF = one chain per state
+     * exactly as SamplerManager. */
     uint32_t chain_replica_degree;
     /* Second-order slot initialisation: 0 auto, 1 lazy (first query, as
      * manager.cpp:35-56), 2 eager (all slots before the walk; identical

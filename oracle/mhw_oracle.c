@@ -729,7 +729,35 @@ typedef struct {
     uint32_t* group;   /* n+1 exclusive prefix of (R-1) */
     uint64_t base;     /* n*G */
     uint32_t G;
+    double* scale;     /* metapath2vec: per node type visit scale (NULL: weight = degree) */
 } replica_layout_t;
+
+/* Replica weight of node v (walk.cu rep_weight): the degree, or for
+ * metapath2vec floor(deg * F[type]) with F_t = (count_t * arcs) /
+ * (cycle_len * arcs incident to type t) over the metapath's steady cycle. */
+static uint32_t rep_weight(const og_graph* g, const replica_layout_t* rl, uint32_t v) {
+    const uint32_t d = deg_of(g, v);
+    if (!rl->scale) return d;
+    const double x = (double)d * rl->scale[g->ntype[v]];
+    return x >= 2147483647.0 ? 0x7FFFFFFFu : (uint32_t)x;
+}
+
+static double* metapath_rep_scale(const og_graph* g, const og_model* m) {
+    const uint32_t T = g->n_ntypes ? g->n_ntypes : 1;
+    double* F = (double*)calloc(T, sizeof(double));
+    double* count = (double*)calloc(T, sizeof(double));
+    uint64_t* arcs = (uint64_t*)calloc(T, sizeof(uint64_t));
+    for (uint32_t v = 0; v < g->n; ++v) arcs[g->ntype[v]] += deg_of(g, v);
+    const uint32_t L = m->mp_len;
+    const uint32_t b = (L > 1 && m->metapath[0] == m->metapath[L - 1]) ? 1 : 0;
+    for (uint32_t i = b; i < L; ++i) count[m->metapath[i]] += 1.0;
+    const double cycle = (double)(L - b);
+    for (uint32_t t = 0; t < T; ++t)
+        if (arcs[t]) F[t] = (count[t] * (double)g->m) / (cycle * (double)arcs[t]);
+    free(count);
+    free(arcs);
+    return F;
+}
 
 static uint32_t chain_replicas(uint32_t deg, uint32_t D) {
     if (D == OG_NO_REPLICAS || deg < D) return 1;
@@ -743,7 +771,7 @@ static uint64_t engine_slot(const og_graph* g, const og_model* m, const replica_
                             uint32_t affix, uint64_t walker) {
     const uint64_t base = slot_index(g, m, v, affix);
     if (m->kind != OG_DEEPWALK && m->kind != OG_METAPATH2VEC) return base;
-    const uint32_t R = chain_replicas(deg_of(g, v), rl->D);
+    const uint32_t R = chain_replicas(rep_weight(g, rl, v), rl->D);
     if (R == 1) return base;
     const uint32_t r = (uint32_t)((walker * 0x9E3779B97F4A7C15ULL) >> 40) & (R - 1);
     if (r == 0) return base;
@@ -1032,16 +1060,18 @@ int og_generate_walks(const og_graph* g, const og_model* m, const og_config* c, 
     rl.G = m->kind == OG_METAPATH2VEC ? m->num_types : 1;
     rl.base = slots;
     rl.group = NULL;
+    rl.scale = NULL;
     if ((m->kind == OG_DEEPWALK || m->kind == OG_METAPATH2VEC) && rl.D != OG_NO_REPLICAS) {
+        if (m->kind == OG_METAPATH2VEC) rl.scale = metapath_rep_scale(g, m);
         if (rl.D == 0) {
-            /* automatic layout (walk.cu session_create): metapath2vec 128;
+            /* automatic layout (walk.cu session_create): metapath2vec 32 (visit weights);
              * deepwalk the smallest power-of-two D whose replica region
              * holds at most 8M chain words */
-            rl.D = 128;
+            rl.D = 32;
             if (m->kind == OG_DEEPWALK) {
                 uint64_t hist[33] = {0};
                 for (uint32_t v = 0; v < g->n; ++v) {
-                    uint32_t d = deg_of(g, v), b = 0;
+                    uint32_t d = rep_weight(g, &rl, v), b = 0;
                     if (!d) continue;
                     while (d >>= 1) ++b;
                     ++hist[b];
@@ -1057,12 +1087,17 @@ int og_generate_walks(const og_graph* g, const og_model* m, const og_config* c, 
             }
         }
         rl.group = (uint32_t*)calloc((size_t)g->n + 1, sizeof(uint32_t));
-        for (uint32_t v = 0; v < g->n; ++v) rl.group[v + 1] = rl.group[v] + chain_replicas(deg_of(g, v), rl.D) - 1;
+        for (uint32_t v = 0; v < g->n; ++v) rl.group[v + 1] = rl.group[v] + chain_replicas(rep_weight(g, &rl, v), rl.D) - 1;
         slots += (uint64_t)rl.group[g->n] * rl.G;
     } else {
         rl.D = OG_NO_REPLICAS;
     }
-    if (slots > ((uint64_t)1 << 40)) { snprintf(err, errlen, "sampler layout too large"); free(rl.group); return OG_ERR_INVALID; }
+    if (slots > ((uint64_t)1 << 40)) {
+        snprintf(err, errlen, "sampler layout too large");
+        free(rl.group);
+        free(rl.scale);
+        return OG_ERR_INVALID;
+    }
     chain_t ch;
     ch.status = (uint8_t*)calloc(slots ? slots : 1, 1);
     ch.last = (uint32_t*)calloc(slots ? slots : 1, sizeof(uint32_t));
@@ -1145,6 +1180,7 @@ int og_generate_walks(const og_graph* g, const og_model* m, const og_config* c, 
     free(ch.status);
     free(ch.last);
     free(rl.group);
+    free(rl.scale);
     if (c->sampler != OG_SAMPLER_MH) {
         const uint64_t rs = og_slot_count(g, m);
         for (uint64_t i = 0; i < rs; ++i) { free(bt.aprob[i]); free(bt.aalias[i]); }

@@ -199,10 +199,11 @@ struct DevCfg {
     uint32_t rep_max;            // replica cap (power of two)
     uint64_t rep_base_slot;      // first slot of the replica region (= n * G)
     const uint32_t* rep_group;   // per node: first replica group (hubs only)
+    const double* rep_scale;     // metapath2vec: per node type visit scale (nullptr: weight = degree)
 };
 
 constexpr uint32_t kNoReplicas = 0xFFFFFFFFu;
-constexpr uint32_t kDefaultRepDeg = 128;
+constexpr uint32_t kDefaultRepDeg = 32;  // metapath2vec auto replica weight threshold
 constexpr uint32_t kMaxReplicas = 65536;
 constexpr uint64_t kAutoReplicaSlots = uint64_t(8) << 20;  // auto D budget (32 MB of chain words)
 
@@ -222,12 +223,28 @@ __host__ __device__ __forceinline__ uint32_t walker_replica(uint64_t walker, uin
     return (uint32_t)((walker * 0x9E3779B97F4A7C15ull) >> 40) & (R - 1);
 }
 
+// Replica weight of a node-keyed state: its expected visits in degree units.
+// deepwalk: the degree (visits of an undirected walk are proportional to it).
+// metapath2vec: deg * F[type], F_t = (share of metapath steps at type t) *
+// arcs / (arcs incident to type-t nodes) -- a type visited every fourth
+// step by walkers funnelled through few nodes (cfg3's V venues) weighs far
+// more than its degree. floor of one IEEE product, identical in the oracle.
+__host__ __device__ __forceinline__ uint32_t rep_weight(uint32_t deg, const double* scale, uint16_t type) {
+    if (!scale) return deg;
+#ifdef __CUDA_ARCH__
+    const double x = __dmul_rn((double)deg, __ldg(scale + type));
+#else
+    const double x = (double)deg * scale[type];
+#endif
+    return x >= 2147483647.0 ? 0x7FFFFFFFu : (uint32_t)x;
+}
+
 // Slot of node-keyed state (v, t) for `walker`: G slots per node (1 for
 // deepwalk, num_types for metapath2vec), replicas after the n*G base slots.
 __device__ __forceinline__ uint64_t node_slot(const DevCfg& cfg, uint32_t G, uint32_t v, uint32_t deg,
-                                              uint32_t t, uint64_t walker) {
+                                              uint32_t t, uint64_t walker, uint16_t vtype = 0) {
     const uint64_t base = (uint64_t)v * G + t;
-    const uint32_t R = chain_replicas(deg, cfg.rep_deg, cfg.rep_max);
+    const uint32_t R = chain_replicas(rep_weight(deg, cfg.rep_scale, vtype), cfg.rep_deg, cfg.rep_max);
     if (R == 1) return base;
     const uint32_t r = walker_replica(walker, R);
     if (r == 0) return base;
@@ -553,7 +570,7 @@ template <int KIND>
 __device__ __forceinline__ uint64_t slot_of(const DevModel& m, const DevCfg& cfg, const SCtx& c, uint32_t affix,
                                             uint64_t walker) {
     if (KIND == DEEPWALK) return node_slot(cfg, 1, c.v, c.deg, 0, walker);
-    if (KIND == METAPATH2VEC) return node_slot(cfg, m.num_types, c.v, c.deg, c.req, walker);
+    if (KIND == METAPATH2VEC) return node_slot(cfg, m.num_types, c.v, c.deg, c.req, walker, c.vtype);
     return (uint64_t)c.off + affix;
 }
 

@@ -360,7 +360,7 @@ __global__ void __launch_bounds__(kWalkBlock) __maxnreg__(REGS) k_walk(RunParams
             } else if (KIND == METAPATH2VEC) {
                 affix = metapath_next(P.m, affix);
                 c.req = P.m.metapath[metapath_next(P.m, affix)];
-                slot = node_slot(P.cfg, P.m.num_types, next, rn.deg, c.req, walker);
+                slot = node_slot(P.cfg, P.m.num_types, next, rn.deg, c.req, walker, rn.type);
             } else {
                 // rev[off(v) + chosen], fetched above (CC: only checked on a
                 // graph not verified symmetric; the chain word is located by
@@ -635,13 +635,14 @@ __global__ void k_pack(const uint32_t* __restrict__ src, uint32_t stride, const 
 // Histogram of floor(log2 deg) over nodes of degree >= 1 (33 bins): with a
 // power-of-two D, chain_replicas(d, D) depends on floor(log2 d) alone, so the
 // host sizes the replica region for any D from it.
-__global__ void k_deg_log2_hist(DevGraph g, unsigned long long* __restrict__ hist) {
+__global__ void k_deg_log2_hist(DevGraph g, const double* __restrict__ scale, unsigned long long* __restrict__ hist) {
     __shared__ unsigned int h[33];
     if (threadIdx.x < 33) h[threadIdx.x] = 0;
     __syncthreads();
     for (uint64_t v = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; v < g.n;
          v += (uint64_t)gridDim.x * blockDim.x) {
-        const uint32_t d = load_node(g, (uint32_t)v).deg;
+        const NodeRec r = load_node(g, (uint32_t)v);
+        const uint32_t d = rep_weight(r.deg, scale, r.type);
         if (d) atomicAdd(&h[31 - __clz(d)], 1u);
     }
     __syncthreads();
@@ -649,10 +650,22 @@ __global__ void k_deg_log2_hist(DevGraph g, unsigned long long* __restrict__ his
 }
 
 // Replica groups per node (chain_replicas - 1).
-__global__ void k_rep_counts(DevGraph g, uint32_t D, uint32_t cap, uint32_t* __restrict__ cnt) {
+__global__ void k_rep_counts(DevGraph g, uint32_t D, uint32_t cap, const double* __restrict__ scale,
+                             uint32_t* __restrict__ cnt) {
     for (uint64_t v = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; v < g.n;
-         v += (uint64_t)gridDim.x * blockDim.x)
-        cnt[v] = chain_replicas(load_node(g, (uint32_t)v).deg, D, cap) - 1;
+         v += (uint64_t)gridDim.x * blockDim.x) {
+        const NodeRec r = load_node(g, (uint32_t)v);
+        cnt[v] = chain_replicas(rep_weight(r.deg, scale, r.type), D, cap) - 1;
+    }
+}
+
+// Arcs incident to the nodes of each type (metapath2vec replica weights).
+__global__ void k_type_arcs(DevGraph g, unsigned long long* __restrict__ out) {
+    for (uint64_t v = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; v < g.n;
+         v += (uint64_t)gridDim.x * blockDim.x) {
+        const NodeRec r = load_node(g, (uint32_t)v);
+        if (r.deg) atomicAdd(out + r.type, (unsigned long long)r.deg);
+    }
 }
 
 // Rows of valid starts on isolated nodes: [v], an early termination each.
@@ -1121,6 +1134,8 @@ Session::~Session() {
     if (stream) cudaStreamDestroy(stream);
 }
 
+static std::vector<double> metapath_rep_scale(const std::vector<uint16_t>& mp, const Graph& g, cudaStream_t st);
+
 void session_create(Session& s, Graph& g, const mhw_model_desc& md, const mhw_walk_config& wc) {
     DeviceGuard dg(g.device);
     if (wc.walks_per_node == 0 || wc.walk_length == 0)
@@ -1157,12 +1172,21 @@ void session_create(Session& s, Graph& g, const mhw_model_desc& md, const mhw_wa
     s.cfg.rep_max = kMaxReplicas;
     s.cfg.rep_base_slot = s.slots;
     s.cfg.rep_group = nullptr;
+    s.cfg.rep_scale = nullptr;
     if (!second_order(m.kind) && wc.chain_replica_degree != kNoReplicas && g.n && g.max_deg) {
         const uint64_t G = m.kind == METAPATH2VEC ? g.n_ntypes : 1;
-        // replica groups for power-of-two D from the log2-degree histogram
+        if (m.kind == METAPATH2VEC) {
+            // visit scale per node type (rep_weight): share of the metapath's
+            // steady cycle spent at type t, times arcs / arcs incident to t
+            const std::vector<double> F = metapath_rep_scale(s.model.h_metapath, g, st);
+            s.rep_scale.alloc(F.size());
+            MHW_CK(cudaMemcpyAsync(s.rep_scale.p, F.data(), F.size() * sizeof(double), cudaMemcpyHostToDevice, st));
+            s.cfg.rep_scale = s.rep_scale.p;
+        }
+        // replica groups for power-of-two D from the log2-weight histogram
         DBuf<unsigned long long> hist(33);
         MHW_CK(cudaMemsetAsync(hist.p, 0, 33 * 8, st));
-        k_deg_log2_hist<<<grid_for(g.n), 256, 0, st>>>(g.view(), hist.p);
+        k_deg_log2_hist<<<grid_for(g.n), 256, 0, st>>>(g.view(), s.cfg.rep_scale, hist.p);
         MHW_CK(cudaGetLastError());
         unsigned long long hh[33];
         MHW_CK(cudaMemcpyAsync(hh, hist.p, sizeof hh, cudaMemcpyDeviceToHost, st));
@@ -1177,10 +1201,13 @@ void session_create(Session& s, Graph& g, const mhw_model_desc& md, const mhw_wa
         };
         uint32_t D = wc.chain_replica_degree;
         if (!D) {
-            // auto: metapath2vec keeps kDefaultRepDeg (its inits scan typed
-            // neighbours, so extra chains cost more than the contention they
-            // remove); deepwalk takes the smallest power-of-two D whose
-            // replica region fits kAutoReplicaSlots (L2-resident chain table)
+            // auto: metapath2vec replicates states whose visit weight
+            // (rep_weight: degree scaled by how often the metapath visits
+            // the node's type) reaches kDefaultRepDeg = 32 (cfg3a: the V
+            // venues; D = 128 59.2 ms, 32 54.0, 16 56.1, 8 60.2 -- each
+            // replica's lazy init scans the typed neighbours); deepwalk
+            // takes the smallest power-of-two D whose replica region fits
+            // kAutoReplicaSlots (L2-resident chain table)
             D = kDefaultRepDeg;
             if (m.kind == DEEPWALK)
                 for (uint32_t lg = 0; lg < 31; ++lg)
@@ -1193,11 +1220,14 @@ void session_create(Session& s, Graph& g, const mhw_model_desc& md, const mhw_wa
                 invalid("sampler layout too large: chain_replica_degree " + std::to_string(D) + " gives " +
                         std::to_string(groups_for(lg)) + " replica groups");
         }
-        if (g.max_deg >= D) {
+        uint32_t top = 0;  // highest occupied log2-weight bin
+        for (uint32_t b = 0; b < 33; ++b)
+            if (hh[b]) top = b;
+        if (((uint64_t(2) << top) - 1) >= D) {
             DBuf<uint32_t> cnt(g.n + 1);
             s.rep_group.alloc(g.n + 1);
             MHW_CK(cudaMemsetAsync(cnt.p, 0, (g.n + 1) * 4, st));
-            k_rep_counts<<<grid_for(g.n), 256, 0, st>>>(g.view(), D, s.cfg.rep_max, cnt.p);
+            k_rep_counts<<<grid_for(g.n), 256, 0, st>>>(g.view(), D, s.cfg.rep_max, s.cfg.rep_scale, cnt.p);
             MHW_CK(cudaGetLastError());
             size_t bytes = 0;
             MHW_CK(cub::DeviceScan::ExclusiveSum(nullptr, bytes, cnt.p, s.rep_group.p, (int64_t)g.n + 1, st));
@@ -1339,6 +1369,30 @@ static void l2_window(cudaStream_t st, void* p, size_t bytes) {
     attr.accessPolicyWindow.hitProp = bytes ? cudaAccessPropertyPersisting : cudaAccessPropertyNormal;
     attr.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
     MHW_CK(cudaStreamSetAttribute(st, cudaStreamAttributeAccessPolicyWindow, &attr));
+}
+
+// Per node type visit scale of metapath2vec's replica weights (rep_weight):
+// the steady cycle of metapath indices (metapath_next: after the last index,
+// 1 if first == last else 0, models.hpp:77-85) spends count_t of its
+// cycle_len steps at type t; walkers reach a type-t node in proportion to
+// its arcs among the arcs_t incident to type t.
+static std::vector<double> metapath_rep_scale(const std::vector<uint16_t>& mp, const Graph& g, cudaStream_t st) {
+    const uint32_t T = std::max<uint32_t>(g.n_ntypes, 1);
+    DBuf<unsigned long long> arcs(T);
+    MHW_CK(cudaMemsetAsync(arcs.p, 0, T * 8ull, st));
+    k_type_arcs<<<grid_for(g.n), 256, 0, st>>>(g.view(), arcs.p);
+    MHW_CK(cudaGetLastError());
+    std::vector<unsigned long long> a(T);
+    MHW_CK(cudaMemcpyAsync(a.data(), arcs.p, T * 8ull, cudaMemcpyDeviceToHost, st));
+    MHW_CK(cudaStreamSynchronize(st));
+    const size_t L = mp.size();
+    const size_t b = (L > 1 && mp[0] == mp[L - 1]) ? 1 : 0;
+    std::vector<double> count(T, 0.0), F(T, 0.0);
+    for (size_t i = b; i < L; ++i) count[mp[i]] += 1.0;
+    const double cycle = (double)(L - b);
+    for (uint32_t t = 0; t < T; ++t)
+        if (a[t]) F[t] = (count[t] * (double)g.m) / (cycle * (double)a[t]);
+    return F;
 }
 
 uint64_t k_slots(int kind, const Graph& g) {

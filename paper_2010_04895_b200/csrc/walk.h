@@ -54,6 +54,7 @@ struct Session {
     uint64_t n_items = 0, rows = 0, skipped = 0, slots = 0;
     uint32_t stride = 0;
     DBuf<uint32_t> chain, out, lens, rep_group;
+    DBuf<double> rep_scale;  // metapath2vec replica weights per node type
     DBuf<uint4> ac;          // session arc records (+ colocated chain words, second order)
     uint32_t rec_u32 = 4;    // u32 words per record: 4, 8 (typed models), 2 (narrow node2vec records)
     std::unique_ptr<ExactState> ex;  // alias / direct / rejection baselines (exact.cu)
