@@ -137,6 +137,8 @@ DevGraph Graph::view() const {
     d.wtotal = wtotal.n ? wtotal.p : nullptr;
     d.wblk = wblk.n ? wblk.p : nullptr;
     d.tcount = tcount.n ? tcount.p : nullptr;
+    d.tperm = tperm.n ? tperm.p : nullptr;
+    d.tbase = tbase.n ? tbase.p : nullptr;
     d.htab = htab.n ? htab.p : nullptr;
     d.arc = arc.n ? arc.p : nullptr;
     d.bloom = bloom.n ? bloom.p : nullptr;
@@ -149,7 +151,7 @@ DevGraph Graph::view() const {
 
 uint64_t Graph::device_bytes() const {
     return nodes.bytes() + ids.bytes() + w.bytes() + ntype.bytes() + etype.bytes() + rev.bytes() +
-           wtotal.bytes() + wblk.bytes() + tcount.bytes() + htab.bytes() + arc.bytes() + bloom.bytes();
+           wtotal.bytes() + wblk.bytes() + tcount.bytes() + tperm.bytes() + tbase.bytes() + htab.bytes() + arc.bytes() + bloom.bytes();
 }
 
 namespace {
@@ -412,6 +414,67 @@ __global__ void k_tcount(DevGraph g, uint32_t* __restrict__ tc) {
         for (uint32_t i = lane; i < r.deg; i += 32) {
             const uint16_t t = load_node(g, load_id(g, r.off + i)).type;
             atomicAdd(tc + v * T + t, 1u);
+        }
+    }
+}
+
+// Typed neighbour index (metapath2vec's random_positive, samplers.cpp:22-33):
+// each slice's indices ordered by key = 2 * type(u) + (w > 0 ? 0 : 1), index
+// order kept within a key, and per (node, type) the start of its positive
+// block and its length. Three passes, warp per node: key counts, exclusive
+// bases (thread per node), stable scatter (match_any ranks per 32 arcs).
+__device__ __forceinline__ uint32_t tidx_key(const DevGraph& g, uint64_t a) {
+    const uint16_t t = load_node(g, load_id(g, a)).type;
+    const bool pos = g.w ? __ldg(g.w + a) > 0.0f : true;
+    return 2u * t + (pos ? 0u : 1u);
+}
+
+__global__ void k_tidx_count(DevGraph g, uint32_t* __restrict__ cnt) {
+    const unsigned lane = threadIdx.x & 31;
+    const uint64_t wid = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    const uint32_t K = 2u * g.n_ntypes;
+    for (uint64_t v = wid; v < g.n; v += nw) {
+        const NodeRec r = load_node(g, (uint32_t)v);
+        for (uint32_t i = lane; i < r.deg; i += 32) atomicAdd(cnt + v * K + tidx_key(g, r.off + i), 1u);
+    }
+}
+
+__global__ void k_tidx_base(DevGraph g, uint32_t* __restrict__ cnt, uint2* __restrict__ base) {
+    const uint32_t K = 2u * g.n_ntypes;
+    for (uint64_t v = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; v < g.n;
+         v += (uint64_t)gridDim.x * blockDim.x) {
+        uint32_t run = 0;
+        for (uint32_t k = 0; k < K; ++k) {
+            const uint32_t c = cnt[v * K + k];
+            cnt[v * K + k] = run;  // becomes the scatter cursor of key k
+            if (!(k & 1)) base[v * g.n_ntypes + k / 2] = make_uint2(run, c);
+            run += c;
+        }
+    }
+}
+
+__global__ void k_tidx_scatter(DevGraph g, uint32_t* __restrict__ cur, uint32_t* __restrict__ perm) {
+    const unsigned lane = threadIdx.x & 31;
+    const uint64_t wid = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    const uint32_t K = 2u * g.n_ntypes;
+    for (uint64_t v = wid; v < g.n; v += nw) {
+        const NodeRec r = load_node(g, (uint32_t)v);
+        uint32_t* cv = cur + v * K;
+        for (uint32_t i0 = 0; i0 < r.deg; i0 += 32) {
+            const uint32_t i = i0 + lane;
+            const bool live = i < r.deg;
+            const uint32_t key = live ? tidx_key(g, r.off + i) : 0xFFFFFFFFu;
+            const unsigned peers = __match_any_sync(0xFFFFFFFFu, key);
+            const uint32_t rank = __popc(peers & ((1u << lane) - 1));
+            const uint32_t b = live ? cv[key] : 0;
+            __syncwarp();
+            if (live) {
+                perm[r.off + b + rank] = i;
+                if (rank == 0) cv[key] = b + __popc(peers);
+            }
+            __syncwarp();
         }
     }
 }
@@ -767,6 +830,8 @@ void graph_finalize(Graph& g, const int64_t* d_off, const uint16_t* d_ntypes) {
     g.wtotal.reset();
     g.wblk.reset();
     g.tcount.reset();
+    g.tperm.reset();
+    g.tbase.reset();
     g.htab.reset();
     g.arc.reset();
     g.bloom.reset();
@@ -985,6 +1050,8 @@ void graph_set_node_types(Graph& g, const uint16_t* types, uint16_t num_types) {
     MHW_CK(cudaStreamSynchronize(g.stream));
     g.n_ntypes = num_types;
     g.tcount.reset();
+    g.tperm.reset();
+    g.tbase.reset();
 }
 
 void graph_set_edge_types(Graph& g, const uint16_t* types, uint16_t num_types) {
@@ -1018,6 +1085,8 @@ void graph_replicate(const Graph& s, Graph& d, int device) {
     copy_buf(s.wtotal, s.device, d.wtotal, device, d.stream);
     copy_buf(s.wblk, s.device, d.wblk, device, d.stream);
     copy_buf(s.tcount, s.device, d.tcount, device, d.stream);
+    copy_buf(s.tperm, s.device, d.tperm, device, d.stream);
+    copy_buf(s.tbase, s.device, d.tbase, device, d.stream);
     copy_buf(s.htab, s.device, d.htab, device, d.stream);
     copy_buf(s.arc, s.device, d.arc, device, d.stream);
     MHW_CK(cudaStreamSynchronize(d.stream));
@@ -1161,6 +1230,21 @@ void graph_ensure_tcount(Graph& g) {
     g.tcount.alloc((size_t)g.n * g.n_ntypes);
     MHW_CK(cudaMemsetAsync(g.tcount.p, 0, g.tcount.bytes(), g.stream));
     k_tcount<<<grid_for((uint64_t)g.n * 32), kBlock, 0, g.stream>>>(g.view(), g.tcount.p);
+    MHW_CK(cudaGetLastError());
+    MHW_CK(cudaStreamSynchronize(g.stream));
+}
+
+void graph_ensure_typed_index(Graph& g) {
+    if (g.tbase.n || !g.n || !g.m || !g.n_ntypes || g.n_ntypes > 64) return;
+    DeviceGuard dg(g.device);
+    const uint64_t K = 2ull * g.n_ntypes;
+    DBuf<uint32_t> cnt(g.n * K);
+    MHW_CK(cudaMemsetAsync(cnt.p, 0, cnt.bytes(), g.stream));
+    g.tperm.alloc(g.m);
+    g.tbase.alloc((size_t)g.n * g.n_ntypes);
+    k_tidx_count<<<grid_for((uint64_t)g.n * 32), kBlock, 0, g.stream>>>(g.view(), cnt.p);
+    k_tidx_base<<<grid_for(g.n), kBlock, 0, g.stream>>>(g.view(), cnt.p, g.tbase.p);
+    k_tidx_scatter<<<grid_for((uint64_t)g.n * 32), kBlock, 0, g.stream>>>(g.view(), cnt.p, g.tperm.p);
     MHW_CK(cudaGetLastError());
     MHW_CK(cudaStreamSynchronize(g.stream));
 }

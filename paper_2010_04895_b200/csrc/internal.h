@@ -106,6 +106,8 @@ struct Graph {
     DBuf<double> wtotal;     // lazily built
     DBuf<double> wblk;       // bootstrap block prefix sums, built with wtotal
     DBuf<uint32_t> tcount;   // lazily built
+    DBuf<uint32_t> tperm;    // typed neighbour index (metapath2vec init), lazily built
+    DBuf<uint2> tbase;
     DBuf<uint32_t> htab;     // adjacency hash sets, lazily built
     DBuf<uint32_t> bloom;    // edge Bloom filter (second-order alpha), lazily built
     uint32_t bloom_blocks = 0;
@@ -140,6 +142,7 @@ void graph_download(const Graph& g, int64_t* offsets, int32_t* nbr, float* w, ui
 void graph_ensure_rev(Graph& g);
 void graph_ensure_wtotal(Graph& g);
 void graph_ensure_tcount(Graph& g);
+void graph_ensure_typed_index(Graph& g);
 void graph_ensure_hash(Graph& g);
 void graph_ensure_bloom(Graph& g);
 bool graph_ensure_arcrec(Graph& g);  // deepwalk arc records (fp32 weight aux)

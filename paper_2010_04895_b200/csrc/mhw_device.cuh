@@ -67,6 +67,8 @@ struct DevGraph {
     const uint32_t* __restrict__ htab;    // adjacency hash sets (nullptr: not built)
     const uint4* __restrict__ arc;        // arc records (nullptr: not built)
     const uint32_t* __restrict__ bloom;   // edge Bloom filter, 8 words per block (nullptr: not built)
+    const uint32_t* __restrict__ tperm;   // per slice: neighbour indices ordered by (type, w > 0 first, index)
+    const uint2* __restrict__ tbase;      // per (node, type): {start in tperm slice, count of w > 0}
     uint32_t bloom_blocks;
     uint16_t n_ntypes;
     uint16_t n_etypes;
@@ -588,6 +590,17 @@ __device__ bool random_positive(const DevGraph& g, const DevModel& m, const SCtx
                                 double* w_out) {
     Draw d;
     d.open(key, slot, blk);
+    if (KIND == METAPATH2VEC && g.tbase) {
+        // w' > 0 exactly for the neighbours of the required type with w > 0
+        // (models.cpp:91-94); the typed index lists them in index order, so
+        // the pick-th positive is one lookup instead of two slice scans.
+        const uint2 b = __ldg(g.tbase + (size_t)c.v * g.n_ntypes + c.req);
+        if (b.y == 0) return false;
+        const uint32_t i = __ldg(g.tperm + c.off + b.x + d.index(b.y));
+        *out = i;
+        *w_out = eval_index<KIND>(g, m, c, i, cls_out);
+        return true;
+    }
     if (all_positive<KIND>(m, c)) {
         const uint32_t pick = d.index(c.deg);
         *out = pick;

@@ -1100,6 +1100,7 @@ void model_bind(Model& mb, Graph& g, const mhw_model_desc& d) {
         MHW_CK(cudaMemcpy(mb.metapath.p, d.metapath, d.metapath_len * 2, cudaMemcpyHostToDevice));
         m.metapath = mb.metapath.p;
         m.mp_len = d.metapath_len;
+        graph_ensure_typed_index(g);  // O(1) random_positive for slot inits
     }
     if (k == EDGE2VEC) {
         const uint32_t dim = g.etype.n ? g.n_etypes : (uint32_t)(g.n_ntypes * g.n_ntypes);
