@@ -304,3 +304,30 @@ def test_slot_init_equals_oracle(mhw, oracle, kind, init):
             slot = int(g.offsets[v]) + a
         want = oracle.init_philox(g, md, cfg, v, a, slot)
         assert (O.NO_AFFIX if want is None else want) == got[i], (i, v, a)
+
+
+@pytest.mark.parametrize("init", [O.INIT_RANDOM, O.INIT_HIGH_WEIGHT, O.INIT_BURN_IN])
+def test_metapath_typed_index_init_equals_scan(mhw, oracle, init):
+    """metapath2vec slot inits pick the pick-th positive (required type, w > 0)
+    through the typed neighbour index; the oracle scans the slice
+    (samplers.cpp:22-33). Zero weights, three types, hubs of degree > 32."""
+    rng = O.XoRng(77)
+    g = O.random_graph(300, 24.0, True, rng)
+    O.assign_random_types(g, 3, rng)
+    r = np.random.default_rng(5)
+    w = g.w.copy()
+    zero = r.uniform(size=g.m) < 0.25
+    w[zero] = 0.0
+    g.w = w
+    md = model_desc(O.METAPATH2VEC, g, metapath=(0, 1, 2, 1, 0))
+    cfg = O.WalkCfg(K=1, L=1, seed=99, init_kind=init, burn_in_steps=7, hw_sample_size=4)
+    n = g.n
+    pos = np.repeat(np.arange(n, dtype=np.uint32), 5)
+    aff = np.tile(np.arange(5, dtype=np.uint32), n)
+    got = mhw.init_states(device_graph(g), walk_model(md), walk_config(cfg), pos, aff)
+    mp = md.metapath
+    for i in range(len(pos)):
+        v, a = int(pos[i]), int(aff[i])
+        nxt = a + 1 if a + 1 < len(mp) else (1 if mp[0] == mp[-1] else 0)
+        want = oracle.init_philox(g, md, cfg, v, a, v * g.n_ntypes + mp[nxt])
+        assert (O.NO_AFFIX if want is None else want) == got[i], (i, v, a)
