@@ -1172,21 +1172,30 @@ void graph_ensure_hash(Graph& g) {
     MHW_CK(cudaStreamSynchronize(g.stream));
 }
 
-// Edge Bloom filter for the alpha test: 4 bits per arc (8 per undirected
-// edge, ~2.4% false positives), built only when it stays small enough to
-// live in L2 (MHW_BLOOM_MB, default 64 MB; MHW_BLOOM_BITS overrides the
-// density). Measured on cfg2: 4 bits/arc 41.2 ms, 8 bits 43.2, 16 bits
-// 46.5, none 48.8 -- L2 residency beats a lower false-positive rate.
-// MHW_BLOOM=0 disables it.
+// Edge Bloom filter for the alpha test. Small graphs: 4 bits per arc (8 per
+// undirected edge, ~2.4% false positives) when that fits 64 MB and can live
+// in L2 (measured on cfg2: 4 bits/arc 41.2 ms, 8 bits 43.2, 16 bits 46.5,
+// none 48.8 -- residency beats a lower false-positive rate; cfg4's 64 MB:
+// 176 ms vs 190 without). Larger graphs: the filter is DRAM-resident anyway,
+// and one sector probe still settles most non-adjacent pairs ahead of a hash
+// probe or slice search, so it is built at 8 bits per arc when it takes at
+// most 1/8 of free device memory (cfg5, 2.08 G arcs: 1185 ms without, 1111
+// at 4 bits, 1099 at 8). MHW_BLOOM_MB / MHW_BLOOM_BITS override the budget
+// and density; MHW_BLOOM=0 disables it.
 void graph_ensure_bloom(Graph& g) {
     if (g.bloom.n || !g.m) return;
     const char* off = std::getenv("MHW_BLOOM");
     if (off && off[0] == '0') return;
     const char* mb = std::getenv("MHW_BLOOM_MB");
-    const uint64_t budget = (uint64_t)(mb ? std::atoll(mb) : 64) << 20;
     const char* bits = std::getenv("MHW_BLOOM_BITS");
-    const uint64_t bytes = g.m * (uint64_t)(bits ? std::atoi(bits) : 4) / 8;  // bits per arc
-    if (bytes > budget || bytes < 32) return;
+    uint64_t bytes = g.m * (uint64_t)(bits ? std::atoi(bits) : 4) / 8;  // bits per arc
+    if (mb) {
+        if (bytes > ((uint64_t)std::atoll(mb) << 20)) return;
+    } else if (bytes > (64ull << 20)) {
+        if (!bits) bytes = g.m;  // 8 bits per arc
+        if (bytes > dev_available_bytes() / 8) return;
+    }
+    if (bytes < 32) return;
     const uint64_t blocks = (bytes + 31) / 32;
     if (blocks >= (1ull << 32)) return;
     DeviceGuard dg(g.device);
