@@ -1172,11 +1172,12 @@ void graph_ensure_hash(Graph& g) {
     MHW_CK(cudaStreamSynchronize(g.stream));
 }
 
-// Edge Bloom filter for the alpha test. Small graphs: 4 bits per arc (8 per
-// undirected edge, ~2.4% false positives) when that fits 64 MB and can live
-// in L2 (measured on cfg2: 4 bits/arc 41.2 ms, 8 bits 43.2, 16 bits 46.5,
-// none 48.8 -- residency beats a lower false-positive rate; cfg4's 64 MB:
-// 176 ms vs 190 without). Larger graphs: the filter is DRAM-resident anyway,
+// Edge Bloom filter for the alpha test. Small graphs: the densest of 4 / 3 /
+// 2 bits per arc (4 bits: 8 per undirected edge, ~2.4% false positives) that
+// fits 32 MB and so lives in L2 (measured on cfg2: 4 bits/arc 41.2 ms, 8 bits
+// 43.2, 16 bits 46.5, none 48.8 -- residency beats a lower false-positive
+// rate; cfg4: 2 bits (32 MB) 174.9 ms, 4 bits (64 MB) 176.7, none 189.8).
+// Larger graphs: the filter is DRAM-resident anyway,
 // and one sector probe still settles most non-adjacent pairs ahead of a hash
 // probe or slice search, so it is built at 8 bits per arc when it takes at
 // most 1/8 of free device memory (cfg5, 2.08 G arcs: 1185 ms without, 1111
@@ -1191,9 +1192,15 @@ void graph_ensure_bloom(Graph& g) {
     uint64_t bytes = g.m * (uint64_t)(bits ? std::atoi(bits) : 4) / 8;  // bits per arc
     if (mb) {
         if (bytes > ((uint64_t)std::atoll(mb) << 20)) return;
-    } else if (bytes > (64ull << 20)) {
-        if (!bits) bytes = g.m;  // 8 bits per arc
+    } else if (!bits) {
+        // densest of 4 / 3 / 2 bits per arc within 32 MB (L2-resident),
+        // else 8 bits per arc in DRAM
+        for (uint64_t b = 4; b >= 2 && (bytes = g.m * b / 8) > (32ull << 20); --b) {
+        }
+        if (bytes > (32ull << 20)) bytes = g.m;
         if (bytes > dev_available_bytes() / 8) return;
+    } else if (bytes > dev_available_bytes() / 8) {
+        return;
     }
     if (bytes < 32) return;
     const uint64_t blocks = (bytes + 31) / 32;
