@@ -1314,9 +1314,10 @@ void session_create(Session& s, Graph& g, const mhw_model_desc& md, const mhw_wa
         const bool dense = (double)s.n_items * s.cfg.L >= 8.0 * (double)s.slots;
         s.eager_init = second_order(m.kind) && (wc.init_mode == 2 || (wc.init_mode == 0 && dense));
         s.minb = walk_minb(m.kind, s.eager_init);
-        // pin a small edge filter in L2 (cfg2: 16 MB, +3%; a 64 MB window
+        // pin an L2-sized edge filter (<= 32 MB by construction) in L2
+        // (cfg2: 16 MB, +3%; cfg4: 32 MB, 174.3 -> 167.5 ms; a 64 MB window
         // starves the rest of the working set: cfg4 -30%)
-        if (g.bloom.n && g.bloom.bytes() <= (24ull << 20)) {
+        if (g.bloom.n && g.bloom.bytes() <= (33ull << 20)) {
             int dev = 0, max_persist = 0;
             MHW_CK(cudaGetDevice(&dev));
             MHW_CK(cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, dev));
