@@ -1317,17 +1317,34 @@ void session_create(Session& s, Graph& g, const mhw_model_desc& md, const mhw_wa
         // pin an L2-sized edge filter (<= 32 MB by construction) in L2
         // (cfg2: 16 MB, +3%; cfg4: 32 MB, 174.3 -> 167.5 ms; a 64 MB window
         // starves the rest of the working set: cfg4 -30%)
-        if (g.bloom.n && g.bloom.bytes() <= (33ull << 20)) {
+        // fairwalk with p = q = 1 has no alpha test (no filter): its per-
+        // (node, type) group sizes, read for every candidate, take the window
+        void* pin_p = nullptr;
+        size_t pin_bytes = 0;
+        if (g.bloom.n && !m.alpha_trivial) {
+            pin_p = g.bloom.p;
+            pin_bytes = g.bloom.bytes();
+        } else if (m.kind == FAIRWALK && g.tcount.n) {
+            pin_p = g.tcount.p;
+            pin_bytes = g.tcount.bytes();
+        }
+        const char* pe = std::getenv("MHW_L2_PIN");
+        const bool pin_ok = !(pe && pe[0] == '0');
+        auto try_pin = [&](void* p, size_t bytes) {
+            if (!pin_ok || !p || bytes > (33ull << 20)) return;
             int dev = 0, max_persist = 0;
             MHW_CK(cudaGetDevice(&dev));
             MHW_CK(cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, dev));
             size_t cur = 0;
             MHW_CK(cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize));
-            if ((size_t)max_persist >= g.bloom.bytes()) {
-                if (cur < g.bloom.bytes()) MHW_CK(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, g.bloom.bytes()));
+            if ((size_t)max_persist >= bytes) {
+                if (cur < bytes) MHW_CK(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, bytes));
                 s.l2_pin = true;
+                s.pin_p = p;
+                s.pin_bytes = bytes;
             }
-        }
+        };
+        try_pin(pin_p, pin_bytes);
         // arc records (after the session buffers, so the memory check sees them)
         const char* ar_env = std::getenv("MHW_ARC_RECORDS");
         const bool want_ar = !(ar_env && ar_env[0] == '0');
@@ -1349,6 +1366,8 @@ void session_create(Session& s, Graph& g, const mhw_model_desc& md, const mhw_wa
         }
         if (!s.ac.n || !second_order(m.kind)) s.chain.alloc(std::max<uint64_t>(s.slots, 1));
         else s.chain.alloc(1);
+        // node-keyed models: the chain table itself (hub replicas included)
+        if (!s.l2_pin && !second_order(m.kind)) try_pin(s.chain.p, s.chain.bytes());
         if (want_ar && m.kind == DEEPWALK) s.use_ar = graph_ensure_arcrec(g);
         dispatch(m.kind, [&](auto kc) {
             constexpr int KIND = decltype(kc)::value;
@@ -1444,8 +1463,8 @@ void session_run(Session& s, cudaStream_t user) {
     s.launches = 0;
     // A small edge filter is pinned in L2 for the walk (persisting access
     // window on the launch stream, cleared again after the launches).
-    const bool pin = s.l2_pin && s.g->bloom.n;
-    if (pin) l2_window(st, s.g->bloom.p, s.g->bloom.bytes());
+    const bool pin = s.l2_pin;
+    if (pin) l2_window(st, s.pin_p, s.pin_bytes);
     const bool preloaded = s.chain_loaded;  // mhw_session_load_chain: table already initialised
     s.chain_loaded = false;
     if (!preloaded) MHW_CK(cudaMemsetAsync(s.chain.p, 0xFF, s.chain.bytes(), st));
@@ -1730,8 +1749,8 @@ void session_run_packed(Session& s, uint32_t* h_nodes, uint64_t cap_nodes, uint6
         if (s.n_iso)
             k_iso_rows<<<grid_for((uint64_t)s.n_iso * s.cfg.K), 256, 0, S>>>(s.iso.p, s.iso_row.p, s.n_iso, s.cfg.K,
                                                                              s.out.p, s.stride, s.lens.p);
-        const bool pin = s.l2_pin && s.g->bloom.n;
-        if (pin) l2_window(S, s.g->bloom.p, s.g->bloom.bytes());
+        const bool pin = s.l2_pin;
+        if (pin) l2_window(S, s.pin_p, s.pin_bytes);
         MHW_CK(cudaEventRecord(s.ev0, S));
         const double t_setup = ms_since(ta);
         dispatch(s.model.dev.kind, [&](auto kc) {

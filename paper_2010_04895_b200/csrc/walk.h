@@ -68,7 +68,9 @@ struct Session {
     int grid = 0;
     bool eager_init = false;
     bool chain_loaded = false;  // mhw_session_load_chain installed the initial table
-    bool l2_pin = false;        // persisting L2 window over the edge filter during runs
+    bool l2_pin = false;        // persisting L2 window during runs (edge filter, or fairwalk group sizes)
+    void* pin_p = nullptr;
+    size_t pin_bytes = 0;
     bool use_ar = false;     // arc-record walk kernel variant
     int minb = 1;
     uint32_t launches = 0;
