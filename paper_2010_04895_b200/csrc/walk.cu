@@ -471,18 +471,68 @@ __global__ void __launch_bounds__(256, KIND == NODE2VEC ? 8 : 4) k_init_range(Ru
 // k_init_range, permuted so that the install (k_load_rec) is a coalesced
 // strided copy instead of a random scatter. out == nullptr: write straight
 // into the session records (eager init in record order).
+// State (s, v) of record a = arc s -> v, built from what record order gives
+// for free: v, deg(v), off(v) (and v's type and the arc's edge type in typed
+// records) come from the session record itself -- a coalesced load -- and s
+// is the owner of arc a, shared by neighbouring threads (cached search), so
+// the two random loads of make_ctx (N(v)[affix] and v's node record) go.
+template <int KIND>
+__device__ __forceinline__ SCtx rec_ctx(const RunParams& P, uint64_t a) {
+    const DevGraph& g = P.g;
+    SCtx c;
+    uint32_t et = 0;
+    if (P.ac && P.rec_u32 == 4) {
+        const uint4 r = __ldg(P.ac + a);
+        c.v = r.x;
+        c.deg = r.y & 0x7FFFFFFFu;
+        c.off = (long long)r.z;
+        c.vtype = 0;
+        c.vflags = (r.y >> 31) ? NF_ALLPOS : 0;
+    } else if (P.ac && P.rec_u32 == 8) {
+        uint4 r0, r1;
+        ldg256(P.ac + 2 * a, r0, r1);
+        c.v = r0.x;
+        c.deg = r0.y & 0x7FFFFFFFu;
+        c.off = (long long)r0.z;
+        c.vtype = (uint16_t)(r1.x & 0xFFFFu);
+        c.vflags = (r0.y >> 31) ? NF_ALLPOS : 0;
+        et = r1.x >> 16;
+    } else {
+        c.v = load_id(g, a);
+        const NodeRec r = load_node(g, c.v);
+        c.off = r.off;
+        c.deg = r.deg;
+        c.vtype = r.type;
+        c.vflags = r.flags;
+    }
+    uint32_t lo = 0, hi = g.n;  // s: the last node whose slice starts at or before a
+    while (hi - lo > 1) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if ((uint64_t)__ldg(&g.nodes[mid].off) <= a) lo = mid;
+        else hi = mid;
+    }
+    const NodeRec rs = load_node(g, lo);
+    c.s = lo;
+    c.off_s = rs.off;
+    c.deg_s = rs.deg;
+    c.req = 0;
+    c.boot = false;
+    c.in_type = 0;
+    if (KIND == EDGE2VEC) c.in_type = (P.ac && P.rec_u32 == 8) ? et : edge_type_of(g, a, rs.type, c.vtype);
+    return c;
+}
+
 template <int KIND>
 __global__ void __launch_bounds__(256, KIND == NODE2VEC ? 8 : 4) k_init_rec(RunParams P, uint64_t b, uint64_t e, uint32_t* __restrict__ out) {
     const DevGraph& g = P.g;
     unsigned long long inits = 0;
     for (uint64_t a = b + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; a < e;
          a += (uint64_t)gridDim.x * blockDim.x) {
-        const uint32_t v = load_id(g, a);
         const uint32_t affix = __ldg(g.rev + a);
         uint32_t w = kEmpty;  // no back arc: no state (s, v) can ever use this record
         double wl = 0.0;
         if (affix != kNoBack) {
-            const SCtx c = make_ctx<KIND>(g, P.m, v, affix);
+            const SCtx c = rec_ctx<KIND>(P, a);
             w = init_slot<KIND>(g, P.m, P.cfg, c, (uint64_t)c.off + affix, &wl);
             ++inits;
         }
