@@ -1254,6 +1254,9 @@ void graph_ensure_typed_index(Graph& g) {
     if (g.tbase.n || !g.n || !g.m || !g.n_ntypes || g.n_ntypes > 64) return;
     DeviceGuard dg(g.device);
     const uint64_t K = 2ull * g.n_ntypes;
+    // index + bases + build counters; optional (inits fall back to the scan)
+    const uint64_t need = 4 * g.m + 8ull * g.n * g.n_ntypes + 4 * g.n * K;
+    if (need > dev_available_bytes() / 4) return;
     DBuf<uint32_t> cnt(g.n * K);
     MHW_CK(cudaMemsetAsync(cnt.p, 0, cnt.bytes(), g.stream));
     g.tperm.alloc(g.m);
