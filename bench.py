@@ -112,7 +112,7 @@ def shard_init_pays(cfg, g):
     Then N ranks share one initialisation (each inits 1/N of the records,
     all-gather, coalesced install) instead of each rank initialising, eagerly
     or lazily, most of the table itself. cfg5 (steps = 5 x slots, lazy at N=1,
-    every slot touched): 8 shards 205 -> 154 ms per rank
+    every slot touched): 8 shards 205 -> 146 ms per rank
     (profiles/shard_scaling_r01.md)."""
     off = g.download()["offsets"]
     walkers = int(np.count_nonzero(np.diff(off))) * cfg["K"]
