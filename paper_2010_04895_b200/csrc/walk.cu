@@ -1361,7 +1361,19 @@ void session_create(Session& s, Graph& g, const mhw_model_desc& md, const mhw_wa
     } else {
         // Eager slot init when walks will touch most arc-keyed slots anyway
         // (identical chain values: init randomness is slot-keyed).
-        const bool dense = (double)s.n_items * s.cfg.L >= 8.0 * (double)s.slots;
+        // Eager init order: record order builds each state from its own
+        // (coalesced) session record, slot order keeps a warp on one N(v)
+        // (burn-in draws ~11 candidates from it). Record order where the
+        // records carry deg/off (wide or typed) and init draws few
+        // candidates: cfg5 (random init, wide records) 1105 ms lazy, 1137
+        // eager in slot order, 1066 in record order; cfg2 (burn-in, narrow
+        // records) 34.6 slot vs 35.6 record. With the cheaper record-order
+        // init, eager pays from 2 walker steps per slot (cfg5: 5) instead of 8.
+        const char* io = std::getenv("MHW_INIT_ORDER");
+        const char* nw0 = std::getenv("MHW_NARROW");
+        const bool narrow_pred = m.kind == NODE2VEC && (nw0 ? nw0[0] == '1' : 16ull * g.n <= (32ull << 20));
+        s.init_rec_order = io ? io[0] == 'r' : (!narrow_pred && s.cfg.init_kind != INIT_BURN_IN);
+        const bool dense = (double)s.n_items * s.cfg.L >= (s.init_rec_order ? 2.0 : 8.0) * (double)s.slots;
         s.eager_init = second_order(m.kind) && (wc.init_mode == 2 || (wc.init_mode == 0 && dense));
         s.minb = walk_minb(m.kind, s.eager_init);
         // pin an L2-sized edge filter (<= 32 MB by construction) in L2
@@ -1494,14 +1506,11 @@ RunParams Session::params() const {
 // Eager init of every arc-keyed slot: slot order (k_init_all: a warp's
 // threads share v, so the burn-in candidates of N(v) are local; the words
 // scatter into the records) or record order (k_init_rec: coalesced writes,
-// scattered N(v) reads). MHW_INIT_ORDER=rec|slot; default slot.
+// state from the record, scattered N(v) reads); chosen in session_create
+// (MHW_INIT_ORDER=rec|slot overrides).
 template <int KIND>
 static void launch_init_all(const Session& s, const RunParams& P, cudaStream_t st) {
-    static const int rec = [] {
-        const char* e = std::getenv("MHW_INIT_ORDER");
-        return e && e[0] == 'r' ? 1 : 0;
-    }();
-    if (rec && s.ac.n) k_init_rec<KIND><<<grid_for(s.g->m), 256, 0, st>>>(P, 0, s.g->m, nullptr);
+    if (s.init_rec_order && s.ac.n) k_init_rec<KIND><<<grid_for(s.g->m), 256, 0, st>>>(P, 0, s.g->m, nullptr);
     else k_init_all<KIND><<<grid_for(s.g->m), 256, 0, st>>>(P);
     MHW_CK(cudaGetLastError());
 }

@@ -67,6 +67,7 @@ struct Session {
     int sort_bits = 1;
     int grid = 0;
     bool eager_init = false;
+    bool init_rec_order = false;  // eager init in record order (k_init_rec) rather than slot order
     bool chain_loaded = false;  // mhw_session_load_chain installed the initial table
     bool l2_pin = false;        // persisting L2 window during runs (edge filter, or fairwalk group sizes)
     void* pin_p = nullptr;
