@@ -375,26 +375,47 @@ def run_mine(args, cfg):
         torch.cuda.synchronize(dev)
 
     per = 0
+    PIECES = 4  # all-gather pieces: piece j+1 is in flight while piece j installs
     if shard_init:
         S = sess.chain_size()
         W = sess.record_width()  # u32 words per record entry (3: typed records carry w'(Last))
-        per = (S + world - 1) // world
+        pc = (((S + world - 1) // world) + PIECES - 1) // PIECES  # entries per piece per rank
+        per = pc * PIECES
         shard = torch.empty(per * W, dtype=torch.int32, device=dev)
-        full = torch.empty(per * world * W, dtype=torch.int32, device=dev)
+        full = torch.empty(PIECES * world * pc * W, dtype=torch.int32, device=dev)
         lo, hi = min(S, rank * per), min(S, (rank + 1) * per)
 
     def one_run():
+        n_launch = 0
         if shard_init:
             sess.init_records(lo, hi, shard.data_ptr(), stream.cuda_stream)
-            if host_coll:
-                parts = [torch.empty(per * W, dtype=torch.int32) for _ in range(world)]
-                dist.all_gather(parts, shard.cpu())
-                full.copy_(torch.cat(parts).to(dev))
-            else:
-                dist.all_gather_into_tensor(full, shard)
-            sess.load_records(full.data_ptr(), stream.cuda_stream)
+            n_launch += 1
+            # piece j of every rank's shard: records [q*per + j*pc, +pc) of rank q,
+            # gathered into full[j] (world x pc entries) and installed as soon as
+            # it lands while piece j+1 is in flight
+            works = []
+            for j in range(PIECES):
+                out_j = full[j * world * pc * W:(j + 1) * world * pc * W]
+                src = shard[j * pc * W:(j + 1) * pc * W]
+                if host_coll:  # gloo (ranks sharing one GPU): through host memory
+                    parts = [torch.empty(pc * W, dtype=torch.int32) for _ in range(world)]
+                    dist.all_gather(parts, src.cpu())
+                    out_j.copy_(torch.cat(parts).to(dev))
+                    works.append(None)
+                else:
+                    works.append(dist.all_gather_into_tensor(out_j, src, async_op=True))
+            for j in range(PIECES):
+                if works[j] is not None:
+                    works[j].wait()  # the install stream waits for piece j only
+                base = full.data_ptr() + 4 * j * world * pc * W
+                for q in range(world):
+                    b = min(S, q * per + j * pc)
+                    e = min(S, q * per + (j + 1) * pc)
+                    if e > b:
+                        sess.load_records_range(b, e, base + 4 * q * pc * W, stream.cuda_stream)
+                        n_launch += 1
         sess.run(stream.cuda_stream)
-        return sess.launches() + (2 if shard_init else 0)
+        return sess.launches() + n_launch
 
     for _ in range(args.warmup):
         one_run()

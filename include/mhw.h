@@ -330,6 +330,12 @@ MHW_API mhw_status mhw_session_record_width(const mhw_session* s, uint32_t* widt
 MHW_API mhw_status mhw_session_init_records(mhw_session* s, uint64_t begin, uint64_t end, uint32_t* d_words,
                                             void* stream);
 MHW_API mhw_status mhw_session_load_records(mhw_session* s, const uint32_t* d_words, void* stream);
+/* Installs entries [begin, end) only (d_words points at entry begin): lets a
+ * caller install each piece of the table as soon as its all-gather lands,
+ * overlapping the next piece's transfer. The next run counts the table as
+ * loaded; the caller installs every piece before it. */
+MHW_API mhw_status mhw_session_load_records_range(mhw_session* s, uint64_t begin, uint64_t end,
+                                                  const uint32_t* d_words, void* stream);
 MHW_API void mhw_session_free(mhw_session* s);
 
 /* ---- parity entry points ---------------------------------------------- */

@@ -100,6 +100,7 @@ SIGNATURES = {
     "mhw_session_init_records": (C.c_int32, [_P, C.c_uint64, C.c_uint64, _P, _P]),
     "mhw_session_load_records": (C.c_int32, [_P, _P, _P]),
     "mhw_session_record_width": (C.c_int32, [_P, _P]),
+    "mhw_session_load_records_range": (C.c_int32, [_P, C.c_uint64, C.c_uint64, _P, _P]),
     "mhw_session_free": (None, [_P]),
     "mhw_decide": (C.c_int32, [_P, C.POINTER(ModelDescC), C.c_uint64, _P, _P, _P, _P, _P, _P, _P, _P]),
     "mhw_alias_tables": (C.c_int32, [_P, _P, _P]),

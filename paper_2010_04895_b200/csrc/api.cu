@@ -615,6 +615,15 @@ mhw_status mhw_session_record_width(const mhw_session* s, uint32_t* width) {
     });
 }
 
+mhw_status mhw_session_load_records_range(mhw_session* s, uint64_t begin, uint64_t end, const uint32_t* d_words,
+                                          void* stream) {
+    return guard([&] {
+        need(s, "session");
+        if (end > begin) need(d_words, "d_words");
+        mhw::session_load_records_range(*s, begin, end, d_words, static_cast<cudaStream_t>(stream));
+    });
+}
+
 mhw_status mhw_session_load_records(mhw_session* s, const uint32_t* d_words, void* stream) {
     return guard([&] {
         need(s, "session");

@@ -561,18 +561,19 @@ __global__ void __launch_bounds__(256, KIND == NODE2VEC ? 8 : 4) k_init_rec(RunP
 // record; typed records take {word, w'(Last)} (3 words per record). Without
 // session records the words go to their slots (chain table in slot order).
 __global__ void k_load_rec(RunParams P, const uint32_t* __restrict__ w, uint32_t* __restrict__ ac, uint32_t rw,
-                           uint32_t* __restrict__ chain) {
+                           uint32_t* __restrict__ chain, uint64_t b, uint64_t end) {
     const DevGraph& g = P.g;
-    for (uint64_t a = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; a < g.m;
+    for (uint64_t a = b + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; a < end;
          a += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t i = a - b;  // entry of record a in w
         if (ac && rw == 8) {
             uint32_t* rec = ac + a * rw;
-            rec[5] = __ldg(w + 3 * a);
-            rec[6] = __ldg(w + 3 * a + 1);
-            rec[7] = __ldg(w + 3 * a + 2);
+            rec[5] = __ldg(w + 3 * i);
+            rec[6] = __ldg(w + 3 * i + 1);
+            rec[7] = __ldg(w + 3 * i + 2);
             continue;
         }
-        const uint32_t e = __ldg(w + a);
+        const uint32_t e = __ldg(w + i);
         if (ac) {
             ac[a * rw + chain_word_off(rw)] = e;
             continue;
@@ -1648,6 +1649,10 @@ void session_init_chain(Session& s, uint64_t begin, uint64_t end, uint32_t* d_wo
 }
 
 void session_load_chain(Session& s, const uint32_t* d_words, cudaStream_t user, bool rec_order) {
+    if (rec_order) {
+        session_load_records_range(s, 0, s.g->m, d_words, user);
+        return;
+    }
     DeviceGuard dg(s.g->device);
     if (!second_order(s.model.dev.kind) || s.ex || s.wc.schedule == MHW_SCHEDULE_DETERMINISTIC)
         invalid("chain preloading applies to second-order models on the throughput schedule");
@@ -1657,11 +1662,29 @@ void session_load_chain(Session& s, const uint32_t* d_words, cudaStream_t user, 
         dispatch(s.model.dev.kind, [&](auto kc) {
             constexpr int KIND = decltype(kc)::value;
             uint32_t* const ac = s.ac.n ? reinterpret_cast<uint32_t*>(s.ac.p) : nullptr;
-            if constexpr (second_order(KIND)) {
-                if (rec_order) k_load_rec<<<grid_for(s.g->m), 256, 0, st>>>(P, d_words, ac, s.rec_u32, s.chain.p);
-                else k_load_chain<KIND><<<grid_for(s.g->m), 256, 0, st>>>(P, d_words, ac, s.rec_u32, s.chain.p);
-            }
+            if constexpr (second_order(KIND))
+                k_load_chain<KIND><<<grid_for(s.g->m), 256, 0, st>>>(P, d_words, ac, s.rec_u32, s.chain.p);
         });
+        MHW_CK(cudaGetLastError());
+    }
+    s.chain_loaded = true;
+}
+
+// Installs entries [begin, end) of a record-order table (d_words points at
+// entry begin). A table installed piecewise (e.g. each piece as soon as its
+// all-gather lands) counts as loaded for the next run once the caller has
+// installed every piece.
+void session_load_records_range(Session& s, uint64_t begin, uint64_t end, const uint32_t* d_words,
+                                cudaStream_t user) {
+    DeviceGuard dg(s.g->device);
+    if (!second_order(s.model.dev.kind) || s.ex || s.wc.schedule == MHW_SCHEDULE_DETERMINISTIC)
+        invalid("chain preloading applies to second-order models on the throughput schedule");
+    if (begin > end || end > s.g->m) invalid("record range out of bounds");
+    cudaStream_t st = user ? user : s.stream;
+    if (end > begin) {
+        const RunParams P = s.params();
+        uint32_t* const ac = s.ac.n ? reinterpret_cast<uint32_t*>(s.ac.p) : nullptr;
+        k_load_rec<<<grid_for(end - begin), 256, 0, st>>>(P, d_words, ac, s.rec_u32, s.chain.p, begin, end);
         MHW_CK(cudaGetLastError());
     }
     s.chain_loaded = true;

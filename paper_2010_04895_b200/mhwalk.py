@@ -550,6 +550,11 @@ class Session:
         _check(L.lib().mhw_session_record_width(self._h, C.byref(w)))
         return w.value
 
+    def load_records_range(self, begin: int, end: int, d_words: int, stream: int | None = None):
+        """Installs entries [begin, end) of a record-order table (d_words -> entry begin)."""
+        _check(L.lib().mhw_session_load_records_range(self._h, begin, end, C.c_void_p(d_words),
+                                                      C.c_void_p(stream) if stream else None))
+
     def load_records(self, d_words: int, stream: int | None = None):
         """Installs a full record-order table for the next run."""
         _check(L.lib().mhw_session_load_records(self._h, C.c_void_p(d_words), C.c_void_p(stream) if stream else None))

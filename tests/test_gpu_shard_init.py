@@ -133,3 +133,39 @@ def test_record_order_preload_run_passes_chi_square(mhw, oracle, kind):
     rows, lens = s.download()
     ok, msg = gate(audit(g, oracle, md, rows, lens, min_visits=5000))
     assert ok, msg
+
+
+@pytest.mark.parametrize("kind", [O.NODE2VEC, O.EDGE2VEC])
+def test_piecewise_install_as_bench_pipelines_it(mhw, oracle, kind):
+    """bench.py's multi-GPU exchange: 3 emulated ranks, each shard in 4 pieces,
+    piece j of every rank installed with load_records_range as it lands; the
+    run needs no init of its own and passes the chain chi-square gate."""
+    g = typed_random_graph(610 + kind, 40, 4.0, weighted=True, types=2)
+    md = model_desc(kind, g, p=0.5, q=2.0, M=np.random.default_rng(kind).uniform(0.5, 2.0, (4, 4)))
+    cfg = O.WalkCfg(K=400, L=80, seed=81, init_kind=O.INIT_BURN_IN, burn_in_steps=5)
+    s = mhw.Session(device_graph(g), walk_model(md), walk_config(cfg, threads=8, init_mode=2))
+    S, W = s.chain_size(), s.record_width()
+    world, pieces = 3, 4
+    pc = (((S + world - 1) // world) + pieces - 1) // pieces
+    per = pc * pieces
+    shards = []
+    for r in range(world):
+        sh = torch.zeros(per * W, dtype=torch.int32, device="cuda")
+        lo, hi = min(S, r * per), min(S, (r + 1) * per)
+        if hi > lo:
+            s.init_records(lo, hi, sh.data_ptr())
+        shards.append(sh)
+    full = torch.empty(pieces * world * pc * W, dtype=torch.int32, device="cuda")
+    for j in range(pieces):
+        out_j = full[j * world * pc * W:(j + 1) * world * pc * W]
+        out_j.copy_(torch.cat([sh[j * pc * W:(j + 1) * pc * W] for sh in shards]))
+        base = full.data_ptr() + 4 * j * world * pc * W
+        for q in range(world):
+            b, e = min(S, q * per + j * pc), min(S, q * per + (j + 1) * pc)
+            if e > b:
+                s.load_records_range(b, e, base + 4 * q * pc * W)
+    s.run()
+    assert s.stats().slot_inits == 0
+    rows, lens = s.download()
+    ok, msg = gate(audit(g, oracle, md, rows, lens, min_visits=5000))
+    assert ok, msg
