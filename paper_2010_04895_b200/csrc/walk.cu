@@ -206,6 +206,17 @@ __global__ void __launch_bounds__(kWalkBlock) __maxnreg__(REGS) k_walk(RunParams
                 }
                 const uint32_t cand = d.index(c.deg);
                 const double u = d.unit();
+                // fairwalk: v's group sizes (one row of <= 4 types) are read
+                // with the candidate's record instead of after it
+                uint32_t grp0 = 0, grp1 = 0, grp2 = 0, grp3 = 0;
+                const bool grp_pre = KIND == FAIRWALK && TYPED && g.n_ntypes <= 4;
+                if (grp_pre) {
+                    const uint32_t* row = g.tcount + (size_t)c.v * g.n_ntypes;
+                    grp0 = __ldg(row);
+                    if (g.n_ntypes > 1) grp1 = __ldg(row + 1);
+                    if (g.n_ntypes > 2) grp2 = __ldg(row + 2);
+                    if (g.n_ntypes > 3) grp3 = __ldg(row + 3);
+                }
                 uint32_t uc;
                 uint4 ac = make_uint4(0, 0, 0, 0), bc = make_uint4(0, 0, 0, 0);
                 NodeRec rc{};
@@ -244,7 +255,14 @@ __global__ void __launch_bounds__(kWalkBlock) __maxnreg__(REGS) k_walk(RunParams
                     second_order(KIND) ? alpha_class(g, P.m, c, uc, rc_early ? &rc : nullptr, pre_bloom) : 0u;
                 double wc;
                 if (AR && KIND == DEEPWALK) wc = (double)__uint_as_float(ac.w);
-                else if (TYPED) wc = wprime_v<KIND>(g, P.m, c, (double)__uint_as_float(ac.w), rc.type, bc.x >> 16, cls_c);
+                else if (grp_pre) {
+                    // w' = (alpha * w) / group (models.cpp:115-119)
+                    const uint32_t t = rc.type;
+                    const uint32_t grp = t == 0 ? grp0 : (t == 1 ? grp1 : (t == 2 ? grp2 : grp3));
+                    wc = c.boot ? (double)__uint_as_float(ac.w)
+                                : __ddiv_rn(__dmul_rn(alpha_value(P.m, cls_c), (double)__uint_as_float(ac.w)),
+                                            (double)grp);
+                } else if (TYPED) wc = wprime_v<KIND>(g, P.m, c, (double)__uint_as_float(ac.w), rc.type, bc.x >> 16, cls_c);
                 else wc = wprime<KIND>(g, P.m, c, cand, rc.type, cls_c);
                 if (e == kLocked) {
                     unsigned ns = 32;
