@@ -465,7 +465,12 @@ def run_mine(args, cfg):
                 traffic = json.load(f).get("dram_bytes_per_launch")
         roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                 "traffic": traffic, "peak_source": peak_kind, "sectors_per_step": S, "E_sigma": es,
-                "kernel": "k_walk<%s>" % cfg["model"], "kernel_ms": kernel_ms}
+                "kernel": "k_walk<%s>" % cfg["model"] + (
+                    " + eager chain init (k_init_all / k_init_rec)"
+                    if cfg["model"] in ("node2vec", "edge2vec", "fairwalk") and st.slot_inits >= info["arc_count"]
+                    else ""),
+                "kernel_ms": kernel_ms,
+                "kernel_ms_note": "device time of one generate_walks' walk kernels (CUDA events on the launch stream)"}
         if cfg.get("sampler", "mh") != "mh":
             roof = None  # the canonical sector count is the M-H path's
         line = {
