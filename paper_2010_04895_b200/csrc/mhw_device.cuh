@@ -182,6 +182,7 @@ struct DevModel {
     int kind;
     double inv_p, inv_q;     // 1.0/p, 1.0/q computed on the host (models.cpp:77-79)
     int alpha_trivial;       // 1/p == 1 == 1/q: alpha is 1.0 whatever the class
+    uint32_t spec_cls;       // the unique heaviest alpha class (3: none); its Lasts are fetched early
     const uint16_t* metapath;
     uint32_t mp_len;
     const double* M;         // edge2vec type matrix, M_dim x M_dim
