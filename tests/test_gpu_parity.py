@@ -331,3 +331,28 @@ def test_metapath_typed_index_init_equals_scan(mhw, oracle, init):
         nxt = a + 1 if a + 1 < len(mp) else (1 if mp[0] == mp[-1] else 0)
         want = oracle.init_philox(g, md, cfg, v, a, v * g.n_ntypes + mp[nxt])
         assert (O.NO_AFFIX if want is None else want) == got[i], (i, v, a)
+
+
+@pytest.mark.parametrize("bits", ["2", "8", "0"])
+@pytest.mark.parametrize("kind", [O.NODE2VEC, O.EDGE2VEC])
+def test_decide_bit_exact_any_edge_filter_density(mhw, oracle, kind, bits, monkeypatch):
+    """The edge filter only ever short-cuts to 'not adjacent' on a miss: the
+    alpha classes, hence the decisions, are the same at every density the
+    build policy picks (2 bits/arc L2-resident, 8 bits/arc DRAM-resident) and
+    without a filter (MHW_BLOOM=0)."""
+    if bits == "0":
+        monkeypatch.setenv("MHW_BLOOM", "0")
+    else:
+        monkeypatch.setenv("MHW_BLOOM_BITS", bits)
+    rng = O.XoRng(700 + kind)
+    g = O.preferential_attachment(600, 6, rng)  # hubs: hash sets and long slices
+    O.assign_random_types(g, 2, rng)
+    g.w = np.array([float(np.float32(0.5 + rng.uniform_real())) for _ in range(g.m)])
+    md = model_desc(kind, g, p=0.37, q=1.9)
+    dg = device_graph(g)
+    pos, aff, cand, last, u = random_triples(g, md, 20000, seed=kind + 11)
+    owc, owl, oacc = oracle.decide(g, md, pos, aff, cand, last, u)
+    gwc, gwl, gacc = mhw.decide(dg, walk_model(md), pos, aff, cand, last, u)
+    assert np.array_equal(owc.view(np.uint64), gwc.view(np.uint64))
+    assert np.array_equal(owl.view(np.uint64), gwl.view(np.uint64))
+    assert np.array_equal(oacc, gacc)
