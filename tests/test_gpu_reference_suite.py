@@ -336,8 +336,10 @@ def test_node2vec_record_layouts_pass_chain_chi_square(mhw, oracle, narrow, monk
     monkeypatch.setenv("MHW_NARROW", narrow)
     g = typed_random_graph(901, 40, 4.0, weighted=False, types=2)
     md = model_desc(O.NODE2VEC, g, p=0.25, q=4.0)
-    for init_mode in (1, 2):
-        cfg = O.WalkCfg(K=400, L=80, seed=79 + init_mode, init_kind=O.INIT_BURN_IN, burn_in_steps=4)
+    # burn-in: eager init in slot order; random init on wide records: eager
+    # init in record order (the cfg5 path)
+    for init_mode, init_kind in ((1, O.INIT_BURN_IN), (2, O.INIT_BURN_IN), (2, O.INIT_RANDOM)):
+        cfg = O.WalkCfg(K=400, L=80, seed=79 + init_mode + init_kind, init_kind=init_kind, burn_in_steps=4)
         c = mhw.generate_walks(device_graph(g, weighted=False), walk_model(md),
                                walk_config(cfg, threads=8, init_mode=init_mode))
         ok, msg = gate(audit(g, oracle, md, c.rows, c.lengths, min_visits=5000))
