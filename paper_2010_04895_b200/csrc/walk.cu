@@ -559,7 +559,9 @@ __device__ __forceinline__ SCtx rec_ctx(const RunParams& P, uint64_t a) {
 }
 
 template <int KIND>
-__global__ void __launch_bounds__(256, KIND == NODE2VEC ? 8 : 4) k_init_rec(RunParams P, uint64_t b, uint64_t e, uint32_t* __restrict__ out) {
+// node2vec at 6 blocks/SM (~40 registers): at 8 (32 registers) the record-order
+// state build spills 352 bytes per thread (cfg5: 1064 ms vs 1055; 4 blocks: 1087)
+__global__ void __launch_bounds__(256, KIND == NODE2VEC ? 6 : 4) k_init_rec(RunParams P, uint64_t b, uint64_t e, uint32_t* __restrict__ out) {
     const DevGraph& g = P.g;
     unsigned long long inits = 0;
     for (uint64_t a = b + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; a < e;
