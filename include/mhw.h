@@ -62,8 +62,9 @@ typedef enum {
     MHW_SAMPLER_REJECTION = 3
 } mhw_sampler_kind;
 
-/* throughput: persistent kernel, chain updates linearised by CAS (exact M-H
- * per slot, interleaving order not reproducible).
+/* throughput: persistent kernel; a walker takes its state's chain word as a
+ * lock (atomic exchange) for the transition, so every chain is an exact
+ * sequential M-H chain (interleaving order not reproducible).
  * deterministic: step-synchronous, same-slot contenders folded in walker-id
  * order; byte-reproducible (the GPU counterpart of threads=1,
  * engine.hpp:43-46). */
@@ -124,11 +125,23 @@ typedef struct mhw_walk_config {
      * manager.cpp:35-56), 2 eager (all slots before the walk; identical
      * values because init randomness is keyed by the slot). */
     int32_t init_mode;
+    /* M-H proposal (north star (2)): MHW_PROPOSAL_UNIFORM
+     * draws the candidate uniformly over N(v) exactly as mh_transition
+     * (samplers.hpp:21); MHW_PROPOSAL_ALIAS draws it from v's static-weight
+     * alias table (alias_sample, samplers.hpp:68-71, tables of alias_build,
+     * samplers.cpp:95-131) and accepts with the Hastings-corrected ratio
+     * min(1, (w'(c) * w(l)) / (w'(l) * w(c))), w = static weight. */
+    int32_t proposal;
 } mhw_walk_config;
 
-/* Replaces mhwalk::RunStats (engine.hpp:28-36). init_seconds is not
- * separable inside the fused kernel and is reported as 0; walk_seconds is the
- * device time of the walk kernels (CUDA events). */
+typedef enum { MHW_PROPOSAL_UNIFORM = 0, MHW_PROPOSAL_ALIAS = 1 } mhw_proposal;
+
+/* Replaces mhwalk::RunStats (engine.hpp:28-36). init_seconds (T_i) is the
+ * device time of the eager chain-table initialisation launch and walk_seconds
+ * (T_w) that of the walk kernels (CUDA events on the launch stream); a lazy
+ * run initialises slots on first touch inside the walk kernel, so its T_i is
+ * 0 and T_w holds the init. steps_per_sec = steps / (T_i + T_w), including
+ * init as engine.cpp:231-232 does. */
 typedef struct mhw_walk_stats {
     uint64_t walks;
     uint64_t early_terminations;
@@ -292,6 +305,13 @@ MHW_API mhw_status mhw_session_create(const mhw_graph* g, const mhw_model_desc* 
  * session's own): chain table reset to EMPTY, then the walk kernels. The
  * corpus stays in HBM. */
 MHW_API mhw_status mhw_session_run(mhw_session* s, void* stream);
+/* Restricts the next runs to the given start nodes (strictly ascending,
+ * inside the session's node range): the corpus holds their K walks each in
+ * the reference order (engine.cpp:178-191 over that subset); count 0 with
+ * starts NULL restores the whole range. Walker ids, chains and draws are the
+ * ones of the full run (walker v*K + k), so a single-start selection with
+ * K = 1 runs one walker alone, deterministically. */
+MHW_API mhw_status mhw_session_select_starts(mhw_session* s, uint32_t count, const uint32_t* starts);
 /* Synchronizes and fetches the counters of the last run. */
 MHW_API mhw_status mhw_session_stats(mhw_session* s, mhw_walk_stats* stats);
 /* Device pointers of the padded walk buffer (rows x stride) and lengths. */

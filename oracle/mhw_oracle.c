@@ -616,6 +616,11 @@ typedef struct {
     const og_graph* g;
     const og_model* m;
     uint32_t v, affix, n;
+    /* optional (og_walk_isolated): per node, every static weight > 0 and the
+     * model cannot zero a weight -- then random_positive's pick-th positive is
+     * simply the pick-th index, and the two O(deg) scans are skipped (the GPU
+     * engine's all_positive fast path, mhw_device.cuh) */
+    const uint8_t* allpos;
 } st_t;
 
 static inline double st_w(const st_t* s, uint32_t i) { return og_weight(s->g, s->m, s->v, s->affix, i); }
@@ -631,6 +636,10 @@ static uint32_t mh_transition(const st_t* s, uint32_t last, draw_t* d) {
 
 /* random_positive, samplers.cpp:22-33 */
 static int random_positive(const st_t* s, draw_t* d, uint32_t* out) {
+    if (s->allpos && s->allpos[s->v]) {
+        *out = draw_index(d, s->n);
+        return 1;
+    }
     uint32_t positive = 0;
     for (uint32_t i = 0; i < s->n; ++i) if (st_w(s, i) > 0) ++positive;
     if (positive == 0) return 0;
@@ -849,10 +858,32 @@ void og_check(const og_graph* g, const og_model* m, uint64_t seed, uint64_t n_st
 
 enum { ST_EMPTY = 0, ST_READY = 2, ST_DEAD = 3 };
 
+/* Chain table: dense arrays indexed by slot (SamplerManager's layout), or a
+ * small open-addressing map of the slots one isolated walker touches
+ * (og_walk_isolated: a walker alone with a fresh manager). */
 typedef struct {
     uint8_t* status;
     uint32_t* last;
+    uint64_t* keys;  /* sparse: slot + 1, 0 = free */
+    uint32_t cap;    /* sparse capacity (power of two) */
+    const uint8_t* allpos;  /* st_t.allpos for the inits of this table (NULL: scan) */
 } chain_t;
+
+static uint32_t ch_at(chain_t* ch, uint64_t slot) {
+    if (!ch->keys) return (uint32_t)0;
+    uint32_t h = (uint32_t)((slot * 0x9E3779B97F4A7C15ULL) >> 40) & (ch->cap - 1);
+    for (;;) {
+        if (ch->keys[h] == slot + 1) return h;
+        if (ch->keys[h] == 0) {
+            ch->keys[h] = slot + 1;
+            ch->status[h] = ST_EMPTY;
+            return h;
+        }
+        h = (h + 1) & (ch->cap - 1);
+    }
+}
+static uint8_t* ch_status(chain_t* ch, uint64_t slot) { return ch->keys ? &ch->status[ch_at(ch, slot)] : &ch->status[slot]; }
+static uint32_t* ch_last(chain_t* ch, uint64_t slot) { return ch->keys ? &ch->last[ch_at(ch, slot)] : &ch->last[slot]; }
 
 typedef struct {
     uint32_t v, affix;
@@ -913,9 +944,9 @@ static uint32_t alias_draw(const double* prob, const uint32_t* alias, uint32_t n
 
 /* One next_edge of the alias / direct / rejection sampler. Philox layout:
  * direct -> unit of the walk block; alias -> index + unit of the walk block;
- * rejection trial t -> block (walker, step) of DOM_REJECT with sub-counter
- * t<<16 (index + unit of the proposal), then sub (t<<16)|0x8000 (the accept
- * unit). 1 stepped, 0 dead end, -1 error. */
+ * rejection trial t -> block (walker, step) under key DOM_REJECT + (t >> 16)
+ * with sub-counter (t & 0xFFFF) << 16 (index + unit of the proposal), then
+ * that sub | 0x8000 (the accept unit). 1 stepped, 0 dead end, -1 error. */
 static int baseline_step(const og_graph* g, const og_model* m, const og_config* c, baseline_t* bt,
                          const walker_t* w, uint32_t step, draw_t* d, uint32_t* edge, og_stats* st,
                          char* err, size_t errlen) {
@@ -960,17 +991,21 @@ static int baseline_step(const og_graph* g, const og_model* m, const og_config* 
             return -1;
         }
     }
-    uint32_t rkey[2];
-    og_philox_key(c->seed, DOM_REJECT, rkey);
-    for (uint32_t t = 0;; ++t) {
+    for (uint64_t t = 0;; ++t) {
+        /* trial epochs of 65536 trials under distinct keys DOM_REJECT + (t >> 16):
+         * the 16-bit trial field of the sub-counter never wraps onto an earlier
+         * trial's draws */
+        uint32_t rkey[2];
+        og_philox_key(c->seed, DOM_REJECT + (uint32_t)(t >> 16), rkey);
+        const uint32_t sub = (uint32_t)(t & 0xFFFFu) << 16;
         st->trials++;
         draw_t a;
-        draw_open_sub(&a, philox, d->xo, rkey, w->walker, step, t << 16);
+        draw_open_sub(&a, philox, d->xo, rkey, w->walker, step, sub);
         const uint32_t i = alias_draw(bt->pprob[v], bt->palias[v], deg, &a);
         const double accept = bt->wbuf[i] / (bt->bound * ws[i]);
         if (accept >= 1.0) { *edge = i; return 1; }
         draw_t b;
-        draw_open_sub(&b, philox, d->xo, rkey, w->walker, step, (t << 16) | 0x8000u);
+        draw_open_sub(&b, philox, d->xo, rkey, w->walker, step, sub | 0x8000u);
         if (draw_real(&b) < accept) { *edge = i; return 1; }
     }
 }
@@ -1000,8 +1035,10 @@ static int walker_step(const og_graph* g, const og_model* m, const og_config* c,
     } else {
         /* SamplerManager::sample, manager.cpp:30-72 */
         const uint64_t slot = engine_slot(g, m, rl, v, w->affix, w->walker);
-        st_t s = {g, m, v, w->affix, deg};
-        if (ch->status[slot] == ST_EMPTY) {
+        st_t s = {g, m, v, w->affix, deg, ch->allpos};
+        uint8_t* const status = ch_status(ch, slot);
+        uint32_t* const lastp = ch_last(ch, slot);
+        if (*status == ST_EMPTY) {
             init_src_t src;
             src.philox = philox;
             src.xo = &w->xo;
@@ -1010,18 +1047,18 @@ static int walker_step(const og_graph* g, const og_model* m, const og_config* c,
             uint32_t init;
             st->init_calls++;
             if (mh_init(&s, c, &src, &init)) {
-                ch->last[slot] = init;
-                ch->status[slot] = ST_READY;
+                *lastp = init;
+                *status = ST_READY;
             } else {
-                ch->status[slot] = ST_DEAD;
+                *status = ST_DEAD;
             }
         }
-        if (ch->status[slot] == ST_DEAD) return 0;
-        const uint32_t last = ch->last[slot];
+        if (*status == ST_DEAD) return 0;
+        const uint32_t last = *lastp;
         /* the philox block is (walker, step); xoshiro continues the stream */
         if (philox) draw_open(&d, 1, NULL, wkey, w->walker, step);
         const uint32_t next = mh_transition(&s, last, &d);
-        if (next != last) ch->last[slot] = next;
+        if (next != last) *lastp = next;
         edge = next;
     }
     const uint32_t nxt = g->nbr[g->offsets[v] + edge];
@@ -1045,15 +1082,10 @@ static int walker_step(const og_graph* g, const og_model* m, const og_config* c,
     return 1;
 }
 
-int og_generate_walks(const og_graph* g, const og_model* m, const og_config* c, uint32_t stride,
-                      uint32_t* rows, uint32_t* lens, uint64_t* n_rows, og_stats* stats,
-                      char* err, size_t errlen) {
-    memset(stats, 0, sizeof(*stats));
-    if (c->K == 0 || c->L == 0) {
-        snprintf(err, errlen, "walks_per_node, walk_length and threads must be positive");
-        return OG_ERR_INVALID;
-    }
-    if (stride < c->L + 1) { snprintf(err, errlen, "row stride too small"); return OG_ERR_INVALID; }
+/* Engine chain layout of a run: base slots plus hub replicas for node-keyed
+ * models (walk.cu session_create). Returns 0 when the layout is too large. */
+static int layout_init(const og_graph* g, const og_model* m, const og_config* c, replica_layout_t* out,
+                       uint64_t* slots_out) {
     uint64_t slots = og_slot_count(g, m);
     replica_layout_t rl;
     rl.D = c->replica_degree;
@@ -1093,14 +1125,36 @@ int og_generate_walks(const og_graph* g, const og_model* m, const og_config* c, 
         rl.D = OG_NO_REPLICAS;
     }
     if (slots > ((uint64_t)1 << 40)) {
-        snprintf(err, errlen, "sampler layout too large");
         free(rl.group);
         free(rl.scale);
+        return 0;
+    }
+    *out = rl;
+    *slots_out = slots;
+    return 1;
+}
+
+int og_generate_walks(const og_graph* g, const og_model* m, const og_config* c, uint32_t stride,
+                      uint32_t* rows, uint32_t* lens, uint64_t* n_rows, og_stats* stats,
+                      char* err, size_t errlen) {
+    memset(stats, 0, sizeof(*stats));
+    if (c->K == 0 || c->L == 0) {
+        snprintf(err, errlen, "walks_per_node, walk_length and threads must be positive");
+        return OG_ERR_INVALID;
+    }
+    if (stride < c->L + 1) { snprintf(err, errlen, "row stride too small"); return OG_ERR_INVALID; }
+    uint64_t slots = 0;
+    replica_layout_t rl;
+    if (!layout_init(g, m, c, &rl, &slots)) {
+        snprintf(err, errlen, "sampler layout too large");
         return OG_ERR_INVALID;
     }
     chain_t ch;
     ch.status = (uint8_t*)calloc(slots ? slots : 1, 1);
     ch.last = (uint32_t*)calloc(slots ? slots : 1, sizeof(uint32_t));
+    ch.keys = NULL;
+    ch.cap = 0;
+    ch.allpos = NULL;
     baseline_t bt;
     memset(&bt, 0, sizeof(bt));
     if (c->sampler != OG_SAMPLER_MH) {
@@ -1188,5 +1242,89 @@ int og_generate_walks(const og_graph* g, const og_model* m, const og_config* c, 
         free(bt.wbuf); free(bt.astat); free(bt.aprob); free(bt.aalias);
         free(bt.pstat); free(bt.pprob); free(bt.palias);
     }
+    return rc;
+}
+
+/* Each walker of `starts` (K walkers per start, walker id v*K + k) run ALONE
+ * with a fresh SamplerManager, walker-major, under the Philox layout: the
+ * corpus a GPU session restricted to that one start (mhw_session_select_starts,
+ * K = 1) must produce, whatever its kernel variant. Rows in start order. */
+int og_walk_isolated(const og_graph* g, const og_model* m, const og_config* cfg, uint64_t count,
+                     const uint32_t* starts, uint32_t stride, uint32_t* rows, uint32_t* lens, uint64_t* n_rows,
+                     og_stats* stats, char* err, size_t errlen) {
+    og_config cc = *cfg;
+    cc.rng = OG_RNG_PHILOX;
+    const og_config* c = &cc;
+    memset(stats, 0, sizeof(*stats));
+    if (c->K == 0 || c->L == 0) {
+        snprintf(err, errlen, "walks_per_node, walk_length and threads must be positive");
+        return OG_ERR_INVALID;
+    }
+    if (stride < c->L + 1) { snprintf(err, errlen, "row stride too small"); return OG_ERR_INVALID; }
+    if (c->sampler != OG_SAMPLER_MH) { snprintf(err, errlen, "isolated walkers: mh sampler only"); return OG_ERR_INVALID; }
+    uint64_t slots = 0;
+    replica_layout_t rl;
+    if (!layout_init(g, m, c, &rl, &slots)) {
+        snprintf(err, errlen, "sampler layout too large");
+        return OG_ERR_INVALID;
+    }
+    chain_t ch;
+    ch.cap = 1;
+    while (ch.cap < 4 * (c->L + 1)) ch.cap <<= 1;
+    ch.keys = (uint64_t*)malloc(ch.cap * sizeof(uint64_t));
+    ch.status = (uint8_t*)malloc(ch.cap);
+    ch.last = (uint32_t*)malloc(ch.cap * sizeof(uint32_t));
+    /* all-positive nodes (mhw_device.cuh all_positive): every static weight
+     * > 0, and a model that keeps w' > 0 (not metapath2vec; edge2vec only
+     * with a positive M) */
+    uint8_t* allpos = NULL;
+    int model_pos = m->kind != OG_METAPATH2VEC;
+    if (m->kind == OG_EDGE2VEC)
+        for (uint32_t i = 0; i < m->M_dim * m->M_dim; ++i) if (!(m->M[i] > 0)) model_pos = 0;
+    if (model_pos) {
+        allpos = (uint8_t*)malloc(g->n ? g->n : 1);
+        for (uint32_t v = 0; v < g->n; ++v) {
+            uint8_t ok = 1;
+            for (uint64_t a = g->offsets[v]; a < g->offsets[v + 1]; ++a) if (!(g->w[a] > 0)) { ok = 0; break; }
+            allpos[v] = ok;
+        }
+    }
+    ch.allpos = allpos;
+    int rc = OG_OK;
+    uint64_t row = 0;
+    for (uint64_t j = 0; j < count && rc == OG_OK; ++j) {
+        const uint32_t v = starts[j];
+        if (v >= g->n) { snprintf(err, errlen, "start node outside the graph"); rc = OG_ERR_INVALID; break; }
+        for (uint32_t k = 0; k < c->K && rc == OG_OK; ++k) {
+            walker_t w;
+            w.v = v;
+            w.walker = (uint64_t)v * c->K + k;
+            xo_walker(&w.xo, c->seed, w.v, k);
+            if (m->kind == OG_METAPATH2VEC) {
+                if (g->ntype[w.v] != m->metapath[0]) { stats->skipped++; continue; }
+                w.affix = 0;
+            } else {
+                w.affix = OG_NO_AFFIX;
+            }
+            memset(ch.keys, 0, ch.cap * sizeof(uint64_t));
+            w.row = row++;
+            rows[w.row * stride] = w.v;
+            w.len = 1;
+            for (uint32_t step = 0; step < c->L; ++step) {
+                const int r = walker_step(g, m, c, &ch, &rl, NULL, &w, step, stride, rows, stats, err, errlen);
+                if (r < 0) { rc = OG_ERR_INVALID; break; }
+                if (r == 0) { stats->early++; break; }
+            }
+            lens[w.row] = w.len;
+        }
+    }
+    stats->walks = row;
+    *n_rows = row;
+    free(ch.keys);
+    free(ch.status);
+    free(ch.last);
+    free(allpos);
+    free(rl.group);
+    free(rl.scale);
     return rc;
 }

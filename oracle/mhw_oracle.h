@@ -155,6 +155,13 @@ int og_generate_walks(const og_graph* g, const og_model* m, const og_config* c, 
                       uint32_t* rows, uint32_t* lens, uint64_t* n_rows, og_stats* stats,
                       char* err, size_t errlen);
 
+/* Every walker of the given starts (K each, walker id v*K + k) run alone with a
+ * fresh manager, walker-major, Philox layout (cfg->rng / order ignored). Rows:
+ * count*K x stride. */
+int og_walk_isolated(const og_graph* g, const og_model* m, const og_config* c, uint64_t count,
+                     const uint32_t* starts, uint32_t stride, uint32_t* rows, uint32_t* lens, uint64_t* n_rows,
+                     og_stats* stats, char* err, size_t errlen);
+
 #ifdef __cplusplus
 }
 #endif

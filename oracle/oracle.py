@@ -196,6 +196,9 @@ class Oracle:
         L.og_generate_walks.argtypes = [C.POINTER(_OgGraph), C.POINTER(_OgModel), C.POINTER(_OgConfig),
                                         C.c_uint32, _u32p, _u32p, _u64p, C.POINTER(_OgStats),
                                         C.c_char_p, C.c_size_t]
+        L.og_walk_isolated.argtypes = [C.POINTER(_OgGraph), C.POINTER(_OgModel), C.POINTER(_OgConfig), C.c_uint64,
+                                       _u32p, C.c_uint32, _u32p, _u32p, _u64p, C.POINTER(_OgStats), C.c_char_p,
+                                       C.c_size_t]
 
     # ---------------------------------------------------------------- rng
     def philox(self, ctr, key):
@@ -353,6 +356,29 @@ class Oracle:
         rc = self.lib.og_generate_walks(C.byref(gs), C.byref(ms), C.byref(c), stride,
                                         _ptr(rows, _u32p), _ptr(lens, _u32p), C.byref(nrows),
                                         C.byref(st), err, 512)
+        if rc:
+            raise OracleError(rc, err.value.decode())
+        k = nrows.value
+        stats = dict(walks=st.walks, early_terminations=st.early, skipped_starts=st.skipped,
+                     steps=st.steps, init_calls=st.init_calls, trials=st.trials)
+        return rows[:k], lens[:k], stats
+
+    def walk_isolated(self, g, md, cfg: WalkCfg, starts, stride=None):
+        """og_walk_isolated: each walker of `starts` (K per start, walker id
+        v*K + k) alone with a fresh manager, Philox layout, walker-major.
+        Returns (rows, lens, stats) like generate_walks."""
+        gs, ms, keep = self.bind(g, md)
+        c = self._cfg(cfg, RNG_PHILOX, ORDER_WALKER)
+        stride = stride or cfg.L + 1
+        st_ = np.ascontiguousarray(starts, dtype=np.uint32)
+        total = len(st_) * cfg.K
+        rows = np.zeros((max(total, 1), stride), dtype=np.uint32)
+        lens = np.zeros(max(total, 1), dtype=np.uint32)
+        nrows = C.c_uint64()
+        st = _OgStats()
+        err = C.create_string_buffer(512)
+        rc = self.lib.og_walk_isolated(C.byref(gs), C.byref(ms), C.byref(c), len(st_), _ptr(st_, _u32p), stride,
+                                       _ptr(rows, _u32p), _ptr(lens, _u32p), C.byref(nrows), C.byref(st), err, 512)
         if rc:
             raise OracleError(rc, err.value.decode())
         k = nrows.value

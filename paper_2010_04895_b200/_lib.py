@@ -27,7 +27,8 @@ class WalkConfigC(C.Structure):
     _fields_ = [("walks_per_node", C.c_uint32), ("walk_length", C.c_uint32), ("seed", C.c_uint64),
                 ("sampler", C.c_int32), ("init_kind", C.c_int32), ("burn_in_steps", C.c_uint32),
                 ("hw_sample_size", C.c_uint32), ("schedule", C.c_int32), ("node_begin", C.c_uint32),
-                ("node_end", C.c_uint32), ("chain_replica_degree", C.c_uint32), ("init_mode", C.c_int32)]
+                ("node_end", C.c_uint32), ("chain_replica_degree", C.c_uint32), ("init_mode", C.c_int32),
+                ("proposal", C.c_int32)]
 
 
 class WalkStatsC(C.Structure):
@@ -90,6 +91,7 @@ SIGNATURES = {
     "mhw_partition_nodes": (C.c_int32, [_P, C.POINTER(ModelDescC), C.c_int32, _P]),
     "mhw_session_create": (C.c_int32, [_P, C.POINTER(ModelDescC), C.POINTER(WalkConfigC), _PP]),
     "mhw_session_run": (C.c_int32, [_P, _P]),
+    "mhw_session_select_starts": (C.c_int32, [_P, C.c_uint32, _P]),
     "mhw_session_stats": (C.c_int32, [_P, C.POINTER(WalkStatsC)]),
     "mhw_session_buffers": (C.c_int32, [_P, _PP, _PP, C.POINTER(C.c_uint64), C.POINTER(C.c_uint32)]),
     "mhw_session_download": (C.c_int32, [_P, _P, _P, _P]),

@@ -81,7 +81,7 @@ void run_into(const mhw_graph* gc, const mhw_model_desc* model, const mhw_walk_c
     mhw::DeviceGuard dg(g->device);
     mhw_session s;
     mhw::session_create(s, *g, *model, *cfg);
-    if (nodes && s.rows > capacity) mhw::invalid("output buffer too small for the corpus");
+    if ((nodes || lens) && s.rows > capacity) mhw::invalid("output buffer too small for the corpus");
     mhw::session_run(s, nullptr);
     mhw_walk_stats st{};
     mhw::session_stats(s, st);
@@ -544,6 +544,13 @@ mhw_status mhw_session_run(mhw_session* s, void* stream) {
     return guard([&] {
         need(s, "session");
         mhw::session_run(*s, static_cast<cudaStream_t>(stream));
+    });
+}
+
+mhw_status mhw_session_select_starts(mhw_session* s, uint32_t count, const uint32_t* starts) {
+    return guard([&] {
+        need(s, "session");
+        mhw::session_select_starts(*s, count, starts);
     });
 }
 

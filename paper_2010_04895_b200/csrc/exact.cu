@@ -7,8 +7,10 @@
 //   direct    : unit of the walk block (walker, step)      -- samplers.cpp:133-146
 //   alias     : index + unit of the walk block, per-state tables built on
 //               first visit by the visiting warp            -- samplers.cpp:95-131
-//   rejection : trial t = DOM_REJECT block (walker, step), sub-counter t<<16
-//               (proposal index + unit), sub (t<<16)|0x8000 (accept unit);
+//   rejection : trial t = block (walker, step) under key DOM_REJECT + (t >> 16)
+//               (a fresh key every 65536 trials, so the streams never wrap),
+//               sub-counter (t & 0xFFFF) << 16 (proposal index + unit), sub
+//               ((t & 0xFFFF) << 16) | 0x8000 (accept unit);
 //               32 trials evaluated per warp round, the first accepted wins
 //                                                           -- samplers.cpp:148-170
 // They are comparison baselines (tools/mhwalk.cpp:298-429), not the product.
@@ -275,17 +277,21 @@ __global__ void __launch_bounds__(kExBlock) k_walk_exact(RunParams P, ExParams X
                 }
                 // The envelope target <= bound * w holds by construction
                 // (rejection_bound; M >= 0 is enforced by bind).
-                for (uint32_t t0 = 0;; t0 += 32) {
-                    const uint32_t t = t0 + lane;
+                for (uint64_t t0 = 0;; t0 += 32) {
+                    const uint64_t t = t0 + lane;
+                    // trial epochs of 65536 under distinct keys: the 16-bit
+                    // sub-counter field never wraps onto an earlier trial
+                    const uint2 tkey = make_uint2(rkey.x, rkey.y ^ DOM_REJECT ^ (DOM_REJECT + (uint32_t)(t >> 16)));
+                    const uint32_t sub = (uint32_t)(t & 0xFFFFu) << 16;
                     Draw a;
-                    a.open_sub(rkey, walker, step, t << 16);
+                    a.open_sub(tkey, walker, step, sub);
                     uint32_t i = a.index(c.deg);
                     if (!(a.unit() < __ldg(X.sprob + c.off + i))) i = __ldg(X.salias + c.off + i);
                     const double acc = __ddiv_rn(fw(i), __dmul_rn(X.bound, static_w(g, c.off + i)));
                     bool ok = acc >= 1.0;
                     if (!ok) {
                         Draw b;
-                        b.open_sub(rkey, walker, step, (t << 16) | 0x8000u);
+                        b.open_sub(tkey, walker, step, sub | 0x8000u);
                         ok = b.unit() < acc;
                     }
                     const unsigned bal = __ballot_sync(kFull, ok);

@@ -7,10 +7,12 @@
 //
 // Two schedules share the device functors of mhw_device.cuh:
 //  * throughput: one persistent kernel; each thread owns a walker for all L
-//    steps in registers; the chain table (one uint32 per state, HBM) is
-//    updated with CAS so every slot's chain is a linearisable sequential M-H
-//    chain (no lost updates); lazily initialised with slot-keyed
-//    randomness so racing initialisers agree.
+//    steps in registers; a state's chain word (one uint32 per state, HBM,
+//    colocated with the session arc records for second-order models) is taken
+//    as a lock with an atomic exchange for the whole transition, so every
+//    state runs an exact sequential M-H chain (no lost updates);
+//    slots are initialised eagerly or on first touch with slot-keyed
+//    randomness, so any initialiser computes the same word.
 //  * deterministic: step-synchronous; same-slot contenders are folded in
 //    walker-id order; byte-reproducible and equal to the CPU oracle's
 //    (philox, step-major) mode.
@@ -21,6 +23,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 
 #include "exact.h"
 #include "internal.h"
@@ -1048,12 +1051,13 @@ __global__ void k_state_degrees(DevGraph g, const uint32_t* __restrict__ pos, ui
         d[j] = j < n ? load_node(g, pos[j]).deg : 0;
 }
 
-// Session setup: classify start nodes of [b, e).
+// Session setup: classify start nodes of [b, e), or of the list ids[0, e - b)
+// when ids is given.
 __global__ void k_classify(DevGraph g, DevModel m, uint32_t b, uint32_t e, uint8_t* __restrict__ valid,
-                           uint8_t* __restrict__ act, uint8_t* __restrict__ iso) {
+                           uint8_t* __restrict__ act, uint8_t* __restrict__ iso, const uint32_t* __restrict__ ids = nullptr) {
     for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < (uint64_t)(e - b);
          t += (uint64_t)gridDim.x * blockDim.x) {
-        const NodeRec r = load_node(g, (uint32_t)(b + t));
+        const NodeRec r = load_node(g, ids ? ids[t] : (uint32_t)(b + t));
         const bool ok = m.kind != METAPATH2VEC || r.type == m.metapath[0];  // initial_state, models.cpp:138-144
         valid[t] = ok;
         act[t] = ok && r.deg > 0;
@@ -1067,11 +1071,17 @@ __global__ void k_iota_from(uint32_t* p, uint32_t n, uint32_t base) {
         p[i] = base + (uint32_t)i;
 }
 
-__global__ void k_rows_of(const uint32_t* __restrict__ nodes, uint32_t n, uint32_t b,
+// pos: positions in the start list (selected by flag); nodes[i] = ids[pos[i]],
+// rows[i] = first corpus row of that start (rank of its position among the
+// valid starts, times K).
+__global__ void k_rows_of(uint32_t* __restrict__ nodes, uint32_t n, const uint32_t* __restrict__ ids,
                           const uint32_t* __restrict__ rank, uint32_t K, uint64_t* __restrict__ rows) {
     for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-         i += (uint64_t)gridDim.x * blockDim.x)
-        rows[i] = (uint64_t)rank[nodes[i] - b] * K;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t p = nodes[i];
+        rows[i] = (uint64_t)rank[p] * K;
+        nodes[i] = ids[p];
+    }
 }
 
 int sms() {
@@ -1086,10 +1096,11 @@ unsigned grid_for(uint64_t work, int block = 256) {
     return (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(g, (uint64_t)sms() * 16));
 }
 
-// Register-cap variant of the walk kernel (occupancy vs spills trade-off,
-// measured in profiles/); MHW_WALK_REGS selects it at session creation.
-// Defaults from the sweep in profiles/: deepwalk 80 (4.84 vs 5.27 ms on cfg1),
-// second-order models uncapped (no spills; 65.7 vs 69-71 ms on cfg2).
+// Register-cap variant of the walk kernel (occupancy vs spills trade-off);
+// MHW_WALK_REGS selects it at session creation. Defaults from the A/B runs of
+// scripts/exp_regs.sh: deepwalk 80; node2vec uncapped
+// (a 64-register cap, 4 blocks/SM: cfg2 36.8 vs 34.6 ms, no spills either way);
+// eagerly initialised edge2vec / fairwalk 80.
 int walk_minb(int kind, bool eager) {
     const char* e = std::getenv("MHW_WALK_REGS");
     // deepwalk: 80; eagerly initialised edge2vec / fairwalk: 80 (84-86 -> 80
@@ -1224,13 +1235,103 @@ void model_bind(Model& mb, Graph& g, const mhw_model_desc& d) {
 }
 
 // ------------------------------------------------------------- sessions
+// The persisting-L2 set-aside is a device-wide limit: the first session that
+// raises it saves the previous value, the last one to go restores it and
+// resets the persisting lines (nothing may outlive the sessions).
+namespace {
+std::mutex g_l2_mu;
+int g_l2_users[64] = {};
+size_t g_l2_saved[64] = {};
+
+void l2_limit_acquire(int dev, size_t bytes) {
+    std::lock_guard<std::mutex> lk(g_l2_mu);
+    size_t cur = 0;
+    MHW_CK(cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize));
+    if (g_l2_users[dev & 63]++ == 0) g_l2_saved[dev & 63] = cur;
+    if (cur < bytes) MHW_CK(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, bytes));
+}
+
+void l2_limit_release(int dev) {
+    std::lock_guard<std::mutex> lk(g_l2_mu);
+    if (g_l2_users[dev & 63] == 0 || --g_l2_users[dev & 63] != 0) return;
+    cudaCtxResetPersistingL2Cache();
+    cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, g_l2_saved[dev & 63]);
+}
+}  // namespace
+
 Session::~Session() {
+    if (l2_pin && g) {
+        DeviceGuard dg(g->device);
+        l2_limit_release(g->device);
+    }
     if (ev0) cudaEventDestroy(ev0);
+    if (evm) cudaEventDestroy(evm);
     if (ev1) cudaEventDestroy(ev1);
     if (stream) cudaStreamDestroy(stream);
 }
 
 static std::vector<double> metapath_rep_scale(const std::vector<uint16_t>& mp, const Graph& g, cudaStream_t st);
+
+// Start-node lists of a session: the valid starts among ids[0, span) (device
+// list, ascending) in list order (initial_state, models.cpp:138-144), split
+// into active (degree > 0) and isolated starts, with their first corpus
+// rows; rows, skipped and n_items follow (engine.cpp:187-191).
+static void session_classify_starts(Session& s, const uint32_t* d_ids, uint32_t span) {
+    cudaStream_t st = s.stream;
+    const DevGraph gv = s.g->view();
+    uint32_t n_valid = 0;
+    s.n_act = s.n_iso = 0;
+    if (span) {
+        DBuf<uint8_t> valid(span), act(span), iso(span);
+        DBuf<uint32_t> rank(span + 1), pos(span);
+        k_classify<<<grid_for(span), 256, 0, st>>>(gv, s.model.dev, 0, span, valid.p, act.p, iso.p, d_ids);
+        k_iota_from<<<grid_for(span), 256, 0, st>>>(pos.p, span, 0);
+        MHW_CK(cudaGetLastError());
+        size_t bytes = 0;
+        MHW_CK(cub::DeviceScan::ExclusiveSum(nullptr, bytes, valid.p, rank.p, (int64_t)span, st));
+        DBuf<uint8_t> temp(std::max<size_t>(bytes, 1));
+        MHW_CK(cub::DeviceScan::ExclusiveSum(temp.p, bytes, valid.p, rank.p, (int64_t)span, st));
+        uint32_t last_rank = 0;
+        uint8_t last_valid = 0;
+        MHW_CK(cudaMemcpyAsync(&last_rank, rank.p + span - 1, 4, cudaMemcpyDeviceToHost, st));
+        MHW_CK(cudaMemcpyAsync(&last_valid, valid.p + span - 1, 1, cudaMemcpyDeviceToHost, st));
+        MHW_CK(cudaStreamSynchronize(st));
+        n_valid = last_rank + last_valid;
+        if (s.act.n < span) s.act.alloc(span);
+        if (s.iso.n < span) s.iso.alloc(span);
+        select_flagged(pos.p, act.p, s.act.p, span, &s.n_act, st);
+        select_flagged(pos.p, iso.p, s.iso.p, span, &s.n_iso, st);
+        if (s.act_row.n < std::max<uint32_t>(s.n_act, 1)) s.act_row.alloc(std::max<uint32_t>(s.n_act, 1));
+        if (s.iso_row.n < std::max<uint32_t>(s.n_iso, 1)) s.iso_row.alloc(std::max<uint32_t>(s.n_iso, 1));
+        if (s.n_act) k_rows_of<<<grid_for(s.n_act), 256, 0, st>>>(s.act.p, s.n_act, d_ids, rank.p, s.cfg.K, s.act_row.p);
+        if (s.n_iso) k_rows_of<<<grid_for(s.n_iso), 256, 0, st>>>(s.iso.p, s.n_iso, d_ids, rank.p, s.cfg.K, s.iso_row.p);
+        MHW_CK(cudaGetLastError());
+        MHW_CK(cudaStreamSynchronize(st));
+    }
+    s.rows = (uint64_t)n_valid * s.cfg.K;
+    s.skipped = (uint64_t)(span - n_valid) * s.cfg.K;
+    s.n_items = (uint64_t)s.n_act * s.cfg.K;
+}
+
+void session_select_starts(Session& s, uint32_t count, const uint32_t* starts) {
+    DeviceGuard dg(s.g->device);
+    if (count && !starts) invalid("starts must not be NULL");
+    for (uint32_t i = 0; i < count; ++i) {
+        if (starts[i] < s.node_begin || starts[i] >= s.node_end) invalid("start node outside the session's node range");
+        if (i && starts[i] <= starts[i - 1]) invalid("start nodes must be strictly ascending");
+    }
+    DBuf<uint32_t> ids(std::max<uint32_t>(count, 1));
+    if (count) MHW_CK(cudaMemcpyAsync(ids.p, starts, count * 4ull, cudaMemcpyHostToDevice, s.stream));
+    if (!count && !starts) {  // back to the whole node range
+        const uint32_t span = s.node_end - s.node_begin;
+        ids.alloc(std::max<uint32_t>(span, 1));
+        if (span) k_iota_from<<<grid_for(span), 256, 0, s.stream>>>(ids.p, span, s.node_begin);
+        MHW_CK(cudaGetLastError());
+        count = span;
+    }
+    session_classify_starts(s, ids.p, count);
+    if (s.rows > s.rows_cap || s.n_items > s.items_cap) invalid("start selection larger than the session");
+}
 
 void session_create(Session& s, Graph& g, const mhw_model_desc& md, const mhw_walk_config& wc) {
     DeviceGuard dg(g.device);
@@ -1259,6 +1360,7 @@ void session_create(Session& s, Graph& g, const mhw_model_desc& md, const mhw_wa
     s.stride = (wc.walk_length + 1 + 3) & ~3u;
     MHW_CK(cudaStreamCreateWithFlags(&s.stream, cudaStreamNonBlocking));
     MHW_CK(cudaEventCreate(&s.ev0));
+    MHW_CK(cudaEventCreate(&s.evm));
     MHW_CK(cudaEventCreate(&s.ev1));
     cudaStream_t st = s.stream;
     // slot layout (manager.cpp:14-21): base slots, then hub replicas for
@@ -1338,38 +1440,15 @@ void session_create(Session& s, Graph& g, const mhw_model_desc& md, const mhw_wa
         }
     }
     if (s.slots > (uint64_t(1) << 40)) invalid("sampler layout too large: " + std::to_string(s.slots) + " slots");
-    const uint32_t span = s.node_end - s.node_begin;
-    DBuf<uint8_t> valid(std::max<uint32_t>(span, 1)), act(std::max<uint32_t>(span, 1)), iso(std::max<uint32_t>(span, 1));
-    DBuf<uint32_t> rank(std::max<uint32_t>(span, 1) + 1), ids(std::max<uint32_t>(span, 1));
-    const DevGraph gv = g.view();
-    uint32_t n_valid = 0;
-    if (span) {
-        k_classify<<<grid_for(span), 256, 0, st>>>(gv, m, s.node_begin, s.node_end, valid.p, act.p, iso.p);
-        k_iota_from<<<grid_for(span), 256, 0, st>>>(ids.p, span, s.node_begin);
+    {
+        const uint32_t span = s.node_end - s.node_begin;
+        DBuf<uint32_t> ids(std::max<uint32_t>(span, 1));
+        if (span) k_iota_from<<<grid_for(span), 256, 0, st>>>(ids.p, span, s.node_begin);
         MHW_CK(cudaGetLastError());
-        size_t bytes = 0;
-        MHW_CK(cub::DeviceScan::ExclusiveSum(nullptr, bytes, valid.p, rank.p, (int64_t)span, st));
-        DBuf<uint8_t> temp(std::max<size_t>(bytes, 1));
-        MHW_CK(cub::DeviceScan::ExclusiveSum(temp.p, bytes, valid.p, rank.p, (int64_t)span, st));
-        uint32_t last_rank = 0;
-        uint8_t last_valid = 0;
-        MHW_CK(cudaMemcpyAsync(&last_rank, rank.p + span - 1, 4, cudaMemcpyDeviceToHost, st));
-        MHW_CK(cudaMemcpyAsync(&last_valid, valid.p + span - 1, 1, cudaMemcpyDeviceToHost, st));
-        MHW_CK(cudaStreamSynchronize(st));
-        n_valid = last_rank + last_valid;
-        s.act.alloc(span);
-        s.iso.alloc(span);
-        select_flagged(ids.p, act.p, s.act.p, span, &s.n_act, st);
-        select_flagged(ids.p, iso.p, s.iso.p, span, &s.n_iso, st);
-        s.act_row.alloc(std::max<uint32_t>(s.n_act, 1));
-        s.iso_row.alloc(std::max<uint32_t>(s.n_iso, 1));
-        if (s.n_act) k_rows_of<<<grid_for(s.n_act), 256, 0, st>>>(s.act.p, s.n_act, s.node_begin, rank.p, s.cfg.K, s.act_row.p);
-        if (s.n_iso) k_rows_of<<<grid_for(s.n_iso), 256, 0, st>>>(s.iso.p, s.n_iso, s.node_begin, rank.p, s.cfg.K, s.iso_row.p);
-        MHW_CK(cudaGetLastError());
+        session_classify_starts(s, ids.p, span);
     }
-    s.rows = (uint64_t)n_valid * s.cfg.K;
-    s.skipped = (uint64_t)(span - n_valid) * s.cfg.K;
-    s.n_items = (uint64_t)s.n_act * s.cfg.K;
+    s.rows_cap = s.rows;
+    s.items_cap = s.n_items;
     s.out.alloc(std::max<uint64_t>(s.rows * s.stride, 4));
     s.lens.alloc(std::max<uint64_t>(s.rows, 1));
     s.ctr.alloc(8);
@@ -1442,10 +1521,8 @@ void session_create(Session& s, Graph& g, const mhw_model_desc& md, const mhw_wa
             int dev = 0, max_persist = 0;
             MHW_CK(cudaGetDevice(&dev));
             MHW_CK(cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, dev));
-            size_t cur = 0;
-            MHW_CK(cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize));
             if ((size_t)max_persist >= bytes) {
-                if (cur < bytes) MHW_CK(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, bytes));
+                l2_limit_acquire(dev, bytes);
                 s.l2_pin = true;
                 s.pin_p = p;
                 s.pin_bytes = bytes;
@@ -1487,8 +1564,19 @@ void session_create(Session& s, Graph& g, const mhw_model_desc& md, const mhw_wa
     if (trace) std::fprintf(stderr, "[mhw] session_create: model_bind %.2f ms, total %.2f ms\n", t_bind, tms());
 }
 
-// Persisting L2 access window over [p, p + bytes) on stream st (bytes 0
-// clears it). The device's persisting set-aside is raised once to fit.
+// Persisting L2 access window over [p, p + bytes) on stream st. The caller's
+// own window on that stream is saved by l2_window_save and put back by
+// l2_window_restore after the session's launches.
+static cudaStreamAttrValue l2_window_save(cudaStream_t st) {
+    cudaStreamAttrValue prev{};
+    MHW_CK(cudaStreamGetAttribute(st, cudaStreamAttributeAccessPolicyWindow, &prev));
+    return prev;
+}
+
+static void l2_window_restore(cudaStream_t st, const cudaStreamAttrValue& prev) {
+    MHW_CK(cudaStreamSetAttribute(st, cudaStreamAttributeAccessPolicyWindow, &prev));
+}
+
 static void l2_window(cudaStream_t st, void* p, size_t bytes) {
     cudaStreamAttrValue attr{};
     attr.accessPolicyWindow.base_ptr = p;
@@ -1568,7 +1656,11 @@ void session_run(Session& s, cudaStream_t user) {
     // A small edge filter is pinned in L2 for the walk (persisting access
     // window on the launch stream, cleared again after the launches).
     const bool pin = s.l2_pin;
-    if (pin) l2_window(st, s.pin_p, s.pin_bytes);
+    cudaStreamAttrValue prev_window{};
+    if (pin) {
+        prev_window = l2_window_save(st);
+        l2_window(st, s.pin_p, s.pin_bytes);
+    }
     const bool preloaded = s.chain_loaded;  // mhw_session_load_chain: table already initialised
     s.chain_loaded = false;
     if (!preloaded) MHW_CK(cudaMemsetAsync(s.chain.p, 0xFF, s.chain.bytes(), st));
@@ -1583,6 +1675,7 @@ void session_run(Session& s, cudaStream_t user) {
         ++s.launches;
     }
     MHW_CK(cudaEventRecord(s.ev0, st));
+    bool evm_done = false;
     if (s.n_items) {
         if (s.ex) {
             exact_launch(s, P, st);
@@ -1627,6 +1720,8 @@ void session_run(Session& s, cudaStream_t user) {
                         ++s.launches;
                     }
                 }
+                MHW_CK(cudaEventRecord(s.evm, st));
+                evm_done = true;
                 with_variant<KIND>(s.minb, !s.eager_init, s.ar_mode(), [&](auto rg, auto lz, auto ar) {
                     k_walk<KIND, decltype(rg)::value, decltype(lz)::value, decltype(ar)::value>
                         <<<s.grid, kWalkBlock, 0, st>>>(P);
@@ -1636,7 +1731,8 @@ void session_run(Session& s, cudaStream_t user) {
         }
         MHW_CK(cudaGetLastError());
     }
-    if (pin) l2_window(st, nullptr, 0);
+    if (!evm_done) MHW_CK(cudaEventRecord(s.evm, st));  // init fused into the walk (lazy / deterministic)
+    if (pin) l2_window_restore(st, prev_window);
     MHW_CK(cudaEventRecord(s.ev1, st));
 }
 
@@ -1746,8 +1842,9 @@ void session_stats(Session& s, mhw_walk_stats& out) {
         invalid("second-order walk on asymmetric adjacency: no back edge " + std::to_string(from) + "->" +
                 std::to_string(to));
     }
-    float ms = 0.f;
+    float ms = 0.f, ms_init = 0.f;
     MHW_CK(cudaEventElapsedTime(&ms, s.ev0, s.ev1));
+    MHW_CK(cudaEventElapsedTime(&ms_init, s.ev0, s.evm));
     out.walks = s.rows;
     out.early_terminations = h[2] + (uint64_t)s.n_iso * s.cfg.K;
     out.skipped_starts = s.skipped;
@@ -1755,8 +1852,12 @@ void session_stats(Session& s, mhw_walk_stats& out) {
     out.slot_inits = h[3];
     out.chain_retries = h[6];
     out.rejection_trials = h[7];
-    out.walk_seconds = ms * 1e-3;
-    out.init_seconds = 0.0;
+    // T_i / T_w (manager.cpp:39-44, engine.cpp:228-232): device time of the
+    // eager chain-table init launch and of the walk kernels; a lazy run
+    // initialises inside the walk (T_i = 0, as the reference's T_w then holds
+    // it too). steps_per_sec counts both, like engine.cpp:231-232.
+    out.init_seconds = ms_init * 1e-3;
+    out.walk_seconds = (ms - ms_init) * 1e-3;
     out.steps_per_sec = ms > 0 ? (double)h[1] / (ms * 1e-3) : 0.0;
 }
 
@@ -1866,25 +1967,30 @@ void session_run_packed(Session& s, uint32_t* h_nodes, uint64_t cap_nodes, uint6
         size_t scan_bytes = 0;
         MHW_CK(cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, len64.p, goff.p, (int64_t)s.rows + 1, S));
         DBuf<uint8_t> scan_tmp(std::max<size_t>(scan_bytes, 1));
-        // sampler reset + isolated rows + eager init (as session_run)
+        // sampler reset + isolated rows + eager init (as session_run); a table
+        // installed with mhw_session_load_chain / _load_records is used as is
         RunParams P = s.params();
-        MHW_CK(cudaMemsetAsync(s.chain.p, 0xFF, s.chain.bytes(), S));
+        const bool preloaded = s.chain_loaded;
+        s.chain_loaded = false;
+        if (!preloaded) MHW_CK(cudaMemsetAsync(s.chain.p, 0xFF, s.chain.bytes(), S));
         MHW_CK(cudaMemsetAsync(s.ctr.p, 0, s.ctr.bytes(), S));
-        if (s.ac.n && second_order(s.model.dev.kind) && (!s.eager_init || !s.g->verified_sym))
+        if (!preloaded && s.ac.n && second_order(s.model.dev.kind) && (!s.eager_init || !s.g->verified_sym))
             k_ac_reset<<<grid_for(s.g->m), 256, 0, S>>>(reinterpret_cast<uint32_t*>(s.ac.p), s.g->m, s.rec_u32);
         if (s.n_iso)
             k_iso_rows<<<grid_for((uint64_t)s.n_iso * s.cfg.K), 256, 0, S>>>(s.iso.p, s.iso_row.p, s.n_iso, s.cfg.K,
                                                                              s.out.p, s.stride, s.lens.p);
         const bool pin = s.l2_pin;
+        const cudaStreamAttrValue prev_window = pin ? l2_window_save(S) : cudaStreamAttrValue{};
         if (pin) l2_window(S, s.pin_p, s.pin_bytes);
         MHW_CK(cudaEventRecord(s.ev0, S));
         const double t_setup = ms_since(ta);
         dispatch(s.model.dev.kind, [&](auto kc) {
             constexpr int KIND = decltype(kc)::value;
             if constexpr (second_order(KIND)) {
-                if (s.eager_init) launch_init_all<KIND>(s, P, S);
+                if (s.eager_init && !preloaded) launch_init_all<KIND>(s, P, S);
             }
         });
+        MHW_CK(cudaEventRecord(s.evm, S));
         uint64_t H = 0;
         auto issue_copy = [&](int c) {
             MHW_CK(cudaEventSynchronize(ev[c]));
@@ -1924,7 +2030,7 @@ void session_run_packed(Session& s, uint32_t* h_nodes, uint64_t cap_nodes, uint6
             // copy chunk c - 1 while chunk c walks
             if (c >= 1) issue_copy(c - 1);
         }
-        if (pin) l2_window(S, nullptr, 0);
+        if (pin) l2_window_restore(S, prev_window);
         MHW_CK(cudaEventRecord(s.ev1, S));
         MHW_CK(cudaGetLastError());
         issue_copy(chunks - 1);

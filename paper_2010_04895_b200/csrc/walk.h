@@ -52,6 +52,7 @@ struct Session {
     DBuf<uint64_t> act_row, iso_row;
     uint32_t n_act = 0, n_iso = 0;
     uint64_t n_items = 0, rows = 0, skipped = 0, slots = 0;
+    uint64_t rows_cap = 0, items_cap = 0;  // sizes the buffers were made for (start selections must fit)
     uint32_t stride = 0;
     DBuf<uint32_t> chain, out, lens, rep_group;
     DBuf<double> rep_scale;  // metapath2vec replica weights per node type
@@ -76,7 +77,8 @@ struct Session {
     int minb = 1;
     uint32_t launches = 0;
     cudaStream_t stream = nullptr;
-    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    // ev0 -> evm: eager chain-table init (T_i); evm -> ev1: the walk kernels (T_w)
+    cudaEvent_t ev0 = nullptr, evm = nullptr, ev1 = nullptr;
 
     Session() = default;
     Session(const Session&) = delete;
@@ -89,6 +91,9 @@ struct Session {
 uint64_t k_slots(int kind, const Graph& g);
 void session_create(Session& s, Graph& g, const mhw_model_desc& md, const mhw_walk_config& wc);
 void session_run(Session& s, cudaStream_t stream);
+// Restricts the next runs to the given (ascending) start nodes of the session's
+// range; count 0 with starts NULL restores the whole range.
+void session_select_starts(Session& s, uint32_t count, const uint32_t* starts);
 void walk_rows(Graph& g, const mhw_model_desc& md, const mhw_walk_config& wc, uint64_t* rows, uint32_t* stride);
 void session_init_chain(Session& s, uint64_t begin, uint64_t end, uint32_t* d_words, cudaStream_t stream,
                         bool rec_order = false);

@@ -154,6 +154,7 @@ class WalkConfig:
     node_end: int = 0
     chain_replica_degree: int = 0      # 0: auto; 0xFFFFFFFF: one chain per state
     init_mode: int = 0                 # 0 auto, 1 lazy, 2 eager
+    proposal: int = 0                  # 0 uniform (samplers.hpp:21), 1 static-weight alias + Hastings
 
     def _c(self):
         c = L.WalkConfigC()
@@ -169,6 +170,7 @@ class WalkConfig:
         c.schedule = int(sched)
         c.node_begin, c.node_end = self.node_begin, self.node_end
         c.chain_replica_degree, c.init_mode = self.chain_replica_degree, self.init_mode
+        c.proposal = int(self.proposal)
         return c
 
 
@@ -514,6 +516,19 @@ class Session:
 
     def run(self, stream: int | None = None):
         _check(L.lib().mhw_session_run(self._h, C.c_void_p(stream) if stream else None))
+
+    def select_starts(self, starts=None):
+        """Restrict the next runs to these (ascending) start nodes; None = the
+        whole node range (mhw_session_select_starts)."""
+        if starts is None:
+            _check(L.lib().mhw_session_select_starts(self._h, 0, None))
+        else:
+            a = np.ascontiguousarray(starts, dtype=np.uint32)
+            _check(L.lib().mhw_session_select_starts(self._h, len(a), _ptr(a) if len(a) else None))
+        rows, stride = C.c_uint64(), C.c_uint32()
+        dn, dl = C.c_void_p(), C.c_void_p()
+        _check(L.lib().mhw_session_buffers(self._h, C.byref(dn), C.byref(dl), C.byref(rows), C.byref(stride)))
+        self.rows = rows.value
 
     def stats(self) -> RunStats:
         st = L.WalkStatsC()

@@ -132,3 +132,130 @@ def gate(pvals: np.ndarray, alpha=0.01, family=1e-4):
     binom = st.binom.sf(low - 1, n, alpha) if low else 1.0
     ok = pvals.min() >= family / n and fisher >= family and binom >= family
     return ok, f"n={n} min={pvals.min():.2e} fisher={fisher:.2e} low={low} binom={binom:.2e}"
+
+
+def lumped_chi2(counts: np.ndarray, pi: np.ndarray) -> tuple[float, int, float]:
+    """The chain-CLT chi-square after lumping candidates of equal target
+    weight. Under the uniform-proposal kernel, P(i -> class B) =
+    (|B| / m) min(1, pi_B / pi_i) is the same for every i of a class A, so the
+    class sequence is itself an exact Markov chain (strong lumpability) and the
+    test needs a matrix of (distinct weights) x (distinct weights) only --
+    3 x 3 for unweighted node2vec however large the hub. Zero-weight
+    candidates are proposed (m = all candidates) and never accepted."""
+    m = len(pi)
+    if counts[pi <= 0].sum() > 0:
+        return float("inf"), 0, 0.0
+    vals, inv = np.unique(pi[pi > 0], return_inverse=True)
+    c = np.bincount(inv, weights=counts[pi > 0].astype(np.float64), minlength=len(vals))
+    size = np.bincount(inv, minlength=len(vals)).astype(np.float64)
+    k = len(vals)
+    if k < 2:
+        return 0.0, 0, 1.0
+    Pi = size * vals
+    Pi = Pi / Pi.sum()
+    P = np.zeros((k, k))
+    for a in range(k):
+        P[a] = size / m * np.minimum(1.0, vals / vals[a])
+        P[a, a] = 0.0
+        P[a, a] = 1.0 - P[a].sum()
+    Z = np.linalg.inv(np.eye(k) - P + np.outer(np.ones(k), Pi))
+    D = np.diag(Pi)
+    S = D @ Z + Z.T @ D - D - np.outer(Pi, Pi)
+    N = c.sum()
+    d = c / N - Pi
+    stat = float(N * d @ np.linalg.pinv(S, rcond=1e-10, hermitian=True) @ d)
+    return stat, k - 1, float(st.chi2.sf(stat, k - 1))
+
+
+def transition_counts_gpu(rows, lens, kind, offsets, nbr, metapath=None, min_visits=5000, max_states=40,
+                          max_support=None, max_classes=None, pi_classes=None):
+    """Per-state next-node counts of a (large) corpus, counted on the GPU
+    with torch (test infrastructure only). States as `transitions`: deepwalk
+    v; metapath2vec (v, required type); second order the arc (v -> prev),
+    i.e. state (prev, v) with affix = index of prev in N(v). Returns a list of
+    (v, affix, visits, counts over N(v)) for the `max_states` most visited
+    states with >= min_visits visits (and degree <= max_support if given)."""
+    import torch
+    dev = torch.device("cuda")
+    off = torch.from_numpy(np.asarray(offsets, dtype=np.int64)).to(dev)
+    n = off.numel() - 1
+    deg = off[1:] - off[:-1]
+    src = torch.repeat_interleave(torch.arange(n, device=dev, dtype=torch.int64), deg)
+    arckey = (src << 32) | torch.from_numpy(np.asarray(nbr, dtype=np.int64)).to(dev)
+    del src
+    R = torch.from_numpy(np.ascontiguousarray(rows).view(np.int32)).to(dev)
+    Ln = torch.from_numpy(np.asarray(lens, dtype=np.int64)).to(dev)
+    S = R.shape[1]
+    second = kind in (O.NODE2VEC, O.EDGE2VEC, O.FAIRWALK)
+    first_col = 1 if second else 0
+    cols = torch.arange(first_col, S - 1, device=dev)
+    valid = (cols[None, :] + 1) < Ln[:, None]
+    cur = R[:, first_col:S - 1][valid].long()
+    nxt = R[:, first_col + 1:S][valid].long()
+    if second:
+        prev = R[:, first_col - 1:S - 2][valid].long()
+        sid = torch.searchsorted(arckey, (cur << 32) | prev)
+        n_states = arckey.numel()
+    elif kind == O.METAPATH2VEC:
+        T = int(max(metapath)) + 1
+        req = np.zeros(S, dtype=np.int64)
+        a = 0
+        for i in range(S):
+            req[i] = metapath[_next(a, metapath)]
+            a = _next(a, metapath)
+        reqc = torch.from_numpy(req).to(dev)[cols]
+        sid = cur * T + reqc[None, :].expand_as(valid)[valid]
+        n_states = n * T
+    else:
+        sid = cur
+        n_states = n
+    del R
+    visits = torch.bincount(sid, minlength=n_states)
+    # node of each state and its support
+    if second:
+        node = torch.arange(n_states, device=dev)
+        node = torch.searchsorted(off[1:], node, right=True)
+    elif kind == O.METAPATH2VEC:
+        node = torch.arange(n_states, device=dev) // T
+    else:
+        node = torch.arange(n_states, device=dev)
+    ok = visits >= min_visits
+    if max_support is not None:
+        ok &= deg[node] <= max_support
+    cand = torch.nonzero(ok).flatten()
+    order = torch.argsort(visits[cand], descending=True)[:max_states]
+    chosen = cand[order]
+    flag = torch.full((n_states,), -1, dtype=torch.int64, device=dev)
+    flag[chosen] = torch.arange(chosen.numel(), device=dev)
+    sel = flag[sid]
+    m = sel >= 0
+    cell = torch.searchsorted(arckey, (cur[m] << 32) | nxt[m])
+    cnt = torch.bincount(cell, minlength=arckey.numel())
+    out = []
+    offs = np.asarray(offsets, dtype=np.int64)
+    for st_id, vis in zip(chosen.tolist(), visits[chosen].tolist()):
+        v = int(node[st_id])
+        if second:
+            aff = int(st_id - offs[v])
+        elif kind == O.METAPATH2VEC:
+            r = st_id % T
+            aff = next(a for a in range(len(metapath)) if metapath[_next(a, metapath)] == r)
+        else:
+            aff = O.NO_AFFIX
+        out.append((v, aff, vis, cnt[offs[v]:offs[v + 1]].cpu().numpy()))
+    return out
+
+
+def audit_counts(g: O.HostGraph, oracle: O.Oracle, md: O.ModelDesc, states, dense_max=1024):
+    """p-values of the chain chi-square of (v, affix, visits, counts) states:
+    the full test up to dense_max candidates, the lumped (equal target weight)
+    test beyond, where the distinct weights are few."""
+    pv = []
+    for v, aff, vis, counts in states:
+        pi = O.eval_target(g, oracle, md, v, aff)
+        assert counts.sum() == vis
+        if len(pi) <= dense_max:
+            pv.append(markov_chi2(counts, pi)[2])
+        else:
+            pv.append(lumped_chi2(counts, pi)[2])
+    return np.array(pv)

@@ -46,3 +46,26 @@ def test_exact_samplers_hit_the_exact_target(oracle, sampler):
     freq = np.array([(nxt == 0).mean(), (nxt == 1).mean()])
     assert sel.sum() > 3000
     assert np.allclose(freq, target, atol=0.03)
+
+
+def low_acceptance_graph():
+    """Triangle whose every arc has edge type 0 while edge2vec's M[0][0] is
+    1e-6 of the envelope: a rejection step needs ~10^6 trials, far past the
+    65536 trials one sub-counter epoch holds (the trial field of the
+    sub-counter used to wrap and replay earlier trials forever)."""
+    g = O.triangle()
+    g.ntype, g.n_ntypes = np.zeros(3, dtype=np.uint16), 1
+    g.etype, g.n_etypes = np.zeros(6, dtype=np.uint16), 2
+    md = model_desc(O.EDGE2VEC, g, p=1.0, q=1.0, M=np.array([[1e-6, 1.0], [1.0, 1.0]]))
+    return g, md
+
+
+def test_rejection_streams_do_not_wrap(oracle):
+    g, md = low_acceptance_graph()
+    cfg = O.WalkCfg(K=1, L=3, seed=11, sampler=O.SAMPLER_REJECTION)
+    rows, lens, st = oracle.generate_walks(g, md, cfg, rng=O.RNG_PHILOX, order=O.ORDER_STEP)
+    assert st["steps"] == 9 and st["trials"] > 6 * 65536
+    # every emitted node is a neighbour: the walk terminated normally
+    for r in range(3):
+        w = rows[r, :lens[r]]
+        assert all(int(b) in g.neighbors_of(int(a)) for a, b in zip(w[:-1], w[1:]))

@@ -75,3 +75,15 @@ def test_alias_memory_guard(mhw):
     cfg = mhw.WalkConfig(walks_per_node=1, walk_length=4, threads=8, sampler_kind=mhw.SamplerKind.alias)
     with pytest.raises(mhw.ValidationError, match="alias tables need"):
         mhw.generate_walks(g, m, cfg)
+
+
+def test_rejection_past_one_trial_epoch_equals_oracle(mhw, oracle):
+    """~10^6 rejection trials per step (acceptance 1e-6): the GPU's warp rounds
+    cross many 65536-trial key epochs and still equal the oracle's draws."""
+    from tests.test_exact_samplers_cpu import low_acceptance_graph
+    g, md = low_acceptance_graph()
+    cfg = O.WalkCfg(K=1, L=3, seed=11, sampler=O.SAMPLER_REJECTION)
+    orow, olen, ost = oracle.generate_walks(g, md, cfg, rng=O.RNG_PHILOX, order=O.ORDER_STEP)
+    c = mhw.generate_walks(device_graph(g), walk_model(md), walk_config(cfg, threads=8))
+    assert corpus_equal(orow, olen, c.rows, c.lengths)
+    assert c.stats.rejection_trials == ost["trials"] > 6 * 65536

@@ -53,3 +53,43 @@ def test_oracle_corpus_passes_gate(oracle, kind):
     pv = audit(g, oracle, md, rows, lens, min_visits=5000)
     ok, msg = gate(pv)
     assert ok, msg
+
+
+def _uniform_proposal_chain(pi_w, steps, r, m=None):
+    """An exact uniform-proposal M-H chain (samplers.hpp:18-27) over
+    unnormalised weights pi_w, simulated directly."""
+    m = m or len(pi_w)
+    x = int(np.argmax(pi_w > 0))
+    counts = np.zeros(len(pi_w))
+    cand = r.integers(0, m, steps)
+    u = r.random(steps)
+    for c, uu in zip(cand, u):
+        if pi_w[x] <= 0 or pi_w[c] >= pi_w[x] or uu * pi_w[x] < pi_w[c]:
+            x = int(c)
+        counts[x] += 1
+    return counts
+
+
+def test_lumped_chi2_is_calibrated_and_has_power():
+    """The lumped (equal-weight classes) chain chi-square used for hub states:
+    p-values of exact chains are not small, a 10% mis-weighted class is
+    caught, and it agrees with the full test where both apply."""
+    from tests.stats import lumped_chi2
+    r = np.random.default_rng(7)
+    w = np.concatenate([np.full(1, 4.0), np.full(40, 1.0), np.full(400, 0.25), np.zeros(9)])  # node2vec-like classes
+    pi = w / w.sum()
+    pvals = [lumped_chi2(_uniform_proposal_chain(w, 60000, r), pi)[2] for _ in range(12)]
+    assert min(pvals) > 1e-3
+    counts = _uniform_proposal_chain(w, 200000, r)
+    wrong = w.copy()
+    wrong[1:41] *= 1.10
+    assert lumped_chi2(counts, wrong / wrong.sum())[2] < 1e-6
+    assert lumped_chi2(counts, pi)[2] > 1e-4
+    # a zero-weight candidate in the output fails outright
+    bad = counts.copy()
+    bad[-1] += 1
+    assert lumped_chi2(bad, pi)[2] == 0.0
+    # small support: same verdict as the full test
+    w2 = np.array([1.0, 1.0, 2.0, 2.0, 3.0])
+    c2 = _uniform_proposal_chain(w2, 100000, r)
+    assert lumped_chi2(c2, w2 / w2.sum())[2] > 1e-3 and markov_chi2(c2, w2 / w2.sum())[2] > 1e-3
