@@ -443,6 +443,10 @@ class RefLib:
         L.ref_walk_sample.argtypes = [C.c_void_p, C.c_void_p, C.c_uint32, C.c_uint32, C.c_uint32,
                                       C.c_uint64, C.c_int, C.c_uint32, C.c_uint32, C.c_uint64,
                                       C.c_uint64, C.c_uint64, _u64p, _dp]
+        L.ref_run_new.argtypes = [C.c_void_p, C.c_void_p, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint64,
+                                  C.c_int, C.c_uint32, C.c_uint32, C.POINTER(C.c_void_p)]
+        L.ref_run_free.argtypes = [C.c_void_p]
+        L.ref_run_slice.argtypes = [C.c_void_p, C.c_uint32, C.c_uint32, _u64p, _dp]
 
     def _check(self, rc):
         if rc:
@@ -560,6 +564,34 @@ class _RefModel:
         self.g.ref._check(rc)
         return dict(walks=int(st[0]), early_terminations=int(st[1]), skipped_starts=int(st[2]),
                     steps=int(st[3]), seconds=float(tm[0]), init_seconds=float(tm[1]))
+
+    def full_run(self, cfg: WalkCfg, threads):
+        """One generate_walks-equivalent run over ALL walkers with one shared
+        SamplerManager, executed in time slices (ref_run_slice)."""
+        return _RefRun(self, cfg, threads)
+
+
+class _RefRun:
+    def __init__(self, m: _RefModel, cfg: WalkCfg, threads):
+        self.m = m
+        L = m.g.ref.lib
+        h = C.c_void_p()
+        m.g.ref._check(L.ref_run_new(m.g.h, m.h, cfg.K, cfg.L, threads, cfg.seed, cfg.init_kind,
+                                     cfg.burn_in_steps, cfg.hw_sample_size, C.byref(h)))
+        self.h = h.value
+
+    def slice(self, i, n):
+        st = np.zeros(4, dtype=np.uint64)
+        tm = np.zeros(2)
+        self.m.g.ref._check(self.m.g.ref.lib.ref_run_slice(self.h, i, n, _ptr(st, _u64p), _ptr(tm, _dp)))
+        return dict(walks=int(st[0]), early_terminations=int(st[1]), skipped_starts=int(st[2]),
+                    steps=int(st[3]), seconds=float(tm[0]), init_seconds=float(tm[1]))
+
+    def __del__(self):
+        try:
+            self.m.g.ref.lib.ref_run_free(self.h)
+        except Exception:
+            pass
 
 
 # ------------------------------------------------------------ test graphs

@@ -283,4 +283,111 @@ int ref_walk_sample(void* gp, void* mp, uint32_t K, uint32_t L, uint32_t threads
     });
 }
 
+// ---- the CPU reference arm over the FULL workload, in K time slices.
+// One generate_walks call (engine.cpp:157-234) = one SamplerManager over all
+// walkers, thread t owning walkers [T*t/threads, T*(t+1)/threads). A run
+// handle keeps that manager (and the partition) alive across calls, and call
+// i runs slice i of every thread's block: thread t walks
+// [b_t + (e_t-b_t)*i/S, b_t + (e_t-b_t)*(i+1)/S). After all S slices every
+// walker has walked exactly once against one shared manager, so the summed
+// time is a full run's (lazy init amortised exactly as in generate_walks);
+// each slice is a bounded step of it. The worker body is the engine loop
+// (engine.cpp:186-205) over the public APIs, walks kept per thread as the
+// engine keeps them (released after the slice, outside the timing).
+struct RefRun {
+    const Graph* g;
+    const WalkModel* m;
+    SamplerManager manager;
+    InitStrategy init;
+    uint32_t K, L, threads;
+    uint64_t seed;
+    RefRun(const Graph& gg, const WalkModel& mm) : g(&gg), m(&mm), manager(gg, mm) {}
+};
+
+int ref_run_new(void* gp, void* mp, uint32_t K, uint32_t L, uint32_t threads, uint64_t seed, int init_kind,
+                uint32_t burn_in, uint32_t hw, void** out) {
+    return guarded([&] {
+        if (K == 0 || L == 0 || threads == 0)
+            throw ValidationError("walks_per_node, walk_length and threads must be positive");
+        auto* r = new RefRun(*static_cast<Graph*>(gp), static_cast<RefModel*>(mp)->model);
+        r->init.kind = static_cast<InitStrategy::Kind>(init_kind);
+        r->init.burn_in_steps = burn_in;
+        r->init.hw_sample_size = hw;
+        r->K = K;
+        r->L = L;
+        r->seed = seed;
+        const uint64_t total = static_cast<uint64_t>(r->g->node_count()) * K;
+        r->threads = static_cast<uint32_t>(std::min<uint64_t>(threads, std::max<uint64_t>(total, 1)));
+        *out = r;
+    });
+}
+
+void ref_run_free(void* h) { delete static_cast<RefRun*>(h); }
+
+int ref_run_slice(void* h, uint32_t slice, uint32_t slices, uint64_t* stats, double* times) {
+    return guarded([&] {
+        RefRun& R = *static_cast<RefRun*>(h);
+        const Graph& g = *R.g;
+        const WalkModel& m = *R.m;
+        const uint64_t total = static_cast<uint64_t>(g.node_count()) * R.K;
+        const uint32_t T = R.threads;
+        std::vector<uint64_t> steps(T, 0), walks(T, 0), early(T, 0), skipped(T, 0);
+        std::vector<std::vector<std::vector<NodeId>>> outs(T);
+        const double init0 = R.manager.init_seconds();
+        const auto t0 = std::chrono::steady_clock::now();
+        auto worker = [&](uint32_t t) {
+            const uint64_t tb = total * t / T, te = total * (t + 1) / T;
+            const uint64_t b = tb + (te - tb) * slice / slices, e = tb + (te - tb) * (slice + 1) / slices;
+            for (uint64_t idx = b; idx < e; ++idx) {
+                const NodeId v = static_cast<NodeId>(idx / R.K);
+                Rng rng = walker_stream(R.seed, v, static_cast<uint32_t>(idx % R.K));
+                auto state = m.initial_state(g, v);
+                if (!state) {
+                    ++skipped[t];
+                    continue;
+                }
+                std::vector<NodeId> walk;
+                walk.reserve(R.L + 1);
+                walk.push_back(v);
+                for (uint32_t step = 0; step < R.L; ++step) {
+                    const uint32_t deg = g.degree(state->position);
+                    std::optional<uint32_t> edge;
+                    if (deg == 0) {
+                        edge = std::nullopt;
+                    } else if (m.second_order() && state->affixture == kNoAffix) {
+                        auto w = g.weights_of(state->position);
+                        if (std::accumulate(w.begin(), w.end(), 0.0) <= 0) edge = std::nullopt;
+                        else edge = direct_sample(w, rng);
+                    } else {
+                        edge = R.manager.sample(*state, R.init, rng);
+                    }
+                    if (!edge) {
+                        ++early[t];
+                        break;
+                    }
+                    const EdgeRef chosen{state->position, *edge};
+                    walk.push_back(g.neighbor(chosen.source, chosen.neighbor_index));
+                    *state = m.update_state(g, *state, chosen);
+                    ++steps[t];
+                }
+                outs[t].push_back(std::move(walk));
+                ++walks[t];
+            }
+        };
+        std::vector<std::thread> pool;
+        for (uint32_t t = 0; t < T; ++t) pool.emplace_back(worker, t);
+        for (auto& th : pool) th.join();
+        const auto t1 = std::chrono::steady_clock::now();
+        stats[0] = stats[1] = stats[2] = stats[3] = 0;
+        for (uint32_t t = 0; t < T; ++t) {
+            stats[0] += walks[t];
+            stats[1] += early[t];
+            stats[2] += skipped[t];
+            stats[3] += steps[t];
+        }
+        times[0] = std::chrono::duration<double>(t1 - t0).count();
+        times[1] = R.manager.init_seconds() - init0;
+    });
+}
+
 }  // extern "C"

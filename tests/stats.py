@@ -176,7 +176,7 @@ def transition_counts_gpu(rows, lens, kind, offsets, nbr, metapath=None, min_vis
     (v, affix, visits, counts over N(v)) for the `max_states` most visited
     states with >= min_visits visits (and degree <= max_support if given)."""
     import torch
-    dev = torch.device("cuda")
+    dev = torch.device("cuda" if torch.cuda.is_available() else "cpu")
     off = torch.from_numpy(np.asarray(offsets, dtype=np.int64)).to(dev)
     n = off.numel() - 1
     deg = off[1:] - off[:-1]
@@ -229,11 +229,15 @@ def transition_counts_gpu(rows, lens, kind, offsets, nbr, metapath=None, min_vis
     flag[chosen] = torch.arange(chosen.numel(), device=dev)
     sel = flag[sid]
     m = sel >= 0
-    cell = torch.searchsorted(arckey, (cur[m] << 32) | nxt[m])
-    cnt = torch.bincount(cell, minlength=arckey.numel())
+    # counts per (chosen state, candidate index): several chosen states can
+    # share a node v (second order: (s1, v) and (s2, v)), so the cell is keyed
+    # by the state as well as by the arc v -> next
+    cell = torch.searchsorted(arckey, (cur[m] << 32) | nxt[m]) - off[cur[m]]
+    dmax = int(deg[node[chosen]].max()) if chosen.numel() else 1
+    cnt = torch.bincount(sel[m] * dmax + cell, minlength=max(1, chosen.numel() * dmax))
     out = []
     offs = np.asarray(offsets, dtype=np.int64)
-    for st_id, vis in zip(chosen.tolist(), visits[chosen].tolist()):
+    for i, (st_id, vis) in enumerate(zip(chosen.tolist(), visits[chosen].tolist())):
         v = int(node[st_id])
         if second:
             aff = int(st_id - offs[v])
@@ -242,7 +246,7 @@ def transition_counts_gpu(rows, lens, kind, offsets, nbr, metapath=None, min_vis
             aff = next(a for a in range(len(metapath)) if metapath[_next(a, metapath)] == r)
         else:
             aff = O.NO_AFFIX
-        out.append((v, aff, vis, cnt[offs[v]:offs[v + 1]].cpu().numpy()))
+        out.append((v, aff, vis, cnt[i * dmax:i * dmax + int(offs[v + 1] - offs[v])].cpu().numpy()))
     return out
 
 

@@ -77,17 +77,23 @@ def test_full_corpus_chain_chi_square(mhw, oracle, cfg_name):
         assert sum(hg.ntype[v] == 2 for v, *_ in states) >= 10
 
 
-def pick_start(hg, cfg, lo, hi, max_support):
-    """A start of degree in [lo, hi] whose neighbours mostly have <= max_support
-    neighbours (weighted graphs: the audited states (s, v) need a dense test)."""
+def pick_start(hg, cfg, lo, hi, max_support, need=24):
+    """A start of degree in [lo, hi] with the most neighbours of degree <=
+    max_support (weighted graphs: the audited states (s, v) need a dense
+    test), at least `need` of them (R-MAT neighbours are mostly hubs)."""
     deg = np.diff(hg.offsets.astype(np.int64))
     cands = np.nonzero((deg >= lo) & (deg <= hi))[0]
     r = np.random.default_rng(3)
-    for v in r.permutation(cands)[:2000]:
+    best, best_n = None, -1
+    for v in r.permutation(cands)[:4000]:
         nb = hg.neighbors_of(int(v)).astype(np.int64)
-        if np.mean(deg[nb] <= max_support) >= 0.9:
-            return int(v)
-    raise AssertionError("no start node found")
+        k = int(np.sum(deg[nb] <= max_support))
+        if k > best_n:
+            best, best_n = int(v), k
+        if k >= 0.9 * len(nb):
+            break
+    assert best_n >= need, f"no start node found (best has {best_n} light neighbours)"
+    return best
 
 
 @pytest.mark.parametrize("cfg_name,deg_lo,deg_hi,max_support,walkers_per_arc", [

@@ -74,3 +74,28 @@ def test_model_bind_errors_match(oracle, ref):
         with pytest.raises(O.OracleError) as e2:
             ref.graph(g).model(md)
         assert e1.value.code == e2.value.code == 2
+
+
+@pytest.mark.parametrize("kind", KINDS)
+@pytest.mark.parametrize("threads", [1, 3])
+def test_sliced_full_run_equals_generate_walks(ref, kind, threads):
+    """bench.py --impl reference: one full run in time slices over one shared
+    SamplerManager (ref_run_slice) walks every walker exactly once with the
+    generate_walks partition, so its counts equal generate_walks' (and with one
+    thread, where the run is deterministic, every slot sees the same chain)."""
+    rng = O.XoRng(3000 + kind)
+    g = O.random_graph(90, 5.0, True, rng)
+    O.assign_random_types(g, 2, rng)
+    md = model_desc(kind, g, p=0.5, q=2.0, metapath=(0, 1, 0))
+    cfg = O.WalkCfg(K=3, L=12, seed=5, init_kind=O.INIT_BURN_IN, burn_in_steps=4)
+    rm = ref.graph(g).model(md)
+    _, _, rs = rm.generate_walks(cfg, threads=threads, n_nodes=g.n, with_rows=False)
+    run = rm.full_run(cfg, threads)
+    tot = dict(walks=0, early_terminations=0, skipped_starts=0, steps=0)
+    for i in range(5):
+        st = run.slice(i, 5)
+        for k in tot:
+            tot[k] += st[k]
+    assert tot["walks"] == rs["walks"] and tot["skipped_starts"] == rs["skipped_starts"]
+    if threads == 1:
+        assert tot["steps"] == rs["steps"] and tot["early_terminations"] == rs["early_terminations"]

@@ -93,3 +93,35 @@ def test_lumped_chi2_is_calibrated_and_has_power():
     w2 = np.array([1.0, 1.0, 2.0, 2.0, 3.0])
     c2 = _uniform_proposal_chain(w2, 100000, r)
     assert lumped_chi2(c2, w2 / w2.sum())[2] > 1e-3 and markov_chi2(c2, w2 / w2.sum())[2] > 1e-3
+
+
+@pytest.mark.parametrize("kind", [O.DEEPWALK, O.NODE2VEC, O.METAPATH2VEC, O.FAIRWALK])
+def test_transition_counts_gpu_equals_transitions(oracle, kind):
+    """The torch counter used on BASELINE-size corpora (run here on the CPU)
+    equals the pure-Python per-state counts, including several audited
+    states that share one node v (second order: (s1, v), (s2, v))."""
+    from tests.stats import transition_counts_gpu, transitions
+    rng = O.XoRng(55)
+    g = O.random_graph(12, 3.0, True, rng)
+    O.assign_random_types(g, 2, rng)
+    md = model_desc(kind, g, p=0.5, q=2.0, metapath=(0, 1, 0))
+    cfg = O.WalkCfg(K=300, L=20, seed=3)
+    rows, lens, _ = oracle.generate_walks(g, md, cfg)
+    states = transition_counts_gpu(rows, lens, kind, g.offsets, g.nbr, metapath=md.metapath,
+                                   min_visits=50, max_states=25)
+    ref = transitions(rows, lens, kind, md.metapath)
+    assert len(states) >= 5
+    nodes = [v for v, *_ in states]
+    if kind in (O.NODE2VEC, O.FAIRWALK):
+        assert len(set(nodes)) < len(nodes)  # shared nodes are exercised
+    for v, aff, vis, counts in states:
+        nb = g.neighbors_of(v)
+        if kind == O.DEEPWALK:
+            key = v
+        elif kind == O.METAPATH2VEC:
+            key = (v, int(md.metapath[aff + 1 if aff + 1 < len(md.metapath) else 1]))
+        else:
+            key = (int(nb[aff]), v)
+        exp = np.array([ref[key].get(int(u), 0) for u in nb])
+        assert counts.sum() == vis == exp.sum()
+        assert np.array_equal(counts, exp)
