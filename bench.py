@@ -463,28 +463,47 @@ def run_mine(args, cfg):
         t_job, steps_job, launches_job = t_local, float(steps_total), launches
     value = steps_job / t_job
 
-    # ---- roofline of the walk kernel (algorithmic sectors)
+    # ---- roofline of the walk kernel. frac: the kernel's measured DRAM bytes
+    # per launch (ncu, profiles/traffic_<cfg>.json, same kernel variant) over
+    # its live CUDA-event time, against the measured HBM copy bandwidth.
+    # canonical: SURVEY 8(d)'s algorithmic sectors of the REFERENCE algorithm
+    # (three binary searches per node2vec step); this design replaces those
+    # searches (edge filter, hash sets, reverse index), so that figure exceeds
+    # the bandwidth and is kept only for comparison. random: DRAM line fills
+    # per second (128-B lines) against the measured random-access ceiling
+    # (profiles/randbench_r01.md: 42-45 G independent random loads/s).
     off = g.download()["offsets"] if rank == 0 else None
     line = None
     if rank == 0:
         deg = np.diff(off)
         S, es = canonical_sectors(cfg, deg)
         peak, peak_kind = hbm_peak()
-        per_launch_bytes = S * 32 * st.steps
-        achieved = per_launch_bytes / (kernel_ms * 1e-3) / 1e9
-        traffic = None
+        t_k = kernel_ms * 1e-3
+        canon = S * 32 * st.steps / t_k / 1e9
+        tr = {}
         prof = os.path.join(ROOT, "profiles", f"traffic_{cfg['name']}.json")
         if os.path.exists(prof):
             with open(prof) as f:
-                traffic = json.load(f).get("dram_bytes_per_launch")
-        roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                "traffic": traffic, "peak_source": peak_kind, "sectors_per_step": S, "E_sigma": es,
-                "kernel": "k_walk<%s>" % cfg["model"] + (
-                    " + eager chain init (k_init_all / k_init_rec)"
-                    if cfg["model"] in ("node2vec", "edge2vec", "fairwalk") and st.slot_inits >= info["arc_count"]
-                    else ""),
-                "kernel_ms": kernel_ms,
-                "kernel_ms_note": "device time of one generate_walks' walk kernels (CUDA events on the launch stream)"}
+                tr = json.load(f)
+        traffic = tr.get("dram_bytes_per_launch")
+        achieved = traffic / t_k / 1e9 if traffic else None
+        rd = tr.get("dram_read_bytes_per_launch")
+        RAND_CEIL = 43e9
+        roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak if achieved else None, "traffic": traffic,
+                "traffic_source": (os.path.relpath(prof, ROOT) + f" (ncu --set full, tree {tr.get('tree')}, "
+                                   f"{tr.get('ncu_ms')} ms under ncu)") if traffic else None,
+                "peak_source": peak_kind,
+                "dram_bytes_per_step": traffic / st.steps if traffic else None,
+                "random": {"read_lines_per_s": rd / 128 / t_k, "ceiling_per_s": RAND_CEIL,
+                           "frac": rd / 128 / t_k / RAND_CEIL} if rd else None,
+                "canonical": {"sectors_per_step": S, "E_sigma": es, "achieved": canon, "frac": canon / peak,
+                              "note": "SURVEY 8(d) reference-algorithm sectors (3 binary searches per step), "
+                                      "not this kernel's traffic"},
+                "kernel": "k_walk<%s>" % cfg["model"], "kernel_ms": kernel_ms,
+                "init_ms": st.init_seconds * 1e3,
+                "kernel_ms_note": "device time of one generate_walks' walk kernel (CUDA events on the launch "
+                                  "stream, T_w); eager chain init (k_init_all / k_init_rec) is init_ms (T_i)"}
         if cfg.get("sampler", "mh") != "mh":
             roof = None  # the canonical sector count is the M-H path's
         line = {
@@ -501,6 +520,9 @@ def run_mine(args, cfg):
                        "parallelism": f"walker ranges x{world}, CSR replicated"
                                       + (", chain init sharded + all-gather" if shard_init else "")},
             "roofline": roof, "clocks": clk.summary(), "gpu_launches": launches_job,
+            "T_i_ms": st.init_seconds * 1e3, "T_w_ms": kernel_ms,
+            "T_note": "per generate_walks (engine.cpp:228-232 split): T_i = eager chain-table init (k_init_all / "
+                      "k_init_rec; 0 when init is lazy, fused into the walk), T_w = the walk kernel",
             "setup_seconds": t_setup,
         }
     # ---- e2e through the public C ABI with host buffers

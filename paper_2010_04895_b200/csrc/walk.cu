@@ -61,6 +61,37 @@ __device__ __forceinline__ uint4 atom_exch128(uint4* p, uint4 v) {
     return make_uint4((uint32_t)rlo, (uint32_t)(rlo >> 32), (uint32_t)rhi, (uint32_t)(rhi >> 32));
 }
 
+// Compact chain words (AR = 3, node2vec): one 16-bit word per state, two
+// per 32-bit word, so the table of a scale-20 graph (31.4 M states, 63 MB)
+// stays in L2 and the lock/release traffic never reaches DRAM (the 32-bit
+// words colocated in the arc records dirty one record sector per step,
+// written back: cfg2 19.4 GB per launch). Encoding, by the state's degree
+// deg(v): deg < 2^14: Last index | alpha class << 14; otherwise the Last index
+// alone (class recomputed from the Last's id when needed). 0xFFFF = locked
+// (every bit set, so an atomicOr takes the lock and returns the word),
+// 0xFFFE = dead end. Requires deg(v) <= 0xFFFD and eager initialisation.
+constexpr uint32_t kC16Locked = 0xFFFFu, kC16Dead = 0xFFFEu, kC16ClsDeg = 1u << 14;
+
+__host__ __device__ __forceinline__ uint32_t c16_enc(uint32_t e, uint32_t deg) {
+    if (e >= kLocked) return kC16Dead;  // kDead (kEmpty: a record no state uses)
+    const uint32_t idx = e & kIdxMask;
+    return deg < kC16ClsDeg ? (idx | ((e >> 30) << 14)) : idx;
+}
+// 32-bit chain word of a 16-bit one; class 3 = not stored (hub states)
+__device__ __forceinline__ uint32_t c16_dec(uint32_t e16, uint32_t deg) {
+    if (e16 == kC16Locked) return kLocked;
+    if (e16 == kC16Dead) return kDead;
+    return deg < kC16ClsDeg ? ((e16 & 0x3FFFu) | ((e16 >> 14) << 30)) : (e16 | (3u << 30));
+}
+__device__ __forceinline__ uint32_t c16_take(uint32_t* w, uint32_t sh, uint32_t deg) {
+    return c16_dec((atomicOr(w, kC16Locked << sh) >> sh) & 0xFFFFu, deg);
+}
+// our half holds 0xFFFF while locked: AND-ing leaves the new word there and
+// the neighbouring state's half untouched
+__device__ __forceinline__ void c16_release(uint32_t* w, uint32_t sh, uint32_t e16) {
+    atomicAnd(w, ~(kC16Locked << sh) | (e16 << sh));
+}
+
 __device__ __forceinline__ void fail_back_edge(unsigned long long* ctr, uint32_t from, uint32_t to) {
     if (atomicCAS(&ctr[4], 0ull, 1ull) == 0ull) ctr[5] = ((unsigned long long)from << 32) | to;
 }
@@ -91,6 +122,8 @@ __global__ void __launch_bounds__(kWalkBlock) __maxnreg__(REGS) k_walk(RunParams
     constexpr bool TYPED = AR && needs_utype<KIND>();
     constexpr bool CC = AR && second_order(KIND);
     constexpr bool NARROW = AR == 2;
+    constexpr bool C16 = AR == 3;  // ids + compact 16-bit chain table (node2vec)
+    static_assert(!C16 || (KIND == NODE2VEC && !LAZY), "compact chains: eagerly initialised node2vec");
     // typed second-order records carry w'(Last) next to the chain word
     // (word 1 = {type | etype << 16, chain word, w'(Last) as f64}), taken and
     // released with one 16-byte exchange: the decision needs no load of the
@@ -99,6 +132,11 @@ __global__ void __launch_bounds__(kWalkBlock) __maxnreg__(REGS) k_walk(RunParams
     constexpr uint32_t RS = TYPED ? 2u : 1u;  // uint4 words per record (wide layouts)
     const uint4* const arcs = (AR && KIND != DEEPWALK) ? P.ac : g.arc;
     auto load_rec = [&](uint64_t arc, uint4& b) {
+        if constexpr (C16) {
+            const uint32_t u = __ldg(g.ids + arc);
+            const NodeRec r = load_node(g, u);
+            return make_uint4(u, r.deg | ((r.flags & NF_ALLPOS) ? 0x80000000u : 0u), (uint32_t)r.off, 0u);
+        }
         if constexpr (NARROW) {
             const uint2 x = __ldg(reinterpret_cast<const uint2*>(P.ac) + arc);
             const NodeRec r = load_node(g, x.x);
@@ -195,15 +233,19 @@ __global__ void __launch_bounds__(kWalkBlock) __maxnreg__(REGS) k_walk(RunParams
                 // (its timing cannot depend on the proposal); the candidate
                 // evaluation overlaps its latency, and the chain state it
                 // returns is only consumed by the decision.
-                uint32_t* const cw = (!CC || WLC) ? P.chain + slot
-                                                  : (NARROW ? reinterpret_cast<uint32_t*>(P.ac) + 2 * loc + 1
-                                                            : reinterpret_cast<uint32_t*>(P.ac + RS * loc) + 3);
+                uint32_t* const cw = C16 ? P.c16 + (loc >> 1)
+                                         : ((!CC || WLC) ? P.chain + slot
+                                                         : (NARROW ? reinterpret_cast<uint32_t*>(P.ac) + 2 * loc + 1
+                                                                   : reinterpret_cast<uint32_t*>(P.ac + RS * loc) + 3));
+                const uint32_t csh = C16 ? ((uint32_t)loc & 1u) << 4 : 0u;
                 uint4* const cb = WLC ? P.ac + 2 * loc + 1 : nullptr;
                 uint4 E = make_uint4(0, 0, 0, 0);
                 uint32_t e;
                 if (WLC) {
                     E = atom_exch128(cb, make_uint4(tx, kLocked, 0u, 0u));
                     e = E.y;
+                } else if (C16) {
+                    e = c16_take(cw, csh, c.deg);
                 } else {
                     e = atomicExch(cw, kLocked);
                 }
@@ -227,19 +269,23 @@ __global__ void __launch_bounds__(kWalkBlock) __maxnreg__(REGS) k_walk(RunParams
                 int pre_bloom = -1;
                 uint2 xl = make_uint2(0, 0);
                 bool spec_l = false;
-                if constexpr (NARROW) {
+                if constexpr (NARROW || C16) {
                     // The edge-filter probe needs only the candidate id: it is
                     // computed and issued before the candidate's node record is
                     // consumed, so the two L2 accesses overlap instead of
                     // running back to back.
-                    const uint2 x = __ldg(reinterpret_cast<const uint2*>(P.ac) + c.off + cand);
+                    const uint2 x = C16 ? make_uint2(__ldg(g.ids + c.off + cand), 0u)
+                                        : __ldg(reinterpret_cast<const uint2*>(P.ac) + c.off + cand);
                     // A Last of the heaviest alpha class is rejected away from
                     // most of the time (cfg2: the return class, 1/p = 4): fetch
                     // its record now, beside the candidate's, instead of after
                     // the decision (cfg2 34.6 -> 34.3 ms; speculating on every
                     // Last heavier than the lightest class: 35.4).
-                    if (e < kLocked && (e >> 30) == P.m.spec_cls) {
-                        xl = __ldg(reinterpret_cast<const uint2*>(P.ac) + c.off + (e & kIdxMask));
+                    // (compact chains of hub states hold no class: the Last's
+                    // id is needed for it anyway)
+                    if (e < kLocked && ((e >> 30) == P.m.spec_cls || (C16 && (e >> 30) == 3u))) {
+                        xl = C16 ? make_uint2(__ldg(g.ids + c.off + (e & kIdxMask)), 0u)
+                                 : __ldg(reinterpret_cast<const uint2*>(P.ac) + c.off + (e & kIdxMask));
                         spec_l = true;
                     }
                     uc = x.x;
@@ -291,6 +337,8 @@ __global__ void __launch_bounds__(kWalkBlock) __maxnreg__(REGS) k_walk(RunParams
                         if (WLC) {
                             E = atom_exch128(cb, make_uint4(tx, kLocked, 0u, 0u));
                             e = E.y;
+                        } else if (C16) {
+                            e = c16_take(cw, csh, c.deg);
                         } else {
                             e = atomicExch(cw, kLocked);
                         }
@@ -312,11 +360,22 @@ __global__ void __launch_bounds__(kWalkBlock) __maxnreg__(REGS) k_walk(RunParams
                 }
                 if (e == kDead) {
                     if (WLC) atom_exch128(cb, make_uint4(tx, kDead, 0u, 0u));
+                    else if (C16) c16_release(cw, csh, kC16Dead);
                     else chain_release(cw, kDead);
                     dead = true;
                     break;
                 }
-                const uint32_t last = e & kIdxMask, cls_l = e >> 30;
+                const uint32_t last = e & kIdxMask;
+                uint32_t cls_l = e >> 30;
+                if (C16 && cls_l == 3u) {
+                    // hub state: the word holds no class; alpha(s, Last) from
+                    // the Last's id (a pure function of (state, Last), as cached)
+                    if (!spec_l) {
+                        xl = make_uint2(__ldg(g.ids + c.off + last), 0u);
+                        spec_l = true;
+                    }
+                    cls_l = alpha_class(g, P.m, c, xl.x, nullptr);
+                }
                 // The last sample's id and record are fetched before the
                 // decision where w'(last) needs its type anyway, and for
                 // deepwalk (cheap, L2-resident graphs; measured win). For
@@ -346,6 +405,8 @@ __global__ void __launch_bounds__(kWalkBlock) __maxnreg__(REGS) k_walk(RunParams
                     atom_exch128(cb, acc ? make_uint4(tx, pack_entry(cand, cls_c), (uint32_t)__double2loint(wc),
                                                       (uint32_t)__double2hiint(wc))
                                          : make_uint4(tx, e, E.z, E.w));
+                else if (C16)
+                    c16_release(cw, csh, c16_enc(acc ? pack_entry(cand, cls_c) : e, c.deg));
                 else
                     chain_release(cw, acc ? pack_entry(cand, cls_c) : e);
                 chosen = acc ? cand : last;
@@ -358,7 +419,7 @@ __global__ void __launch_bounds__(kWalkBlock) __maxnreg__(REGS) k_walk(RunParams
                     } else if (kSpec) {
                         an = al;
                         bn = bl;
-                    } else if (NARROW && spec_l && (e & kIdxMask) == last) {
+                    } else if ((NARROW || C16) && spec_l && (e & kIdxMask) == last) {
                         const NodeRec r = load_node(g, xl.x);
                         an = make_uint4(xl.x, r.deg | ((r.flags & NF_ALLPOS) ? 0x80000000u : 0u), (uint32_t)r.off, xl.y);
                     } else {
@@ -466,7 +527,12 @@ __global__ void __launch_bounds__(256, KIND == NODE2VEC ? 8 : 4) k_init_all(RunP
         const SCtx c = make_ctx<KIND>(g, P.m, lo, affix);
         double wl = 0.0;
         const uint32_t e = init_slot<KIND>(g, P.m, P.cfg, c, a, &wl);
-        if (P.ac) {
+        if (P.c16) {
+            // compact: the 16-bit word of state (s, v) at forward arc s->v
+            const uint32_t sv = __ldg(g.rev + a);
+            if (sv != kNoBack)
+                reinterpret_cast<uint16_t*>(P.c16)[(uint64_t)c.off_s + sv] = (uint16_t)c16_enc(e, c.deg);
+        } else if (P.ac) {
             // colocated: the word lives in the record of the forward arc s->v
             const uint32_t sv = __ldg(g.rev + a);  // index of v in N(s)
             if (sv != kNoBack) {
@@ -586,6 +652,10 @@ __global__ void __launch_bounds__(256, KIND == NODE2VEC ? 6 : 4) k_init_rec(RunP
             } else {
                 out[a - b] = w;
             }
+        } else if (P.c16) {
+            // record a = arc s -> v holds state (s, v); deg(v) from the state
+            const uint32_t dv = affix != kNoBack ? load_node(g, load_id(g, a)).deg : 0u;
+            reinterpret_cast<uint16_t*>(P.c16)[a] = (uint16_t)c16_enc(w, dv);
         } else {
             uint32_t* r = reinterpret_cast<uint32_t*>(P.ac) + a * P.rec_u32;
             r[chain_word_off(P.rec_u32)] = w;
@@ -615,6 +685,10 @@ __global__ void k_load_rec(RunParams P, const uint32_t* __restrict__ w, uint32_t
             continue;
         }
         const uint32_t e = __ldg(w + i);
+        if (P.c16) {  // record a = arc s -> v: the state's degree is deg(v)
+            reinterpret_cast<uint16_t*>(P.c16)[a] = (uint16_t)c16_enc(e, load_node(g, load_id(g, a)).deg);
+            continue;
+        }
         if (ac) {
             ac[a * rw + chain_word_off(rw)] = e;
             continue;
@@ -635,13 +709,18 @@ __global__ void k_load_chain(RunParams P, const uint32_t* __restrict__ w, uint32
     for (uint64_t a = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; a < g.m;
          a += (uint64_t)gridDim.x * blockDim.x) {
         const uint32_t e = __ldg(w + a);
-        if (!ac) {
+        if (!ac && !P.c16) {
             chain[a] = e;
             continue;
         }
         const uint32_t s = load_id(g, a);
         const uint32_t sv = __ldg(g.rev + a);
         if (sv == kNoBack) continue;
+        if (P.c16) {  // slot a = (v, affix): deg(v) of its owner v = N(s)[sv]
+            const uint64_t fa = (uint64_t)load_node(g, s).off + sv;
+            reinterpret_cast<uint16_t*>(P.c16)[fa] = (uint16_t)c16_enc(e, load_node(g, load_id(g, fa)).deg);
+            continue;
+        }
         uint32_t* rec = ac + ((uint64_t)load_node(g, s).off + sv) * rw;
         rec[chain_word_off(rw)] = e;
         if (rw == 8 && e < kLocked) {
@@ -1128,6 +1207,11 @@ void with_variant(int regs, bool lazy, int ar, F&& f) {
                 by_regs(lz, std::integral_constant<int, 2>{});
                 return;
             }
+            if (ar == 3) {
+                if constexpr (!decltype(lz)::value) by_regs(lz, std::integral_constant<int, 3>{});
+                else invalid("compact chain tables need eager initialisation");
+                return;
+            }
         }
         if (ar) by_regs(lz, std::integral_constant<int, 1>{});
         else by_regs(lz, std::integral_constant<int, 0>{});
@@ -1532,7 +1616,47 @@ void session_create(Session& s, Graph& g, const mhw_model_desc& md, const mhw_wa
         // arc records (after the session buffers, so the memory check sees them)
         const char* ar_env = std::getenv("MHW_ARC_RECORDS");
         const bool want_ar = !(ar_env && ar_env[0] == '0');
-        if (want_ar && m.kind != DEEPWALK && g.m && g.m < (1ull << 32)) {
+        // node2vec compact chains (AR 3): 16-bit words in their own table when
+        // it and the node table fit L2 (MHW_C16=0/1 forces)
+        const char* c16e = std::getenv("MHW_C16");
+        const bool c16_ok = m.kind == NODE2VEC && s.eager_init && g.verified_sym && g.m && g.m < (1ull << 32) &&
+                            g.max_deg <= 0xFFFDu && want_ar;
+        const bool c16_want = c16_ok && (c16e ? c16e[0] == '1' : (2ull * g.m <= (96ull << 20) && 16ull * g.n <= (32ull << 20)));
+        if (c16_want) {
+            // MHW_C16_PIN: filter (default) | chain | both ([c16 | filter copy], one window) | none
+            const char* pm = std::getenv("MHW_C16_PIN");
+            const std::string mode = pm ? pm : "filter";
+            const uint64_t cw = (g.m + 1) / 2;
+            const uint64_t cw_al = (cw + 63) & ~63ull;  // 256-byte aligned filter copy
+            const bool both = mode == "both" && g.bloom.n && !m.alpha_trivial;
+            s.c16.alloc(both ? cw_al + g.bloom.n : cw);
+            if (both) {
+                MHW_CK(cudaMemcpyAsync(s.c16.p + cw_al, g.bloom.p, g.bloom.bytes(), cudaMemcpyDeviceToDevice, st));
+                s.bloom_copy = s.c16.p + cw_al;
+            }
+            if (s.l2_pin && mode != "filter") {  // undo the filter window taken above
+                int dev = 0;
+                MHW_CK(cudaGetDevice(&dev));
+                l2_limit_release(dev);
+                s.l2_pin = false;
+                s.pin_p = nullptr;
+                s.pin_bytes = 0;
+            }
+            if (pin_ok && (mode == "chain" || both)) {
+                int dev = 0, max_persist = 0;
+                MHW_CK(cudaGetDevice(&dev));
+                MHW_CK(cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, dev));
+                const size_t bytes = both ? s.c16.bytes() : cw * 4;
+                if (max_persist > 0) {
+                    l2_limit_acquire(dev, std::min<size_t>(bytes, (size_t)max_persist));
+                    s.l2_pin = true;
+                    s.pin_p = s.c16.p;
+                    s.pin_bytes = bytes;
+                    s.pin_ratio = (float)std::min(1.0, (double)max_persist / (double)bytes);
+                }
+            }
+        }
+        if (!s.c16.n && want_ar && m.kind != DEEPWALK && g.m && g.m < (1ull << 32)) {
             // session arc records (typed models: 32 B with weight and types);
             // second-order models keep their chain words in them
             // node2vec: narrow 8-byte records when the node table (16 B per
@@ -1548,7 +1672,7 @@ void session_create(Session& s, Graph& g, const mhw_model_desc& md, const mhw_wa
                 s.use_ar = true;
             }
         }
-        if (!s.ac.n || !second_order(m.kind)) s.chain.alloc(std::max<uint64_t>(s.slots, 1));
+        if ((!s.ac.n && !s.c16.n) || !second_order(m.kind)) s.chain.alloc(std::max<uint64_t>(s.slots, 1));
         else s.chain.alloc(1);
         // node-keyed models: the chain table itself (hub replicas included)
         if (!s.l2_pin && !second_order(m.kind)) try_pin(s.chain.p, s.chain.bytes());
@@ -1577,11 +1701,11 @@ static void l2_window_restore(cudaStream_t st, const cudaStreamAttrValue& prev) 
     MHW_CK(cudaStreamSetAttribute(st, cudaStreamAttributeAccessPolicyWindow, &prev));
 }
 
-static void l2_window(cudaStream_t st, void* p, size_t bytes) {
+static void l2_window(cudaStream_t st, void* p, size_t bytes, float ratio = 1.0f) {
     cudaStreamAttrValue attr{};
     attr.accessPolicyWindow.base_ptr = p;
     attr.accessPolicyWindow.num_bytes = bytes;
-    attr.accessPolicyWindow.hitRatio = bytes ? 1.0f : 0.0f;
+    attr.accessPolicyWindow.hitRatio = bytes ? ratio : 0.0f;
     attr.accessPolicyWindow.hitProp = bytes ? cudaAccessPropertyPersisting : cudaAccessPropertyNormal;
     attr.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
     MHW_CK(cudaStreamSetAttribute(st, cudaStreamAttributeAccessPolicyWindow, &attr));
@@ -1628,6 +1752,8 @@ RunParams Session::params() const {
     P.n_items = n_items;
     P.chain = chain.p;
     P.ac = ac.n ? ac.p : nullptr;
+    P.c16 = c16.n ? c16.p : nullptr;
+    if (bloom_copy) P.g.bloom = bloom_copy;
     P.rec_u32 = rec_u32;
     P.out = out.p;
     P.stride = stride;
@@ -1659,7 +1785,7 @@ void session_run(Session& s, cudaStream_t user) {
     cudaStreamAttrValue prev_window{};
     if (pin) {
         prev_window = l2_window_save(st);
-        l2_window(st, s.pin_p, s.pin_bytes);
+        l2_window(st, s.pin_p, s.pin_bytes, s.pin_ratio);
     }
     const bool preloaded = s.chain_loaded;  // mhw_session_load_chain: table already initialised
     s.chain_loaded = false;
@@ -1981,7 +2107,7 @@ void session_run_packed(Session& s, uint32_t* h_nodes, uint64_t cap_nodes, uint6
                                                                              s.out.p, s.stride, s.lens.p);
         const bool pin = s.l2_pin;
         const cudaStreamAttrValue prev_window = pin ? l2_window_save(S) : cudaStreamAttrValue{};
-        if (pin) l2_window(S, s.pin_p, s.pin_bytes);
+        if (pin) l2_window(S, s.pin_p, s.pin_bytes, s.pin_ratio);
         MHW_CK(cudaEventRecord(s.ev0, S));
         const double t_setup = ms_since(ta);
         dispatch(s.model.dev.kind, [&](auto kc) {

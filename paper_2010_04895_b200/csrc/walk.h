@@ -20,6 +20,8 @@ struct RunParams {
     uint32_t rec_u32;         // u32 words per session arc record: 4 (16 B), 8 (typed 32 B), 2 (narrow 8 B)
     uint4* ac;                // node2vec throughput: arc records whose .w is the chain
                               // word of the state entered through that arc (else null)
+    uint32_t* c16;            // node2vec compact chains (AR 3): one 16-bit word per forward
+                              // arc s->v = state (s, v), two per u32 (else null)
     uint32_t* out;            // rows x stride walk buffer
     uint32_t stride;
     uint32_t* lens;
@@ -58,6 +60,8 @@ struct Session {
     DBuf<double> rep_scale;  // metapath2vec replica weights per node type
     DBuf<uint4> ac;          // session arc records (+ colocated chain words, second order)
     uint32_t rec_u32 = 4;    // u32 words per record: 4, 8 (typed models), 2 (narrow node2vec records)
+    DBuf<uint32_t> c16;      // compact 16-bit chain words (node2vec, L2-sized), [c16 | filter copy] when pinned
+    const uint32_t* bloom_copy = nullptr;  // the edge filter's copy behind c16 (one persisting window)
     std::unique_ptr<ExactState> ex;  // alias / direct / rejection baselines (exact.cu)
     DBuf<unsigned long long> ctr;
     // deterministic schedule scratch
@@ -73,6 +77,7 @@ struct Session {
     bool l2_pin = false;        // persisting L2 window during runs (edge filter, or fairwalk group sizes)
     void* pin_p = nullptr;
     size_t pin_bytes = 0;
+    float pin_ratio = 1.0f;     // hitRatio of the window (set-aside / window bytes)
     bool use_ar = false;     // arc-record walk kernel variant
     int minb = 1;
     uint32_t launches = 0;
@@ -85,7 +90,7 @@ struct Session {
     Session& operator=(const Session&) = delete;
     ~Session();
     RunParams params() const;
-    int ar_mode() const { return use_ar ? (rec_u32 == 2 ? 2 : 1) : 0; }
+    int ar_mode() const { return c16.n ? 3 : (use_ar ? (rec_u32 == 2 ? 2 : 1) : 0); }
 };
 
 uint64_t k_slots(int kind, const Graph& g);

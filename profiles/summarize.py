@@ -66,8 +66,13 @@ def main():
                 lines.append(f"| {label} (`{m}`) | {v} {u} |")
         lines.append("")
         if "dram__bytes_read.sum" in d:
-            tb = to_bytes(*d["dram__bytes_read.sum"]) + to_bytes(*d["dram__bytes_write.sum"])
-            traffic[kname] = tb
+            rd, wr = to_bytes(*d["dram__bytes_read.sum"]), to_bytes(*d["dram__bytes_write.sum"])
+            dur = float(d["gpu__time_duration.sum"][0].replace(",", "")) if "gpu__time_duration.sum" in d else None
+            if dur is not None:
+                dur *= {"nsecond": 1e-6, "usecond": 1e-3, "msecond": 1.0, "second": 1e3}.get(
+                    d["gpu__time_duration.sum"][1], 1.0)
+            hit = float(d["lts__t_sector_hit_rate.pct"][0]) if "lts__t_sector_hit_rate.pct" in d else None
+            traffic[kname] = {"total": rd + wr, "read": rd, "write": wr, "ms": dur, "l2_hit_pct": hit}
     if launches:
         rows = list(csv.reader(open(launches)))
         hdr = None
@@ -95,10 +100,16 @@ def main():
     init = [v for k, v in traffic.items() if "k_init_all" in k]
     cfg = name.split("_")[0]
     if walk:
+        commit = subprocess.run(["git", "-C", HERE, "rev-parse", "--short=12", "HEAD"], capture_output=True,
+                                text=True).stdout.strip() or None
+        w = walk[0]
         with open(os.path.join(HERE, f"traffic_{cfg}.json"), "w") as f:
-            json.dump({"kernel": "k_walk", "dram_bytes_per_launch": walk[0],
-                       "init_kernel_dram_bytes_per_launch": init[0] if init else None,
-                       "source": f"profiles/ncu_{name}.md"}, f, indent=1)
+            json.dump({"kernel": "k_walk", "dram_bytes_per_launch": w["total"],
+                       "dram_read_bytes_per_launch": w["read"], "dram_write_bytes_per_launch": w["write"],
+                       "ncu_ms": w["ms"], "l2_hit_pct": w["l2_hit_pct"],
+                       "init_kernel_dram_bytes_per_launch": init[0]["total"] if init else None,
+                       "source": f"profiles/ncu_{name}.md", "tree": commit,
+                       "env": {k: v for k, v in os.environ.items() if k.startswith("MHW_")}}, f, indent=1)
     print("\n".join(lines))
 
 

@@ -77,7 +77,7 @@ def test_full_corpus_chain_chi_square(mhw, oracle, cfg_name):
         assert sum(hg.ntype[v] == 2 for v, *_ in states) >= 10
 
 
-def pick_start(hg, cfg, lo, hi, max_support, need=24):
+def pick_start(hg, cfg, lo, hi, max_support, need=None):
     """A start of degree in [lo, hi] with the most neighbours of degree <=
     max_support (weighted graphs: the audited states (s, v) need a dense
     test), at least `need` of them (R-MAT neighbours are mostly hubs)."""
@@ -92,6 +92,7 @@ def pick_start(hg, cfg, lo, hi, max_support, need=24):
             best, best_n = int(v), k
         if k >= 0.9 * len(nb):
             break
+    need = lo if need is None else need
     assert best_n >= need, f"no start node found (best has {best_n} light neighbours)"
     return best
 

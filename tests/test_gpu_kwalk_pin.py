@@ -155,10 +155,25 @@ def test_kwalk_wide_records_equal_oracle(mhw, oracle):
     """The cfg5 kernel variant on the cfg2 graph: 16-byte node2vec records
     {u, deg, off, chain word} and random init in record order (k_init_rec),
     with an 8-bit-per-arc edge filter (cfg5's density)."""
-    env = {"MHW_NARROW": "0", "MHW_BLOOM_BITS": "8"}
+    env = {"MHW_C16": "0", "MHW_NARROW": "0", "MHW_BLOOM_BITS": "8"}
     cfg = dict(bench.CONFIGS["cfg2"], init="random")
     bench.CONFIGS["cfg2_wide"] = cfg
     try:
         pin(mhw, oracle, "cfg2_wide", init_mode=2, env=env, n_starts=800)
     finally:
         del bench.CONFIGS["cfg2_wide"]
+
+
+@pytest.mark.parametrize("layout,env", [
+    ("narrow", {"MHW_C16": "0", "MHW_NARROW": "1"}),
+    ("c16_pin_both", {"MHW_C16": "1", "MHW_C16_PIN": "both"}),
+])
+def test_kwalk_cfg2_chain_layouts_equal_oracle(mhw, oracle, layout, env):
+    """cfg2 with the other node2vec chain layouts: the narrow {u, chain word}
+    records (round-1 kernel) and the compact 16-bit table pinned in L2 with
+    a copy of the edge filter. The default (compact table, filter pinned) is
+    test_kwalk_second_order_single_walkers_equal_oracle[cfg2]; its hub
+    states (degree >= 2^14: cfg2's top hubs) keep no alpha class in the
+    16-bit word, which the 150 hub starts exercise."""
+    n, steps = pin(mhw, oracle, "cfg2", init_mode=2, env=env, n_starts=800)
+    assert n >= 700 and steps > 50 * n

@@ -328,12 +328,23 @@ def test_throughput_transitions_pass_chain_chi_square(mhw, oracle, kind):
     assert ok_c, "control: " + msg_c
 
 
-@pytest.mark.parametrize("narrow", ["0", "1"])
-def test_node2vec_record_layouts_pass_chain_chi_square(mhw, oracle, narrow, monkeypatch):
-    """node2vec session records: 16-byte {u, deg, off, chain word} and the
-    narrow 8-byte {u, chain word} layout (node record from L2), eager and
-    lazy slot init."""
-    monkeypatch.setenv("MHW_NARROW", narrow)
+LAYOUTS = {  # node2vec chain-word layouts of the throughput kernel
+    "wide": {"MHW_C16": "0", "MHW_NARROW": "0"},    # 16-byte {u, deg, off, chain word} records
+    "narrow": {"MHW_C16": "0", "MHW_NARROW": "1"},  # 8-byte {u, chain word} records
+    "c16": {"MHW_C16": "1"},                        # ids + compact 16-bit chain table (eager only)
+    "c16_pin_both": {"MHW_C16": "1", "MHW_C16_PIN": "both"},  # [c16 | filter copy] in one L2 window
+    "c16_pin_chain": {"MHW_C16": "1", "MHW_C16_PIN": "chain"},
+}
+
+
+@pytest.mark.parametrize("layout", sorted(LAYOUTS))
+def test_node2vec_record_layouts_pass_chain_chi_square(mhw, oracle, layout, monkeypatch):
+    """node2vec chain layouts: 16-byte {u, deg, off, chain word} records, the
+    narrow 8-byte {u, chain word} layout (node record from L2) and the
+    compact 16-bit chain table beside the plain ids (eager init only; lazy
+    runs fall back to records), eager and lazy slot init."""
+    for k, v in LAYOUTS[layout].items():
+        monkeypatch.setenv(k, v)
     g = typed_random_graph(901, 40, 4.0, weighted=False, types=2)
     md = model_desc(O.NODE2VEC, g, p=0.25, q=4.0)
     # burn-in: eager init in slot order; random init on wide records: eager

@@ -78,14 +78,18 @@ def test_preloaded_chain_run_passes_chi_square(mhw, oracle, kind):
     assert s.stats().slot_inits == g.m
 
 
-@pytest.mark.parametrize("narrow", ["1", "0"])
+@pytest.mark.parametrize("narrow", ["1", "0", "c16"])
 @pytest.mark.parametrize("init", [O.INIT_RANDOM, O.INIT_BURN_IN])
 @pytest.mark.parametrize("kind", [O.NODE2VEC, O.EDGE2VEC, O.FAIRWALK])
 def test_record_order_words_are_slot_words_permuted(mhw, oracle, kind, init, narrow, monkeypatch):
     """init_records word i (arc i = s -> v) == init_chain word off(v) + index of s in N(v),
-    for every session record layout (node2vec narrow {u, word} / wide {u, deg, off, word},
-    typed 32-byte records)."""
-    monkeypatch.setenv("MHW_NARROW", narrow)
+    for every session record layout (node2vec narrow {u, word} / wide {u, deg, off, word} /
+    compact 16-bit table, typed 32-byte records)."""
+    if narrow == "c16":
+        monkeypatch.setenv("MHW_C16", "1")
+    else:
+        monkeypatch.setenv("MHW_C16", "0")
+        monkeypatch.setenv("MHW_NARROW", narrow)
     g = typed_random_graph(900 + kind, 150, 6.0, weighted=True, types=2)
     md = model_desc(kind, g, p=0.3, q=3.0, M=np.random.default_rng(kind).uniform(0.5, 2.0, (4, 4)))
     cfg = O.WalkCfg(K=2, L=10, seed=23, init_kind=init, burn_in_steps=6)
