@@ -284,6 +284,51 @@ MHW_API void mhw_walks_free(mhw_walks* w);
  * line, space separated, plus <path>.stats.jsonl. */
 MHW_API mhw_status mhw_walks_write(const mhw_walks* w, const char* path);
 
+/* The stats sidecar line of write_corpus (engine.cpp:248-259): the bytes of
+ * nlohmann::json::dump() of {walks, early_terminations, skipped_starts,
+ * steps, steps_per_sec, init_seconds, walk_seconds} plus '\n' (sorted keys,
+ * shortest round-trip doubles). *len = bytes without the terminating NUL;
+ * status 2 when cap is too small. */
+MHW_API mhw_status mhw_stats_render(const mhw_walk_stats* stats, char* out, size_t cap, size_t* len);
+
+/* cmd_walk's run manifest (tools/mhwalk.cpp:142-169), rendered like
+ * nlohmann's dump(2) plus '\n'. Strings are the CLI's flag values ("" when
+ * unset); checksum = graph_checksum (tools/mhwalk.cpp:107-122, see
+ * mhw_graph_checksum); T_i / T_w = mhw_walk_stats init_seconds / walk_seconds. */
+typedef struct mhw_manifest {
+    const char* input;
+    int32_t weighted;
+    int32_t symmetrize;
+    const char* model;        /* "deepwalk" | "node2vec" | ... */
+    double p;
+    double q;
+    const char* metapath;     /* comma-separated type ids as given */
+    const char* edge_matrix;
+    const char* node_types;
+    const char* edge_types;
+    uint32_t walks_per_node;
+    uint32_t walk_length;
+    const char* sampler;      /* "mh" | "alias" | "direct" | "rejection" */
+    const char* init;         /* "random" | "high_weight" | "burn_in" */
+    uint32_t burn_in_steps;
+    uint32_t hw_sample_size;
+    uint32_t threads;
+    uint64_t seed;
+    const char* output;
+    uint32_t nodes;
+    uint64_t arcs;
+    uint64_t checksum;
+    double T_i;
+    double T_w;
+} mhw_manifest;
+MHW_API mhw_status mhw_manifest_render(const mhw_manifest* m, char* out, size_t cap, size_t* len);
+/* Writes <m->output>.manifest.json. */
+MHW_API mhw_status mhw_manifest_write(const mhw_manifest* m);
+/* graph_checksum (tools/mhwalk.cpp:107-122): FNV-1a over the reference
+ * Graph's offsets (u64), neighbours and f64 weight bits (1.0 when
+ * unweighted), computed from the device CSR. */
+MHW_API mhw_status mhw_graph_checksum(const mhw_graph* g, uint64_t* checksum);
+
 /* generate_walks + write_corpus with the text formatted on the device
  * (integer-to-text kernels, chunked pinned D2H overlapping fwrite); same
  * bytes as write_corpus (engine.cpp:236-259) plus <path>.stats.jsonl. */

@@ -443,6 +443,9 @@ class RefLib:
         L.ref_walk_sample.argtypes = [C.c_void_p, C.c_void_p, C.c_uint32, C.c_uint32, C.c_uint32,
                                       C.c_uint64, C.c_int, C.c_uint32, C.c_uint32, C.c_uint64,
                                       C.c_uint64, C.c_uint64, _u64p, _dp]
+        L.ref_json_double.argtypes = [C.c_double, C.c_char_p, C.c_size_t]
+        L.ref_write_corpus.argtypes = [C.c_char_p, _u32p, _u32p, C.c_uint64, C.c_uint32, _u64p, _dp]
+        L.ref_manifest.argtypes = [C.POINTER(C.c_char_p), _dp, _u64p, C.POINTER(C.c_int), C.c_char_p, C.c_size_t]
         L.ref_run_new.argtypes = [C.c_void_p, C.c_void_p, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint64,
                                   C.c_int, C.c_uint32, C.c_uint32, C.POINTER(C.c_void_p)]
         L.ref_run_free.argtypes = [C.c_void_p]
@@ -451,6 +454,41 @@ class RefLib:
     def _check(self, rc):
         if rc:
             raise OracleError(rc, self.lib.ref_last_error().decode())
+
+    def json_double(self, x: float) -> str:
+        """nlohmann::json(x).dump() (the stats sidecar's number format)."""
+        buf = C.create_string_buffer(64)
+        self._check(self.lib.ref_json_double(float(x), buf, 64))
+        return buf.value.decode()
+
+    def write_corpus(self, path, rows, lens, stats: dict):
+        """The reference's write_corpus (engine.cpp:236-259) on a padded corpus."""
+        rows = np.ascontiguousarray(rows, dtype=np.uint32)
+        lens = np.ascontiguousarray(lens, dtype=np.uint32)
+        st = np.array([stats["walks"], stats["early_terminations"], stats["skipped_starts"], stats["steps"]],
+                      dtype=np.uint64)
+        tm = np.array([stats["steps_per_sec"], stats["init_seconds"], stats["walk_seconds"]], dtype=np.float64)
+        self._check(self.lib.ref_write_corpus(path.encode(), _ptr(rows, _u32p), _ptr(lens, _u32p), len(lens),
+                                              rows.shape[1] if rows.ndim == 2 else 0, _ptr(st, _u64p),
+                                              _ptr(tm, _dp)))
+
+    MANIFEST_STRS = ["input", "model", "metapath", "edge_matrix", "node_types", "edge_types", "sampler", "init",
+                     "output"]
+    MANIFEST_NUMS = ["p", "q", "T_i", "T_w"]
+    MANIFEST_INTS = ["walks_per_node", "walk_length", "burn_in_steps", "hw_sample_size", "threads", "seed",
+                     "nodes", "arcs", "checksum"]
+    MANIFEST_FLAGS = ["weighted", "symmetrize"]
+
+    def manifest(self, **f) -> bytes:
+        """cmd_walk's manifest object (tools/mhwalk.cpp:142-169) dumped by
+        nlohmann with indent 2, plus a newline."""
+        strs = (C.c_char_p * 9)(*[f.get(k, "").encode() for k in self.MANIFEST_STRS])
+        nums = np.array([f.get(k, 0.0) for k in self.MANIFEST_NUMS], dtype=np.float64)
+        ints = np.array([f.get(k, 0) for k in self.MANIFEST_INTS], dtype=np.uint64)
+        flags = (C.c_int * 2)(*[int(f.get(k, 0)) for k in self.MANIFEST_FLAGS])
+        buf = C.create_string_buffer(1 << 16)
+        self._check(self.lib.ref_manifest(strs, _ptr(nums, _dp), _ptr(ints, _u64p), flags, buf, 1 << 16))
+        return buf.value
 
     def graph(self, g: HostGraph):
         return _RefGraph(self, self.lib.ref_graph_new(

@@ -13,6 +13,8 @@
 #include "mhwalk/rng.hpp"
 #include "mhwalk/samplers.hpp"
 
+#include <nlohmann/json.hpp>
+
 #include <chrono>
 #include <cstring>
 #include <numeric>
@@ -387,6 +389,78 @@ int ref_run_slice(void* h, uint32_t slice, uint32_t slices, uint64_t* stats, dou
         }
         times[0] = std::chrono::duration<double>(t1 - t0).count();
         times[1] = R.manager.init_seconds() - init0;
+    });
+}
+
+// ---- JSON sidecars (corpus emission parity, tools/mhwalk.cpp / engine.cpp)
+// nlohmann::json(x).dump() of one double (the stats line's number format).
+int ref_json_double(double x, char* out, size_t cap) {
+    const std::string s = nlohmann::json(x).dump();
+    if (s.size() + 1 > cap) return 1;
+    std::memcpy(out, s.c_str(), s.size() + 1);
+    return 0;
+}
+
+// The reference's own write_corpus (engine.cpp:236-259) over a corpus given
+// as padded rows: corpus text + <path>.stats.jsonl.
+int ref_write_corpus(const char* path, const uint32_t* rows, const uint32_t* lens, uint64_t n_rows,
+                     uint32_t stride, const uint64_t* stats, const double* times) {
+    return guarded([&] {
+        WalkCorpus c;
+        c.walks.resize(n_rows);
+        for (uint64_t r = 0; r < n_rows; ++r) c.walks[r].assign(rows + r * stride, rows + r * stride + lens[r]);
+        c.stats.walks = stats[0];
+        c.stats.early_terminations = stats[1];
+        c.stats.skipped_starts = stats[2];
+        c.stats.steps = stats[3];
+        c.stats.steps_per_sec = times[0];
+        c.stats.init_seconds = times[1];
+        c.stats.walk_seconds = times[2];
+        write_corpus(c, path);
+    });
+}
+
+// cmd_walk's manifest object (tools/mhwalk.cpp:142-169), restated here over
+// the same nlohmann types because the CLI itself does not build (CLI11 is
+// absent); strs = {input, model, metapath, edge_matrix, node_types,
+// edge_types, sampler, init, output}, nums = {p, q, T_i, T_w}, ints = {K, L,
+// burn_in, hw, threads, seed, nodes, arcs, checksum}, flags = {weighted,
+// symmetrize}. Written with dump(2) and a newline, as cmd_walk writes it.
+int ref_manifest(const char* const* strs, const double* nums, const uint64_t* ints, const int* flags,
+                 char* out, size_t cap) {
+    return guarded([&] {
+        nlohmann::json manifest = {
+            {"version", "0.1.0"},
+            {"config",
+             {{"input", std::string(strs[0])},
+              {"weighted", flags[0] != 0},
+              {"symmetrize", flags[1] != 0},
+              {"model", std::string(strs[1])},
+              {"p", nums[0]},
+              {"q", nums[1]},
+              {"metapath", std::string(strs[2])},
+              {"edge_matrix", std::string(strs[3])},
+              {"node_types", std::string(strs[4])},
+              {"edge_types", std::string(strs[5])},
+              {"walks_per_node", static_cast<uint32_t>(ints[0])},
+              {"walk_length", static_cast<uint32_t>(ints[1])},
+              {"walk_length_unit", "steps"},
+              {"sampler", std::string(strs[6])},
+              {"init", std::string(strs[7])},
+              {"burn_in_steps", static_cast<uint32_t>(ints[2])},
+              {"hw_sample_size", static_cast<uint32_t>(ints[3])},
+              {"threads", static_cast<uint32_t>(ints[4])},
+              {"seed", ints[5]},
+              {"output", std::string(strs[8])}}},
+            {"graph",
+             {{"nodes", static_cast<uint32_t>(ints[6])},
+              {"arcs", ints[7]},
+              {"checksum", ints[8]}}},
+            {"timing", {{"T_i", nums[2]}, {"T_w", nums[3]}}},
+        };
+        const std::string s = manifest.dump(2) + "\n";
+        if (s.size() + 1 > cap) throw std::runtime_error("buffer too small");
+        std::memcpy(out, s.c_str(), s.size() + 1);
     });
 }
 

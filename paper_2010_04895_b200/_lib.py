@@ -44,6 +44,16 @@ class GraphInfoC(C.Structure):
                 ("device_bytes", C.c_uint64), ("device", C.c_int32)]
 
 
+class ManifestC(C.Structure):
+    _fields_ = [("input", C.c_char_p), ("weighted", C.c_int32), ("symmetrize", C.c_int32), ("model", C.c_char_p),
+                ("p", C.c_double), ("q", C.c_double), ("metapath", C.c_char_p), ("edge_matrix", C.c_char_p),
+                ("node_types", C.c_char_p), ("edge_types", C.c_char_p), ("walks_per_node", C.c_uint32),
+                ("walk_length", C.c_uint32), ("sampler", C.c_char_p), ("init", C.c_char_p),
+                ("burn_in_steps", C.c_uint32), ("hw_sample_size", C.c_uint32), ("threads", C.c_uint32),
+                ("seed", C.c_uint64), ("output", C.c_char_p), ("nodes", C.c_uint32), ("arcs", C.c_uint64),
+                ("checksum", C.c_uint64), ("T_i", C.c_double), ("T_w", C.c_double)]
+
+
 _P = C.c_void_p
 _PP = C.POINTER(C.c_void_p)
 
@@ -108,6 +118,10 @@ SIGNATURES = {
     "mhw_alias_tables": (C.c_int32, [_P, _P, _P]),
     "mhw_check": (C.c_int32, [_P, C.POINTER(ModelDescC), C.c_uint64, C.c_uint64, _P, _P, C.c_uint64, _P, _P]),
     "mhw_init_states": (C.c_int32, [_P, C.POINTER(ModelDescC), C.POINTER(WalkConfigC), C.c_uint64, _P, _P, _P]),
+    "mhw_stats_render": (C.c_int32, [C.POINTER(WalkStatsC), C.c_char_p, C.c_size_t, C.POINTER(C.c_size_t)]),
+    "mhw_manifest_render": (C.c_int32, [C.POINTER(ManifestC), C.c_char_p, C.c_size_t, C.POINTER(C.c_size_t)]),
+    "mhw_manifest_write": (C.c_int32, [C.POINTER(ManifestC)]),
+    "mhw_graph_checksum": (C.c_int32, [_P, C.POINTER(C.c_uint64)]),
 }
 
 _lib = None

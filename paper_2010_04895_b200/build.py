@@ -14,7 +14,7 @@ CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libmhw.so")
 OBJ = os.path.join(PKG, "_obj")
 SOURCES = ["graph.cu", "walk.cu", "exact.cu", "corpus.cu", "loader.cu", "api.cu"]
-HEADERS = ["mhw_device.cuh", "internal.h", "walk.h", "loader.h"]
+HEADERS = ["mhw_device.cuh", "internal.h", "walk.h", "loader.h", "jsonfmt.h"]
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

@@ -12,6 +12,7 @@
 #include <vector>
 
 #include "internal.h"
+#include "jsonfmt.h"
 #include "loader.h"
 #include "exact.h"
 #include "walk.h"
@@ -431,14 +432,9 @@ mhw_status mhw_walks_write(const mhw_walks* w, const char* path) {
         const std::string side = std::string(path) + ".stats.jsonl";
         FILE* s = std::fopen(side.c_str(), "wb");
         if (!s) throw mhw::Error(MHW_ERR_IO, "cannot open for writing: " + side);
-        const auto& st = w->stats;
-        std::fprintf(s,
-                     "{\"early_terminations\":%llu,\"init_seconds\":%.17g,\"skipped_starts\":%llu,"
-                     "\"steps\":%llu,\"steps_per_sec\":%.17g,\"walk_seconds\":%.17g,\"walks\":%llu}\n",
-                     (unsigned long long)st.early_terminations, st.init_seconds,
-                     (unsigned long long)st.skipped_starts, (unsigned long long)st.steps, st.steps_per_sec,
-                     st.walk_seconds, (unsigned long long)st.walks);
-        std::fclose(s);
+        const std::string line = mhw::stats_line(w->stats);
+        const bool sok = std::fwrite(line.data(), 1, line.size(), s) == line.size();
+        if (std::fclose(s) != 0 || !sok) throw mhw::Error(MHW_ERR_IO, "write failed: " + side);
     });
 }
 
@@ -707,3 +703,111 @@ mhw_status mhw_init_states(const mhw_graph* g, const mhw_model_desc* model, cons
 }
 
 }  // extern "C"
+
+// ------------------------------------------------------- JSON sidecars
+mhw_status mhw_stats_render(const mhw_walk_stats* stats, char* out, size_t cap, size_t* len) {
+    return guard([&] {
+        need(stats, "stats");
+        const std::string line = mhw::stats_line(*stats);
+        if (len) *len = line.size();
+        if (out) {
+            if (cap < line.size() + 1) mhw::invalid("output buffer too small");
+            std::memcpy(out, line.c_str(), line.size() + 1);
+        }
+    });
+}
+
+namespace {
+std::string manifest_text(const mhw_manifest& m) {
+    auto str = [](const char* x) { return std::string(x ? x : ""); };
+    mhw::json::Value root;
+    root["version"] = mhw::json::Value("0.1.0");
+    mhw::json::Value& c = root["config"];
+    c["input"] = str(m.input);
+    c["weighted"] = m.weighted != 0;
+    c["symmetrize"] = m.symmetrize != 0;
+    c["model"] = str(m.model);
+    c["p"] = m.p;
+    c["q"] = m.q;
+    c["metapath"] = str(m.metapath);
+    c["edge_matrix"] = str(m.edge_matrix);
+    c["node_types"] = str(m.node_types);
+    c["edge_types"] = str(m.edge_types);
+    c["walks_per_node"] = m.walks_per_node;
+    c["walk_length"] = m.walk_length;
+    c["walk_length_unit"] = mhw::json::Value("steps");
+    c["sampler"] = str(m.sampler);
+    c["init"] = str(m.init);
+    c["burn_in_steps"] = m.burn_in_steps;
+    c["hw_sample_size"] = m.hw_sample_size;
+    c["threads"] = m.threads;
+    c["seed"] = m.seed;
+    c["output"] = str(m.output);
+    mhw::json::Value& gr = root["graph"];
+    gr["nodes"] = m.nodes;
+    gr["arcs"] = m.arcs;
+    gr["checksum"] = m.checksum;
+    mhw::json::Value& t = root["timing"];
+    t["T_i"] = m.T_i;
+    t["T_w"] = m.T_w;
+    return root.dump(2) + "\n";
+}
+}  // namespace
+
+mhw_status mhw_manifest_render(const mhw_manifest* m, char* out, size_t cap, size_t* len) {
+    return guard([&] {
+        need(m, "manifest");
+        const std::string text = manifest_text(*m);
+        if (len) *len = text.size();
+        if (out) {
+            if (cap < text.size() + 1) mhw::invalid("output buffer too small");
+            std::memcpy(out, text.c_str(), text.size() + 1);
+        }
+    });
+}
+
+mhw_status mhw_manifest_write(const mhw_manifest* m) {
+    return guard([&] {
+        need(m, "manifest");
+        need(m->output, "output");
+        const std::string path = std::string(m->output) + ".manifest.json";
+        const std::string text = manifest_text(*m);
+        FILE* f = std::fopen(path.c_str(), "wb");
+        if (!f) throw mhw::Error(MHW_ERR_IO, "cannot open for writing: " + path);
+        const bool ok = std::fwrite(text.data(), 1, text.size(), f) == text.size();
+        if (std::fclose(f) != 0 || !ok) throw mhw::Error(MHW_ERR_IO, "write failed: " + path);
+    });
+}
+
+mhw_status mhw_graph_checksum(const mhw_graph* g, uint64_t* checksum) {
+    return guard([&] {
+        need(g, "graph");
+        need(checksum, "checksum");
+        mhw::DeviceGuard dg(g->device);
+        const uint64_t m = g->m;
+        std::vector<int64_t> off((size_t)g->n + 1);
+        std::vector<int32_t> ids((size_t)m);
+        std::vector<float> w(g->w.n ? (size_t)m : 0);
+        mhw::graph_download(*g, off.data(), ids.data(), w.empty() ? nullptr : w.data(), nullptr, nullptr);
+        // FNV-1a, tools/mhwalk.cpp:107-122: strictly sequential (h ^= x; h *= P)
+        uint64_t h = 0xcbf29ce484222325ULL;
+        auto mix = [&](uint64_t x) {
+            h ^= x;
+            h *= 0x100000001b3ULL;
+        };
+        for (const int64_t o : off) mix((uint64_t)o);
+        for (const int32_t v : ids) mix((uint64_t)(uint32_t)v);
+        uint64_t one = 0;
+        const double d1 = 1.0;
+        std::memcpy(&one, &d1, 8);
+        for (uint64_t a = 0; a < m; ++a) {
+            uint64_t bits = one;
+            if (!w.empty()) {
+                const double d = (double)w[a];
+                std::memcpy(&bits, &d, 8);
+            }
+            mix(bits);
+        }
+        *checksum = h;
+    });
+}

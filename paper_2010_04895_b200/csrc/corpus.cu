@@ -12,6 +12,7 @@
 #include <string>
 
 #include "internal.h"
+#include "jsonfmt.h"
 #include "exact.h"
 #include "walk.h"
 
@@ -132,12 +133,9 @@ void session_write_corpus(Session& s, const char* path, const mhw_walk_stats& st
     const std::string side = std::string(path) + ".stats.jsonl";
     FILE* sf = std::fopen(side.c_str(), "wb");
     if (!sf) throw Error(MHW_ERR_IO, "cannot open for writing: " + side);
-    std::fprintf(sf,
-                 "{\"early_terminations\":%llu,\"init_seconds\":%.17g,\"skipped_starts\":%llu,"
-                 "\"steps\":%llu,\"steps_per_sec\":%.17g,\"walk_seconds\":%.17g,\"walks\":%llu}\n",
-                 (unsigned long long)st.early_terminations, st.init_seconds, (unsigned long long)st.skipped_starts,
-                 (unsigned long long)st.steps, st.steps_per_sec, st.walk_seconds, (unsigned long long)st.walks);
-    std::fclose(sf);
+    const std::string line = stats_line(st);
+    const bool sok = std::fwrite(line.data(), 1, line.size(), sf) == line.size();
+    if (std::fclose(sf) != 0 || !sok) throw Error(MHW_ERR_IO, "write failed: " + side);
 }
 
 }  // namespace mhw

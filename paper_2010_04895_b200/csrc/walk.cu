@@ -1653,7 +1653,17 @@ void session_create(Session& s, Graph& g, const mhw_model_desc& md, const mhw_wa
                     s.pin_p = s.c16.p;
                     s.pin_bytes = bytes;
                     s.pin_ratio = (float)std::min(1.0, (double)max_persist / (double)bytes);
+                    // the eager init (burn-in over N(v) slices) keeps the
+                    // filter-only window: pinning the chain table there
+                    // starves its slice reads (cfg2 init 4.7 -> 6.8 ms)
+                    if (g.bloom.n && !m.alpha_trivial && g.bloom.bytes() <= (33ull << 20)) {
+                        s.ipin_p = both ? (void*)s.bloom_copy : (void*)g.bloom.p;
+                        s.ipin_bytes = g.bloom.bytes();
+                    }
                 }
+                if (trace)
+                    std::fprintf(stderr, "[mhw] compact chains: pin %s, window %zu B, max persisting %d B, ratio %.3f\n",
+                                 mode.c_str(), bytes, max_persist, (double)s.pin_ratio);
             }
         }
         if (!s.c16.n && want_ar && m.kind != DEEPWALK && g.m && g.m < (1ull << 32)) {
@@ -1785,7 +1795,8 @@ void session_run(Session& s, cudaStream_t user) {
     cudaStreamAttrValue prev_window{};
     if (pin) {
         prev_window = l2_window_save(st);
-        l2_window(st, s.pin_p, s.pin_bytes, s.pin_ratio);
+        if (s.ipin_bytes) l2_window(st, s.ipin_p, s.ipin_bytes);
+        else l2_window(st, s.pin_p, s.pin_bytes, s.pin_ratio);
     }
     const bool preloaded = s.chain_loaded;  // mhw_session_load_chain: table already initialised
     s.chain_loaded = false;
@@ -1848,6 +1859,7 @@ void session_run(Session& s, cudaStream_t user) {
                 }
                 MHW_CK(cudaEventRecord(s.evm, st));
                 evm_done = true;
+                if (pin && s.ipin_bytes) l2_window(st, s.pin_p, s.pin_bytes, s.pin_ratio);
                 with_variant<KIND>(s.minb, !s.eager_init, s.ar_mode(), [&](auto rg, auto lz, auto ar) {
                     k_walk<KIND, decltype(rg)::value, decltype(lz)::value, decltype(ar)::value>
                         <<<s.grid, kWalkBlock, 0, st>>>(P);
@@ -2107,7 +2119,10 @@ void session_run_packed(Session& s, uint32_t* h_nodes, uint64_t cap_nodes, uint6
                                                                              s.out.p, s.stride, s.lens.p);
         const bool pin = s.l2_pin;
         const cudaStreamAttrValue prev_window = pin ? l2_window_save(S) : cudaStreamAttrValue{};
-        if (pin) l2_window(S, s.pin_p, s.pin_bytes, s.pin_ratio);
+        if (pin) {
+            if (s.ipin_bytes) l2_window(S, s.ipin_p, s.ipin_bytes);
+            else l2_window(S, s.pin_p, s.pin_bytes, s.pin_ratio);
+        }
         MHW_CK(cudaEventRecord(s.ev0, S));
         const double t_setup = ms_since(ta);
         dispatch(s.model.dev.kind, [&](auto kc) {
@@ -2117,6 +2132,7 @@ void session_run_packed(Session& s, uint32_t* h_nodes, uint64_t cap_nodes, uint6
             }
         });
         MHW_CK(cudaEventRecord(s.evm, S));
+        if (pin && s.ipin_bytes) l2_window(S, s.pin_p, s.pin_bytes, s.pin_ratio);
         uint64_t H = 0;
         auto issue_copy = [&](int c) {
             MHW_CK(cudaEventSynchronize(ev[c]));

@@ -78,6 +78,8 @@ struct Session {
     void* pin_p = nullptr;
     size_t pin_bytes = 0;
     float pin_ratio = 1.0f;     // hitRatio of the window (set-aside / window bytes)
+    void* ipin_p = nullptr;     // window of the eager-init launch when it differs (the edge filter only)
+    size_t ipin_bytes = 0;
     bool use_ar = false;     // arc-record walk kernel variant
     int minb = 1;
     uint32_t launches = 0;

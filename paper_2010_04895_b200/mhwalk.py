@@ -284,6 +284,12 @@ class Graph:
         _check(L.lib().mhw_graph_info_get(self._h, C.byref(i)))
         return {k: getattr(i, k) for k, _ in L.GraphInfoC._fields_}
 
+    def checksum(self) -> int:
+        """graph_checksum (tools/mhwalk.cpp:107-122) of this CSR."""
+        c = C.c_uint64()
+        _check(L.lib().mhw_graph_checksum(self._h, C.byref(c)))
+        return c.value
+
     def node_count(self) -> int:
         return self.info()["node_count"]
 
@@ -419,11 +425,66 @@ def write_corpus(corpus: WalkCorpus, path: str):
                 f.write("\n")
     except OSError:
         raise IoError(f"cannot open for writing: {path}") from None
-    s = corpus.stats
-    with open(path + ".stats.jsonl", "w") as f:
-        f.write(json.dumps(dict(walks=s.walks, early_terminations=s.early_terminations,
-                                skipped_starts=s.skipped_starts, steps=s.steps, steps_per_sec=s.steps_per_sec,
-                                init_seconds=s.init_seconds, walk_seconds=s.walk_seconds)) + "\n")
+    with open(path + ".stats.jsonl", "wb") as f:
+        f.write(stats_line(corpus.stats))
+
+
+def _stats_c(s) -> "L.WalkStatsC":
+    c = L.WalkStatsC()
+    for k, _ in L.WalkStatsC._fields_:
+        setattr(c, k, getattr(s, k, 0))
+    return c
+
+
+def stats_line(stats) -> bytes:
+    """The `.stats.jsonl` line of write_corpus (engine.cpp:248-259) as the
+    reference's nlohmann dump() renders it (mhw_stats_render)."""
+    c = _stats_c(stats)
+    n = C.c_size_t()
+    _check(L.lib().mhw_stats_render(C.byref(c), None, 0, C.byref(n)))
+    buf = C.create_string_buffer(n.value + 1)
+    _check(L.lib().mhw_stats_render(C.byref(c), buf, n.value + 1, C.byref(n)))
+    return buf.raw[:n.value]
+
+
+MANIFEST_FIELDS = [k for k, _ in L.ManifestC._fields_]
+
+
+def _manifest_c(fields: dict):
+    m = L.ManifestC()
+    for k, t in L.ManifestC._fields_:
+        v = fields.get(k, "" if t is C.c_char_p else 0)
+        setattr(m, k, v.encode() if t is C.c_char_p else v)
+    return m
+
+
+def render_manifest(**fields) -> bytes:
+    """cmd_walk's `.manifest.json` (tools/mhwalk.cpp:142-169), nlohmann
+    dump(2) layout (mhw_manifest_render). Fields: mhw_manifest's."""
+    m = _manifest_c(fields)
+    n = C.c_size_t()
+    _check(L.lib().mhw_manifest_render(C.byref(m), None, 0, C.byref(n)))
+    buf = C.create_string_buffer(n.value + 1)
+    _check(L.lib().mhw_manifest_render(C.byref(m), buf, n.value + 1, C.byref(n)))
+    return buf.raw[:n.value]
+
+
+def write_manifest(graph: "Graph", model: "WalkModel", config: "WalkConfig", stats, output: str, input: str = "",
+                   weighted: bool = False, symmetrize: bool = False, metapath: str = "", edge_matrix: str = "",
+                   node_types: str = "", edge_types: str = ""):
+    """The run manifest cmd_walk writes beside the corpus
+    (<output>.manifest.json: config flags, graph size + checksum, T_i/T_w)."""
+    info = graph.info()
+    fields = dict(input=input, weighted=int(weighted), symmetrize=int(symmetrize), model=model.kind.name,
+                  p=model.p, q=model.q, metapath=metapath, edge_matrix=edge_matrix, node_types=node_types,
+                  edge_types=edge_types, walks_per_node=config.walks_per_node, walk_length=config.walk_length,
+                  sampler=config.sampler_kind.name, init=config.init.kind.name,
+                  burn_in_steps=config.init.burn_in_steps, hw_sample_size=config.init.hw_sample_size,
+                  threads=config.threads, seed=config.seed, output=output, nodes=info["node_count"],
+                  arcs=info["arc_count"], checksum=graph.checksum(), T_i=stats.init_seconds,
+                  T_w=stats.walk_seconds)
+    m = _manifest_c(fields)
+    _check(L.lib().mhw_manifest_write(C.byref(m)))
 
 
 def read_corpus(path: str) -> list:

@@ -94,10 +94,18 @@ def test_one_chain_per_state_layout(mhw, oracle):
     assert c.stats.slot_inits <= g.n
 
 
+def _stats_dict(st):
+    return dict(walks=st.walks, early_terminations=st.early_terminations, skipped_starts=st.skipped_starts,
+                steps=st.steps, steps_per_sec=st.steps_per_sec, init_seconds=st.init_seconds,
+                walk_seconds=st.walk_seconds)
+
+
 @pytest.mark.parametrize("L", [1, 7, 80])
-def test_device_corpus_text_equals_write_corpus(mhw, tmp_path, L):
-    """Text formatted on the GPU (mhw_generate_walks_to_file) == write_corpus
-    of the same corpus (deterministic schedule, so both runs agree)."""
+def test_device_corpus_text_equals_write_corpus(mhw, ref, tmp_path, L):
+    """Text formatted on the GPU (mhw_generate_walks_to_file) and its stats
+    sidecar == the REFERENCE's write_corpus (oracle/_ref, engine.cpp:236-259)
+    of the same corpus and stats (deterministic schedule, so both runs
+    agree), byte for byte."""
     import ctypes as C
     from paper_2010_04895_b200 import _lib as L_
     rng = O.XoRng(8)
@@ -114,9 +122,13 @@ def test_device_corpus_text_equals_write_corpus(mhw, tmp_path, L):
     assert L_.lib().mhw_generate_walks_to_file(dg.handle, C.byref(d), C.byref(cfgw._c()), got.encode(), C.byref(st)) == 0
     assert open(got, "rb").read() == open(want, "rb").read()
     assert st.steps == corpus.stats.steps
+    refp = str(tmp_path / "ref.txt")
+    ref.write_corpus(refp, corpus.rows, corpus.lengths, _stats_dict(st))
+    for suffix in ("", ".stats.jsonl"):
+        assert open(got + suffix, "rb").read() == open(refp + suffix, "rb").read(), suffix
 
 
-def test_walks_write_matches_write_corpus_format(mhw, tmp_path):
+def test_walks_write_matches_write_corpus_format(mhw, ref, tmp_path):
     """mhw_walks_write (C, host) == write_corpus's format (engine.cpp:236-247)."""
     import ctypes as C
     from paper_2010_04895_b200 import _lib as L
@@ -134,9 +146,17 @@ def test_walks_write_matches_write_corpus_format(mhw, tmp_path):
     nodes = np.ctypeslib.as_array(C.cast(lib.mhw_walks_nodes(h), C.POINTER(C.c_uint32)), shape=(rows * stride,))
     lens = np.ctypeslib.as_array(C.cast(lib.mhw_walks_lengths(h), C.POINTER(C.c_uint32)), shape=(rows,))
     want = "".join(" ".join(str(int(x)) for x in nodes[r * stride:r * stride + lens[r]]) + "\n" for r in range(rows))
+    st = L.WalkStatsC()
+    assert lib.mhw_walks_stats(h, C.byref(st)) == 0
+    rows_np = np.array(nodes).reshape(rows, stride)
+    lens_np = np.array(lens)
     lib.mhw_walks_free(h)
     assert open(p).read() == want
-    assert open(p + ".stats.jsonl").read().startswith("{")
+    # the reference's own write_corpus of the same corpus and stats
+    refp = str(tmp_path / "ref.txt")
+    ref.write_corpus(refp, rows_np, lens_np, _stats_dict(st))
+    for suffix in ("", ".stats.jsonl"):
+        assert open(p + suffix, "rb").read() == open(refp + suffix, "rb").read(), suffix
 
 
 def test_mega_hub_star(mhw):
@@ -180,3 +200,25 @@ def test_walk_rows_matches_corpus(mhw):
             assert L.lib().mhw_walk_rows(dg.handle, C.byref(d), C.byref(c), C.byref(rows), C.byref(stride)) == 0
             corpus = mhw.generate_walks(dg, m, cfg)
             assert rows.value == len(corpus) and stride.value == 12
+
+
+def test_manifest_of_a_run_equals_reference(mhw, ref, tmp_path):
+    """cmd_walk's manifest for a device run: graph size and graph_checksum
+    (computed from the device CSR) and T_i / T_w from the run's stats, in the
+    reference's nlohmann dump(2) bytes."""
+    rng = O.XoRng(31)
+    g = O.random_graph(300, 5.0, True, rng)
+    md = model_desc(O.NODE2VEC, g, p=0.5, q=2.0)
+    cfg = O.WalkCfg(K=2, L=10, seed=9, init_kind=O.INIT_BURN_IN, burn_in_steps=7)
+    dg, m, wc = device_graph(g), walk_model(md), walk_config(O.WalkCfg(K=2, L=10, seed=9, init_kind=O.INIT_BURN_IN,
+                                                                       burn_in_steps=7), threads=8)
+    c = mhw.generate_walks(dg, m, wc)
+    out = str(tmp_path / "walks.txt")
+    mhw.write_manifest(dg, m, wc, c.stats, out, input="g.txt", weighted=True, symmetrize=True)
+    w = dg.download()["weights"].astype(np.float64)  # the device CSR's fp32 weights, widened
+    want = ref.manifest(input="g.txt", weighted=1, symmetrize=1, model="node2vec", p=0.5, q=2.0,
+                        walks_per_node=2, walk_length=10, sampler="mh", init="burn_in", burn_in_steps=7,
+                        hw_sample_size=wc.init.hw_sample_size, threads=8, seed=9, output=out, nodes=g.n, arcs=g.m,
+                        checksum=O.Oracle().graph_checksum(g.offsets, g.nbr, w), T_i=c.stats.init_seconds,
+                        T_w=c.stats.walk_seconds)
+    assert open(out + ".manifest.json", "rb").read() == want
