@@ -126,7 +126,8 @@ def make_config(cfg, node_begin=0, node_end=0):
                           schedule=mhw.Schedule.throughput, node_begin=node_begin, node_end=node_end,
                           chain_replica_degree=int(os.environ.get("MHW_REP_DEG", "0")),
                           sampler_kind=mhw.SamplerKind[cfg.get("sampler", "mh")],
-                          init_mode=int(os.environ.get("MHW_INIT_MODE", "0")))
+                          init_mode=int(os.environ.get("MHW_INIT_MODE", "0")),
+                          proposal=1 if cfg.get("proposal") == "alias" else 0)
 
 
 class Clocks:
@@ -481,7 +482,8 @@ def run_mine(args, cfg):
         t_k = kernel_ms * 1e-3
         canon = S * 32 * st.steps / t_k / 1e9
         tr = {}
-        prof = os.path.join(ROOT, "profiles", f"traffic_{cfg['name']}.json")
+        variant = "_alias" if cfg.get("proposal") == "alias" else ""
+        prof = os.path.join(ROOT, "profiles", f"traffic_{cfg['name']}{variant}.json")
         if os.path.exists(prof):
             with open(prof) as f:
                 tr = json.load(f)
@@ -514,7 +516,8 @@ def run_mine(args, cfg):
             "config": {"workload": cfg["workload"], "config": cfg["name"], "nodes": info["node_count"],
                        "arcs": info["arc_count"], "walks": st.walks, "steps_per_run": st.steps,
                        "slot_inits": st.slot_inits, "chain_retries": st.chain_retries,
-                       "sampler": cfg.get("sampler", "mh"), "rejection_trials": st.rejection_trials,
+                       "sampler": cfg.get("sampler", "mh"), "proposal": cfg.get("proposal", "uniform"),
+                       "rejection_trials": st.rejection_trials,
                        "seed": SEED, "walk_seed": WALK_SEED,
                        "l2": "explicit 256 MB L2 flush between timed steps (also inputs > L2)",
                        "parallelism": f"walker ranges x{world}, CSR replicated"
@@ -651,10 +654,13 @@ def main():
     ap.add_argument("--no-e2e", action="store_true", help="skip the host-buffer e2e leg")
     ap.add_argument("--sampler", default="mh", choices=["mh", "alias", "direct", "rejection"],
                     help="exact baseline samplers of next_edge (engine.cpp:88-116) for comparison")
+    ap.add_argument("--proposal", default="uniform", choices=["uniform", "alias"],
+                    help="M-H proposal: uniform (mh_transition) or the static-weight alias table + Hastings")
     args = ap.parse_args()
     cfg = dict(CONFIGS[args.config])
     cfg["name"] = args.config
     cfg["sampler"] = args.sampler
+    cfg["proposal"] = args.proposal
     if args.sampler != "mh":
         args.no_cpu_baseline = True  # the CPU arm times the M-H path
     if args.impl == "reference":

@@ -128,9 +128,13 @@ typedef struct mhw_walk_config {
     /* M-H proposal (north star (2)): MHW_PROPOSAL_UNIFORM
      * draws the candidate uniformly over N(v) exactly as mh_transition
      * (samplers.hpp:21); MHW_PROPOSAL_ALIAS draws it from v's static-weight
-     * alias table (alias_sample, samplers.hpp:68-71, tables of alias_build,
-     * samplers.cpp:95-131) and accepts with the Hastings-corrected ratio
-     * min(1, (w'(c) * w(l)) / (w'(l) * w(c))), w = static weight. */
+     * alias table (alias_sample, samplers.hpp:65-68: index on Philox word 0,
+     * coin on words 1-2; tables of alias_build, samplers.cpp:95-131) and
+     * accepts with the Hastings-corrected ratio min(1, (w'(c) w(l)) / (w'(l)
+     * w(c))) = min(1, r_c / r_l), r = w'/w the model's dynamic factor
+     * (mhw_decide_hastings), with the unit from sub-block 0x80000000 of the
+     * step's Philox block. Throughput schedule and mh sampler only. Chain
+     * init (random / high_weight / burn_in) is mh_init's either way. */
     int32_t proposal;
 } mhw_walk_config;
 
@@ -412,6 +416,16 @@ MHW_API mhw_status mhw_decide(const mhw_graph* g, const mhw_model_desc* model, u
                       const uint32_t* position, const uint32_t* affixture,
                       const uint32_t* candidate, const uint32_t* last, const double* u,
                       double* w_cand, double* w_last, uint8_t* accept);
+
+/* The alias proposal's decision (engine extension, mhw_walk_config.proposal
+ * = MHW_PROPOSAL_ALIAS): r = w'/w, the model's dynamic factor (calculate_weight,
+ * models.cpp:82-123, without the trailing static weight), for candidate and
+ * last, and the Hastings accept of a static-weight proposal:
+ * w(cand) > 0 && (r_l <= 0 || r_c >= r_l || u * r_l < r_c). */
+MHW_API mhw_status mhw_decide_hastings(const mhw_graph* g, const mhw_model_desc* model, uint64_t count,
+                      const uint32_t* position, const uint32_t* affixture,
+                      const uint32_t* candidate, const uint32_t* last, const double* u,
+                      double* r_cand, double* r_last, uint8_t* accept);
 
 /* The `check` audit (tools/mhwalk.cpp:183-264) on the GPU: for each state,
  * random init then `draws` M-H transitions counting the chain's states, and

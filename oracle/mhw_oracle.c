@@ -530,6 +530,43 @@ double og_weight(const og_graph* g, const og_model* m, uint32_t v, uint32_t affi
     }
 }
 
+double og_rfactor(const og_graph* g, const og_model* m, uint32_t v, uint32_t affix, uint32_t i) {
+    const uint64_t base = g->offsets[v];
+    if (m->kind == OG_DEEPWALK) return 1.0;
+    if (m->kind == OG_METAPATH2VEC) return g->ntype[g->nbr[base + i]] == required_type(m, affix) ? 1.0 : 0.0;
+    if (affix == OG_NO_AFFIX) return 1.0;
+    const uint32_t s = g->nbr[base + affix];
+    const uint32_t u = g->nbr[base + i];
+    const double a = alpha(g, m, s, u);
+    switch (m->kind) {
+    case OG_NODE2VEC:
+        return a;
+    case OG_EDGE2VEC: {
+        uint32_t sv = 0;
+        nbr_index(g, s, v, &sv);
+        return a * m->M[(size_t)edge_type(g, s, sv) * m->M_dim + edge_type(g, v, i)];
+    }
+    case OG_FAIRWALK:
+        return a / (double)m->type_counts[(size_t)v * m->num_types + g->ntype[u]];
+    default:
+        return 1.0;
+    }
+}
+
+int og_hastings(double w_c, double r_c, double r_l, double u) {
+    return w_c > 0.0 && (r_l <= 0.0 || r_c >= r_l || u * r_l < r_c);
+}
+
+void og_decide_hastings(const og_graph* g, const og_model* m, uint64_t count, const uint32_t* pos,
+                        const uint32_t* affix, const uint32_t* cand, const uint32_t* last, const double* u,
+                        double* rc, double* rl, uint8_t* accept) {
+    for (uint64_t i = 0; i < count; ++i) {
+        rc[i] = og_rfactor(g, m, pos[i], affix[i], cand[i]);
+        rl[i] = og_rfactor(g, m, pos[i], affix[i], last[i]);
+        accept[i] = (uint8_t)og_hastings(g->w[g->offsets[pos[i]] + cand[i]], rc[i], rl[i], u[i]);
+    }
+}
+
 /* accept rule, samplers.hpp:24 verbatim */
 int og_accept(double wc, double wl, double u) { return wl <= 0.0 || wc >= wl || u * wl < wc; }
 
@@ -942,6 +979,47 @@ static uint32_t alias_draw(const double* prob, const uint32_t* alias, uint32_t n
     return draw_real(d) < prob[i] ? i : alias[i];
 }
 
+/* The static-weight alias table of node v (alias_build over weights_of(v),
+ * engine.cpp:136-146), built on first use; 0 when the weights sum to <= 0. */
+static int static_alias(const og_graph* g, baseline_t* bt, uint32_t v) {
+    if (bt->pstat[v]) return 1;
+    const uint32_t deg = deg_of(g, v);
+    const double* ws = g->w + g->offsets[v];
+    double total = 0.0;
+    for (uint32_t i = 0; i < deg; ++i) total += ws[i];
+    if (total <= 0) return 0;
+    bt->pprob[v] = (double*)malloc(deg * sizeof(double));
+    bt->palias[v] = (uint32_t*)malloc(deg * sizeof(uint32_t));
+    og_alias_build(deg, ws, bt->pprob[v], bt->palias[v]);
+    bt->pstat[v] = 1;
+    return 1;
+}
+
+/* One M-H transition with the static alias proposal (the engine's proposal =
+ * alias extension): candidate = alias_sample of v's static table on the walk
+ * block (index on word 0, coin on words 1-2, as alias_sample draws,
+ * samplers.hpp:65-68), accept unit from block (walker, step) with sub-counter
+ * OG_ACCEPT_SUB (xoshiro: the next real of the stream, drawn only when
+ * needed, as mh_transition draws it). */
+static uint32_t mh_transition_alias(const st_t* s, baseline_t* bt, uint32_t last, draw_t* d, int philox,
+                                    xo_t* xo, const uint32_t key[2], uint64_t walker, uint32_t step) {
+    const uint32_t cand = alias_draw(bt->pprob[s->v], bt->palias[s->v], s->n, d);
+    const double wc = s->g->w[s->g->offsets[s->v] + cand];
+    const double rc = og_rfactor(s->g, s->m, s->v, s->affix, cand);
+    const double rl = og_rfactor(s->g, s->m, s->v, s->affix, last);
+    if (!(wc > 0.0)) return last;
+    if (rl <= 0.0 || rc >= rl) return cand;
+    double u;
+    if (philox) {
+        draw_t b;
+        draw_open_sub(&b, 1, xo, key, walker, step, OG_ACCEPT_SUB);
+        u = draw_real(&b);
+    } else {
+        u = draw_real(d);
+    }
+    return u * rl < rc ? cand : last;
+}
+
 /* One next_edge of the alias / direct / rejection sampler. Philox layout:
  * direct -> unit of the walk block; alias -> index + unit of the walk block;
  * rejection trial t -> block (walker, step) under key DOM_REJECT + (t >> 16)
@@ -974,15 +1052,7 @@ static int baseline_step(const og_graph* g, const og_model* m, const og_config* 
     }
     /* rejection: static proposal per node (engine.cpp:136-146) */
     const double* ws = g->w + g->offsets[v];
-    if (!bt->pstat[v]) {
-        double total = 0.0;
-        for (uint32_t i = 0; i < deg; ++i) total += ws[i];
-        if (total <= 0) return 0;
-        bt->pprob[v] = (double*)malloc(deg * sizeof(double));
-        bt->palias[v] = (uint32_t*)malloc(deg * sizeof(uint32_t));
-        og_alias_build(deg, ws, bt->pprob[v], bt->palias[v]);
-        bt->pstat[v] = 1;
-    }
+    if (!static_alias(g, bt, v)) return 0;
     if (dyn_weights(g, m, v, w->affix, bt->wbuf) <= 0) return 0;
     /* rejection_sample, samplers.cpp:148-170 */
     for (uint32_t i = 0; i < deg; ++i) {
@@ -1057,7 +1127,13 @@ static int walker_step(const og_graph* g, const og_model* m, const og_config* c,
         const uint32_t last = *lastp;
         /* the philox block is (walker, step); xoshiro continues the stream */
         if (philox) draw_open(&d, 1, NULL, wkey, w->walker, step);
-        const uint32_t next = mh_transition(&s, last, &d);
+        uint32_t next;
+        if (c->proposal == OG_PROPOSAL_ALIAS) {
+            if (!static_alias(g, bt, v)) return 0;
+            next = mh_transition_alias(&s, bt, last, &d, philox, &w->xo, wkey, w->walker, step);
+        } else {
+            next = mh_transition(&s, last, &d);
+        }
         if (next != last) *lastp = next;
         edge = next;
     }
@@ -1157,7 +1233,7 @@ int og_generate_walks(const og_graph* g, const og_model* m, const og_config* c, 
     ch.allpos = NULL;
     baseline_t bt;
     memset(&bt, 0, sizeof(bt));
-    if (c->sampler != OG_SAMPLER_MH) {
+    if (c->sampler != OG_SAMPLER_MH || c->proposal == OG_PROPOSAL_ALIAS) {
         uint32_t max_deg = 1;
         for (uint32_t v = 0; v < g->n; ++v) if (deg_of(g, v) > max_deg) max_deg = deg_of(g, v);
         const uint64_t rs = og_slot_count(g, m);
@@ -1235,7 +1311,7 @@ int og_generate_walks(const og_graph* g, const og_model* m, const og_config* c, 
     free(ch.last);
     free(rl.group);
     free(rl.scale);
-    if (c->sampler != OG_SAMPLER_MH) {
+    if (c->sampler != OG_SAMPLER_MH || c->proposal == OG_PROPOSAL_ALIAS) {
         const uint64_t rs = og_slot_count(g, m);
         for (uint64_t i = 0; i < rs; ++i) { free(bt.aprob[i]); free(bt.aalias[i]); }
         for (uint32_t v = 0; v < g->n; ++v) { free(bt.pprob[v]); free(bt.palias[v]); }
@@ -1290,6 +1366,13 @@ int og_walk_isolated(const og_graph* g, const og_model* m, const og_config* cfg,
         }
     }
     ch.allpos = allpos;
+    baseline_t bt;  /* static alias tables (proposal = alias) */
+    memset(&bt, 0, sizeof(bt));
+    if (c->proposal == OG_PROPOSAL_ALIAS) {
+        bt.pstat = (uint8_t*)calloc(g->n ? g->n : 1, 1);
+        bt.pprob = (double**)calloc(g->n ? g->n : 1, sizeof(double*));
+        bt.palias = (uint32_t**)calloc(g->n ? g->n : 1, sizeof(uint32_t*));
+    }
     int rc = OG_OK;
     uint64_t row = 0;
     for (uint64_t j = 0; j < count && rc == OG_OK; ++j) {
@@ -1311,7 +1394,7 @@ int og_walk_isolated(const og_graph* g, const og_model* m, const og_config* cfg,
             rows[w.row * stride] = w.v;
             w.len = 1;
             for (uint32_t step = 0; step < c->L; ++step) {
-                const int r = walker_step(g, m, c, &ch, &rl, NULL, &w, step, stride, rows, stats, err, errlen);
+                const int r = walker_step(g, m, c, &ch, &rl, &bt, &w, step, stride, rows, stats, err, errlen);
                 if (r < 0) { rc = OG_ERR_INVALID; break; }
                 if (r == 0) { stats->early++; break; }
             }
@@ -1320,6 +1403,10 @@ int og_walk_isolated(const og_graph* g, const og_model* m, const og_config* cfg,
     }
     stats->walks = row;
     *n_rows = row;
+    if (bt.pstat) {
+        for (uint32_t v = 0; v < g->n; ++v) { free(bt.pprob[v]); free(bt.palias[v]); }
+        free(bt.pstat); free(bt.pprob); free(bt.palias);
+    }
     free(ch.keys);
     free(ch.status);
     free(ch.last);

@@ -78,7 +78,18 @@ typedef struct {
     /* SamplerKind (engine.hpp:14): mh, or the exact baselines of
      * WalkerContext::next_edge (engine.cpp:88-116) */
     int sampler;
+    /* M-H proposal (engine extension, SURVEY 8(b) proposal {uniform, alias}):
+     * OG_PROPOSAL_UNIFORM = mh_transition (samplers.hpp:18-27); ALIAS = the
+     * node's static-weight alias table (alias_build over weights_of(v),
+     * samplers.cpp:95-131) with the Hastings-corrected accept (og_hastings) */
+    int proposal;
 } og_config;
+
+enum { OG_PROPOSAL_UNIFORM = 0, OG_PROPOSAL_ALIAS = 1 };
+/* Philox sub-counter of the accept unit of an alias-proposal step: block
+ * (walker, step) with ctr.w = this (word 0 of that block is never a Lemire
+ * retry: those use sub-counters 1, 2, ...) */
+#define OG_ACCEPT_SUB 0x80000000u
 
 enum { OG_SAMPLER_MH = 0, OG_SAMPLER_ALIAS = 1, OG_SAMPLER_DIRECT = 2, OG_SAMPLER_REJECTION = 3 };
 
@@ -127,6 +138,18 @@ size_t og_type_counts_size(const og_graph* g);
 double og_weight(const og_graph* g, const og_model* m, uint32_t v, uint32_t affix, uint32_t i);
 int og_accept(double wc, double wl, double u);
 /* (state, cand, last, u) -> (wc, wl, accept), samplers.hpp:21-26 verbatim */
+/* Dynamic factor r = w' / w of candidate i (calculate_weight, models.cpp:82-123,
+ * without the trailing static weight): deepwalk 1, metapath2vec type match ? 1
+ * : 0, bootstrap 1, node2vec alpha, edge2vec alpha * M[in][out], fairwalk
+ * alpha / group. */
+double og_rfactor(const og_graph* g, const og_model* m, uint32_t v, uint32_t affix, uint32_t i);
+/* Hastings accept of an alias (static-weight) proposal: target w' = r * w,
+ * proposal q proportional to w, so min(1, w'_c q_l / (w'_l q_c)) = min(1, r_c / r_l):
+ * accept iff w_c > 0 && (r_l <= 0 || r_c >= r_l || u * r_l < r_c). */
+int og_hastings(double w_c, double r_c, double r_l, double u);
+void og_decide_hastings(const og_graph* g, const og_model* m, uint64_t count, const uint32_t* pos,
+                        const uint32_t* affix, const uint32_t* cand, const uint32_t* last, const double* u,
+                        double* rc, double* rl, uint8_t* accept);
 void og_decide(const og_graph* g, const og_model* m, uint64_t count, const uint32_t* pos,
                const uint32_t* affix, const uint32_t* cand, const uint32_t* last,
                const double* u, double* wc, double* wl, uint8_t* accept);

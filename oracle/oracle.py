@@ -65,7 +65,7 @@ class _OgModel(C.Structure):
 class _OgConfig(C.Structure):
     _fields_ = [("K", C.c_uint32), ("L", C.c_uint32), ("seed", C.c_uint64), ("init_kind", C.c_int),
                 ("burn_in_steps", C.c_uint32), ("hw_sample_size", C.c_uint32), ("rng", C.c_int),
-                ("order", C.c_int), ("replica_degree", C.c_uint32), ("sampler", C.c_int)]
+                ("order", C.c_int), ("replica_degree", C.c_uint32), ("sampler", C.c_int), ("proposal", C.c_int)]
 
 
 class _OgStats(C.Structure):
@@ -145,6 +145,8 @@ class WalkCfg:
     replica_degree: int = 0xFFFFFFFF
     # SamplerKind (engine.hpp:14): 0 mh, 1 alias, 2 direct, 3 rejection
     sampler: int = 0
+    # M-H proposal (engine extension): 0 uniform (mh_transition), 1 static-weight alias + Hastings
+    proposal: int = 0
 
 
 class OracleError(RuntimeError):
@@ -184,6 +186,8 @@ class Oracle:
         L.og_model_bind.argtypes = [C.POINTER(_OgGraph), C.POINTER(_OgModel), C.c_char_p, C.c_size_t]
         L.og_decide.argtypes = [C.POINTER(_OgGraph), C.POINTER(_OgModel), C.c_uint64, _u32p, _u32p,
                                 _u32p, _u32p, _dp, _dp, _dp, _u8p]
+        L.og_decide_hastings.argtypes = [C.POINTER(_OgGraph), C.POINTER(_OgModel), C.c_uint64, _u32p, _u32p,
+                                         _u32p, _u32p, _dp, _dp, _dp, _u8p]
         L.og_alias_build.argtypes = [C.c_uint32, _dp, _dp, _u32p]
         L.og_check.argtypes = [C.POINTER(_OgGraph), C.POINTER(_OgModel), C.c_uint64, C.c_uint64, _u32p, _u32p,
                                C.c_uint64, _u64p, _dp]
@@ -315,6 +319,19 @@ class Oracle:
                            _ptr(uu, _dp), _ptr(wc, _dp), _ptr(wl, _dp), _ptr(acc, _u8p))
         return wc, wl, acc
 
+    def decide_hastings(self, g, md, pos, affix, cand, last, u):
+        """Alias-proposal decisions: (r_c, r_l, accept) with r = w'/w the
+        model's dynamic factor and the Hastings accept of og_hastings."""
+        gs, ms, keep = self.bind(g, md)
+        n = len(pos)
+        arrs = [np.ascontiguousarray(x, dtype=np.uint32) for x in (pos, affix, cand, last)]
+        uu = np.ascontiguousarray(u, dtype=np.float64)
+        rc, rl = np.zeros(n), np.zeros(n)
+        acc = np.zeros(n, dtype=np.uint8)
+        self.lib.og_decide_hastings(C.byref(gs), C.byref(ms), n, *[_ptr(a, _u32p) for a in arrs],
+                                    _ptr(uu, _dp), _ptr(rc, _dp), _ptr(rl, _dp), _ptr(acc, _u8p))
+        return rc, rl, acc
+
     def alias_build(self, w):
         w = np.ascontiguousarray(w, dtype=np.float64)
         prob = np.zeros(len(w))
@@ -340,6 +357,7 @@ class Oracle:
         c.rng, c.order = rng, order
         c.replica_degree = cfg.replica_degree
         c.sampler = cfg.sampler
+        c.proposal = cfg.proposal
         return c
 
     def generate_walks(self, g, md, cfg: WalkCfg, rng=RNG_XOSHIRO, order=ORDER_WALKER, stride=None):

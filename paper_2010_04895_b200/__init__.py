@@ -5,8 +5,8 @@ include/mhw.h); this package is its Python mirror of the reference API.
 """
 from .mhwalk import (  # noqa: F401
     CudaError, Graph, InitKind, InitStrategy, IoError, ModelKind, ParseError, RunStats, SamplerKind,
-    Schedule, Session, ValidationError, WalkConfig, WalkCorpus, WalkModel, alias_tables, decide,
+    Schedule, Session, ValidationError, WalkConfig, WalkCorpus, WalkModel, alias_tables, decide, decide_hastings,
     device_count, generate_walks, generate_walks_multi, init_kind_from_string, init_states, kNoAffix,
     load_edge_list, load_edge_types, load_node_types, model_kind_from_string, partition_nodes, read_corpus,
-    write_corpus,
+    render_manifest, stats_line, write_corpus, write_manifest,
 )

@@ -115,6 +115,7 @@ SIGNATURES = {
     "mhw_session_load_records_range": (C.c_int32, [_P, C.c_uint64, C.c_uint64, _P, _P]),
     "mhw_session_free": (None, [_P]),
     "mhw_decide": (C.c_int32, [_P, C.POINTER(ModelDescC), C.c_uint64, _P, _P, _P, _P, _P, _P, _P, _P]),
+    "mhw_decide_hastings": (C.c_int32, [_P, C.POINTER(ModelDescC), C.c_uint64, _P, _P, _P, _P, _P, _P, _P, _P]),
     "mhw_alias_tables": (C.c_int32, [_P, _P, _P]),
     "mhw_check": (C.c_int32, [_P, C.POINTER(ModelDescC), C.c_uint64, C.c_uint64, _P, _P, C.c_uint64, _P, _P]),
     "mhw_init_states": (C.c_int32, [_P, C.POINTER(ModelDescC), C.POINTER(WalkConfigC), C.c_uint64, _P, _P, _P]),

@@ -663,6 +663,28 @@ mhw_status mhw_decide(const mhw_graph* g, const mhw_model_desc* model, uint64_t 
     });
 }
 
+mhw_status mhw_decide_hastings(const mhw_graph* g, const mhw_model_desc* model, uint64_t count,
+                               const uint32_t* position, const uint32_t* affixture, const uint32_t* candidate,
+                               const uint32_t* last, const double* u, double* r_cand, double* r_last,
+                               uint8_t* accept) {
+    return guard([&] {
+        need(g, "graph");
+        need(model, "model");
+        if (count) {
+            need(position, "position");
+            need(affixture, "affixture");
+            need(candidate, "candidate");
+            need(last, "last");
+            need(u, "u");
+            need(r_cand, "r_cand");
+            need(r_last, "r_last");
+            need(accept, "accept");
+        }
+        mhw::run_decide(*const_cast<mhw_graph*>(g), *model, count, position, affixture, candidate, last, u, r_cand,
+                        r_last, accept, true);
+    });
+}
+
 mhw_status mhw_check(const mhw_graph* g, const mhw_model_desc* model, uint64_t seed, uint64_t count,
                      const uint32_t* position, const uint32_t* affixture, uint64_t draws, double* kl,
                      uint64_t* counts) {

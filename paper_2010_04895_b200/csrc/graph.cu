@@ -142,6 +142,8 @@ DevGraph Graph::view() const {
     d.htab = htab.n ? htab.p : nullptr;
     d.arc = arc.n ? arc.p : nullptr;
     d.bloom = bloom.n ? bloom.p : nullptr;
+    d.sprob = sprob.n ? sprob.p : nullptr;
+    d.salias = salias.n ? salias.p : nullptr;
     d.bloom_blocks = bloom_blocks;
     d.n_ntypes = n_ntypes;
     d.n_etypes = n_etypes;
@@ -151,7 +153,8 @@ DevGraph Graph::view() const {
 
 uint64_t Graph::device_bytes() const {
     return nodes.bytes() + ids.bytes() + w.bytes() + ntype.bytes() + etype.bytes() + rev.bytes() +
-           wtotal.bytes() + wblk.bytes() + tcount.bytes() + tperm.bytes() + tbase.bytes() + htab.bytes() + arc.bytes() + bloom.bytes();
+           wtotal.bytes() + wblk.bytes() + tcount.bytes() + tperm.bytes() + tbase.bytes() + htab.bytes() + arc.bytes() + bloom.bytes() +
+           sprob.bytes() + salias.bytes();
 }
 
 namespace {
@@ -1237,6 +1240,15 @@ void graph_ensure_wtotal(Graph& g) {
         k_wblk<<<grid_for((uint64_t)g.n * 32), 256, 0, g.stream>>>(g.view(), g.wblk.p);
         MHW_CK(cudaGetLastError());
     }
+    MHW_CK(cudaStreamSynchronize(g.stream));
+}
+
+void graph_ensure_static_alias(Graph& g) {
+    if (g.sprob.n || !g.w.n || !g.m) return;
+    DeviceGuard dg(g.device);
+    g.sprob.alloc(g.m);
+    g.salias.alloc(g.m);
+    graph_alias_device(g, g.sprob.p, g.salias.p);
     MHW_CK(cudaStreamSynchronize(g.stream));
 }
 

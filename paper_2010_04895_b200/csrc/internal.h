@@ -112,6 +112,8 @@ struct Graph {
     DBuf<uint32_t> bloom;    // edge Bloom filter (second-order alpha), lazily built
     uint32_t bloom_blocks = 0;
     DBuf<uint4> arc;         // arc records, lazily built (m < 2^32)
+    DBuf<double> sprob;      // static-weight alias tables (alias proposal), lazily built
+    DBuf<uint32_t> salias;
     uint16_t n_ntypes = 0, n_etypes = 0;
     bool symmetric = false;
     bool verified_sym = false;
@@ -149,6 +151,9 @@ bool graph_ensure_arcrec(Graph& g);  // deepwalk arc records (fp32 weight aux)
 void graph_alias_tables(Graph& g, double* prob, uint32_t* alias);
 // Same tables left on the device (prob, alias: m entries each).
 void graph_alias_device(Graph& g, double* prob, uint32_t* alias);
+// The same tables kept on the graph (sprob / salias) for the alias proposal
+// of the M-H walk; unweighted graphs need none (every prob is 1.0).
+void graph_ensure_static_alias(Graph& g);
 
 // Bound model (host validation of WalkModel::bind, models.cpp:29-74).
 struct Model {

@@ -69,6 +69,8 @@ struct DevGraph {
     const uint32_t* __restrict__ bloom;   // edge Bloom filter, 8 words per block (nullptr: not built)
     const uint32_t* __restrict__ tperm;   // per slice: neighbour indices ordered by (type, w > 0 first, index)
     const uint2* __restrict__ tbase;      // per (node, type): {start in tperm slice, count of w > 0}
+    const double* __restrict__ sprob;     // static alias tables per slice (alias proposal; nullptr: none)
+    const uint32_t* __restrict__ salias;
     uint32_t bloom_blocks;
     uint16_t n_ntypes;
     uint16_t n_etypes;
@@ -201,6 +203,7 @@ struct DevCfg {
     uint32_t rep_deg;            // nodes with degree >= rep_deg get replicas
     uint32_t rep_max;            // replica cap (power of two)
     uint64_t rep_base_slot;      // first slot of the replica region (= n * G)
+    int proposal;                // mhw_proposal: 0 uniform, 1 static-weight alias (Hastings accept)
     const uint32_t* rep_group;   // per node: first replica group (hubs only)
     const double* rep_scale;     // metapath2vec: per node type visit scale (nullptr: weight = degree)
 };
@@ -328,6 +331,11 @@ struct Draw {
     // uniform_real (rng.hpp:58-60) on words 1,2
     __device__ __forceinline__ double unit() const { return unit53(w.y, w.z); }
 };
+
+// Sub-counter of the accept unit of an alias-proposal step (oracle
+// OG_ACCEPT_SUB): block (walker, step, sub) words 1-2; Lemire retries use
+// sub-counters 1, 2, ... of the same block and never reach it.
+constexpr uint32_t kAcceptSub = 0x80000000u;
 
 // --------------------------------------------------------------- loads
 __device__ __forceinline__ NodeRec load_node(const DevGraph& g, uint32_t v) {
@@ -494,6 +502,28 @@ __device__ __forceinline__ double wprime(const DevGraph& g, const DevModel& m, c
     return wprime_v<KIND>(g, m, c, w, utype, out_t, cls);
 }
 
+// Dynamic factor r = w'/w of a candidate (node type utype, out edge type
+// out_t, alpha class cls): calculate_weight (models.cpp:82-123) without the
+// trailing static weight -- the Hastings ratio of the alias proposal
+// (q proportional to w) is r_c / r_l. Same association as oracle og_rfactor.
+template <int KIND>
+__device__ __forceinline__ double rfactor(const DevGraph& g, const DevModel& m, const SCtx& c, uint16_t utype,
+                                          uint32_t out_t, uint32_t cls) {
+    if (KIND == DEEPWALK) return 1.0;
+    if (KIND == METAPATH2VEC) return utype == c.req ? 1.0 : 0.0;
+    if (c.boot) return 1.0;
+    const double a = alpha_value(m, cls);
+    if (KIND == NODE2VEC) return a;
+    if (KIND == EDGE2VEC) return __dmul_rn(a, __ldg(m.M + (size_t)c.in_type * m.M_dim + out_t));
+    return __ddiv_rn(a, (double)__ldg(g.tcount + (size_t)c.v * g.n_ntypes + utype));
+}
+
+// Hastings accept of an alias proposal (og_hastings): candidate of static
+// weight w_c, factors r_c, r_l, unit u.
+__device__ __forceinline__ bool hastings_accept(double w_c, double r_c, double r_l, double u) {
+    return w_c > 0.0 && (r_l <= 0.0 || r_c >= r_l || __dmul_rn(u, r_l) < r_c);
+}
+
 template <int KIND>
 __host__ __device__ constexpr bool needs_utype() {
     return KIND == METAPATH2VEC || KIND == FAIRWALK || KIND == EDGE2VEC;
@@ -522,6 +552,31 @@ __device__ __forceinline__ double eval_index(const DevGraph& g, const DevModel& 
     }
     *cls_out = cls;
     return wprime<KIND>(g, m, c, i, utype, cls);
+}
+
+// The same evaluation as eval_index, returning the dynamic factor r = w'/w
+// (rfactor) of candidate i -- the alias proposal's Hastings ratio input.
+template <int KIND>
+__device__ __forceinline__ double eval_rfactor(const DevGraph& g, const DevModel& m, const SCtx& c, uint32_t i) {
+    uint32_t cls = 0;
+    uint16_t utype = 0;
+    if (KIND != DEEPWALK) {
+        const uint32_t u = load_id(g, c.off + i);
+        if (second_order(KIND) && !c.boot && !m.alpha_trivial) {
+            if (needs_utype<KIND>()) {
+                const NodeRec r = load_node(g, u);
+                utype = r.type;
+                cls = alpha_class(g, m, c, u, &r);
+            } else {
+                cls = alpha_class(g, m, c, u, nullptr, -1, true);
+            }
+        } else {
+            if (needs_utype<KIND>()) utype = load_node(g, u).type;
+            if (second_order(KIND)) cls = 1;
+        }
+    }
+    const uint32_t out_t = (KIND == EDGE2VEC && !c.boot) ? edge_type_of(g, c.off + i, c.vtype, utype) : 0u;
+    return rfactor<KIND>(g, m, c, utype, out_t, cls);
 }
 
 // accept rule, samplers.hpp:24

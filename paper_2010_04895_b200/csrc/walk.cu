@@ -116,8 +116,12 @@ __device__ __noinline__ uint32_t init_slot_ool(const DevGraph g, const DevModel 
 // AR = 2 (node2vec, small node tables): narrow 8-byte records {u, chain
 // word}; the candidate's degree and offset come from its L2-resident node
 // record, so the record array the walk gathers from is half as large.
-template <int KIND, int REGS, bool LAZY, int AR>
+// AR = 4: the plain-CSR variant (as AR = 0) with the static-weight alias
+// proposal and the Hastings accept (mhw_walk_config.proposal = ALIAS).
+template <int KIND, int REGS, bool LAZY, int ARV>
 __global__ void __launch_bounds__(kWalkBlock) __maxnreg__(REGS) k_walk(RunParams P) {
+    constexpr bool ALIAS = ARV == 4;
+    constexpr int AR = ALIAS ? 0 : ARV;
     const DevGraph& g = P.g;
     constexpr bool TYPED = AR && needs_utype<KIND>();
     constexpr bool CC = AR && second_order(KIND);
@@ -249,8 +253,21 @@ __global__ void __launch_bounds__(kWalkBlock) __maxnreg__(REGS) k_walk(RunParams
                 } else {
                     e = atomicExch(cw, kLocked);
                 }
-                const uint32_t cand = d.index(c.deg);
-                const double u = d.unit();
+                uint32_t cand;
+                double u;
+                if constexpr (ALIAS) {
+                    // alias_sample (samplers.hpp:65-68) of v's static table:
+                    // index on word 0, coin on words 1-2; the accept unit
+                    // from sub-block kAcceptSub
+                    const uint32_t i = d.index(c.deg);
+                    cand = (!g.sprob || d.unit() < __ldg(g.sprob + c.off + i)) ? i : __ldg(g.salias + c.off + i);
+                    Draw da;
+                    da.open_sub(wkey, walker, step, kAcceptSub);
+                    u = da.unit();
+                } else {
+                    cand = d.index(c.deg);
+                    u = d.unit();
+                }
                 // fairwalk: v's group sizes (one row of <= 4 types) are read
                 // with the candidate's record instead of after it
                 uint32_t grp0 = 0, grp1 = 0, grp2 = 0, grp3 = 0;
@@ -400,7 +417,19 @@ __global__ void __launch_bounds__(kWalkBlock) __maxnreg__(REGS) k_walk(RunParams
                 else if (AR && KIND == DEEPWALK) wl = (double)__uint_as_float(al.w);
                 else if (TYPED) wl = wprime_v<KIND>(g, P.m, c, (double)__uint_as_float(al.w), rl.type, bl.x >> 16, cls_l);
                 else wl = wprime<KIND>(g, P.m, c, last, rl.type, cls_l);
-                const bool acc = mh_accept(wc, wl, u) && cand != last;
+                bool acc;
+                if constexpr (ALIAS) {
+                    // Hastings: target w' = r w, proposal q ~ w -> min(1, r_c / r_l)
+                    const uint32_t ot_c = KIND == EDGE2VEC ? edge_type_of(g, c.off + cand, c.vtype, rc.type) : 0u;
+                    const uint32_t ot_l = KIND == EDGE2VEC ? edge_type_of(g, c.off + last, c.vtype, rl.type) : 0u;
+                    const double r_c = rfactor<KIND>(g, P.m, c, rc.type, ot_c, cls_c);
+                    const double r_l = rfactor<KIND>(g, P.m, c, rl.type, ot_l, cls_l);
+                    acc = hastings_accept(static_w(g, c.off + cand), r_c, r_l, u) && cand != last;
+                    (void)wc;
+                    (void)wl;
+                } else {
+                    acc = mh_accept(wc, wl, u) && cand != last;
+                }
                 if (WLC)
                     atom_exch128(cb, acc ? make_uint4(tx, pack_entry(cand, cls_c), (uint32_t)__double2loint(wc),
                                                       (uint32_t)__double2hiint(wc))
@@ -997,7 +1026,7 @@ __global__ void k_decide(DevGraph g, DevModel m, uint64_t n, const uint32_t* __r
                          const uint32_t* __restrict__ aff, const uint32_t* __restrict__ cand,
                          const uint32_t* __restrict__ last, const double* __restrict__ u,
                          double* __restrict__ wc, double* __restrict__ wl, uint8_t* __restrict__ acc,
-                         unsigned* __restrict__ bad) {
+                         unsigned* __restrict__ bad, int hastings) {
     for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
          i += (uint64_t)gridDim.x * blockDim.x) {
         const uint32_t v = pos[i], a = aff[i];
@@ -1014,6 +1043,14 @@ __global__ void k_decide(DevGraph g, DevModel m, uint64_t n, const uint32_t* __r
             continue;
         }
         const SCtx c = make_ctx<KIND>(g, m, v, a);
+        if (hastings) {  // alias proposal: (r_c, r_l, Hastings accept)
+            const double x = eval_rfactor<KIND>(g, m, c, cand[i]);
+            const double y = eval_rfactor<KIND>(g, m, c, last[i]);
+            wc[i] = x;
+            wl[i] = y;
+            acc[i] = hastings_accept(static_w(g, c.off + cand[i]), x, y, u[i]) ? 1 : 0;
+            continue;
+        }
         uint32_t cls;
         const double x = eval_index<KIND>(g, m, c, cand[i], &cls);
         const double y = eval_index<KIND>(g, m, c, last[i], &cls);
@@ -1213,7 +1250,8 @@ void with_variant(int regs, bool lazy, int ar, F&& f) {
                 return;
             }
         }
-        if (ar) by_regs(lz, std::integral_constant<int, 1>{});
+        if (ar == 4) by_regs(lz, std::integral_constant<int, 4>{});
+        else if (ar) by_regs(lz, std::integral_constant<int, 1>{});
         else by_regs(lz, std::integral_constant<int, 0>{});
     };
     if (lazy) by_ar(T{});
@@ -1424,6 +1462,11 @@ void session_create(Session& s, Graph& g, const mhw_model_desc& md, const mhw_wa
     if (wc.sampler < 0 || wc.sampler > 3) invalid("unknown sampler kind");
     if (wc.init_kind < 0 || wc.init_kind > 2) invalid("unknown init strategy");
     if (wc.schedule < 0 || wc.schedule > 1) invalid("unknown schedule");
+    if (wc.proposal < 0 || wc.proposal > 1) invalid("unknown proposal");
+    if (wc.proposal == MHW_PROPOSAL_ALIAS && wc.sampler != MHW_SAMPLER_MH)
+        invalid("the alias proposal applies to the mh sampler only");
+    if (wc.proposal == MHW_PROPOSAL_ALIAS && wc.schedule == MHW_SCHEDULE_DETERMINISTIC)
+        invalid("the alias proposal runs on the throughput schedule only");
     s.g = &g;
     s.wc = wc;
     const bool trace = std::getenv("MHW_TRACE") != nullptr;
@@ -1438,6 +1481,7 @@ void session_create(Session& s, Graph& g, const mhw_model_desc& md, const mhw_wa
     s.cfg.init_kind = wc.init_kind;
     s.cfg.burn_in = wc.burn_in_steps;
     s.cfg.hw = wc.hw_sample_size;
+    s.cfg.proposal = wc.proposal;
     s.node_begin = wc.node_begin;
     s.node_end = wc.node_end ? wc.node_end : g.n;
     if (s.node_end > g.n || s.node_begin > s.node_end) invalid("node range out of bounds");
@@ -1615,7 +1659,11 @@ void session_create(Session& s, Graph& g, const mhw_model_desc& md, const mhw_wa
         try_pin(pin_p, pin_bytes);
         // arc records (after the session buffers, so the memory check sees them)
         const char* ar_env = std::getenv("MHW_ARC_RECORDS");
-        const bool want_ar = !(ar_env && ar_env[0] == '0');
+        // the alias proposal walks the plain CSR (k_walk AR = 4) with the
+        // graph's static alias tables
+        const bool alias_prop = wc.proposal == MHW_PROPOSAL_ALIAS;
+        if (alias_prop) graph_ensure_static_alias(g);
+        const bool want_ar = !(ar_env && ar_env[0] == '0') && !alias_prop;
         // node2vec compact chains (AR 3): 16-bit words in their own table when
         // it and the node table fit L2 (MHW_C16=0/1 forces)
         const char* c16e = std::getenv("MHW_C16");
@@ -1623,9 +1671,13 @@ void session_create(Session& s, Graph& g, const mhw_model_desc& md, const mhw_wa
                             g.max_deg <= 0xFFFDu && want_ar;
         const bool c16_want = c16_ok && (c16e ? c16e[0] == '1' : (2ull * g.m <= (96ull << 20) && 16ull * g.n <= (32ull << 20)));
         if (c16_want) {
-            // MHW_C16_PIN: filter (default) | chain | both ([c16 | filter copy], one window) | none
+            // MHW_C16_PIN: chain (default: the 16-bit table pinned for the
+            // walk, the edge filter for the eager init) | filter | both
+            // ([c16 | filter copy], one window) | none. cfg2 walk + init:
+            // chain 27.65 + 5.3 ms, both 27.1 + 6.8-9.5, filter 31.6 + 4.7,
+            // none 32.8 + 4.7; narrow records 29.5 + 4.7
             const char* pm = std::getenv("MHW_C16_PIN");
-            const std::string mode = pm ? pm : "filter";
+            const std::string mode = pm ? pm : "chain";
             const uint64_t cw = (g.m + 1) / 2;
             const uint64_t cw_al = (cw + 63) & ~63ull;  // 256-byte aligned filter copy
             const bool both = mode == "both" && g.bloom.n && !m.alpha_trivial;
@@ -2211,7 +2263,7 @@ void session_run_packed(Session& s, uint32_t* h_nodes, uint64_t cap_nodes, uint6
 // ------------------------------------------------------------ parity API
 void run_decide(Graph& g, const mhw_model_desc& md, uint64_t n, const uint32_t* pos, const uint32_t* aff,
                 const uint32_t* cand, const uint32_t* last, const double* u, double* wc, double* wl,
-                uint8_t* acc) {
+                uint8_t* acc, bool hastings) {
     DeviceGuard dg(g.device);
     Model mb;
     model_bind(mb, g, md);
@@ -2231,7 +2283,7 @@ void run_decide(Graph& g, const mhw_model_desc& md, uint64_t n, const uint32_t* 
     dispatch(md.kind, [&](auto kc) {
         constexpr int KIND = decltype(kc)::value;
         k_decide<KIND><<<grid_for(n), 256, 0, st>>>(gv, mb.dev, n, dpos.p, daff.p, dc.p, dl.p, du.p, dwc.p, dwl.p,
-                                                   dacc.p, bad.p);
+                                                   dacc.p, bad.p, hastings ? 1 : 0);
     });
     MHW_CK(cudaGetLastError());
     unsigned hbad = 0;
@@ -2249,7 +2301,7 @@ void run_init_states(Graph& g, const mhw_model_desc& md, const mhw_walk_config& 
     Model mb;
     model_bind(mb, g, md);
     if (!n) return;
-    DevCfg cfg;
+    DevCfg cfg{};
     cfg.seed = wc.seed;
     cfg.K = wc.walks_per_node;
     cfg.L = wc.walk_length;

@@ -92,7 +92,10 @@ struct Session {
     Session& operator=(const Session&) = delete;
     ~Session();
     RunParams params() const;
-    int ar_mode() const { return c16.n ? 3 : (use_ar ? (rec_u32 == 2 ? 2 : 1) : 0); }
+    int ar_mode() const {
+        if (cfg.proposal == MHW_PROPOSAL_ALIAS) return 4;  // plain CSR + alias proposal
+        return c16.n ? 3 : (use_ar ? (rec_u32 == 2 ? 2 : 1) : 0);
+    }
 };
 
 uint64_t k_slots(int kind, const Graph& g);
@@ -118,7 +121,7 @@ void session_download_packed(Session& s, uint32_t* h_nodes, uint64_t cap_nodes, 
                              uint64_t cap_rows, uint64_t* n_nodes, cudaStream_t stream);
 void run_decide(Graph& g, const mhw_model_desc& md, uint64_t n, const uint32_t* pos, const uint32_t* aff,
                 const uint32_t* cand, const uint32_t* last, const double* u, double* wc, double* wl,
-                uint8_t* acc);
+                uint8_t* acc, bool hastings = false);
 void run_init_states(Graph& g, const mhw_model_desc& md, const mhw_walk_config& wc, uint64_t n,
                      const uint32_t* pos, const uint32_t* aff, uint32_t* last);
 void partition_nodes(Graph& g, const mhw_model_desc& md, int parts, uint32_t* cuts);

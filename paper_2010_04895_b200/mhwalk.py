@@ -514,6 +514,20 @@ def decide(graph: Graph, model: WalkModel, position, affixture, candidate, last,
     return wc[:n], wl[:n], acc[:n]
 
 
+def decide_hastings(graph: Graph, model: WalkModel, position, affixture, candidate, last, u):
+    """Alias-proposal decisions on the GPU: (r(cand), r(last), accept) with
+    r = w'/w and the Hastings accept (mhw_decide_hastings)."""
+    d, keep = model._desc()
+    arrs = [np.ascontiguousarray(x, dtype=np.uint32) for x in (position, affixture, candidate, last)]
+    uu = np.ascontiguousarray(u, dtype=np.float64)
+    n = len(uu)
+    rc, rl = np.zeros(max(n, 1)), np.zeros(max(n, 1))
+    acc = np.zeros(max(n, 1), dtype=np.uint8)
+    _check(L.lib().mhw_decide_hastings(graph.handle, C.byref(d), n, *[_ptr(a) for a in arrs], _ptr(uu), _ptr(rc),
+                                       _ptr(rl), _ptr(acc)))
+    return rc[:n], rl[:n], acc[:n]
+
+
 def check(graph: Graph, model: WalkModel, position, affixture, draws: int, seed: int = 0,
           tolerance: float | None = None):
     """cmd_check (tools/mhwalk.cpp:222-264) on the GPU: per-state KL of a

@@ -21,24 +21,29 @@ from scipy import stats as st
 from oracle import oracle as O
 
 
-def mh_kernel(pi: np.ndarray, proposals: int | None = None) -> np.ndarray:
-    """Exact uniform-proposal M-H kernel (tests/oracles.hpp:207-220) on the
-    support pi; `proposals` = size of the proposal set (the full degree:
+def mh_kernel(pi: np.ndarray, proposals: int | None = None, q: np.ndarray | None = None) -> np.ndarray:
+    """Exact M-H kernel on the support pi. Uniform proposal (tests/oracles.hpp:
+    207-220): `proposals` = size of the proposal set (the full degree:
     zero-weight candidates are proposed too and always rejected,
-    samplers.hpp:21)."""
+    samplers.hpp:21). Independent proposal q (the alias proposal, q ~ static
+    weights; q over the support, summing to <= 1 when some proposals fall
+    outside it and are rejected): P_ij = q_j min(1, (pi_j / q_j) / (pi_i / q_i))."""
     n = len(pi)
-    m = proposals or n
     P = np.zeros((n, n))
     for i in range(n):
         with np.errstate(divide="ignore", invalid="ignore"):
-            P[i] = np.minimum(1.0, np.where(pi[i] > 0, pi / pi[i], 1.0)) / m
+            if q is None:
+                P[i] = np.minimum(1.0, np.where(pi[i] > 0, pi / pi[i], 1.0)) / (proposals or n)
+            else:
+                P[i] = q * np.minimum(1.0, (pi / q) / (pi[i] / q[i]))
         P[i, i] = 0.0
         P[i, i] = 1.0 - P[i].sum()
     return P
 
 
-def markov_chi2(counts: np.ndarray, pi: np.ndarray) -> tuple[float, int, float]:
-    """(statistic, dof, p-value) of the chain-CLT chi-square on the support."""
+def markov_chi2(counts: np.ndarray, pi: np.ndarray, q: np.ndarray | None = None) -> tuple[float, int, float]:
+    """(statistic, dof, p-value) of the chain-CLT chi-square on the support.
+    q: the alias proposal's probabilities over all candidates (None: uniform)."""
     sup = pi > 0
     pi_s = pi[sup] / pi[sup].sum()
     c = counts[sup].astype(np.float64)
@@ -47,7 +52,7 @@ def markov_chi2(counts: np.ndarray, pi: np.ndarray) -> tuple[float, int, float]:
     n = len(pi_s)
     if n < 2:
         return 0.0, 0, 1.0
-    P = mh_kernel(pi_s, proposals=len(pi))
+    P = mh_kernel(pi_s, proposals=len(pi), q=None if q is None else q[sup] / q.sum())
     Z = np.linalg.inv(np.eye(n) - P + np.outer(np.ones(n), pi_s))
     D = np.diag(pi_s)
     S = D @ Z + Z.T @ D - D - np.outer(pi_s, pi_s)
@@ -92,8 +97,10 @@ def _mp_index(i, mp):
     return a
 
 
-def audit(g: O.HostGraph, oracle: O.Oracle, md: O.ModelDesc, rows, lens, min_visits=5000, max_states=40):
-    """p-values of the chain chi-square for states visited >= min_visits."""
+def audit(g: O.HostGraph, oracle: O.Oracle, md: O.ModelDesc, rows, lens, min_visits=5000, max_states=40,
+          alias_proposal=False):
+    """p-values of the chain chi-square for states visited >= min_visits
+    (alias_proposal: the chains ran the static-weight alias proposal)."""
     tr = transitions(rows, lens, md.kind, md.metapath)
     pv = []
     for key, nxt in sorted(tr.items(), key=lambda kv: -sum(kv[1].values()))[:max_states]:
@@ -113,7 +120,8 @@ def audit(g: O.HostGraph, oracle: O.Oracle, md: O.ModelDesc, rows, lens, min_vis
         counts = np.zeros(len(nb))
         for u, cnt in nxt.items():
             counts[int(np.searchsorted(nb, u))] += cnt
-        pv.append(markov_chi2(counts, pi)[2])
+        q = g.w[int(g.offsets[v]):int(g.offsets[v + 1])].astype(np.float64) if alias_proposal else None
+        pv.append(markov_chi2(counts, pi, q)[2])
     return np.array(pv)
 
 

@@ -59,10 +59,10 @@ def oracle_model(cfg):
     return md
 
 
-def oracle_cfg(cfg, K, replica_degree):
+def oracle_cfg(cfg, K, replica_degree, proposal=0):
     init = {"random": O.INIT_RANDOM, "high_weight": O.INIT_HIGH_WEIGHT, "burn_in": O.INIT_BURN_IN}[cfg["init"]]
     return O.WalkCfg(K=K, L=cfg["L"], seed=bench.WALK_SEED, init_kind=init, burn_in_steps=cfg.get("burn_in", 100),
-                     hw_sample_size=32, replica_degree=replica_degree)
+                     hw_sample_size=32, replica_degree=replica_degree, proposal=proposal)
 
 
 def pick_starts(hg, cfg, seed):
@@ -78,7 +78,7 @@ def pick_starts(hg, cfg, seed):
     return np.sort(np.concatenate([hubs, rnd])).astype(np.uint32)
 
 
-def pin(mhw, oracle, cfg_name, init_mode=0, env=None, n_starts=None):
+def pin(mhw, oracle, cfg_name, init_mode=0, env=None, n_starts=None, proposal=0):
     cfg = dict(bench.CONFIGS[cfg_name])
     old = {}
     for k, v in (env or {}).items():
@@ -86,7 +86,7 @@ def pin(mhw, oracle, cfg_name, init_mode=0, env=None, n_starts=None):
         os.environ[k] = v
     try:
         dg = bench.build_graph(cfg)
-        wc = dataclasses.replace(bench.make_config(cfg), walks_per_node=1, init_mode=init_mode)
+        wc = dataclasses.replace(bench.make_config(cfg), walks_per_node=1, init_mode=init_mode, proposal=proposal)
         s = mhw.Session(dg, bench.make_model(cfg), wc)
     finally:
         for k, v in old.items():
@@ -108,7 +108,7 @@ def pin(mhw, oracle, cfg_name, init_mode=0, env=None, n_starts=None):
         table = torch.empty(s.chain_size() * s.record_width(), dtype=torch.int32, device="cuda")
         s.init_records(0, s.chain_size(), table.data_ptr())
         torch.cuda.synchronize()
-    orows, olens, ost = oracle.walk_isolated(hg, md, oracle_cfg(cfg, 1, wc.chain_replica_degree), starts)
+    orows, olens, ost = oracle.walk_isolated(hg, md, oracle_cfg(cfg, 1, wc.chain_replica_degree, proposal), starts)
     assert len(olens) == len(starts)
     steps = 0
     for j, v in enumerate(starts):

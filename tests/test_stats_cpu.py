@@ -125,3 +125,65 @@ def test_transition_counts_gpu_equals_transitions(oracle, kind):
         exp = np.array([ref[key].get(int(u), 0) for u in nb])
         assert counts.sum() == vis == exp.sum()
         assert np.array_equal(counts, exp)
+
+
+def test_alias_proposal_kernel_is_calibrated_and_has_power():
+    """The independent-proposal kernel of tests/stats.py (alias proposal, q ~
+    static weights): exact Hastings chains pass, a chain that forgets the
+    correction (accepting with min(1, w'_c / w'_l)) fails."""
+    r = np.random.default_rng(11)
+    w = np.array([1.0, 3.0, 0.5, 2.0, 6.0, 1.5])         # static weights (proposal)
+    f = np.array([4.0, 1.0, 0.25, 1.0, 0.25, 1.0])       # dynamic factors r = w'/w
+    pi = w * f / np.sum(w * f)
+    q = w / w.sum()
+
+    def chain(steps, hastings=True):
+        x, c = 0, np.zeros(len(w))
+        for cand, u in zip(r.choice(len(w), size=steps, p=q), r.random(steps)):
+            a, b = (f[cand], f[x]) if hastings else (w[cand] * f[cand], w[x] * f[x])
+            if a >= b or u * b < a:
+                x = int(cand)
+            c[x] += 1
+        return c
+
+    assert markov_chi2(chain(100000), pi, q)[2] > 1e-3
+    assert markov_chi2(chain(100000, hastings=False), pi, q)[2] < 1e-6
+
+
+@pytest.mark.parametrize("kind", [O.DEEPWALK, O.NODE2VEC, O.METAPATH2VEC, O.EDGE2VEC, O.FAIRWALK])
+def test_oracle_alias_proposal_chains_hit_the_target(oracle, kind):
+    """The oracle's alias-proposal M-H (og_walk: static alias table proposal,
+    og_hastings accept) leaves the per-state targets of calculate_weight
+    invariant: its corpus passes the chain chi-square with the alias kernel."""
+    from tests.stats import audit
+    from tests.helpers import typed_random_graph
+    g = typed_random_graph(700 + kind, 40, 4.0, weighted=True, types=2)
+    md = model_desc(kind, g, p=0.5, q=2.0, M=np.random.default_rng(kind).uniform(0.5, 2.0, (4, 4)),
+                    metapath=(0, 1, 0))
+    cfg = O.WalkCfg(K=400, L=80, seed=5, init_kind=O.INIT_RANDOM, proposal=1)
+    rows, lens, _ = oracle.generate_walks(g, md, cfg, rng=O.RNG_PHILOX, order=O.ORDER_STEP)
+    ok, msg = gate(audit(g, oracle, md, rows, lens, min_visits=5000, alias_proposal=True))
+    assert ok, msg
+
+
+def test_oracle_hastings_decisions_restated(oracle):
+    """og_decide_hastings = the factor ratio rule restated here: r = w'/w
+    (exact for node2vec: alpha), accept iff w_c > 0 and (r_l <= 0 or r_c >= r_l
+    or u r_l < r_c)."""
+    from tests.helpers import random_triples
+    rng = O.XoRng(5)
+    g = O.random_graph(120, 6.0, True, rng)
+    md = model_desc(O.NODE2VEC, g, p=0.3, q=3.0)
+    pos, aff, cand, last, u = random_triples(g, md, 5000, seed=2)
+    rc, rl, acc = oracle.decide_hastings(g, md, pos, aff, cand, last, u)
+    wc, wl, _ = oracle.decide(g, md, pos, aff, cand, last, u)
+    off = g.offsets.astype(np.int64)
+    w_c = g.w[off[pos] + cand]
+    w_l = g.w[off[pos] + last]
+    boot = aff == O.NO_AFFIX
+    assert np.all(rc[boot] == 1.0)
+    alpha_ok = np.isin(rc[~boot], [1 / 0.3, 1.0, 1 / 3.0])
+    assert np.all(alpha_ok)
+    assert np.array_equal(wc, rc * w_c) and np.array_equal(wl, rl * w_l)  # node2vec: a * w
+    want = (w_c > 0) & ((rl <= 0) | (rc >= rl) | (u * rl < rc))
+    assert np.array_equal(acc.astype(bool), want)
