@@ -245,6 +245,20 @@ __global__ void __launch_bounds__(kWalkBlock) __maxnreg__(REGS) k_walk(RunParams
                 uint4* const cb = WLC ? P.ac + 2 * loc + 1 : nullptr;
                 uint4 E = make_uint4(0, 0, 0, 0);
                 uint32_t e;
+                uint32_t cand;
+                double u;
+                uint32_t c16_uc = 0;
+                if constexpr (C16) {
+                    // compact chains: the candidate id load (DRAM) is issued
+                    // first and the lock right after it, with no dependency
+                    // between them (the lock's timing still cannot depend on
+                    // the proposal); otherwise the scheduler waits for the
+                    // atomic's return before issuing the load (ncu: 13% of the
+                    // stall samples on the decode of the lock word)
+                    cand = d.index(c.deg);
+                    u = d.unit();
+                    c16_uc = __ldg(g.ids + c.off + cand);
+                }
                 if (WLC) {
                     E = atom_exch128(cb, make_uint4(tx, kLocked, 0u, 0u));
                     e = E.y;
@@ -253,9 +267,8 @@ __global__ void __launch_bounds__(kWalkBlock) __maxnreg__(REGS) k_walk(RunParams
                 } else {
                     e = atomicExch(cw, kLocked);
                 }
-                uint32_t cand;
-                double u;
-                if constexpr (ALIAS) {
+                if constexpr (C16) {
+                } else if constexpr (ALIAS) {
                     // alias_sample (samplers.hpp:65-68) of v's static table:
                     // index on word 0, coin on words 1-2; the accept unit
                     // from sub-block kAcceptSub
@@ -291,7 +304,7 @@ __global__ void __launch_bounds__(kWalkBlock) __maxnreg__(REGS) k_walk(RunParams
                     // computed and issued before the candidate's node record is
                     // consumed, so the two L2 accesses overlap instead of
                     // running back to back.
-                    const uint2 x = C16 ? make_uint2(__ldg(g.ids + c.off + cand), 0u)
+                    const uint2 x = C16 ? make_uint2(c16_uc, 0u)
                                         : __ldg(reinterpret_cast<const uint2*>(P.ac) + c.off + cand);
                     // A Last of the heaviest alpha class is rejected away from
                     // most of the time (cfg2: the return class, 1/p = 4): fetch
@@ -434,7 +447,7 @@ __global__ void __launch_bounds__(kWalkBlock) __maxnreg__(REGS) k_walk(RunParams
                     atom_exch128(cb, acc ? make_uint4(tx, pack_entry(cand, cls_c), (uint32_t)__double2loint(wc),
                                                       (uint32_t)__double2hiint(wc))
                                          : make_uint4(tx, e, E.z, E.w));
-                else if (C16)
+                else if (C16)  // (a 16-bit store release measured the same: 25.44 vs 25.25 ms)
                     c16_release(cw, csh, c16_enc(acc ? pack_entry(cand, cls_c) : e, c.deg));
                 else
                     chain_release(cw, acc ? pack_entry(cand, cls_c) : e);
@@ -1708,9 +1721,15 @@ void session_create(Session& s, Graph& g, const mhw_model_desc& md, const mhw_wa
                     // the eager init (burn-in over N(v) slices) keeps the
                     // filter-only window: pinning the chain table there
                     // starves its slice reads (cfg2 init 4.7 -> 6.8 ms)
-                    if (g.bloom.n && !m.alpha_trivial && g.bloom.bytes() <= (33ull << 20)) {
+                    const char* ip = std::getenv("MHW_C16_INITPIN");  // filter (default) | same | none
+                    const std::string imode = ip ? ip : "filter";
+                    if (imode == "filter" && g.bloom.n && !m.alpha_trivial && g.bloom.bytes() <= (33ull << 20)) {
                         s.ipin_p = both ? (void*)s.bloom_copy : (void*)g.bloom.p;
                         s.ipin_bytes = g.bloom.bytes();
+                    } else if (imode == "none") {
+                        s.ipin_p = s.c16.p;
+                        s.ipin_bytes = 0;
+                        s.init_unpinned = true;
                     }
                 }
                 if (trace)
@@ -1847,7 +1866,7 @@ void session_run(Session& s, cudaStream_t user) {
     cudaStreamAttrValue prev_window{};
     if (pin) {
         prev_window = l2_window_save(st);
-        if (s.ipin_bytes) l2_window(st, s.ipin_p, s.ipin_bytes);
+        if (s.ipin_bytes || s.init_unpinned) l2_window(st, s.ipin_p, s.ipin_bytes);
         else l2_window(st, s.pin_p, s.pin_bytes, s.pin_ratio);
     }
     const bool preloaded = s.chain_loaded;  // mhw_session_load_chain: table already initialised
@@ -1911,7 +1930,7 @@ void session_run(Session& s, cudaStream_t user) {
                 }
                 MHW_CK(cudaEventRecord(s.evm, st));
                 evm_done = true;
-                if (pin && s.ipin_bytes) l2_window(st, s.pin_p, s.pin_bytes, s.pin_ratio);
+                if (pin && (s.ipin_bytes || s.init_unpinned)) l2_window(st, s.pin_p, s.pin_bytes, s.pin_ratio);
                 with_variant<KIND>(s.minb, !s.eager_init, s.ar_mode(), [&](auto rg, auto lz, auto ar) {
                     k_walk<KIND, decltype(rg)::value, decltype(lz)::value, decltype(ar)::value>
                         <<<s.grid, kWalkBlock, 0, st>>>(P);
@@ -2172,7 +2191,7 @@ void session_run_packed(Session& s, uint32_t* h_nodes, uint64_t cap_nodes, uint6
         const bool pin = s.l2_pin;
         const cudaStreamAttrValue prev_window = pin ? l2_window_save(S) : cudaStreamAttrValue{};
         if (pin) {
-            if (s.ipin_bytes) l2_window(S, s.ipin_p, s.ipin_bytes);
+            if (s.ipin_bytes || s.init_unpinned) l2_window(S, s.ipin_p, s.ipin_bytes);
             else l2_window(S, s.pin_p, s.pin_bytes, s.pin_ratio);
         }
         MHW_CK(cudaEventRecord(s.ev0, S));
@@ -2184,7 +2203,7 @@ void session_run_packed(Session& s, uint32_t* h_nodes, uint64_t cap_nodes, uint6
             }
         });
         MHW_CK(cudaEventRecord(s.evm, S));
-        if (pin && s.ipin_bytes) l2_window(S, s.pin_p, s.pin_bytes, s.pin_ratio);
+        if (pin && (s.ipin_bytes || s.init_unpinned)) l2_window(S, s.pin_p, s.pin_bytes, s.pin_ratio);
         uint64_t H = 0;
         auto issue_copy = [&](int c) {
             MHW_CK(cudaEventSynchronize(ev[c]));

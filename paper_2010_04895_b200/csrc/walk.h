@@ -80,6 +80,7 @@ struct Session {
     float pin_ratio = 1.0f;     // hitRatio of the window (set-aside / window bytes)
     void* ipin_p = nullptr;     // window of the eager-init launch when it differs (the edge filter only)
     size_t ipin_bytes = 0;
+    bool init_unpinned = false;  // the eager-init launch runs without a window
     bool use_ar = false;     // arc-record walk kernel variant
     int minb = 1;
     uint32_t launches = 0;
