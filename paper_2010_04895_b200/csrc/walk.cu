@@ -138,8 +138,8 @@ __global__ void __launch_bounds__(kWalkBlock) __maxnreg__(REGS) k_walk(RunParams
     auto load_rec = [&](uint64_t arc, uint4& b) {
         if constexpr (C16) {
             const uint32_t u = __ldg(g.ids + arc);
-            const NodeRec r = load_node(g, u);
-            return make_uint4(u, r.deg | ((r.flags & NF_ALLPOS) ? 0x80000000u : 0u), (uint32_t)r.off, 0u);
+            const uint2 r = __ldg(P.nodes8 + u);
+            return make_uint4(u, r.y, r.x, 0u);
         }
         if constexpr (NARROW) {
             const uint2 x = __ldg(reinterpret_cast<const uint2*>(P.ac) + arc);
@@ -319,13 +319,25 @@ __global__ void __launch_bounds__(kWalkBlock) __maxnreg__(REGS) k_walk(RunParams
                         spec_l = true;
                     }
                     uc = x.x;
-                    const int4 nraw = __ldg(reinterpret_cast<const int4*>(g.nodes) + uc);  // issued first
-                    if (g.bloom && !P.m.alpha_trivial && uc != c.s) pre_bloom = bloom_maybe(g, c.s, uc) ? 1 : 0;
-                    rc.off = ((long long)(uint32_t)nraw.y << 32) | (uint32_t)nraw.x;
-                    rc.deg = (uint32_t)nraw.z;
-                    rc.type = (uint16_t)((uint32_t)nraw.w & 0xFFFFu);
-                    rc.flags = (uint16_t)((uint32_t)nraw.w >> 16);
-                    ac = make_uint4(uc, rc.deg | ((rc.flags & NF_ALLPOS) ? 0x80000000u : 0u), (uint32_t)rc.off, x.y);
+                    if constexpr (C16) {
+                        // 8-byte node record {off, deg | allpos << 31}
+                        const uint2 nr = __ldg(P.nodes8 + uc);  // issued first
+                        if (g.bloom && !P.m.alpha_trivial && uc != c.s) pre_bloom = bloom_maybe(g, c.s, uc) ? 1 : 0;
+                        rc.off = nr.x;
+                        rc.deg = nr.y & 0x7FFFFFFFu;
+                        rc.type = 0;
+                        rc.flags = (nr.y >> 31) ? NF_ALLPOS : 0;
+                        ac = make_uint4(uc, nr.y, nr.x, 0u);
+                    } else {
+                        const int4 nraw = __ldg(reinterpret_cast<const int4*>(g.nodes) + uc);  // issued first
+                        if (g.bloom && !P.m.alpha_trivial && uc != c.s) pre_bloom = bloom_maybe(g, c.s, uc) ? 1 : 0;
+                        rc.off = ((long long)(uint32_t)nraw.y << 32) | (uint32_t)nraw.x;
+                        rc.deg = (uint32_t)nraw.z;
+                        rc.type = (uint16_t)((uint32_t)nraw.w & 0xFFFFu);
+                        rc.flags = (uint16_t)((uint32_t)nraw.w >> 16);
+                        ac = make_uint4(uc, rc.deg | ((rc.flags & NF_ALLPOS) ? 0x80000000u : 0u), (uint32_t)rc.off,
+                                        x.y);
+                    }
                     rc_early = true;
                 } else if constexpr (AR) {
                     ac = load_rec(c.off + cand, bc);
@@ -461,7 +473,10 @@ __global__ void __launch_bounds__(kWalkBlock) __maxnreg__(REGS) k_walk(RunParams
                     } else if (kSpec) {
                         an = al;
                         bn = bl;
-                    } else if ((NARROW || C16) && spec_l && (e & kIdxMask) == last) {
+                    } else if (C16 && spec_l) {
+                        const uint2 r = __ldg(P.nodes8 + xl.x);
+                        an = make_uint4(xl.x, r.y, r.x, 0u);
+                    } else if (NARROW && spec_l && (e & kIdxMask) == last) {
                         const NodeRec r = load_node(g, xl.x);
                         an = make_uint4(xl.x, r.deg | ((r.flags & NF_ALLPOS) ? 0x80000000u : 0u), (uint32_t)r.off, xl.y);
                     } else {
@@ -815,6 +830,15 @@ __global__ void k_arc_chain(DevGraph g, uint4* __restrict__ out, uint32_t rw) {
                 out[rs * a] = make_uint4(u, dw, (uint32_t)r.off, kEmpty);
             }
         }
+    }
+}
+
+// 8-byte node records of the compact-chain walk: {off, deg | allpos << 31}
+// (arcs < 2^32); half the L2 footprint of the 16-byte NodeRec.
+__global__ void k_nodes8(DevGraph g, uint2* __restrict__ out) {
+    for (uint64_t v = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; v < g.n; v += (uint64_t)gridDim.x * blockDim.x) {
+        const NodeRec r = load_node(g, (uint32_t)v);
+        out[v] = make_uint2((uint32_t)r.off, r.deg | ((r.flags & NF_ALLPOS) ? 0x80000000u : 0u));
     }
 }
 
@@ -1695,6 +1719,13 @@ void session_create(Session& s, Graph& g, const mhw_model_desc& md, const mhw_wa
             const uint64_t cw_al = (cw + 63) & ~63ull;  // 256-byte aligned filter copy
             const bool both = mode == "both" && g.bloom.n && !m.alpha_trivial;
             s.c16.alloc(both ? cw_al + g.bloom.n : cw);
+            s.nodes8.alloc(std::max<uint32_t>(g.n, 1));
+            k_nodes8<<<grid_for(g.n), 256, 0, st>>>(g.view(), s.nodes8.p);
+            MHW_CK(cudaGetLastError());
+            // 64-register cap (4 blocks/SM, a 40-byte stack frame): cfg2 walk
+            // 24.64 -> 23.84 ms (more walkers in flight outweigh the spills
+            // and the extra lock retries, 1.97 M -> 2.35 M)
+            if (!std::getenv("MHW_WALK_REGS")) s.minb = 64;
             if (both) {
                 MHW_CK(cudaMemcpyAsync(s.c16.p + cw_al, g.bloom.p, g.bloom.bytes(), cudaMemcpyDeviceToDevice, st));
                 s.bloom_copy = s.c16.p + cw_al;
@@ -1834,6 +1865,7 @@ RunParams Session::params() const {
     P.chain = chain.p;
     P.ac = ac.n ? ac.p : nullptr;
     P.c16 = c16.n ? c16.p : nullptr;
+    P.nodes8 = nodes8.n ? nodes8.p : nullptr;
     if (bloom_copy) P.g.bloom = bloom_copy;
     P.rec_u32 = rec_u32;
     P.out = out.p;

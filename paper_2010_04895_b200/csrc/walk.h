@@ -22,6 +22,7 @@ struct RunParams {
                               // word of the state entered through that arc (else null)
     uint32_t* c16;            // node2vec compact chains (AR 3): one 16-bit word per forward
                               // arc s->v = state (s, v), two per u32 (else null)
+    const uint2* nodes8;      // compact chains: 8-byte node records {off, deg | allpos << 31}
     uint32_t* out;            // rows x stride walk buffer
     uint32_t stride;
     uint32_t* lens;
@@ -62,6 +63,7 @@ struct Session {
     uint32_t rec_u32 = 4;    // u32 words per record: 4, 8 (typed models), 2 (narrow node2vec records)
     DBuf<uint32_t> c16;      // compact 16-bit chain words (node2vec, L2-sized), [c16 | filter copy] when pinned
     const uint32_t* bloom_copy = nullptr;  // the edge filter's copy behind c16 (one persisting window)
+    DBuf<uint2> nodes8;      // compact chains: 8-byte node records (half the L2 footprint of NodeRec)
     std::unique_ptr<ExactState> ex;  // alias / direct / rejection baselines (exact.cu)
     DBuf<unsigned long long> ctr;
     // deterministic schedule scratch
