@@ -313,7 +313,10 @@ __global__ void __launch_bounds__(kWalkBlock) __maxnreg__(REGS) k_walk(RunParams
                     // Last heavier than the lightest class: 35.4).
                     // (compact chains of hub states hold no class: the Last's
                     // id is needed for it anyway)
-                    if (e < kLocked && ((e >> 30) == P.m.spec_cls || (C16 && (e >> 30) == 3u))) {
+                    // (compact chains: a Last of the return class IS s -- its
+                    // id and slice are in registers, nothing to fetch)
+                    if (e < kLocked && (C16 ? ((e >> 30) == 3u || ((e >> 30) == P.m.spec_cls && (e >> 30) != 0u))
+                                            : (e >> 30) == P.m.spec_cls)) {
                         xl = C16 ? make_uint2(__ldg(g.ids + c.off + (e & kIdxMask)), 0u)
                                  : __ldg(reinterpret_cast<const uint2*>(P.ac) + c.off + (e & kIdxMask));
                         spec_l = true;
@@ -473,6 +476,11 @@ __global__ void __launch_bounds__(kWalkBlock) __maxnreg__(REGS) k_walk(RunParams
                     } else if (kSpec) {
                         an = al;
                         bn = bl;
+                    } else if (C16 && cls_l == 0u) {
+                        // return class: the Last is s itself (its id, offset and
+                        // degree are the state's; the all-positive flag only
+                        // drives lazy inits, which this eager variant has none of)
+                        an = make_uint4(c.s, c.deg_s, (uint32_t)c.off_s, 0u);
                     } else if (C16 && spec_l) {
                         const uint2 r = __ldg(P.nodes8 + xl.x);
                         an = make_uint4(xl.x, r.y, r.x, 0u);
