@@ -185,6 +185,12 @@ struct DevModel {
     double inv_p, inv_q;     // 1.0/p, 1.0/q computed on the host (models.cpp:77-79)
     int alpha_trivial;       // 1/p == 1 == 1/q: alpha is 1.0 whatever the class
     uint32_t spec_cls;       // the unique heaviest alpha class (3: none); its Lasts are fetched early
+    // load-free rejections (compact chains, unweighted node2vec): with the
+    // Last of the return class (w'(Last) = inv_p) and every other class
+    // lighter (ret_wmax = max(1, inv_q) < inv_p), a proposal is rejected
+    // whatever its class when u * inv_p >= ret_wmax, or when it is the Last
+    int ret_skip;
+    double ret_wmax;
     const uint16_t* metapath;
     uint32_t mp_len;
     const double* M;         // edge2vec type matrix, M_dim x M_dim

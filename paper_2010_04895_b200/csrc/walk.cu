@@ -254,7 +254,7 @@ __global__ void __launch_bounds__(kWalkBlock) __maxnreg__(REGS) k_walk(RunParams
                     // between them (the lock's timing still cannot depend on
                     // the proposal); otherwise the scheduler waits for the
                     // atomic's return before issuing the load (ncu: 13% of the
-                    // stall samples on the decode of the lock word)
+                    // stall samples on the decode of the lock word).
                     cand = d.index(c.deg);
                     u = d.unit();
                     c16_uc = __ldg(g.ids + c.off + cand);
@@ -268,6 +268,25 @@ __global__ void __launch_bounds__(kWalkBlock) __maxnreg__(REGS) k_walk(RunParams
                     e = atomicExch(cw, kLocked);
                 }
                 if constexpr (C16) {
+                    if (P.m.ret_skip) {
+                        // Last of the return class (it is s): a proposal of it,
+                        // or any proposal once u * w'(Last) reaches the heaviest
+                        // other class, is rejected whatever the candidate is --
+                        // the decision of mh_accept (samplers.hpp:24) without
+                        // the candidate's id, record or alpha probe; the walker
+                        // steps back to s (id and slice in registers)
+                        if (e < kLocked && (e >> 30) == 0u &&
+                            (cand == (e & kIdxMask) || __dmul_rn(u, P.m.inv_p) >= P.m.ret_wmax)) {
+                            c16_release(cw, csh, c16_enc(e, c.deg));
+                            chosen = e & kIdxMask;
+                            next = c.s;
+                            rn.off = c.off_s;
+                            rn.deg = c.deg_s;
+                            rn.type = 0;
+                            rn.flags = 0;
+                            goto emit;
+                        }
+                    }
                 } else if constexpr (ALIAS) {
                     // alias_sample (samplers.hpp:65-68) of v's static table:
                     // index on word 0, coin on words 1-2; the accept unit
@@ -476,10 +495,11 @@ __global__ void __launch_bounds__(kWalkBlock) __maxnreg__(REGS) k_walk(RunParams
                     } else if (kSpec) {
                         an = al;
                         bn = bl;
-                    } else if (C16 && cls_l == 0u) {
+                    } else if (KIND == NODE2VEC && CC && cls_l == 0u) {
                         // return class: the Last is s itself (its id, offset and
-                        // degree are the state's; the all-positive flag only
-                        // drives lazy inits, which this eager variant has none of)
+                        // degree are the state's, no record load; the all-positive
+                        // flag, left clear, only selects a lazy init's fast path,
+                        // which returns the same index as the full scan)
                         an = make_uint4(c.s, c.deg_s, (uint32_t)c.off_s, 0u);
                     } else if (C16 && spec_l) {
                         const uint2 r = __ldg(P.nodes8 + xl.x);
@@ -507,6 +527,7 @@ __global__ void __launch_bounds__(kWalkBlock) __maxnreg__(REGS) k_walk(RunParams
                     if (second_order(KIND)) back_c = __ldg(g.rev + c.off + chosen);
                 }
             }
+        emit:
             // emit: 4 ids buffered in registers, one 16-byte store
             switch (len & 3) {
                 case 0: b0 = next; break;
@@ -574,8 +595,8 @@ __global__ void __launch_bounds__(kWalkBlock) __maxnreg__(REGS) k_walk(RunParams
 // independent random-gather chains, and occupancy wins (cfg2: 64 regs
 // 40.1 ms step, 40 regs 39.6, 32 regs 39.1); the typed models spill more at
 // 32 registers and keep 4 blocks/SM (cfg3b 112 vs 117 ms).
-template <int KIND>
-__global__ void __launch_bounds__(256, KIND == NODE2VEC ? 8 : 4) k_init_all(RunParams P) {
+template <int KIND, int MINB = (KIND == NODE2VEC ? 6 : 4)>
+__global__ void __launch_bounds__(256, MINB) k_init_all(RunParams P) {
     const DevGraph& g = P.g;
     unsigned long long inits = 0;
     for (uint64_t a = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; a < g.m;
@@ -1363,6 +1384,9 @@ void model_bind(Model& mb, Graph& g, const mhw_model_desc& d) {
         const bool unique = (h == 0 || a[0] < a[h]) && (h == 1 || a[1] < a[h]) && (h == 2 || a[2] < a[h]);
         m.spec_cls = (!m.alpha_trivial && unique) ? (uint32_t)h : 3u;
     }
+    m.ret_wmax = std::max(1.0, m.inv_q);
+    m.ret_skip = (k == NODE2VEC && !m.alpha_trivial && !g.w.n && m.ret_wmax < m.inv_p) ? 1 : 0;
+    if (const char* rs = std::getenv("MHW_RET_SKIP")) m.ret_skip = m.ret_skip && rs[0] != '0';
     m.num_types = g.n_ntypes;
     if (k == METAPATH2VEC) {
         if (d.metapath_len < 2 || !d.metapath) invalid("metapath needs at least 2 types");
@@ -1891,7 +1915,14 @@ RunParams Session::params() const {
 template <int KIND>
 static void launch_init_all(const Session& s, const RunParams& P, cudaStream_t st) {
     if (s.init_rec_order && s.ac.n) k_init_rec<KIND><<<grid_for(s.g->m), 256, 0, st>>>(P, 0, s.g->m, nullptr);
-    else k_init_all<KIND><<<grid_for(s.g->m), 256, 0, st>>>(P);
+    else {
+        const char* e = std::getenv("MHW_INIT_MINB");  // blocks/SM of the slot-order init (A/B)
+        const int mb = e ? std::atoi(e) : 0;
+        if (mb == 8) k_init_all<KIND, 8><<<grid_for(s.g->m), 256, 0, st>>>(P);
+        else if (mb == 4) k_init_all<KIND, 4><<<grid_for(s.g->m), 256, 0, st>>>(P);
+        else if (mb == 5) k_init_all<KIND, 5><<<grid_for(s.g->m), 256, 0, st>>>(P);
+        else k_init_all<KIND><<<grid_for(s.g->m), 256, 0, st>>>(P);
+    }
     MHW_CK(cudaGetLastError());
 }
 
