@@ -130,6 +130,67 @@ def make_config(cfg, node_begin=0, node_end=0):
                           proposal=1 if cfg.get("proposal") == "alias" else 0)
 
 
+class ShardInit:
+    """Sharded chain-table initialisation of an N-rank run (the one exchange
+    of the multi-GPU path; the walk itself has none). The initial table is a
+    pure function of the slot (slot-keyed init draws), so each rank computes
+    the words of a contiguous 1/N of the records (record order: arc s -> v
+    holds state (s, v)), the words are all-gathered in PIECES pieces, and
+    piece j of every rank is installed (mhw_session_load_records_range, a
+    coalesced strided write) as soon as it lands while piece j+1 is in
+    flight. Every rank ends with the table a single-GPU run builds
+    (tests/test_gpu_dist_shard.py). host_coll: ranks sharing one GPU
+    (gloo, through host memory; a path check, never timed)."""
+
+    PIECES = 4
+
+    def __init__(self, sess, rank, world, dist, dev, host_coll):
+        import torch
+        self.sess, self.rank, self.world, self.dist, self.host_coll = sess, rank, world, dist, host_coll
+        S = self.S = sess.chain_size()
+        W = self.W = sess.record_width()  # u32 words per entry (3: typed records carry w'(Last))
+        P = self.PIECES
+        self.pc = pc = (((S + world - 1) // world) + P - 1) // P  # entries per piece per rank
+        self.per = per = pc * P
+        self.shard = torch.empty(max(per * W, 1), dtype=torch.int32, device=dev)
+        self.full = torch.empty(max(P * world * pc * W, 1), dtype=torch.int32, device=dev)
+        self.lo, self.hi = min(S, rank * per), min(S, (rank + 1) * per)
+        self.dev = dev
+
+    def __call__(self, stream) -> int:
+        import torch
+        sess, world, pc, W, S, per = self.sess, self.world, self.pc, self.W, self.S, self.per
+        n_launch = 0
+        if self.hi > self.lo:
+            sess.init_records(self.lo, self.hi, self.shard.data_ptr(), stream.cuda_stream)
+            n_launch += 1
+        works = []
+        for j in range(self.PIECES):
+            out_j = self.full[j * world * pc * W:(j + 1) * world * pc * W]
+            src = self.shard[j * pc * W:(j + 1) * pc * W]
+            if self.host_coll:
+                torch.cuda.current_stream().wait_stream(stream)
+                torch.cuda.synchronize(self.dev)
+                parts = [torch.empty(pc * W, dtype=torch.int32) for _ in range(world)]
+                self.dist.all_gather(parts, src.cpu())
+                out_j.copy_(torch.cat(parts).to(self.dev))
+                torch.cuda.synchronize(self.dev)
+                works.append(None)
+            else:
+                works.append(self.dist.all_gather_into_tensor(out_j, src, async_op=True))
+        for j in range(self.PIECES):
+            if works[j] is not None:
+                works[j].wait()  # the install stream waits for piece j only
+            base = self.full.data_ptr() + 4 * j * world * pc * W
+            for q in range(world):
+                b = min(S, q * per + j * pc)
+                e = min(S, q * per + (j + 1) * pc)
+                if e > b:
+                    sess.load_records_range(b, e, base + 4 * q * pc * W, stream.cuda_stream)
+                    n_launch += 1
+        return n_launch
+
+
 class Clocks:
     """SM clock + throttle-reason sampling during the timed region.
 
@@ -370,7 +431,9 @@ def run_mine(args, cfg):
     # table is a pure function of the slot, so each rank initialises 1/N of
     # the records (record order: the install is a coalesced strided copy) and
     # the words are all-gathered (the walk itself has no exchange).
-    shard_init = (world > 1 and cfg["model"] in ("node2vec", "edge2vec", "fairwalk")
+    # --chain-init local: every rank initialises its own table (no collective
+    # at all; the A/B of the exchange against the redundant per-rank init)
+    shard_init = (world > 1 and args.chain_init == "sharded" and cfg["model"] in ("node2vec", "edge2vec", "fairwalk")
                   and cfg.get("sampler", "mh") == "mh" and shard_init_pays(cfg, g))
     if shard_init:
         wcfg.init_mode = 2
@@ -389,46 +452,10 @@ def run_mine(args, cfg):
             dist.barrier()
         torch.cuda.synchronize(dev)
 
-    per = 0
-    PIECES = 4  # all-gather pieces: piece j+1 is in flight while piece j installs
-    if shard_init:
-        S = sess.chain_size()
-        W = sess.record_width()  # u32 words per record entry (3: typed records carry w'(Last))
-        pc = (((S + world - 1) // world) + PIECES - 1) // PIECES  # entries per piece per rank
-        per = pc * PIECES
-        shard = torch.empty(per * W, dtype=torch.int32, device=dev)
-        full = torch.empty(PIECES * world * pc * W, dtype=torch.int32, device=dev)
-        lo, hi = min(S, rank * per), min(S, (rank + 1) * per)
+    shard = ShardInit(sess, rank, world, dist, dev, host_coll) if shard_init else None
 
     def one_run():
-        n_launch = 0
-        if shard_init:
-            sess.init_records(lo, hi, shard.data_ptr(), stream.cuda_stream)
-            n_launch += 1
-            # piece j of every rank's shard: records [q*per + j*pc, +pc) of rank q,
-            # gathered into full[j] (world x pc entries) and installed as soon as
-            # it lands while piece j+1 is in flight
-            works = []
-            for j in range(PIECES):
-                out_j = full[j * world * pc * W:(j + 1) * world * pc * W]
-                src = shard[j * pc * W:(j + 1) * pc * W]
-                if host_coll:  # gloo (ranks sharing one GPU): through host memory
-                    parts = [torch.empty(pc * W, dtype=torch.int32) for _ in range(world)]
-                    dist.all_gather(parts, src.cpu())
-                    out_j.copy_(torch.cat(parts).to(dev))
-                    works.append(None)
-                else:
-                    works.append(dist.all_gather_into_tensor(out_j, src, async_op=True))
-            for j in range(PIECES):
-                if works[j] is not None:
-                    works[j].wait()  # the install stream waits for piece j only
-                base = full.data_ptr() + 4 * j * world * pc * W
-                for q in range(world):
-                    b = min(S, q * per + j * pc)
-                    e = min(S, q * per + (j + 1) * pc)
-                    if e > b:
-                        sess.load_records_range(b, e, base + 4 * q * pc * W, stream.cuda_stream)
-                        n_launch += 1
+        n_launch = shard(stream) if shard else 0
         sess.run(stream.cuda_stream)
         return sess.launches() + n_launch
 
@@ -521,7 +548,9 @@ def run_mine(args, cfg):
                        "seed": SEED, "walk_seed": WALK_SEED,
                        "l2": "explicit 256 MB L2 flush between timed steps (also inputs > L2)",
                        "parallelism": f"walker ranges x{world}, CSR replicated"
-                                      + (", chain init sharded + all-gather" if shard_init else "")},
+                                      + (", chain init sharded + all-gather" if shard_init else ""),
+                       "chain_init": ("sharded + all-gather" if shard_init else
+                                      ("per-rank" if world > 1 else "local"))},
             "roofline": roof, "clocks": clk.summary(), "gpu_launches": launches_job,
             "T_i_ms": st.init_seconds * 1e3, "T_w_ms": kernel_ms,
             "T_note": "per generate_walks (engine.cpp:228-232 split): T_i = eager chain-table init (k_init_all / "
@@ -654,6 +683,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true", help="skip the host-buffer e2e leg")
     ap.add_argument("--sampler", default="mh", choices=["mh", "alias", "direct", "rejection"],
                     help="exact baseline samplers of next_edge (engine.cpp:88-116) for comparison")
+    ap.add_argument("--chain-init", default="sharded", choices=["sharded", "local"],
+                    help="N > 1, second-order models: sharded init + all-gather (default) or per-rank init")
     ap.add_argument("--proposal", default="uniform", choices=["uniform", "alias"],
                     help="M-H proposal: uniform (mh_transition) or the static-weight alias table + Hastings")
     args = ap.parse_args()

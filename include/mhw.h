@@ -385,6 +385,15 @@ MHW_API mhw_status mhw_session_chain_size(const mhw_session* s, uint64_t* words)
 MHW_API mhw_status mhw_session_init_chain(mhw_session* s, uint64_t begin, uint64_t end, uint32_t* d_words,
                                           void* stream);
 MHW_API mhw_status mhw_session_load_chain(mhw_session* s, const uint32_t* d_words, void* stream);
+/* Resets and eagerly initialises the session's own chain table (what
+ * mhw_session_run does before its walk) without walking; the next run starts
+ * from it. Lazy sessions (init_mode 1) get an empty table. */
+MHW_API mhw_status mhw_session_prepare(mhw_session* s, void* stream);
+/* The installed chain table, one u32 per arc a (chain_size entries, device
+ * pointer): the compact 16-bit word (node2vec compact chains), the colocated
+ * word of record a, or the slot-order word a -- comparable between sessions
+ * of one layout (e.g. a sharded install against a local one). */
+MHW_API mhw_status mhw_session_export_table(mhw_session* s, uint32_t* d_words, void* stream);
 /* The same table in RECORD order: word i belongs to arc i = (s -> v), i.e.
  * to state (s, v), slot off(v) + index of s in N(v). Sessions keep each
  * second-order chain word in the record of the arc that enters its state, so

@@ -109,6 +109,8 @@ SIGNATURES = {
     "mhw_session_chain_size": (C.c_int32, [_P, C.POINTER(C.c_uint64)]),
     "mhw_session_init_chain": (C.c_int32, [_P, C.c_uint64, C.c_uint64, _P, _P]),
     "mhw_session_load_chain": (C.c_int32, [_P, _P, _P]),
+    "mhw_session_prepare": (C.c_int32, [_P, _P]),
+    "mhw_session_export_table": (C.c_int32, [_P, _P, _P]),
     "mhw_session_init_records": (C.c_int32, [_P, C.c_uint64, C.c_uint64, _P, _P]),
     "mhw_session_load_records": (C.c_int32, [_P, _P, _P]),
     "mhw_session_record_width": (C.c_int32, [_P, _P]),

@@ -602,6 +602,21 @@ mhw_status mhw_session_load_chain(mhw_session* s, const uint32_t* d_words, void*
     });
 }
 
+mhw_status mhw_session_prepare(mhw_session* s, void* stream) {
+    return guard([&] {
+        need(s, "session");
+        mhw::session_prepare(*s, static_cast<cudaStream_t>(stream));
+    });
+}
+
+mhw_status mhw_session_export_table(mhw_session* s, uint32_t* d_words, void* stream) {
+    return guard([&] {
+        need(s, "session");
+        need(d_words, "d_words");
+        mhw::session_export_table(*s, d_words, static_cast<cudaStream_t>(stream));
+    });
+}
+
 mhw_status mhw_session_init_records(mhw_session* s, uint64_t begin, uint64_t end, uint32_t* d_words, void* stream) {
     return guard([&] {
         need(s, "session");

@@ -2068,6 +2068,50 @@ void session_init_chain(Session& s, uint64_t begin, uint64_t end, uint32_t* d_wo
     MHW_CK(cudaGetLastError());
 }
 
+// Reset + eager initialisation of the session's chain table without a walk
+// (what session_run does before its walk kernel); the next run starts from
+// this table (chain_loaded). Lazy sessions get an empty table.
+void session_prepare(Session& s, cudaStream_t user) {
+    DeviceGuard dg(s.g->device);
+    if (!second_order(s.model.dev.kind) || s.ex || s.wc.schedule == MHW_SCHEDULE_DETERMINISTIC)
+        invalid("chain preloading applies to second-order models on the throughput schedule");
+    cudaStream_t st = user ? user : s.stream;
+    const RunParams P = s.params();
+    MHW_CK(cudaMemsetAsync(s.chain.p, 0xFF, s.chain.bytes(), st));
+    if (s.ac.n && (!s.eager_init || !s.g->verified_sym))
+        k_ac_reset<<<grid_for(s.g->m), 256, 0, st>>>(reinterpret_cast<uint32_t*>(s.ac.p), s.g->m, s.rec_u32);
+    if (s.eager_init && s.g->m) {
+        dispatch(s.model.dev.kind, [&](auto kc) {
+            constexpr int KIND = decltype(kc)::value;
+            if constexpr (second_order(KIND)) launch_init_all<KIND>(s, P, st);
+        });
+    }
+    MHW_CK(cudaGetLastError());
+    s.chain_loaded = true;
+}
+
+// Entry of arc a of the session's chain table as installed: the 16-bit
+// compact word, the colocated 32-bit word of record a, or chain[a] (slot
+// order) -- for comparing tables of sessions with the same layout.
+__global__ void k_export_table(RunParams P, uint64_t m, uint32_t* __restrict__ out) {
+    for (uint64_t a = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; a < m; a += (uint64_t)gridDim.x * blockDim.x) {
+        uint32_t w;
+        if (P.c16) w = reinterpret_cast<const uint16_t*>(P.c16)[a];
+        else if (P.ac) w = reinterpret_cast<const uint32_t*>(P.ac)[a * P.rec_u32 + chain_word_off(P.rec_u32)];
+        else w = P.chain[a];
+        out[a] = w;
+    }
+}
+
+void session_export_table(Session& s, uint32_t* d_words, cudaStream_t user) {
+    DeviceGuard dg(s.g->device);
+    if (!second_order(s.model.dev.kind) || s.ex || s.wc.schedule == MHW_SCHEDULE_DETERMINISTIC)
+        invalid("chain tables are exported for second-order models on the throughput schedule");
+    cudaStream_t st = user ? user : s.stream;
+    if (s.g->m) k_export_table<<<grid_for(s.g->m), 256, 0, st>>>(s.params(), s.g->m, d_words);
+    MHW_CK(cudaGetLastError());
+}
+
 void session_load_chain(Session& s, const uint32_t* d_words, cudaStream_t user, bool rec_order) {
     if (rec_order) {
         session_load_records_range(s, 0, s.g->m, d_words, user);

@@ -111,6 +111,8 @@ void walk_rows(Graph& g, const mhw_model_desc& md, const mhw_walk_config& wc, ui
 void session_init_chain(Session& s, uint64_t begin, uint64_t end, uint32_t* d_words, cudaStream_t stream,
                         bool rec_order = false);
 void session_load_chain(Session& s, const uint32_t* d_words, cudaStream_t stream, bool rec_order = false);
+void session_prepare(Session& s, cudaStream_t stream);
+void session_export_table(Session& s, uint32_t* d_words, cudaStream_t stream);
 void session_load_records_range(Session& s, uint64_t begin, uint64_t end, const uint32_t* d_words,
                                 cudaStream_t stream);
 // u32 words per record of a record-order table (3: typed records carry w'(Last)).

@@ -628,6 +628,15 @@ class Session:
         """Installs a full initial table (chain_size words) for the next run."""
         _check(L.lib().mhw_session_load_chain(self._h, C.c_void_p(d_words), C.c_void_p(stream) if stream else None))
 
+    def prepare(self, stream: int | None = None):
+        """Reset + eager init of the session's own table without a walk; the
+        next run starts from it (mhw_session_prepare)."""
+        _check(L.lib().mhw_session_prepare(self._h, C.c_void_p(stream) if stream else None))
+
+    def export_table(self, d_words: int, stream: int | None = None):
+        """The installed chain table, one u32 per arc (chain_size entries)."""
+        _check(L.lib().mhw_session_export_table(self._h, C.c_void_p(d_words), C.c_void_p(stream) if stream else None))
+
     def init_records(self, begin: int, end: int, d_words: int, stream: int | None = None):
         """Initial words of records (arcs) [begin, end): the chain table in the
         order the session stores it (coalesced install by load_records)."""
