@@ -79,7 +79,7 @@ def _worker(rank, world, port, model, env, out):
     sess.export_table(tab.data_ptr(), stream.cuda_stream)
     torch.cuda.synchronize()
     sess.run(stream.cuda_stream)
-    rows, lens = sess.download()
+    rows, lens = sess.download(stream=stream.cuda_stream)  # same stream as the walk
     out[rank] = dict(table=tab.cpu().numpy().view(np.uint32).copy(), rows=rows, lens=lens,
                      cuts=(int(cuts[rank]), int(cuts[rank + 1])))
     sess.close()
@@ -133,7 +133,8 @@ def test_two_rank_shard_path_equals_single_gpu(case):
     rows = np.concatenate([res[r]["rows"] for r in range(2)])
     lens = np.concatenate([res[r]["lens"] for r in range(2)])
     assert len(lens) == len(lens1)
-    assert np.array_equal(rows[:, 0], rows1[:, 0])  # same walkers in the same (reference) order
+    bad = np.nonzero(rows[:, 0] != rows1[:, 0])[0]
+    assert len(bad) == 0, (case, res[0]["cuts"], bad[:5], rows[bad[:5], 0], rows1[bad[:5], 0], len(res[0]["lens"]))
     d = g.download()
     off = d["offsets"].astype(np.int64)
     nb = d["neighbors"].astype(np.int64)
@@ -141,6 +142,7 @@ def test_two_rank_shard_path_equals_single_gpu(case):
     arcs = set(zip(np.repeat(np.arange(len(deg)), deg).tolist(), nb.tolist()))
     for i in range(len(lens)):
         w = rows[i, :lens[i]].astype(np.int64)
-        assert lens[i] == cfg["L"] + 1  # symmetric graphs, positive weights: no dead ends
+        # symmetric graphs, positive weights: no dead ends (isolated starts: the start alone)
+        assert lens[i] == (cfg["L"] + 1 if deg[w[0]] else 1)
         for a, b in zip(w[:-1], w[1:]):
             assert (int(a), int(b)) in arcs
