@@ -1164,15 +1164,17 @@ void graph_ensure_rev(Graph& g) {
     g.verified_sym = h == 0;
 }
 
-void graph_ensure_hash(Graph& g) {
+// st: the stream to build on (nullptr: the graph's); sync = wait for it.
+void graph_ensure_hash(Graph& g, cudaStream_t st, bool sync) {
     if (g.htab.n || !g.m || g.max_deg < kHashMinDeg) return;
     DeviceGuard dg(g.device);
+    if (!st) st = g.stream;
     const uint64_t buckets = (g.m >> 2) + g.n + 1;
     g.htab.alloc(8 * buckets);
-    MHW_CK(cudaMemsetAsync(g.htab.p, 0xFF, g.htab.bytes(), g.stream));
-    k_hash_build<<<grid_for(g.m), kBlock, 0, g.stream>>>(g.view(), g.htab.p);
+    MHW_CK(cudaMemsetAsync(g.htab.p, 0xFF, g.htab.bytes(), st));
+    k_hash_build<<<grid_for(g.m), kBlock, 0, st>>>(g.view(), g.htab.p);
     MHW_CK(cudaGetLastError());
-    MHW_CK(cudaStreamSynchronize(g.stream));
+    if (sync) MHW_CK(cudaStreamSynchronize(st));
 }
 
 // Edge Bloom filter for the alpha test. Small graphs: the densest of 4 / 3 /
@@ -1186,8 +1188,9 @@ void graph_ensure_hash(Graph& g) {
 // most 1/8 of free device memory (cfg5, 2.08 G arcs: 1185 ms without, 1111
 // at 4 bits, 1099 at 8). MHW_BLOOM_MB / MHW_BLOOM_BITS override the budget
 // and density; MHW_BLOOM=0 disables it.
-void graph_ensure_bloom(Graph& g) {
+void graph_ensure_bloom(Graph& g, cudaStream_t st, bool sync) {
     if (g.bloom.n || !g.m) return;
+    if (!st) st = g.stream;
     const char* off = std::getenv("MHW_BLOOM");
     if (off && off[0] == '0') return;
     const char* mb = std::getenv("MHW_BLOOM_MB");
@@ -1211,10 +1214,42 @@ void graph_ensure_bloom(Graph& g) {
     DeviceGuard dg(g.device);
     g.bloom.alloc(8 * blocks);
     g.bloom_blocks = (uint32_t)blocks;
-    MHW_CK(cudaMemsetAsync(g.bloom.p, 0, g.bloom.bytes(), g.stream));
-    k_bloom_build<<<grid_for(g.n * 32ull), kBlock, 0, g.stream>>>(g.view(), g.bloom.p, g.bloom_blocks);
+    MHW_CK(cudaMemsetAsync(g.bloom.p, 0, g.bloom.bytes(), st));
+    k_bloom_build<<<grid_for(g.n * 32ull), kBlock, 0, st>>>(g.view(), g.bloom.p, g.bloom_blocks);
     MHW_CK(cudaGetLastError());
-    MHW_CK(cudaStreamSynchronize(g.stream));
+    if (sync) MHW_CK(cudaStreamSynchronize(st));
+}
+
+// The alpha-test structures of a second-order model built concurrently: the
+// hash sets and the edge filter on two side streams while the reverse index
+// (a radix sort) runs on the graph's stream (e2e session setup: each is a
+// few scatter-bound kernels).
+void graph_ensure_second_order(Graph& g, bool alpha) {
+    DeviceGuard dg(g.device);
+    cudaStream_t s1 = nullptr, s2 = nullptr;
+    const bool side = alpha && g.m && (!g.htab.n || !g.bloom.n);
+    if (side) {
+        MHW_CK(cudaStreamCreateWithFlags(&s1, cudaStreamNonBlocking));
+        MHW_CK(cudaStreamCreateWithFlags(&s2, cudaStreamNonBlocking));
+    }
+    try {
+        if (side) {
+            graph_ensure_hash(g, s1, false);
+            graph_ensure_bloom(g, s2, false);
+        }
+        graph_ensure_rev(g);
+        graph_ensure_wtotal(g);
+        if (side) {
+            MHW_CK(cudaStreamSynchronize(s1));
+            MHW_CK(cudaStreamSynchronize(s2));
+        }
+    } catch (...) {
+        if (s1) cudaStreamDestroy(s1);
+        if (s2) cudaStreamDestroy(s2);
+        throw;
+    }
+    if (s1) cudaStreamDestroy(s1);
+    if (s2) cudaStreamDestroy(s2);
 }
 
 bool graph_ensure_arcrec(Graph& g) {
