@@ -8,6 +8,3 @@ for c in cfg1 cfg3a cfg3b cfg4; do
   python bench.py --config $c --steps 5 --warmup 3 --no-cpu-baseline > gpurun_out/all_$c.log 2>&1
 done
 timeout 900 python bench.py --config cfg5 --steps 3 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/all_cfg5.log 2>&1
-timeout 600 python bench.py --impl reference --config cfg2 --steps 2 --warmup 1 > gpurun_out/all_ref_cfg2.log 2>&1
-timeout 300 python bench.py --impl reference --config cfg1 --steps 3 --warmup 1 > gpurun_out/all_ref_cfg1.log 2>&1
-python scripts/summ.py gpurun_out/all_*.log
