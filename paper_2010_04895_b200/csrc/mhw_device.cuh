@@ -742,56 +742,6 @@ __device__ uint32_t init_slot(const DevGraph& g, const DevModel& m, const DevCfg
         return found ? pack_entry(best, best_cls) : kDead;
     }
     // burn-in
-    if constexpr (KIND == NODE2VEC) {
-        // Unweighted node2vec: w' = alpha(s, u) in {1/p, 1, 1/q}; the return
-        // candidate is index affix = slot - off(v) (N(v)[affix] = s), every
-        // other class is one of {1, 1/q}. Classes are resolved (id load +
-        // alpha probe) only when the M-H outcome depends on them -- the
-        // decisions, and so the chain word, are those of the eager loop below.
-        if (!g.w && !m.alpha_trivial && !c.boot) {
-            const uint32_t affix = (uint32_t)(slot - (uint64_t)c.off);
-            constexpr uint32_t kUnk = 3u;
-            auto w_of = [&](uint32_t k) { return alpha_value(m, k); };
-            auto resolve = [&](uint32_t i) {
-                return alpha_class(g, m, c, load_id(g, c.off + i), nullptr, -1, true);
-            };
-            Draw d0;
-            d0.open(key, slot, 0);
-            last = d0.index(c.deg);  // random_positive, every weight positive
-            cls = last == affix ? 0u : kUnk;
-            for (uint32_t i = 0; i < cfg.burn_in; ++i) {
-                Draw d;
-                d.open(key, slot, 1 + i);
-                const uint32_t cand = d.index(c.deg);
-                const double u = d.unit();
-                uint32_t cc = cand == affix ? 0u : kUnk;
-                // outcome over the classes still possible for (cand, last)
-                auto outcome = [&](uint32_t a, uint32_t b) -> int {  // 1 accept, 0 reject, -1 undecided
-                    const uint32_t a0 = a == kUnk ? 1u : a, a1 = a == kUnk ? 2u : a;
-                    const uint32_t b0 = b == kUnk ? 1u : b, b1 = b == kUnk ? 2u : b;
-                    const bool r00 = mh_accept(w_of(a0), w_of(b0), u), r01 = mh_accept(w_of(a0), w_of(b1), u);
-                    const bool r10 = mh_accept(w_of(a1), w_of(b0), u), r11 = mh_accept(w_of(a1), w_of(b1), u);
-                    return (r00 == r01 && r00 == r10 && r00 == r11) ? (r00 ? 1 : 0) : -1;
-                };
-                int o = cand == last ? 0 : outcome(cc, cls);
-                if (o < 0 && cc == kUnk) {
-                    cc = resolve(cand);
-                    o = outcome(cc, cls);
-                }
-                if (o < 0 && cls == kUnk) {
-                    cls = resolve(last);
-                    o = outcome(cc, cls);
-                }
-                if (o == 1) {
-                    last = cand;
-                    cls = cc;
-                }
-            }
-            if (cls == kUnk) cls = resolve(last);
-            if (w_out) *w_out = w_of(cls);
-            return pack_entry(last, cls);
-        }
-    }
     if (!random_positive<KIND>(g, m, c, key, slot, 0, &last, &cls, &wl)) return kDead;
     for (uint32_t i = 0; i < cfg.burn_in; ++i) {
         Draw d;
