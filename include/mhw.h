@@ -152,7 +152,7 @@ typedef struct mhw_walk_stats {
     uint64_t skipped_starts;
     uint64_t steps;
     uint64_t slot_inits;
-    uint64_t chain_retries;   /* CAS retries on contended chain slots */
+    uint64_t chain_retries;   /* lock retries: chain words found locked by another walker */
     double steps_per_sec;
     double init_seconds;
     double walk_seconds;
