@@ -134,13 +134,14 @@ class ShardInit:
     """Sharded chain-table initialisation of an N-rank run (the one exchange
     of the multi-GPU path; the walk itself has none). The initial table is a
     pure function of the slot (slot-keyed init draws), so each rank computes
-    the words of a contiguous 1/N of the records (record order: arc s -> v
-    holds state (s, v)), the words are all-gathered in PIECES pieces, and
-    piece j of every rank is installed (mhw_session_load_records_range, a
-    coalesced strided write) as soon as it lands while piece j+1 is in
+    a contiguous 1/N of the entries in the session's exchange format
+    (mhw_session_init_shard: compact node2vec chains -> 2-byte words in slot
+    order; other layouts -> record-order entries, 4 or 12 bytes), the entries
+    are all-gathered in PIECES pieces, and piece j of every rank is installed
+    (mhw_session_load_shard_range) as soon as it lands while piece j+1 is in
     flight. Every rank ends with the table a single-GPU run builds
-    (tests/test_gpu_dist_shard.py). host_coll: ranks sharing one GPU
-    (gloo, through host memory; a path check, never timed)."""
+    (tests/test_gpu_dist_shard.py). host_coll: ranks sharing one GPU (gloo,
+    through host memory; a path check, never timed)."""
 
     PIECES = 4
 
@@ -148,30 +149,30 @@ class ShardInit:
         import torch
         self.sess, self.rank, self.world, self.dist, self.host_coll = sess, rank, world, dist, host_coll
         S = self.S = sess.chain_size()
-        W = self.W = sess.record_width()  # u32 words per entry (3: typed records carry w'(Last))
+        B = self.B = sess.shard_entry_bytes()
         P = self.PIECES
         self.pc = pc = (((S + world - 1) // world) + P - 1) // P  # entries per piece per rank
         self.per = per = pc * P
-        self.shard = torch.empty(max(per * W, 1), dtype=torch.int32, device=dev)
-        self.full = torch.empty(max(P * world * pc * W, 1), dtype=torch.int32, device=dev)
+        self.shard = torch.empty(max(per * B, 1), dtype=torch.uint8, device=dev)
+        self.full = torch.empty(max(P * world * pc * B, 1), dtype=torch.uint8, device=dev)
         self.lo, self.hi = min(S, rank * per), min(S, (rank + 1) * per)
         self.dev = dev
 
     def __call__(self, stream) -> int:
         import torch
-        sess, world, pc, W, S, per = self.sess, self.world, self.pc, self.W, self.S, self.per
+        sess, world, pc, B, S, per = self.sess, self.world, self.pc, self.B, self.S, self.per
         n_launch = 0
         if self.hi > self.lo:
-            sess.init_records(self.lo, self.hi, self.shard.data_ptr(), stream.cuda_stream)
+            sess.init_shard(self.lo, self.hi, self.shard.data_ptr(), stream.cuda_stream)
             n_launch += 1
         works = []
         for j in range(self.PIECES):
-            out_j = self.full[j * world * pc * W:(j + 1) * world * pc * W]
-            src = self.shard[j * pc * W:(j + 1) * pc * W]
+            out_j = self.full[j * world * pc * B:(j + 1) * world * pc * B]
+            src = self.shard[j * pc * B:(j + 1) * pc * B]
             if self.host_coll:
                 torch.cuda.current_stream().wait_stream(stream)
                 torch.cuda.synchronize(self.dev)
-                parts = [torch.empty(pc * W, dtype=torch.int32) for _ in range(world)]
+                parts = [torch.empty(pc * B, dtype=torch.uint8) for _ in range(world)]
                 self.dist.all_gather(parts, src.cpu())
                 out_j.copy_(torch.cat(parts).to(self.dev))
                 torch.cuda.synchronize(self.dev)
@@ -181,12 +182,12 @@ class ShardInit:
         for j in range(self.PIECES):
             if works[j] is not None:
                 works[j].wait()  # the install stream waits for piece j only
-            base = self.full.data_ptr() + 4 * j * world * pc * W
+            base = self.full.data_ptr() + j * world * pc * B
             for q in range(world):
                 b = min(S, q * per + j * pc)
                 e = min(S, q * per + (j + 1) * pc)
                 if e > b:
-                    sess.load_records_range(b, e, base + 4 * q * pc * W, stream.cuda_stream)
+                    sess.load_shard_range(b, e, base + q * pc * B, stream.cuda_stream)
                     n_launch += 1
         return n_launch
 

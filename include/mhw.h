@@ -414,6 +414,17 @@ MHW_API mhw_status mhw_session_load_records(mhw_session* s, const uint32_t* d_wo
  * loaded; the caller installs every piece before it. */
 MHW_API mhw_status mhw_session_load_records_range(mhw_session* s, uint64_t begin, uint64_t end,
                                                   const uint32_t* d_words, void* stream);
+/* Sharded chain-table initialisation in the exchange format the session
+ * prefers (what bench.py's multi-GPU path uses): entries [begin, end) of
+ * chain_size are computed by init_shard into d_out (entry_bytes each), the
+ * ranks all-gather them, and load_shard_range installs any range. Compact
+ * node2vec chains exchange 2-byte words in slot order (slot-order init keeps
+ * N(v) locality; install scatters into the records); other layouts exchange
+ * record-order entries (mhw_session_init_records / _load_records_range). */
+MHW_API mhw_status mhw_session_shard_entry_bytes(const mhw_session* s, uint32_t* bytes);
+MHW_API mhw_status mhw_session_init_shard(mhw_session* s, uint64_t begin, uint64_t end, void* d_out, void* stream);
+MHW_API mhw_status mhw_session_load_shard_range(mhw_session* s, uint64_t begin, uint64_t end, const void* d_in,
+                                                void* stream);
 MHW_API void mhw_session_free(mhw_session* s);
 
 /* ---- parity entry points ---------------------------------------------- */

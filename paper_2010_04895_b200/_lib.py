@@ -110,6 +110,9 @@ SIGNATURES = {
     "mhw_session_init_chain": (C.c_int32, [_P, C.c_uint64, C.c_uint64, _P, _P]),
     "mhw_session_load_chain": (C.c_int32, [_P, _P, _P]),
     "mhw_session_prepare": (C.c_int32, [_P, _P]),
+    "mhw_session_shard_entry_bytes": (C.c_int32, [_P, C.POINTER(C.c_uint32)]),
+    "mhw_session_init_shard": (C.c_int32, [_P, C.c_uint64, C.c_uint64, _P, _P]),
+    "mhw_session_load_shard_range": (C.c_int32, [_P, C.c_uint64, C.c_uint64, _P, _P]),
     "mhw_session_export_table": (C.c_int32, [_P, _P, _P]),
     "mhw_session_init_records": (C.c_int32, [_P, C.c_uint64, C.c_uint64, _P, _P]),
     "mhw_session_load_records": (C.c_int32, [_P, _P, _P]),

@@ -602,6 +602,31 @@ mhw_status mhw_session_load_chain(mhw_session* s, const uint32_t* d_words, void*
     });
 }
 
+mhw_status mhw_session_shard_entry_bytes(const mhw_session* s, uint32_t* bytes) {
+    return guard([&] {
+        need(s, "session");
+        need(bytes, "bytes");
+        *bytes = mhw::session_shard_entry_bytes(*s);
+    });
+}
+
+mhw_status mhw_session_init_shard(mhw_session* s, uint64_t begin, uint64_t end, void* d_out, void* stream) {
+    return guard([&] {
+        need(s, "session");
+        if (end > begin) need(d_out, "d_out");
+        mhw::session_init_shard(*s, begin, end, d_out, static_cast<cudaStream_t>(stream));
+    });
+}
+
+mhw_status mhw_session_load_shard_range(mhw_session* s, uint64_t begin, uint64_t end, const void* d_in,
+                                        void* stream) {
+    return guard([&] {
+        need(s, "session");
+        if (end > begin) need(d_in, "d_in");
+        mhw::session_load_shard_range(*s, begin, end, d_in, static_cast<cudaStream_t>(stream));
+    });
+}
+
 mhw_status mhw_session_prepare(mhw_session* s, void* stream) {
     return guard([&] {
         need(s, "session");

@@ -640,7 +640,7 @@ __global__ void __launch_bounds__(256, MINB) k_init_all(RunParams P) {
 // Initial chain words of slots [b, e) (sharded init): k_init_all's work for
 // a slot range, written contiguously.
 template <int KIND>
-__global__ void __launch_bounds__(256, KIND == NODE2VEC ? 8 : 4) k_init_range(RunParams P, uint64_t b, uint64_t e, uint32_t* __restrict__ out) {
+__global__ void __launch_bounds__(256, KIND == NODE2VEC ? 6 : 4) k_init_range(RunParams P, uint64_t b, uint64_t e, uint32_t* __restrict__ out) {
     const DevGraph& g = P.g;
     for (uint64_t a = b + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; a < e;
          a += (uint64_t)gridDim.x * blockDim.x) {
@@ -653,6 +653,41 @@ __global__ void __launch_bounds__(256, KIND == NODE2VEC ? 8 : 4) k_init_range(Ru
         const NodeRec r = load_node(g, lo);
         const SCtx c = make_ctx<KIND>(g, P.m, lo, (uint32_t)(a - (uint64_t)r.off));
         out[a - b] = init_slot<KIND>(g, P.m, P.cfg, c, a);
+    }
+}
+
+// Shard exchange of compact chains (node2vec, AR 3): slot order (k_init_all's
+// N(v) locality: a warp's slots share v), 16-bit words already encoded with
+// deg(v) -- half the all-gather volume of 32-bit words -- installed by
+// k_load_slot16 into the record position of each slot.
+__global__ void __launch_bounds__(256, 6) k_init_range16(RunParams P, uint64_t b, uint64_t e,
+                                                         uint16_t* __restrict__ out) {
+    const DevGraph& g = P.g;
+    for (uint64_t a = b + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; a < e;
+         a += (uint64_t)gridDim.x * blockDim.x) {
+        uint32_t lo = 0, hi = g.n;
+        while (hi - lo > 1) {
+            const uint32_t mid = (lo + hi) >> 1;
+            if ((uint64_t)__ldg(&g.nodes[mid].off) <= a) lo = mid;
+            else hi = mid;
+        }
+        const NodeRec r = load_node(g, lo);
+        const SCtx c = make_ctx<NODE2VEC>(g, P.m, lo, (uint32_t)(a - (uint64_t)r.off));
+        out[a - b] = (uint16_t)c16_enc(init_slot<NODE2VEC>(g, P.m, P.cfg, c, a), c.deg);
+    }
+}
+
+// Slot a = (v, affix) holds state (s, v), s = N(v)[affix]; its compact word
+// lives at the forward arc s -> v = off(s) + rev[a] (coalesced reads of ids /
+// rev, one L2 node record, one 2-byte write into the L2-sized table).
+__global__ void k_load_slot16(RunParams P, const uint16_t* __restrict__ w, uint64_t b, uint64_t e) {
+    const DevGraph& g = P.g;
+    for (uint64_t a = b + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; a < e;
+         a += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t sv = __ldg(g.rev + a);
+        if (sv == kNoBack) continue;
+        const uint32_t src = load_id(g, a);
+        reinterpret_cast<uint16_t*>(P.c16)[(uint64_t)__ldg(P.nodes8 + src).x + sv] = __ldg(w + (a - b));
     }
 }
 
@@ -2148,6 +2183,39 @@ void session_load_records_range(Session& s, uint64_t begin, uint64_t end, const 
 }
 
 uint32_t session_record_width(const Session& s) { return (s.ac.n && s.rec_u32 == 8) ? 3u : 1u; }
+
+// The exchange format a sharded init should use (mhw_session_init_shard /
+// _load_shard_range): compact chains -> slot order, 2-byte encoded words;
+// otherwise record order with session_record_width u32 words per entry.
+uint32_t session_shard_entry_bytes(const Session& s) { return s.c16.n ? 2u : 4u * session_record_width(s); }
+
+void session_init_shard(Session& s, uint64_t begin, uint64_t end, void* d_out, cudaStream_t user) {
+    if (!s.c16.n) {
+        session_init_chain(s, begin, end, static_cast<uint32_t*>(d_out), user, true);
+        return;
+    }
+    DeviceGuard dg(s.g->device);
+    if (begin > end || end > s.g->m) invalid("shard range out of bounds");
+    if (begin == end) return;
+    cudaStream_t st = user ? user : s.stream;
+    k_init_range16<<<grid_for(end - begin), 256, 0, st>>>(s.params(), begin, end, static_cast<uint16_t*>(d_out));
+    MHW_CK(cudaGetLastError());
+}
+
+void session_load_shard_range(Session& s, uint64_t begin, uint64_t end, const void* d_in, cudaStream_t user) {
+    if (!s.c16.n) {
+        session_load_records_range(s, begin, end, static_cast<const uint32_t*>(d_in), user);
+        return;
+    }
+    DeviceGuard dg(s.g->device);
+    if (begin > end || end > s.g->m) invalid("shard range out of bounds");
+    cudaStream_t st = user ? user : s.stream;
+    if (end > begin) {
+        k_load_slot16<<<grid_for(end - begin), 256, 0, st>>>(s.params(), static_cast<const uint16_t*>(d_in), begin, end);
+        MHW_CK(cudaGetLastError());
+    }
+    s.chain_loaded = true;
+}
 
 void session_stats(Session& s, mhw_walk_stats& out) {
     DeviceGuard dg(s.g->device);

@@ -117,6 +117,11 @@ void session_load_records_range(Session& s, uint64_t begin, uint64_t end, const 
                                 cudaStream_t stream);
 // u32 words per record of a record-order table (3: typed records carry w'(Last)).
 uint32_t session_record_width(const Session& s);
+// Sharded init in the session's best exchange format (bytes per entry: 2 =
+// compact chains, slot order; else record order, 4 x record width).
+uint32_t session_shard_entry_bytes(const Session& s);
+void session_init_shard(Session& s, uint64_t begin, uint64_t end, void* d_out, cudaStream_t stream);
+void session_load_shard_range(Session& s, uint64_t begin, uint64_t end, const void* d_in, cudaStream_t stream);
 void session_stats(Session& s, mhw_walk_stats& out);
 void session_download(Session& s, uint32_t* nodes, uint32_t* lens, cudaStream_t stream);
 void session_write_corpus(Session& s, const char* path, const mhw_walk_stats& st);

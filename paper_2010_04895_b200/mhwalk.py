@@ -628,6 +628,22 @@ class Session:
         """Installs a full initial table (chain_size words) for the next run."""
         _check(L.lib().mhw_session_load_chain(self._h, C.c_void_p(d_words), C.c_void_p(stream) if stream else None))
 
+    def shard_entry_bytes(self) -> int:
+        """Bytes per entry of the session's shard exchange (2: compact chains, slot order)."""
+        b = C.c_uint32()
+        _check(L.lib().mhw_session_shard_entry_bytes(self._h, C.byref(b)))
+        return b.value
+
+    def init_shard(self, begin: int, end: int, d_out: int, stream: int | None = None):
+        """Entries [begin, end) of the sharded-init exchange (mhw_session_init_shard)."""
+        _check(L.lib().mhw_session_init_shard(self._h, begin, end, C.c_void_p(d_out),
+                                              C.c_void_p(stream) if stream else None))
+
+    def load_shard_range(self, begin: int, end: int, d_in: int, stream: int | None = None):
+        """Installs exchange entries [begin, end) (d_in -> entry begin) for the next run."""
+        _check(L.lib().mhw_session_load_shard_range(self._h, begin, end, C.c_void_p(d_in),
+                                                    C.c_void_p(stream) if stream else None))
+
     def prepare(self, stream: int | None = None):
         """Reset + eager init of the session's own table without a walk; the
         next run starts from it (mhw_session_prepare)."""

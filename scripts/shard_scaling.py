@@ -41,7 +41,7 @@ def main():
     ap.add_argument("--parts", type=int, nargs="+", default=[1, 2, 4, 8])
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=1)
-    ap.add_argument("--order", default="rec", choices=["rec", "slot"],
+    ap.add_argument("--order", default="shard", choices=["shard", "rec", "slot"],
                     help="sharded-init table order: record order (coalesced install) or slot order")
     ap.add_argument("--shard-init", action="store_true",
                     help="shard the eager chain init even where one GPU would initialise lazily")
@@ -69,24 +69,29 @@ def main():
             if shard_init:
                 wcfg.init_mode = 2
             sess = mhw.Session(g, model, wcfg)
-            init_fn = sess.init_records if args.order == "rec" else sess.init_chain
-            load_fn = sess.load_records if args.order == "rec" else sess.load_chain
+            S = sess.chain_size()
+            if args.order == "shard":  # the session's exchange format (bench.ShardInit)
+                init_fn = sess.init_shard
+                load_fn = lambda ptr, st: sess.load_shard_range(0, S, ptr, st)  # noqa: E731
+                B = sess.shard_entry_bytes()
+            else:
+                init_fn = sess.init_records if args.order == "rec" else sess.init_chain
+                load_fn = sess.load_records if args.order == "rec" else sess.load_chain
+                B = 4 * (sess.record_width() if args.order == "rec" else 1)
             if shard_init:
-                S = sess.chain_size()
-                W = sess.record_width() if args.order == "rec" else 1
                 per = (S + N - 1) // N
                 lo, hi = min(S, r * per), min(S, (r + 1) * per)
-                full = torch.empty(max(per * N * W, 1), dtype=torch.int32, device=dev)
+                full = torch.empty(max(per * N * B, 4), dtype=torch.uint8, device=dev)
                 # the all-gathered table every rank loads: built once here
                 for q in range(N):
                     ql, qh = min(S, q * per), min(S, (q + 1) * per)
                     if qh > ql:
-                        init_fn(ql, qh, full.data_ptr() + 4 * W * ql, stream.cuda_stream)
+                        init_fn(ql, qh, full.data_ptr() + B * ql, stream.cuda_stream)
 
             def step(evs=None):
                 if shard_init:
                     if hi > lo:
-                        init_fn(lo, hi, full.data_ptr() + 4 * W * lo, stream.cuda_stream)
+                        init_fn(lo, hi, full.data_ptr() + B * lo, stream.cuda_stream)
                     if evs:
                         evs[0].record(stream)
                     load_fn(full.data_ptr(), stream.cuda_stream)
@@ -131,7 +136,7 @@ def main():
                 "note": "each rank's shard timed alone on one B200 (CUDA events, median of reps); "
                         "the walk has no inter-rank exchange, so the N-GPU time is the max over ranks"}
         if shard_init:
-            line["allgather_bytes_excluded"] = 4 * W * int(S)
+            line["allgather_bytes_excluded"] = B * int(S)
         print(json.dumps(line), flush=True)
 
 

@@ -173,3 +173,44 @@ def test_piecewise_install_as_bench_pipelines_it(mhw, oracle, kind):
     rows, lens = s.download()
     ok, msg = gate(audit(g, oracle, md, rows, lens, min_visits=5000))
     assert ok, msg
+
+
+@pytest.mark.parametrize("layout", ["c16", "narrow"])
+@pytest.mark.parametrize("init", [O.INIT_RANDOM, O.INIT_BURN_IN])
+def test_shard_exchange_installs_the_local_table(mhw, oracle, init, layout, monkeypatch):
+    """mhw_session_init_shard over ragged ranges + load_shard_range (the
+    session's exchange format: 2-byte slot-order words for compact chains,
+    record-order words otherwise) installs exactly the table the session's
+    own eager init builds (mhw_session_prepare), and the preloaded run passes
+    the chi-square gate."""
+    from tests.stats import audit, gate
+    if layout == "c16":
+        monkeypatch.setenv("MHW_C16", "1")
+    else:
+        monkeypatch.setenv("MHW_C16", "0")
+        monkeypatch.setenv("MHW_NARROW", "1")
+    g = typed_random_graph(930 + init, 60, 5.0, weighted=False, types=2)
+    md = model_desc(O.NODE2VEC, g, p=0.3, q=3.0)
+    cfg = O.WalkCfg(K=400, L=80, seed=29, init_kind=init, burn_in_steps=6)
+    s = mhw.Session(device_graph(g, weighted=False), walk_model(md), walk_config(cfg, threads=8, init_mode=2))
+    S = s.chain_size()
+    B = s.shard_entry_bytes()
+    assert B == (2 if layout == "c16" else 4)
+    want = torch.empty(S, dtype=torch.int32, device="cuda")
+    s.prepare()
+    s.export_table(want.data_ptr())
+    buf = torch.empty(S * B, dtype=torch.uint8, device="cuda")
+    cuts = [0, S // 3 + 1, S // 2, S]
+    for b, e in zip(cuts[:-1], cuts[1:]):
+        s.init_shard(b, e, buf.data_ptr() + B * b)
+    for b, e in reversed(list(zip(cuts[:-1], cuts[1:]))):
+        s.load_shard_range(b, e, buf.data_ptr() + B * b)
+    got = torch.empty(S, dtype=torch.int32, device="cuda")
+    s.export_table(got.data_ptr())
+    torch.cuda.synchronize()
+    assert torch.equal(got, want)
+    s.run()
+    assert s.stats().slot_inits == 0
+    rows, lens = s.download()
+    ok, msg = gate(audit(g, oracle, md, rows, lens, min_visits=5000))
+    assert ok, msg
