@@ -177,3 +177,81 @@ def test_kwalk_cfg2_chain_layouts_equal_oracle(mhw, oracle, layout, env):
     16-bit word, which the 150 hub starts exercise."""
     n, steps = pin(mhw, oracle, "cfg2", init_mode=2, env=env, n_starts=800)
     assert n >= 700 and steps > 50 * n
+
+
+def _hub_graph(hub_deg=20000, seed=5):
+    """An unweighted hub of degree >= 2^14 (compact chain words of its states
+    hold no alpha class) inside a ring of leaves with random chords, so that
+    candidates of every alpha class occur at the hub."""
+    r = np.random.default_rng(seed)
+    n = hub_deg + 1
+    pairs = {(0, i) for i in range(1, n)}
+    pairs |= {(min(i, i % hub_deg + 1), max(i, i % hub_deg + 1)) for i in range(1, n)}
+    a = r.integers(1, n, 3 * hub_deg)
+    b = r.integers(1, n, 3 * hub_deg)
+    pairs |= {(int(min(x, y)), int(max(x, y))) for x, y in zip(a, b) if x != y}
+    edges = [(x, y, 1.0) for x, y in pairs] + [(y, x, 1.0) for x, y in pairs]  # symmetric, no duplicates
+    return O.make_graph(n, edges, symmetric=True)
+
+
+def test_kwalk_compact_hub_states_equal_oracle(mhw, oracle):
+    """Compact chains at a hub of degree 20,000 (>= 2^14): the walker
+    recomputes the Last's alpha class from its id; single walkers equal the
+    oracle byte for byte."""
+    import os as _os
+    from tests.helpers import device_graph, model_desc, walk_config
+    g = _hub_graph()
+    md = model_desc(O.NODE2VEC, g, p=0.25, q=4.0)
+    cfg = O.WalkCfg(K=1, L=40, seed=11, init_kind=O.INIT_BURN_IN, burn_in_steps=10)
+    old = _os.environ.get("MHW_C16")
+    _os.environ["MHW_C16"] = "1"
+    try:
+        dg = device_graph(g, weighted=False)
+        s = mhw.Session(dg, mhw.WalkModel(kind=mhw.ModelKind.node2vec, p=0.25, q=4.0),
+                        walk_config(cfg, threads=8, init_mode=2))
+    finally:
+        if old is None:
+            _os.environ.pop("MHW_C16", None)
+        else:
+            _os.environ["MHW_C16"] = old
+    assert s.shard_entry_bytes() == 2  # compact chains are in use
+    starts = np.concatenate([[0], np.arange(1, g.n, 97)]).astype(np.uint32)
+    orows, olens, _ = oracle.walk_isolated(g, md, cfg, starts)
+    hub_visits = 0
+    for j, v in enumerate(starts):
+        s.select_starts([int(v)])
+        s.run()
+        rows, lens = s.download()
+        assert lens[0] == olens[j] and np.array_equal(rows[0, :lens[0]], orows[j, :olens[j]]), int(v)
+        hub_visits += int(np.sum(rows[0, 1:lens[0]] == 0))
+    assert hub_visits > 100  # the hub states were walked through
+    s.close()
+
+
+def test_compact_hub_states_pass_chain_chi_square(mhw, oracle):
+    """Throughput corpus on the hub graph with compact chains: the states
+    entering the hub (class recomputed per step) pass the lumped chain
+    chi-square."""
+    import os as _os
+    from tests.helpers import device_graph, model_desc, walk_config
+    from tests.stats import audit_counts, gate, transition_counts_gpu
+    g = _hub_graph()
+    md = model_desc(O.NODE2VEC, g, p=0.25, q=4.0)
+    # 20 leaf starts x 20,000 walkers: their first steps enter the hub states (x, 0)
+    cfg = O.WalkCfg(K=20000, L=40, seed=13, init_kind=O.INIT_BURN_IN, burn_in_steps=10)
+    old = _os.environ.get("MHW_C16")
+    _os.environ["MHW_C16"] = "1"
+    try:
+        c = mhw.generate_walks(device_graph(g, weighted=False),
+                               mhw.WalkModel(kind=mhw.ModelKind.node2vec, p=0.25, q=4.0),
+                               walk_config(cfg, threads=8, init_mode=2, node_begin=1, node_end=21))
+    finally:
+        if old is None:
+            _os.environ.pop("MHW_C16", None)
+        else:
+            _os.environ["MHW_C16"] = old
+    states = transition_counts_gpu(c.rows, c.lengths, O.NODE2VEC, g.offsets, g.nbr, min_visits=5000, max_states=30)
+    hub = [st for st in states if st[0] == 0]
+    assert len(hub) >= 5, len(hub)
+    ok, msg = gate(audit_counts(g, oracle, md, states))
+    assert ok, msg
