@@ -258,14 +258,40 @@ def transition_counts_gpu(rows, lens, kind, offsets, nbr, metapath=None, min_vis
     return out
 
 
-def audit_counts(g: O.HostGraph, oracle: O.Oracle, md: O.ModelDesc, states, dense_max=1024):
+def min_class_entries(pi: np.ndarray, visits: int) -> float:
+    """Smallest expected number of entries, over `visits` transitions, into a
+    class of equal target weight of a uniform-proposal chain (stationary
+    entries into B per step = Pi_B (1 - P_BB)). The chain CLT behind the test
+    needs many of them: a hub state whose heavy class is one candidate among
+    20,000 is entered about once per 20,000 proposals, so at 5,000-10,000
+    visits its count is a Poisson number of excursions, not Gaussian -- any
+    correct implementation then scores heavy-tailed p-values (SURVEY 8(c):
+    "expected cell >= 5")."""
+    vals, inv = np.unique(pi[pi > 0], return_inverse=True)
+    size = np.bincount(inv, minlength=len(vals)).astype(np.float64)
+    k, m = len(vals), len(pi)
+    if k < 2:
+        return float("inf")
+    Pi = size * vals / np.sum(size * vals)
+    out = []
+    for a in range(k):
+        stay = 1.0 - np.sum(np.delete(size / m * np.minimum(1.0, vals / vals[a]), a))
+        out.append(visits * Pi[a] * (1.0 - stay))
+    return float(min(out))
+
+
+def audit_counts(g: O.HostGraph, oracle: O.Oracle, md: O.ModelDesc, states, dense_max=1024, min_entries=None):
     """p-values of the chain chi-square of (v, affix, visits, counts) states:
     the full test up to dense_max candidates, the lumped (equal target weight)
-    test beyond, where the distinct weights are few."""
+    test beyond, where the distinct weights are few. min_entries: audit only
+    states whose every weight class is expected to be entered at least that
+    often (min_class_entries)."""
     pv = []
     for v, aff, vis, counts in states:
         pi = O.eval_target(g, oracle, md, v, aff)
         assert counts.sum() == vis
+        if min_entries is not None and min_class_entries(pi, vis) < min_entries:
+            continue
         if len(pi) <= dense_max:
             pv.append(markov_chi2(counts, pi)[2])
         else:

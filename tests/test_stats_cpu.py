@@ -187,3 +187,14 @@ def test_oracle_hastings_decisions_restated(oracle):
     assert np.array_equal(wc, rc * w_c) and np.array_equal(wl, rl * w_l)  # node2vec: a * w
     want = (w_c > 0) & ((rl <= 0) | (rc >= rl) | (u * rl < rc))
     assert np.array_equal(acc.astype(bool), want)
+
+
+def test_class_entries_flag_slow_hub_chains():
+    """The validity guard of audit_counts(min_entries=...): at 8,000 visits a
+    hub state whose heavy class is a single candidate among 20,000 enters it
+    well under once, an ordinary state's classes hundreds of times."""
+    from tests.stats import min_class_entries
+    hub = np.concatenate([[4.0], np.full(8, 1.0), np.full(19991, 0.25)])
+    assert min_class_entries(hub, 8000) < 1
+    leaf = np.array([4.0, 1.0, 1.0, 0.25, 0.25, 0.25, 0.25, 0.25])
+    assert min_class_entries(leaf, 8000) > 100
