@@ -59,7 +59,8 @@ def check(mhw, oracle, cfg_name, hg, rows, lens, max_support, min_states=20, max
                                    metapath=cfg.get("metapath"), min_visits=5000, max_states=max_states,
                                    max_support=max_support)
     assert len(states) >= min_states, f"{cfg_name}: only {len(states)} states with >= 5000 visits"
-    pv = audit_counts(hg, oracle, md, states)
+    pv = audit_counts(hg, oracle, md, states, min_entries=5)
+    assert len(pv) >= min_states // 2, f"{cfg_name}: only {len(pv)} of {len(states)} states are valid for the test"
     ok, msg = gate(pv)
     assert ok, f"{cfg_name}: {msg}"
     return states, pv

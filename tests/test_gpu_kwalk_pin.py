@@ -254,7 +254,7 @@ def test_compact_hub_states_pass_chain_chi_square(mhw, oracle):
             _os.environ["MHW_C16"] = old
     assert c.stats.chain_retries > 0
     states = transition_counts_gpu(c.rows, c.lengths, O.NODE2VEC, g.offsets, g.nbr, min_visits=100_000,
-                                   max_states=10)
+                                   max_states=80)
     hub = [st for st in states if st[0] == 0]
     assert len(hub) == 5, [(st[0], st[2]) for st in states]
     pv = audit_counts(g, oracle, md, hub, min_entries=5)
