@@ -283,14 +283,16 @@ def min_class_entries(pi: np.ndarray, visits: int) -> float:
 def audit_counts(g: O.HostGraph, oracle: O.Oracle, md: O.ModelDesc, states, dense_max=1024, min_entries=None):
     """p-values of the chain chi-square of (v, affix, visits, counts) states:
     the full test up to dense_max candidates, the lumped (equal target weight)
-    test beyond, where the distinct weights are few. min_entries: audit only
-    states whose every weight class is expected to be entered at least that
-    often (min_class_entries)."""
+    test beyond, where the distinct weights are few. min_entries: audit a
+    lumped state only if every weight class is expected to be entered at
+    least that often (min_class_entries)."""
     pv = []
     for v, aff, vis, counts in states:
         pi = O.eval_target(g, oracle, md, v, aff)
         assert counts.sum() == vis
-        if min_entries is not None and min_class_entries(pi, vis) < min_entries:
+        # (the guard applies to the lumped test: its classes can be single,
+        # sticky candidates at hubs; the dense test's cells are candidates)
+        if min_entries is not None and len(pi) > dense_max and min_class_entries(pi, vis) < min_entries:
             continue
         if len(pi) <= dense_max:
             pv.append(markov_chi2(counts, pi)[2])
