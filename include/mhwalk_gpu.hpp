@@ -88,7 +88,10 @@ struct ModelDesc {
     }
 };
 
-inline mhw_walk_config to_config(const mhwalk::WalkConfig& c) {
+// The M-H proposal (an engine extension; the reference proposes uniformly).
+enum class Proposal { uniform = MHW_PROPOSAL_UNIFORM, alias = MHW_PROPOSAL_ALIAS };
+
+inline mhw_walk_config to_config(const mhwalk::WalkConfig& c, Proposal proposal = Proposal::uniform) {
     if (c.threads == 0) throw mhwalk::ValidationError("walks_per_node, walk_length and threads must be positive");
     mhw_walk_config w{};
     w.walks_per_node = c.walks_per_node;
@@ -99,13 +102,14 @@ inline mhw_walk_config to_config(const mhwalk::WalkConfig& c) {
     w.burn_in_steps = c.init.burn_in_steps;
     w.hw_sample_size = c.init.hw_sample_size;
     w.schedule = c.threads == 1 ? MHW_SCHEDULE_DETERMINISTIC : MHW_SCHEDULE_THROUGHPUT;
+    w.proposal = static_cast<int32_t>(proposal);
     return w;
 }
 
 inline mhwalk::WalkCorpus generate_walks(const DeviceGraph& g, const mhwalk::WalkModel& model,
-                                         const mhwalk::WalkConfig& config) {
+                                         const mhwalk::WalkConfig& config, Proposal proposal = Proposal::uniform) {
     ModelDesc md(model);
-    const mhw_walk_config wc = to_config(config);
+    const mhw_walk_config wc = to_config(config, proposal);
     mhw_walks* w = nullptr;
     check(mhw_generate_walks(g.get(), &md.d, &wc, &w));
     std::unique_ptr<mhw_walks, void (*)(mhw_walks*)> hold(w, mhw_walks_free);
@@ -130,9 +134,9 @@ inline mhwalk::WalkCorpus generate_walks(const DeviceGraph& g, const mhwalk::Wal
 
 // Drop-in for mhwalk::generate_walks (uploads the graph for this call).
 inline mhwalk::WalkCorpus generate_walks(const mhwalk::Graph& graph, const mhwalk::WalkModel& model,
-                                         const mhwalk::WalkConfig& config) {
+                                         const mhwalk::WalkConfig& config, Proposal proposal = Proposal::uniform) {
     DeviceGraph g(graph);
-    return generate_walks(g, model, config);
+    return generate_walks(g, model, config, proposal);
 }
 
 }  // namespace mhwalk_gpu

@@ -128,6 +128,18 @@ int main() {
         CHECK(c.walks.size() == 10000);
         CHECK(walks_valid(g, c));
     }
+    {   // the engine's alias proposal (extension): valid walks for every model
+        Rng rng(1009);
+        Graph g = oracles::random_graph(300, 6.0, true, rng);
+        oracles::assign_random_types(g, 2, rng);
+        WalkConfig config{.walks_per_node = 4, .walk_length = 20, .threads = 8, .seed = 9};
+        for (ModelKind kind : {ModelKind::deepwalk, ModelKind::node2vec, ModelKind::fairwalk}) {
+            WalkCorpus c = mhwalk_gpu::generate_walks(g, make_bound(kind, g, 0.5, 2.0), config,
+                                                      mhwalk_gpu::Proposal::alias);
+            CHECK(c.walks.size() == 1200);
+            CHECK(walks_valid(g, c));
+        }
+    }
     {   // errors: second-order on an asymmetric graph -> ValidationError from bind
         Graph g = oracles::make_graph(2, {{0, 1, 1.0}}, false);
         WalkModel m;
