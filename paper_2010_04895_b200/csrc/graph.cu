@@ -1188,7 +1188,7 @@ void graph_ensure_hash(Graph& g, cudaStream_t st, bool sync) {
 // most 1/8 of free device memory (cfg5, 2.08 G arcs: 1185 ms without, 1111
 // at 4 bits, 1099 at 8). MHW_BLOOM_MB / MHW_BLOOM_BITS override the budget
 // and density; MHW_BLOOM=0 disables it.
-void graph_ensure_bloom(Graph& g, cudaStream_t st, bool sync) {
+void graph_ensure_bloom(Graph& g, cudaStream_t st, bool sync, uint32_t max_bits) {
     if (g.bloom.n || !g.m) return;
     if (!st) st = g.stream;
     const char* off = std::getenv("MHW_BLOOM");
@@ -1201,7 +1201,7 @@ void graph_ensure_bloom(Graph& g, cudaStream_t st, bool sync) {
     } else if (!bits) {
         // densest of 4 / 3 / 2 bits per arc within 32 MB (L2-resident),
         // else 8 bits per arc in DRAM
-        for (uint64_t b = 4; b >= 2 && (bytes = g.m * b / 8) > (32ull << 20); --b) {
+        for (uint64_t b = max_bits; b >= 2 && (bytes = g.m * b / 8) > (32ull << 20); --b) {
         }
         if (bytes > (32ull << 20)) bytes = g.m;
         if (bytes > dev_available_bytes() / 8) return;
@@ -1224,7 +1224,7 @@ void graph_ensure_bloom(Graph& g, cudaStream_t st, bool sync) {
 // hash sets and the edge filter on two side streams while the reverse index
 // (a radix sort) runs on the graph's stream (e2e session setup: each is a
 // few scatter-bound kernels).
-void graph_ensure_second_order(Graph& g, bool alpha) {
+void graph_ensure_second_order(Graph& g, bool alpha, uint32_t bloom_bits) {
     DeviceGuard dg(g.device);
     cudaStream_t s1 = nullptr, s2 = nullptr;
     const bool side = alpha && g.m && (!g.htab.n || !g.bloom.n);
@@ -1235,7 +1235,7 @@ void graph_ensure_second_order(Graph& g, bool alpha) {
     try {
         if (side) {
             graph_ensure_hash(g, s1, false);
-            graph_ensure_bloom(g, s2, false);
+            graph_ensure_bloom(g, s2, false, bloom_bits);
         }
         graph_ensure_rev(g);
         graph_ensure_wtotal(g);

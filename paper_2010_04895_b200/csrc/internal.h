@@ -146,9 +146,9 @@ void graph_ensure_wtotal(Graph& g);
 void graph_ensure_tcount(Graph& g);
 void graph_ensure_typed_index(Graph& g);
 void graph_ensure_hash(Graph& g, cudaStream_t st = nullptr, bool sync = true);
-void graph_ensure_bloom(Graph& g, cudaStream_t st = nullptr, bool sync = true);
+void graph_ensure_bloom(Graph& g, cudaStream_t st = nullptr, bool sync = true, uint32_t max_bits = 4);
 // rev + wtotal, and (alpha) hash sets + edge filter concurrently.
-void graph_ensure_second_order(Graph& g, bool alpha);
+void graph_ensure_second_order(Graph& g, bool alpha, uint32_t bloom_bits = 4);
 bool graph_ensure_arcrec(Graph& g);  // deepwalk arc records (fp32 weight aux)
 void graph_alias_tables(Graph& g, double* prob, uint32_t* alias);
 // Same tables left on the device (prob, alias: m entries each).

@@ -1449,7 +1449,14 @@ void model_bind(Model& mb, Graph& g, const mhw_model_desc& d) {
         m.M_dim = dim;
         m.M_allpos = allpos ? 1 : 0;
     }
-    if (second_order(k)) graph_ensure_second_order(g, !m.alpha_trivial);
+    if (second_order(k)) {
+        // node2vec graphs that take the compact chain table (2 * arcs <= 96 MB,
+        // node table <= 32 MB) get a 3-bit-per-arc edge filter: its 11.8 MB
+        // leave more L2 beside the pinned 63 MB table (cfg2 walk 23.48 ->
+        // 22.66 ms, init 4.76 -> 5.0; 2 bits: 23.41 / 5.58, 8 bits: 25.67 / 4.69)
+        const bool c16_graph = k == NODE2VEC && 2ull * g.m <= (96ull << 20) && 16ull * g.n <= (32ull << 20);
+        graph_ensure_second_order(g, !m.alpha_trivial, c16_graph ? 3u : 4u);
+    }
     if (k == FAIRWALK) graph_ensure_tcount(g);
 }
 
