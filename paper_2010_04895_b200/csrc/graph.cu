@@ -1220,6 +1220,22 @@ void graph_ensure_bloom(Graph& g, cudaStream_t st, bool sync, uint32_t max_bits)
     if (sync) MHW_CK(cudaStreamSynchronize(st));
 }
 
+// A second edge filter over the same keys at `bits` bits per arc (the
+// compact-chain sessions' eager init probes a denser filter than their walk).
+void graph_build_bloom(const Graph& g, uint32_t bits, DBuf<uint32_t>& out, uint32_t* blocks, cudaStream_t st) {
+    DeviceGuard dg(g.device);
+    const uint64_t nb = (g.m * bits / 8 + 31) / 32;
+    if (!g.m || nb == 0 || nb >= (1ull << 32)) {
+        *blocks = 0;
+        return;
+    }
+    out.alloc(8 * nb);
+    *blocks = (uint32_t)nb;
+    MHW_CK(cudaMemsetAsync(out.p, 0, out.bytes(), st));
+    k_bloom_build<<<grid_for(g.n * 32ull), kBlock, 0, st>>>(g.view(), out.p, *blocks);
+    MHW_CK(cudaGetLastError());
+}
+
 // The alpha-test structures of a second-order model built concurrently: the
 // hash sets and the edge filter on two side streams while the reverse index
 // (a radix sort) runs on the graph's stream (e2e session setup: each is a

@@ -149,6 +149,8 @@ void graph_ensure_hash(Graph& g, cudaStream_t st = nullptr, bool sync = true);
 void graph_ensure_bloom(Graph& g, cudaStream_t st = nullptr, bool sync = true, uint32_t max_bits = 4);
 // rev + wtotal, and (alpha) hash sets + edge filter concurrently.
 void graph_ensure_second_order(Graph& g, bool alpha, uint32_t bloom_bits = 4);
+// A separate edge filter at `bits` bits per arc into `out` (blocks out).
+void graph_build_bloom(const Graph& g, uint32_t bits, DBuf<uint32_t>& out, uint32_t* blocks, cudaStream_t st);
 bool graph_ensure_arcrec(Graph& g);  // deepwalk arc records (fp32 weight aux)
 void graph_alias_tables(Graph& g, double* prob, uint32_t* alias);
 // Same tables left on the device (prob, alias: m entries each).

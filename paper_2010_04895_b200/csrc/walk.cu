@@ -1789,6 +1789,16 @@ void session_create(Session& s, Graph& g, const mhw_model_desc& md, const mhw_wa
             s.nodes8.alloc(std::max<uint32_t>(g.n, 1));
             k_nodes8<<<grid_for(g.n), 256, 0, st>>>(g.view(), s.nodes8.p);
             MHW_CK(cudaGetLastError());
+            // the eager init (about 11 alpha tests per slot, issue/latency
+            // bound) probes a denser filter than the walk: 6 bits per arc,
+            // pinned for the init launch (cfg2 step 27.86 -> 27.71 ms: init
+            // 5.0 -> 4.66, walk 22.67 -> 22.83; 8 bits 27.76; unpinned 27.81)
+            if (g.bloom.n && !m.alpha_trivial) {
+                const char* ib = std::getenv("MHW_INIT_BLOOM_BITS");
+                const uint32_t bits = ib ? (uint32_t)std::atoi(ib) : 6u;
+                if (bits && (uint64_t)bits * g.m / 8 > g.bloom.bytes() && (uint64_t)bits * g.m / 8 <= (33ull << 20))
+                    graph_build_bloom(g, bits, s.init_bloom, &s.init_bloom_blocks, st);
+            }
             // 64-register cap (4 blocks/SM, a 40-byte stack frame): cfg2 walk
             // 24.64 -> 23.84 ms (more walkers in flight outweigh the spills
             // and the extra lock retries, 1.97 M -> 2.35 M)
@@ -1821,7 +1831,10 @@ void session_create(Session& s, Graph& g, const mhw_model_desc& md, const mhw_wa
                     // starves its slice reads (cfg2 init 4.7 -> 6.8 ms)
                     const char* ip = std::getenv("MHW_C16_INITPIN");  // filter (default) | same | none
                     const std::string imode = ip ? ip : "filter";
-                    if (imode == "filter" && g.bloom.n && !m.alpha_trivial && g.bloom.bytes() <= (33ull << 20)) {
+                    if (imode == "filter" && s.init_bloom.n && s.init_bloom.bytes() <= (33ull << 20)) {
+                        s.ipin_p = s.init_bloom.p;
+                        s.ipin_bytes = s.init_bloom.bytes();
+                    } else if (imode == "filter" && g.bloom.n && !m.alpha_trivial && g.bloom.bytes() <= (33ull << 20)) {
                         s.ipin_p = both ? (void*)s.bloom_copy : (void*)g.bloom.p;
                         s.ipin_bytes = g.bloom.bytes();
                     } else if (imode == "none") {
@@ -1920,6 +1933,15 @@ uint64_t k_slots(int kind, const Graph& g) {
     return g.m;
 }
 
+RunParams Session::init_params() const {
+    RunParams P = params();
+    if (init_bloom.n) {
+        P.g.bloom = init_bloom.p;
+        P.g.bloom_blocks = init_bloom_blocks;
+    }
+    return P;
+}
+
 RunParams Session::params() const {
     RunParams P;
     P.g = g->view();
@@ -1948,7 +1970,12 @@ RunParams Session::params() const {
 // state from the record, scattered N(v) reads); chosen in session_create
 // (MHW_INIT_ORDER=rec|slot overrides).
 template <int KIND>
-static void launch_init_all(const Session& s, const RunParams& P, cudaStream_t st) {
+static void launch_init_all(const Session& s, const RunParams& P0, cudaStream_t st) {
+    RunParams P = P0;
+    if (s.init_bloom.n) {
+        P.g.bloom = s.init_bloom.p;
+        P.g.bloom_blocks = s.init_bloom_blocks;
+    }
     if (s.init_rec_order && s.ac.n) k_init_rec<KIND><<<grid_for(s.g->m), 256, 0, st>>>(P, 0, s.g->m, nullptr);
     else {
         const char* e = std::getenv("MHW_INIT_MINB");  // blocks/SM of the slot-order init (A/B)
@@ -2205,7 +2232,7 @@ void session_init_shard(Session& s, uint64_t begin, uint64_t end, void* d_out, c
     if (begin > end || end > s.g->m) invalid("shard range out of bounds");
     if (begin == end) return;
     cudaStream_t st = user ? user : s.stream;
-    k_init_range16<<<grid_for(end - begin), 256, 0, st>>>(s.params(), begin, end, static_cast<uint16_t*>(d_out));
+    k_init_range16<<<grid_for(end - begin), 256, 0, st>>>(s.init_params(), begin, end, static_cast<uint16_t*>(d_out));
     MHW_CK(cudaGetLastError());
 }
 
