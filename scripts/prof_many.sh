@@ -14,6 +14,9 @@ for spec in "$@"; do
   cp profiles/traffic_${cfg}.json gpurun_out/profiles/traffic_${cfg}_${tag}.json 2>/dev/null
   ncu -i gpurun_out/prof_${cfg}_${tag}.ncu-rep --page source --csv --print-source sass > gpurun_out/src_${cfg}_${tag}.csv 2>/dev/null
   python profiles/sass_top.py gpurun_out/src_${cfg}_${tag}.csv 40 > gpurun_out/profiles/sass_${cfg}_${tag}.txt 2>&1
+  ncu -i gpurun_out/prof_${cfg}_${tag}.ncu-rep --page source --csv --print-source cuda > gpurun_out/srccu_${cfg}_${tag}.csv 2>/dev/null
+  python profiles/cuda_top.py gpurun_out/srccu_${cfg}_${tag}.csv 40 > gpurun_out/profiles/cuda_${cfg}_${tag}.txt 2>&1
+  rm -f gpurun_out/srccu_${cfg}_${tag}.csv
   rm -f gpurun_out/prof_${cfg}_${tag}.ncu-rep gpurun_out/src_${cfg}_${tag}.csv
 done
 ls -la gpurun_out/profiles
