@@ -142,8 +142,7 @@ DevGraph Graph::view() const {
     d.htab = htab.n ? htab.p : nullptr;
     d.arc = arc.n ? arc.p : nullptr;
     d.bloom = bloom.n ? bloom.p : nullptr;
-    d.sprob = sprob.n ? sprob.p : nullptr;
-    d.salias = salias.n ? salias.p : nullptr;
+    d.sal = sal.n ? sal.p : nullptr;
     d.bloom_blocks = bloom_blocks;
     d.n_ntypes = n_ntypes;
     d.n_etypes = n_etypes;
@@ -154,7 +153,7 @@ DevGraph Graph::view() const {
 uint64_t Graph::device_bytes() const {
     return nodes.bytes() + ids.bytes() + w.bytes() + ntype.bytes() + etype.bytes() + rev.bytes() +
            wtotal.bytes() + wblk.bytes() + tcount.bytes() + tperm.bytes() + tbase.bytes() + htab.bytes() + arc.bytes() + bloom.bytes() +
-           sprob.bytes() + salias.bytes();
+           sal.bytes();
 }
 
 namespace {
@@ -500,6 +499,15 @@ __global__ void k_bloom_build(DevGraph g, uint32_t* __restrict__ bloom, uint32_t
                 atomicOr(blk + (bit >> 5), 1u << (bit & 31));
             }
         }
+    }
+}
+
+// {prob, alias} of every arc in one 16-byte entry (one load per proposal).
+__global__ void k_pack_alias(const double* __restrict__ prob, const uint32_t* __restrict__ alias, uint64_t m,
+                             uint4* __restrict__ out) {
+    for (uint64_t a = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; a < m; a += (uint64_t)gridDim.x * blockDim.x) {
+        const double p = prob[a];
+        out[a] = make_uint4((uint32_t)__double2loint(p), (uint32_t)__double2hiint(p), alias[a], 0u);
     }
 }
 
@@ -1295,11 +1303,14 @@ void graph_ensure_wtotal(Graph& g) {
 }
 
 void graph_ensure_static_alias(Graph& g) {
-    if (g.sprob.n || !g.w.n || !g.m) return;
+    if (g.sal.n || !g.w.n || !g.m) return;
     DeviceGuard dg(g.device);
-    g.sprob.alloc(g.m);
-    g.salias.alloc(g.m);
-    graph_alias_device(g, g.sprob.p, g.salias.p);
+    DBuf<double> prob(g.m);
+    DBuf<uint32_t> alias(g.m);
+    graph_alias_device(g, prob.p, alias.p);
+    g.sal.alloc(g.m);
+    k_pack_alias<<<grid_for(g.m), kBlock, 0, g.stream>>>(prob.p, alias.p, g.m, g.sal.p);
+    MHW_CK(cudaGetLastError());
     MHW_CK(cudaStreamSynchronize(g.stream));
 }
 

@@ -112,8 +112,7 @@ struct Graph {
     DBuf<uint32_t> bloom;    // edge Bloom filter (second-order alpha), lazily built
     uint32_t bloom_blocks = 0;
     DBuf<uint4> arc;         // arc records, lazily built (m < 2^32)
-    DBuf<double> sprob;      // static-weight alias tables (alias proposal), lazily built
-    DBuf<uint32_t> salias;
+    DBuf<uint4> sal;         // static-weight alias tables (alias proposal), {prob f64, alias, 0} per arc, lazily built
     uint16_t n_ntypes = 0, n_etypes = 0;
     bool symmetric = false;
     bool verified_sym = false;
@@ -155,7 +154,7 @@ bool graph_ensure_arcrec(Graph& g);  // deepwalk arc records (fp32 weight aux)
 void graph_alias_tables(Graph& g, double* prob, uint32_t* alias);
 // Same tables left on the device (prob, alias: m entries each).
 void graph_alias_device(Graph& g, double* prob, uint32_t* alias);
-// The same tables kept on the graph (sprob / salias) for the alias proposal
+// The same tables kept on the graph (packed {prob, alias}: sal) for the alias proposal
 // of the M-H walk; unweighted graphs need none (every prob is 1.0).
 void graph_ensure_static_alias(Graph& g);
 

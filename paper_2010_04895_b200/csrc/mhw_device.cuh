@@ -69,8 +69,7 @@ struct DevGraph {
     const uint32_t* __restrict__ bloom;   // edge Bloom filter, 8 words per block (nullptr: not built)
     const uint32_t* __restrict__ tperm;   // per slice: neighbour indices ordered by (type, w > 0 first, index)
     const uint2* __restrict__ tbase;      // per (node, type): {start in tperm slice, count of w > 0}
-    const double* __restrict__ sprob;     // static alias tables per slice (alias proposal; nullptr: none)
-    const uint32_t* __restrict__ salias;
+    const uint4* __restrict__ sal;        // static alias tables per slice, {prob f64, alias, 0} (alias proposal; nullptr: none)
     uint32_t bloom_blocks;
     uint16_t n_ntypes;
     uint16_t n_etypes;

@@ -120,8 +120,8 @@ __device__ __noinline__ uint32_t init_slot_ool(const DevGraph g, const DevModel 
 // proposal and the Hastings accept (mhw_walk_config.proposal = ALIAS).
 template <int KIND, int REGS, bool LAZY, int ARV>
 __global__ void __launch_bounds__(kWalkBlock) __maxnreg__(REGS) k_walk(RunParams P) {
-    constexpr bool ALIAS = ARV == 4;
-    constexpr int AR = ALIAS ? 0 : ARV;
+    constexpr bool ALIAS = ARV == 4 || ARV == 5;  // 4: plain CSR, 5: arc records
+    constexpr int AR = ARV == 4 ? 0 : (ARV == 5 ? 1 : ARV);
     const DevGraph& g = P.g;
     constexpr bool TYPED = AR && needs_utype<KIND>();
     constexpr bool CC = AR && second_order(KIND);
@@ -292,7 +292,13 @@ __global__ void __launch_bounds__(kWalkBlock) __maxnreg__(REGS) k_walk(RunParams
                     // index on word 0, coin on words 1-2; the accept unit
                     // from sub-block kAcceptSub
                     const uint32_t i = d.index(c.deg);
-                    cand = (!g.sprob || d.unit() < __ldg(g.sprob + c.off + i)) ? i : __ldg(g.salias + c.off + i);
+                    // {prob f64, alias} of index i in one 16-byte load
+                    if (g.sal) {
+                        const uint4 t = __ldg(g.sal + c.off + i);
+                        cand = d.unit() < __hiloint2double((int)t.y, (int)t.x) ? i : t.z;
+                    } else {
+                        cand = i;  // unweighted: every prob is 1.0
+                    }
                     Draw da;
                     da.open_sub(wkey, walker, step, kAcceptSub);
                     u = da.unit();
@@ -445,7 +451,9 @@ __global__ void __launch_bounds__(kWalkBlock) __maxnreg__(REGS) k_walk(RunParams
                 // deepwalk (cheap, L2-resident graphs; measured win). For
                 // node2vec/edge2vec the extra sectors cost more than the
                 // shorter rejection path saves (profiles/, round 1).
-                constexpr bool kSpec = !WLC && (needs_utype<KIND>() || KIND == DEEPWALK);
+                // (the alias proposal's Hastings ratio needs the Last's own
+                // type / edge type, not the w'(Last) typed records cache)
+                constexpr bool kSpec = (!WLC || ALIAS) && (needs_utype<KIND>() || KIND == DEEPWALK);
                 uint32_t ul = 0;
                 NodeRec rl{};
                 uint4 al = make_uint4(0, 0, 0, 0), bl = make_uint4(0, 0, 0, 0);
@@ -467,11 +475,16 @@ __global__ void __launch_bounds__(kWalkBlock) __maxnreg__(REGS) k_walk(RunParams
                 bool acc;
                 if constexpr (ALIAS) {
                     // Hastings: target w' = r w, proposal q ~ w -> min(1, r_c / r_l)
-                    const uint32_t ot_c = KIND == EDGE2VEC ? edge_type_of(g, c.off + cand, c.vtype, rc.type) : 0u;
-                    const uint32_t ot_l = KIND == EDGE2VEC ? edge_type_of(g, c.off + last, c.vtype, rl.type) : 0u;
+                    // records carry the edge type and the static weight
+                    const uint32_t ot_c = KIND != EDGE2VEC ? 0u
+                                          : (TYPED ? (bc.x >> 16) : edge_type_of(g, c.off + cand, c.vtype, rc.type));
+                    const uint32_t ot_l = KIND != EDGE2VEC ? 0u
+                                          : (TYPED ? (bl.x >> 16) : edge_type_of(g, c.off + last, c.vtype, rl.type));
                     const double r_c = rfactor<KIND>(g, P.m, c, rc.type, ot_c, cls_c);
                     const double r_l = rfactor<KIND>(g, P.m, c, rl.type, ot_l, cls_l);
-                    acc = hastings_accept(static_w(g, c.off + cand), r_c, r_l, u) && cand != last;
+                    const double w_c = (AR && (KIND == DEEPWALK || TYPED)) ? (double)__uint_as_float(ac.w)
+                                                                           : static_w(g, c.off + cand);
+                    acc = hastings_accept(w_c, r_c, r_l, u) && cand != last;
                     (void)wc;
                     (void)wl;
                 } else {
@@ -1352,6 +1365,7 @@ void with_variant(int regs, bool lazy, int ar, F&& f) {
             }
         }
         if (ar == 4) by_regs(lz, std::integral_constant<int, 4>{});
+        else if (ar == 5) by_regs(lz, std::integral_constant<int, 5>{});
         else if (ar) by_regs(lz, std::integral_constant<int, 1>{});
         else by_regs(lz, std::integral_constant<int, 0>{});
     };
@@ -1767,11 +1781,11 @@ void session_create(Session& s, Graph& g, const mhw_model_desc& md, const mhw_wa
         // graph's static alias tables
         const bool alias_prop = wc.proposal == MHW_PROPOSAL_ALIAS;
         if (alias_prop) graph_ensure_static_alias(g);
-        const bool want_ar = !(ar_env && ar_env[0] == '0') && !alias_prop;
+        const bool want_ar = !(ar_env && ar_env[0] == '0');
         // node2vec compact chains (AR 3): 16-bit words in their own table when
         // it and the node table fit L2 (MHW_C16=0/1 forces)
         const char* c16e = std::getenv("MHW_C16");
-        const bool c16_ok = m.kind == NODE2VEC && s.eager_init && g.verified_sym && g.m && g.m < (1ull << 32) &&
+        const bool c16_ok = !alias_prop && m.kind == NODE2VEC && s.eager_init && g.verified_sym && g.m && g.m < (1ull << 32) &&
                             g.max_deg <= 0xFFFDu && want_ar;
         const bool c16_want = c16_ok && (c16e ? c16e[0] == '1' : (2ull * g.m <= (96ull << 20) && 16ull * g.n <= (32ull << 20)));
         if (c16_want) {
@@ -1854,7 +1868,7 @@ void session_create(Session& s, Graph& g, const mhw_model_desc& md, const mhw_wa
             // node2vec: narrow 8-byte records when the node table (16 B per
             // node) is small enough to stay in L2 (MHW_NARROW=0/1 forces)
             const char* nw = std::getenv("MHW_NARROW");
-            const bool narrow = m.kind == NODE2VEC && (nw ? nw[0] == '1' : 16ull * g.n <= (32ull << 20));
+            const bool narrow = !alias_prop && m.kind == NODE2VEC && (nw ? nw[0] == '1' : 16ull * g.n <= (32ull << 20));
             s.rec_u32 = typed_kind(m.kind) ? 8 : (narrow ? 2 : 4);
             const uint64_t need = 4ull * s.rec_u32 * g.m;
             if (dev_available_bytes() >= need + (2ull << 30)) {

@@ -99,7 +99,7 @@ struct Session {
     ~Session();
     RunParams params() const;
     int ar_mode() const {
-        if (cfg.proposal == MHW_PROPOSAL_ALIAS) return 4;  // plain CSR + alias proposal
+        if (cfg.proposal == MHW_PROPOSAL_ALIAS) return use_ar ? 5 : 4;  // alias proposal on records / plain CSR
         return c16.n ? 3 : (use_ar ? (rec_u32 == 2 ? 2 : 1) : 0);
     }
 };

@@ -73,9 +73,13 @@ def isolated_equal(mhw, oracle, g, md, cfg, starts, weighted=True, **wkw):
     s.close()
 
 
+@pytest.mark.parametrize("records", ["1", "0"])
 @pytest.mark.parametrize("init", INITS)
 @pytest.mark.parametrize("kind", KINDS)
-def test_single_walkers_equal_oracle(mhw, oracle, kind, init):
+def test_single_walkers_equal_oracle(mhw, oracle, kind, init, records, monkeypatch):
+    """Both alias variants of k_walk: on the arc records (AR 5, default) and
+    on the plain CSR (AR 4, MHW_ARC_RECORDS=0)."""
+    monkeypatch.setenv("MHW_ARC_RECORDS", records)
     g = typed_random_graph(60 + kind, 120, 5.0, weighted=True, types=2)
     md = model_desc(kind, g, p=0.4, q=2.5, M=np.random.default_rng(kind).uniform(0.5, 2.0, (4, 4)))
     deg = np.diff(g.offsets.astype(np.int64))
