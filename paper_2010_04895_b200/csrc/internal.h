@@ -111,6 +111,8 @@ struct Graph {
     DBuf<uint32_t> htab;     // adjacency hash sets, lazily built
     DBuf<uint32_t> bloom;    // edge Bloom filter (second-order alpha), lazily built
     uint32_t bloom_blocks = 0;
+    DBuf<uint32_t> bloom2;   // the same filter at twice the blocks (bloom = its fold); compact-chain graphs
+    uint32_t bloom2_blocks = 0;
     DBuf<uint4> arc;         // arc records, lazily built (m < 2^32)
     DBuf<uint4> sal;         // static-weight alias tables (alias proposal), {prob f64, alias, 0} per arc, lazily built
     uint16_t n_ntypes = 0, n_etypes = 0;

@@ -86,6 +86,71 @@ __device__ __forceinline__ void ldg256(const void* p, uint4& lo, uint4& hi) {
                  : "l"(p));
 }
 
+// The same load with an L2 eviction priority (HINT 1: evict-first,
+// LDG.E.EFL2.256; 2: evict-last, LDG.E.ELL2.256; 0: normal). Build-time
+// experiment knobs MHW_HASH_HINT / MHW_BLOOM_HINT / MHW_NODE8_HINT /
+// MHW_STORE_HINT (scripts/build_variant.sh); results in DESIGN.md section 3.
+template <int HINT>
+__device__ __forceinline__ void ldg256h(const void* p, uint4& lo, uint4& hi) {
+    if constexpr (HINT == 1)
+        asm("ld.global.nc.L2::evict_first.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                     : "=r"(lo.x), "=r"(lo.y), "=r"(lo.z), "=r"(lo.w), "=r"(hi.x), "=r"(hi.y), "=r"(hi.z), "=r"(hi.w)
+                     : "l"(p));
+    else if constexpr (HINT == 2)
+        asm("ld.global.nc.L2::evict_last.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                     : "=r"(lo.x), "=r"(lo.y), "=r"(lo.z), "=r"(lo.w), "=r"(hi.x), "=r"(hi.y), "=r"(hi.z), "=r"(hi.w)
+                     : "l"(p));
+    else
+        ldg256(p, lo, hi);
+}
+#ifndef MHW_HASH_HINT
+#define MHW_HASH_HINT 0
+#endif
+#ifndef MHW_BLOOM_HINT
+#define MHW_BLOOM_HINT 0
+#endif
+#ifndef MHW_NODE8_HINT
+#define MHW_NODE8_HINT 0
+#endif
+#ifndef MHW_STORE_HINT
+#define MHW_STORE_HINT 0
+#endif
+#ifndef MHW_IDS_HINT
+#define MHW_IDS_HINT 0
+#endif
+
+template <int HINT>
+__device__ __forceinline__ unsigned long long l2_policy() {
+    unsigned long long pol = 0;
+    if constexpr (HINT == 1) asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    if constexpr (HINT == 2) asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+template <int HINT>
+__device__ __forceinline__ uint2 ldg64h(const uint2* p) {
+    if constexpr (HINT == 0) return __ldg(p);
+    uint2 r;
+    asm("ld.global.nc.L2::cache_hint.v2.u32 {%0,%1}, [%2], %3;" : "=r"(r.x), "=r"(r.y) : "l"(p), "l"(l2_policy<HINT>()));
+    return r;
+}
+template <int HINT>
+__device__ __forceinline__ uint32_t ldg32h(const uint32_t* p) {
+    if constexpr (HINT == 0) return __ldg(p);
+    uint32_t r;
+    asm("ld.global.nc.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(r) : "l"(p), "l"(l2_policy<HINT>()));
+    return r;
+}
+template <int HINT>
+__device__ __forceinline__ void stg128h(uint4* p, uint4 v) {
+    if constexpr (HINT == 0) {
+        *p = v;
+    } else {
+        asm volatile("st.global.L2::cache_hint.v4.u32 [%0], {%1,%2,%3,%4}, %5;" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z),
+                     "r"(v.w), "l"(l2_policy<HINT>())
+                     : "memory");
+    }
+}
+
 // ------------------------------------------------------------ arc records
 // For graphs with < 2^32 arcs, arc a = (v -> u) has a 16-byte record
 // {u, deg(u) | NF_ALLPOS(u) << 31, off(u), fp32 w(a)} (graph records, used by
@@ -146,7 +211,7 @@ __device__ __forceinline__ bool bloom_maybe(const DevGraph& g, uint32_t a, uint3
     const uint64_t x = bloom_key(a, b);
     const uint4* blk = reinterpret_cast<const uint4*>(g.bloom) + 2 * (uint64_t)bloom_block(x, g.bloom_blocks);
     uint4 lo, hi;
-    ldg256(blk, lo, hi);
+    ldg256h<MHW_BLOOM_HINT>(blk, lo, hi);
     // 256-bit block as eight 32-bit words, selected by predicated moves (no
     // branches, no local array)
     bool all = true;
@@ -163,6 +228,11 @@ __device__ __forceinline__ bool bloom_maybe(const DevGraph& g, uint32_t a, uint3
     return all;
 }
 
+// HH: L2 eviction priority of the bucket loads (ldg256h). The compact-chain
+// walk probes with evict-first: its pinned chain table leaves little L2, and
+// a bucket of the 8 B/arc hash table is not reused (cfg2 walk 22.85 -> 22.63
+// ms; cfg4, nothing pinned but the filter: 156.1 -> 157.1, so not there).
+template <int HH = MHW_HASH_HINT>
 __device__ __forceinline__ bool hash_contains(const uint32_t* __restrict__ tab, long long off, uint32_t v,
                                               uint32_t deg, uint32_t key) {
     const uint32_t nb = hash_buckets(deg);
@@ -170,7 +240,7 @@ __device__ __forceinline__ bool hash_contains(const uint32_t* __restrict__ tab, 
     uint32_t b = hash_bucket(key, nb);
     for (;;) {
         uint4 x, y;
-        ldg256(base + 2 * b, x, y);
+        ldg256h<HH>(base + 2 * b, x, y);
         if (x.x == key || x.y == key || x.z == key || x.w == key || y.x == key || y.y == key || y.z == key ||
             y.w == key)
             return true;
@@ -431,6 +501,7 @@ __device__ __forceinline__ uint32_t edge_type_of(const DevGraph& g, long long ar
 // candidate's record here when (and only when) the shorter-slice choice needs
 // it -- callers keep a single call site, so lanes that need the record and
 // lanes that do not stay converged through the filter probe.
+template <int HH = MHW_HASH_HINT>
 __device__ __forceinline__ uint32_t alpha_class(const DevGraph& g, const DevModel& m, const SCtx& c,
                                                 uint32_t u, const NodeRec* urec, int bloom = -1,
                                                 bool load_urec = false) {
@@ -441,7 +512,7 @@ __device__ __forceinline__ uint32_t alpha_class(const DevGraph& g, const DevMode
     if (g.bloom && !(bloom >= 0 ? bloom != 0 : bloom_maybe(g, c.s, u))) return 2;
     // s's own hash set needs nothing about u: probe it without waiting for
     // the candidate's node record (shorter dependency chain per step).
-    if (g.htab && c.deg_s >= kHashMinDeg) return hash_contains(g.htab, c.off_s, c.s, c.deg_s, u) ? 1u : 2u;
+    if (g.htab && c.deg_s >= kHashMinDeg) return hash_contains<HH>(g.htab, c.off_s, c.s, c.deg_s, u) ? 1u : 2u;
     // is_adjacent(s, u): u in N(s), or s in N(u) when every arc has its
     // back arc. Cheapest structure first: a <= 8-entry slice (one sector),
     // else a hash set (one sector), else binary search of the shorter slice.
@@ -464,8 +535,8 @@ __device__ __forceinline__ uint32_t alpha_class(const DevGraph& g, const DevMode
         }
     }
     if (deg_a > 8 && g.htab) {
-        if (deg_a >= kHashMinDeg) return hash_contains(g.htab, off_a, node_a, deg_a, key_a) ? 1u : 2u;
-        if (both && deg_b >= kHashMinDeg) return hash_contains(g.htab, off_b, node_b, deg_b, key_b) ? 1u : 2u;
+        if (deg_a >= kHashMinDeg) return hash_contains<HH>(g.htab, off_a, node_a, deg_a, key_a) ? 1u : 2u;
+        if (both && deg_b >= kHashMinDeg) return hash_contains<HH>(g.htab, off_b, node_b, deg_b, key_b) ? 1u : 2u;
     }
     return adj_search(g.ids, off_a, deg_a, key_a) ? 1u : 2u;
 }

@@ -127,6 +127,7 @@ __global__ void __launch_bounds__(kWalkBlock) __maxnreg__(REGS) k_walk(RunParams
     constexpr bool CC = AR && second_order(KIND);
     constexpr bool NARROW = AR == 2;
     constexpr bool C16 = AR == 3;  // ids + compact 16-bit chain table (node2vec)
+    constexpr int kHashHint = C16 ? 1 : MHW_HASH_HINT;  // hash buckets evict-first beside the pinned table
     static_assert(!C16 || (KIND == NODE2VEC && !LAZY), "compact chains: eagerly initialised node2vec");
     // typed second-order records carry w'(Last) next to the chain word
     // (word 1 = {type | etype << 16, chain word, w'(Last) as f64}), taken and
@@ -257,7 +258,7 @@ __global__ void __launch_bounds__(kWalkBlock) __maxnreg__(REGS) k_walk(RunParams
                     // stall samples on the decode of the lock word).
                     cand = d.index(c.deg);
                     u = d.unit();
-                    c16_uc = __ldg(g.ids + c.off + cand);
+                    c16_uc = ldg32h<MHW_IDS_HINT>(g.ids + c.off + cand);
                 }
                 if (WLC) {
                     E = atom_exch128(cb, make_uint4(tx, kLocked, 0u, 0u));
@@ -349,7 +350,7 @@ __global__ void __launch_bounds__(kWalkBlock) __maxnreg__(REGS) k_walk(RunParams
                     uc = x.x;
                     if constexpr (C16) {
                         // 8-byte node record {off, deg | allpos << 31}
-                        const uint2 nr = __ldg(P.nodes8 + uc);  // issued first
+                        const uint2 nr = ldg64h<MHW_NODE8_HINT>(P.nodes8 + uc);  // issued first
                         if (g.bloom && !P.m.alpha_trivial && uc != c.s) pre_bloom = bloom_maybe(g, c.s, uc) ? 1 : 0;
                         rc.off = nr.x;
                         rc.deg = nr.y & 0x7FFFFFFFu;
@@ -382,7 +383,7 @@ __global__ void __launch_bounds__(kWalkBlock) __maxnreg__(REGS) k_walk(RunParams
                     if (rc_early) rc = load_node(g, uc);
                 }
                 const uint32_t cls_c =
-                    second_order(KIND) ? alpha_class(g, P.m, c, uc, rc_early ? &rc : nullptr, pre_bloom) : 0u;
+                    second_order(KIND) ? alpha_class<kHashHint>(g, P.m, c, uc, rc_early ? &rc : nullptr, pre_bloom) : 0u;
                 double wc;
                 if (AR && KIND == DEEPWALK) wc = (double)__uint_as_float(ac.w);
                 else if (grp_pre) {
@@ -444,7 +445,7 @@ __global__ void __launch_bounds__(kWalkBlock) __maxnreg__(REGS) k_walk(RunParams
                         xl = make_uint2(__ldg(g.ids + c.off + last), 0u);
                         spec_l = true;
                     }
-                    cls_l = alpha_class(g, P.m, c, xl.x, nullptr);
+                    cls_l = alpha_class<kHashHint>(g, P.m, c, xl.x, nullptr);
                 }
                 // The last sample's id and record are fetched before the
                 // decision where w'(last) needs its type anyway, and for
@@ -515,7 +516,7 @@ __global__ void __launch_bounds__(kWalkBlock) __maxnreg__(REGS) k_walk(RunParams
                         // which returns the same index as the full scan)
                         an = make_uint4(c.s, c.deg_s, (uint32_t)c.off_s, 0u);
                     } else if (C16 && spec_l) {
-                        const uint2 r = __ldg(P.nodes8 + xl.x);
+                        const uint2 r = ldg64h<MHW_NODE8_HINT>(P.nodes8 + xl.x);
                         an = make_uint4(xl.x, r.y, r.x, 0u);
                     } else if (NARROW && spec_l && (e & kIdxMask) == last) {
                         const NodeRec r = load_node(g, xl.x);
@@ -548,7 +549,7 @@ __global__ void __launch_bounds__(kWalkBlock) __maxnreg__(REGS) k_walk(RunParams
                 case 2: b2 = next; break;
                 default:
                     b3 = next;
-                    *reinterpret_cast<uint4*>(orow + (len & ~3u)) = make_uint4(b0, b1, b2, b3);
+                    stg128h<MHW_STORE_HINT>(reinterpret_cast<uint4*>(orow + (len & ~3u)), make_uint4(b0, b1, b2, b3));
                     break;
             }
             ++len;
@@ -1810,8 +1811,16 @@ void session_create(Session& s, Graph& g, const mhw_model_desc& md, const mhw_wa
             if (g.bloom.n && !m.alpha_trivial) {
                 const char* ib = std::getenv("MHW_INIT_BLOOM_BITS");
                 const uint32_t bits = ib ? (uint32_t)std::atoi(ib) : 6u;
-                if (bits && (uint64_t)bits * g.m / 8 > g.bloom.bytes() && (uint64_t)bits * g.m / 8 <= (33ull << 20))
+                if (!ib && g.bloom2.n) {
+                    // built with the walk's filter (its fold), graph_ensure_bloom
+                    s.ib_p = g.bloom2.p;
+                    s.ib_bytes = g.bloom2.bytes();
+                    s.init_bloom_blocks = g.bloom2_blocks;
+                } else if (bits && (uint64_t)bits * g.m / 8 > g.bloom.bytes() && (uint64_t)bits * g.m / 8 <= (33ull << 20)) {
                     graph_build_bloom(g, bits, s.init_bloom, &s.init_bloom_blocks, st);
+                    s.ib_p = s.init_bloom.p;
+                    s.ib_bytes = s.init_bloom.bytes();
+                }
             }
             // 64-register cap (4 blocks/SM, a 40-byte stack frame): cfg2 walk
             // 24.64 -> 23.84 ms (more walkers in flight outweigh the spills
@@ -1845,9 +1854,9 @@ void session_create(Session& s, Graph& g, const mhw_model_desc& md, const mhw_wa
                     // starves its slice reads (cfg2 init 4.7 -> 6.8 ms)
                     const char* ip = std::getenv("MHW_C16_INITPIN");  // filter (default) | same | none
                     const std::string imode = ip ? ip : "filter";
-                    if (imode == "filter" && s.init_bloom.n && s.init_bloom.bytes() <= (33ull << 20)) {
-                        s.ipin_p = s.init_bloom.p;
-                        s.ipin_bytes = s.init_bloom.bytes();
+                    if (imode == "filter" && s.ib_p && s.ib_bytes <= (33ull << 20)) {
+                        s.ipin_p = const_cast<uint32_t*>(s.ib_p);
+                        s.ipin_bytes = s.ib_bytes;
                     } else if (imode == "filter" && g.bloom.n && !m.alpha_trivial && g.bloom.bytes() <= (33ull << 20)) {
                         s.ipin_p = both ? (void*)s.bloom_copy : (void*)g.bloom.p;
                         s.ipin_bytes = g.bloom.bytes();
@@ -1949,8 +1958,8 @@ uint64_t k_slots(int kind, const Graph& g) {
 
 RunParams Session::init_params() const {
     RunParams P = params();
-    if (init_bloom.n) {
-        P.g.bloom = init_bloom.p;
+    if (ib_p) {
+        P.g.bloom = ib_p;
         P.g.bloom_blocks = init_bloom_blocks;
     }
     return P;
@@ -1986,8 +1995,8 @@ RunParams Session::params() const {
 template <int KIND>
 static void launch_init_all(const Session& s, const RunParams& P0, cudaStream_t st) {
     RunParams P = P0;
-    if (s.init_bloom.n) {
-        P.g.bloom = s.init_bloom.p;
+    if (s.ib_p) {
+        P.g.bloom = s.ib_p;
         P.g.bloom_blocks = s.init_bloom_blocks;
     }
     if (s.init_rec_order && s.ac.n) k_init_rec<KIND><<<grid_for(s.g->m), 256, 0, st>>>(P, 0, s.g->m, nullptr);

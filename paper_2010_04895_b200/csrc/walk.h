@@ -64,7 +64,9 @@ struct Session {
     DBuf<uint32_t> c16;      // compact 16-bit chain words (node2vec, L2-sized), [c16 | filter copy] when pinned
     const uint32_t* bloom_copy = nullptr;  // the edge filter's copy behind c16 (one persisting window)
     DBuf<uint2> nodes8;      // compact chains: 8-byte node records (half the L2 footprint of NodeRec)
-    DBuf<uint32_t> init_bloom;  // compact chains: the eager init's denser edge filter
+    DBuf<uint32_t> init_bloom;  // compact chains: the eager init's denser edge filter (own build: MHW_INIT_BLOOM_BITS)
+    const uint32_t* ib_p = nullptr;  // the init's filter: init_bloom, or the graph's dense filter (Graph::bloom2)
+    size_t ib_bytes = 0;
     uint32_t init_bloom_blocks = 0;
     RunParams init_params() const;  // params() with the init's edge filter
     std::unique_ptr<ExactState> ex;  // alias / direct / rejection baselines (exact.cu)
