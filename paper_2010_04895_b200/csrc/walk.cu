@@ -33,7 +33,13 @@ namespace mhw {
 
 namespace {
 
-constexpr int kWalkBlock = 256;
+#ifndef MHW_WALK_BLOCK
+#define MHW_WALK_BLOCK 256
+#endif
+#ifndef MHW_REG80  // experiment: the register cap the "80" variants compile to
+#define MHW_REG80 80
+#endif
+constexpr int kWalkBlock = MHW_WALK_BLOCK;
 constexpr uint32_t kDeadMark = 0xFFFFFFFEu;
 
 // Releases a chain slot taken with atomicExch(kLocked). The lock protects
@@ -119,7 +125,7 @@ __device__ __noinline__ uint32_t init_slot_ool(const DevGraph g, const DevModel 
 // AR = 4: the plain-CSR variant (as AR = 0) with the static-weight alias
 // proposal and the Hastings accept (mhw_walk_config.proposal = ALIAS).
 template <int KIND, int REGS, bool LAZY, int ARV>
-__global__ void __launch_bounds__(kWalkBlock) __maxnreg__(REGS) k_walk(RunParams P) {
+__global__ void __launch_bounds__(kWalkBlock) __maxnreg__(REGS == 80 ? MHW_REG80 : REGS) k_walk(RunParams P) {
     constexpr bool ALIAS = ARV == 4 || ARV == 5;  // 4: plain CSR, 5: arc records
     constexpr int AR = ARV == 4 ? 0 : (ARV == 5 ? 1 : ARV);
     const DevGraph& g = P.g;
