@@ -1342,8 +1342,11 @@ int walk_minb(int kind, bool eager) {
     const char* e = std::getenv("MHW_WALK_REGS");
     // deepwalk: 80; eagerly initialised edge2vec / fairwalk: 80 (84-86 -> 80
     // registers without spills lifts occupancy from 2 to 3 blocks/SM: cfg3b
-    // 99.5 -> 94.3 ms, cfg4 181 -> 176 ms); the lazy variants would spill
-    const bool cap = kind == DEEPWALK || (eager && (kind == EDGE2VEC || kind == FAIRWALK));
+    // 99.5 -> 94.3 ms, cfg4 181 -> 176 ms); their lazy variants would spill.
+    // metapath2vec (lazily initialised, 120 registers = 2 blocks/SM): the cap
+    // spills 56 bytes, all in the first-touch init path: cfg3a 48.45 -> 45.2
+    // ms at 80 (64: 48.75)
+    const bool cap = kind == DEEPWALK || kind == METAPATH2VEC || (eager && (kind == EDGE2VEC || kind == FAIRWALK));
     const int v = e ? std::atoi(e) : (cap ? 80 : 255);
     return v == 64 ? 64 : (v == 80 ? 80 : 255);
 }
