@@ -608,6 +608,32 @@ __global__ void __launch_bounds__(kWalkBlock) __maxnreg__(REGS == 80 ? MHW_REG80
     if (retries) atomicAdd(&P.ctr[6], retries);
 }
 
+// Node of arc a: the session's per-arc source array when it has one (one
+// coalesced load; built for eagerly initialised second-order sessions), else
+// the last v with nodes[v].off <= a (skips isolated nodes; ~log2(n)
+// dependent loads per thread: 7-9% of k_init_all's stall samples on cfg2).
+__device__ __forceinline__ uint32_t arc_owner(const RunParams& P, uint64_t a) {
+    if (P.src) return __ldg(P.src + a);
+    const DevGraph& g = P.g;
+    uint32_t lo = 0, hi = g.n;
+    while (hi - lo > 1) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if ((uint64_t)__ldg(&g.nodes[mid].off) <= a) lo = mid;
+        else hi = mid;
+    }
+    return lo;
+}
+
+__global__ void k_arc_src(DevGraph g, uint32_t* __restrict__ out) {
+    const unsigned lane = threadIdx.x & 31;
+    const uint64_t wid = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    for (uint64_t v = wid; v < g.n; v += nw) {
+        const NodeRec r = load_node(g, (uint32_t)v);
+        for (uint32_t i = lane; i < r.deg; i += 32) out[r.off + i] = (uint32_t)v;
+    }
+}
+
 // Eager chain-table initialisation of every arc-keyed slot (second-order
 // models). Result-identical to the lazy path (init randomness is keyed by the
 // slot), but runs with full warps and neighbouring threads share the node v.
@@ -622,12 +648,7 @@ __global__ void __launch_bounds__(256, MINB) k_init_all(RunParams P) {
     for (uint64_t a = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; a < g.m;
          a += (uint64_t)gridDim.x * blockDim.x) {
         // node of arc a: the last v with nodes[v].off <= a (skips isolated nodes)
-        uint32_t lo = 0, hi = g.n;
-        while (hi - lo > 1) {
-            const uint32_t mid = (lo + hi) >> 1;
-            if ((uint64_t)__ldg(&g.nodes[mid].off) <= a) lo = mid;
-            else hi = mid;
-        }
+        const uint32_t lo = arc_owner(P, a);
         const NodeRec r = load_node(g, lo);
         const uint32_t affix = (uint32_t)(a - (uint64_t)r.off);
         const SCtx c = make_ctx<KIND>(g, P.m, lo, affix);
@@ -664,12 +685,7 @@ __global__ void __launch_bounds__(256, KIND == NODE2VEC ? 6 : 4) k_init_range(Ru
     const DevGraph& g = P.g;
     for (uint64_t a = b + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; a < e;
          a += (uint64_t)gridDim.x * blockDim.x) {
-        uint32_t lo = 0, hi = g.n;
-        while (hi - lo > 1) {
-            const uint32_t mid = (lo + hi) >> 1;
-            if ((uint64_t)__ldg(&g.nodes[mid].off) <= a) lo = mid;
-            else hi = mid;
-        }
+        const uint32_t lo = arc_owner(P, a);
         const NodeRec r = load_node(g, lo);
         const SCtx c = make_ctx<KIND>(g, P.m, lo, (uint32_t)(a - (uint64_t)r.off));
         out[a - b] = init_slot<KIND>(g, P.m, P.cfg, c, a);
@@ -685,12 +701,7 @@ __global__ void __launch_bounds__(256, 6) k_init_range16(RunParams P, uint64_t b
     const DevGraph& g = P.g;
     for (uint64_t a = b + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; a < e;
          a += (uint64_t)gridDim.x * blockDim.x) {
-        uint32_t lo = 0, hi = g.n;
-        while (hi - lo > 1) {
-            const uint32_t mid = (lo + hi) >> 1;
-            if ((uint64_t)__ldg(&g.nodes[mid].off) <= a) lo = mid;
-            else hi = mid;
-        }
+        const uint32_t lo = arc_owner(P, a);
         const NodeRec r = load_node(g, lo);
         const SCtx c = make_ctx<NODE2VEC>(g, P.m, lo, (uint32_t)(a - (uint64_t)r.off));
         out[a - b] = (uint16_t)c16_enc(init_slot<NODE2VEC>(g, P.m, P.cfg, c, a), c.deg);
@@ -1752,8 +1763,15 @@ void session_create(Session& s, Graph& g, const mhw_model_desc& md, const mhw_wa
         const char* io = std::getenv("MHW_INIT_ORDER");
         const char* nw0 = std::getenv("MHW_NARROW");
         const bool narrow_pred = m.kind == NODE2VEC && (nw0 ? nw0[0] == '1' : 16ull * g.n <= (32ull << 20));
-        s.init_rec_order = io ? io[0] == 'r' : (!narrow_pred && s.cfg.init_kind != INIT_BURN_IN);
-        const bool dense = (double)s.n_items * s.cfg.L >= (s.init_rec_order ? 2.0 : 8.0) * (double)s.slots;
+        const bool rec_pred = io ? io[0] == 'r' : (!narrow_pred && s.cfg.init_kind != INIT_BURN_IN);
+        // With the per-arc source array (s.src, graphs up to 2^28 arcs) the
+        // slot-order init needs no owner search and beats record order there
+        // too: cfg4 init 12.66 -> 11.6 ms, cfg3b 1.56 -> 1.32 (cfg5, 2.08 G
+        // arcs, no source array: slot order 198 vs 136 ms)
+        const char* se0 = std::getenv("MHW_ARC_SRC");
+        const bool src_ok = g.m < (1ull << 28) && !(se0 && se0[0] == '0');
+        s.init_rec_order = io ? rec_pred : (rec_pred && !src_ok);
+        const bool dense = (double)s.n_items * s.cfg.L >= (rec_pred ? 2.0 : 8.0) * (double)s.slots;
         s.eager_init = second_order(m.kind) && (wc.init_mode == 2 || (wc.init_mode == 0 && dense));
         s.minb = walk_minb(m.kind, s.eager_init);
         // pin an L2-sized edge filter (<= 32 MB by construction) in L2
@@ -1896,6 +1914,18 @@ void session_create(Session& s, Graph& g, const mhw_model_desc& md, const mhw_wa
                 s.use_ar = true;
             }
         }
+        // per-arc source nodes for the slot-order init kernels (k_init_all,
+        // k_init_range*): one coalesced load instead of an owner search per
+        // slot (MHW_ARC_SRC=0 for the A/B)
+        {
+            const char* se = std::getenv("MHW_ARC_SRC");
+            if (s.eager_init && second_order(m.kind) && !(s.init_rec_order && s.ac.n) && g.m && g.m < (1ull << 32) &&
+                !(se && se[0] == '0') && dev_available_bytes() >= 4ull * g.m + (2ull << 30)) {
+                s.src.alloc(g.m);
+                k_arc_src<<<grid_for(g.n * 32ull), 256, 0, st>>>(g.view(), s.src.p);
+                MHW_CK(cudaGetLastError());
+            }
+        }
         if ((!s.ac.n && !s.c16.n) || !second_order(m.kind)) s.chain.alloc(std::max<uint64_t>(s.slots, 1));
         else s.chain.alloc(1);
         // node-keyed models: the chain table itself (hub replicas included)
@@ -1987,6 +2017,7 @@ RunParams Session::params() const {
     P.ac = ac.n ? ac.p : nullptr;
     P.c16 = c16.n ? c16.p : nullptr;
     P.nodes8 = nodes8.n ? nodes8.p : nullptr;
+    P.src = src.n ? src.p : nullptr;
     if (bloom_copy) P.g.bloom = bloom_copy;
     P.rec_u32 = rec_u32;
     P.out = out.p;

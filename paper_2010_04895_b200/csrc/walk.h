@@ -23,6 +23,7 @@ struct RunParams {
     uint32_t* c16;            // node2vec compact chains (AR 3): one 16-bit word per forward
                               // arc s->v = state (s, v), two per u32 (else null)
     const uint2* nodes8;      // compact chains: 8-byte node records {off, deg | allpos << 31}
+    const uint32_t* src;      // source node of every arc (slot-order init kernels), nullptr: owner search
     uint32_t* out;            // rows x stride walk buffer
     uint32_t stride;
     uint32_t* lens;
@@ -64,6 +65,7 @@ struct Session {
     DBuf<uint32_t> c16;      // compact 16-bit chain words (node2vec, L2-sized), [c16 | filter copy] when pinned
     const uint32_t* bloom_copy = nullptr;  // the edge filter's copy behind c16 (one persisting window)
     DBuf<uint2> nodes8;      // compact chains: 8-byte node records (half the L2 footprint of NodeRec)
+    DBuf<uint32_t> src;      // source node per arc for the slot-order init (eager second-order sessions)
     DBuf<uint32_t> init_bloom;  // compact chains: the eager init's denser edge filter (own build: MHW_INIT_BLOOM_BITS)
     const uint32_t* ib_p = nullptr;  // the init's filter: init_bloom, or the graph's dense filter (Graph::bloom2)
     size_t ib_bytes = 0;
