@@ -140,6 +140,12 @@ __device__ __forceinline__ uint32_t ldg32h(const uint32_t* p) {
     asm("ld.global.nc.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(r) : "l"(p), "l"(l2_policy<HINT>()));
     return r;
 }
+// One aligned 32-byte sector in one store (sm_100: STG.E.ENL2.256).
+__device__ __forceinline__ void stg256(uint32_t* p, uint4 lo, uint4 hi) {
+    asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "r"(lo.x), "r"(lo.y), "r"(lo.z), "r"(lo.w),
+                 "r"(hi.x), "r"(hi.y), "r"(hi.z), "r"(hi.w)
+                 : "memory");
+}
 template <int HINT>
 __device__ __forceinline__ void stg128h(uint4* p, uint4 v) {
     if constexpr (HINT == 0) {

@@ -33,6 +33,9 @@ namespace mhw {
 
 namespace {
 
+#ifndef MHW_ROWBUF_SMEM  // walk rows staged in shared memory, one 32-byte store per 8 steps
+#define MHW_ROWBUF_SMEM 1
+#endif
 #ifndef MHW_WALK_BLOCK
 #define MHW_WALK_BLOCK 256
 #endif
@@ -129,6 +132,9 @@ __global__ void __launch_bounds__(kWalkBlock) __maxnreg__(REGS == 80 ? MHW_REG80
     constexpr bool ALIAS = ARV == 4 || ARV == 5;  // 4: plain CSR, 5: arc records
     constexpr int AR = ARV == 4 ? 0 : (ARV == 5 ? 1 : ARV);
     const DevGraph& g = P.g;
+#if MHW_ROWBUF_SMEM
+    __shared__ uint32_t rowbuf[8][kWalkBlock];
+#endif
     constexpr bool TYPED = AR && needs_utype<KIND>();
     constexpr bool CC = AR && second_order(KIND);
     constexpr bool NARROW = AR == 2;
@@ -206,7 +212,19 @@ __global__ void __launch_bounds__(kWalkBlock) __maxnreg__(REGS == 80 ? MHW_REG80
         if (KIND == METAPATH2VEC) c.req = P.m.metapath[metapath_next(P.m, 0)];
         if (!second_order(KIND)) slot = slot_of<KIND>(P.m, P.cfg, c, 0, walker);
         uint32_t len = 1;
+#if MHW_ROWBUF_SMEM
+        // Row ids are staged in shared memory, 8 per thread (column threadIdx.x
+        // of rowbuf: bank-conflict free), and leave as ONE aligned 32-byte
+        // store per 8 steps: the two 16-byte halves of a sector written 4 steps
+        // (~27 us) apart were evicted separately from the busy L2 (ncu: 4.76 GB
+        // of DRAM writes for 2.2 GB of rows). ph: the row's first id sits at
+        // slot ph (0 or 4) of its 32-byte group (rows are 16-byte aligned).
+        const uint32_t ph = (uint32_t)((row * P.stride) & 7u);
+        uint32_t* const orow_al = orow - ph;
+        rowbuf[ph][threadIdx.x] = v0;
+#else
         uint32_t b0 = v0, b1 = 0, b2 = 0, b3 = 0;
+#endif
         bool dead = false;
         for (uint32_t step = 0; step < L; ++step) {
             if (c.deg == 0) {
@@ -549,6 +567,24 @@ __global__ void __launch_bounds__(kWalkBlock) __maxnreg__(REGS == 80 ? MHW_REG80
             }
         emit:
             // emit: 4 ids buffered in registers, one 16-byte store
+#if MHW_ROWBUF_SMEM
+            {
+                const uint32_t ab = ph + len;  // index from the aligned group base of the row
+                rowbuf[ab & 7u][threadIdx.x] = next;
+                if ((ab & 7u) == 7u) {
+                    if (ab >= 8u || ph == 0u) {
+                        stg256(orow_al + (ab & ~7u),
+                               make_uint4(rowbuf[0][threadIdx.x], rowbuf[1][threadIdx.x], rowbuf[2][threadIdx.x],
+                                          rowbuf[3][threadIdx.x]),
+                               make_uint4(rowbuf[4][threadIdx.x], rowbuf[5][threadIdx.x], rowbuf[6][threadIdx.x],
+                                          rowbuf[7][threadIdx.x]));
+                    } else {  // first group of a row starting mid-sector: its upper half only
+                        *reinterpret_cast<uint4*>(orow) = make_uint4(rowbuf[4][threadIdx.x], rowbuf[5][threadIdx.x],
+                                                                     rowbuf[6][threadIdx.x], rowbuf[7][threadIdx.x]);
+                    }
+                }
+            }
+#else
             switch (len & 3) {
                 case 0: b0 = next; break;
                 case 1: b1 = next; break;
@@ -558,6 +594,7 @@ __global__ void __launch_bounds__(kWalkBlock) __maxnreg__(REGS == 80 ? MHW_REG80
                     stg128h<MHW_STORE_HINT>(reinterpret_cast<uint4*>(orow + (len & ~3u)), make_uint4(b0, b1, b2, b3));
                     break;
             }
+#endif
             ++len;
             ++steps;
             // update_state (models.cpp:125-136)
@@ -594,11 +631,19 @@ __global__ void __launch_bounds__(kWalkBlock) __maxnreg__(REGS == 80 ? MHW_REG80
             c.vtype = rn.type;
             c.vflags = rn.flags;
         }
+#if MHW_ROWBUF_SMEM
+        {
+            const uint32_t ab = ph + len;              // next free index from the aligned base
+            const uint32_t gb = ab & ~7u;              // base of the pending group
+            for (uint32_t sl = gb < ph ? ph : 0u; sl < (ab & 7u); ++sl) orow_al[gb + sl] = rowbuf[sl][threadIdx.x];
+        }
+#else
         const uint32_t base4 = len & ~3u;
         const uint32_t pend = len & 3u;
         if (pend > 0) orow[base4] = b0;
         if (pend > 1) orow[base4 + 1] = b1;
         if (pend > 2) orow[base4 + 2] = b2;
+#endif
         P.lens[row] = len;
         if (dead) ++early;
     }
