@@ -36,6 +36,10 @@ namespace {
 #ifndef MHW_ROWBUF_SMEM  // walk rows staged in shared memory, one 32-byte store per 8 steps
 #define MHW_ROWBUF_SMEM 1
 #endif
+#ifndef MHW_ROWBUF_IDS  // ids staged per thread and flushed together (cfg2 walk: 8 -> 20.79 ms, 16 -> 19.52, 32 -> 19.66)
+#define MHW_ROWBUF_IDS 16
+#endif
+constexpr uint32_t kRowG = MHW_ROWBUF_IDS;
 #ifndef MHW_WALK_BLOCK
 #define MHW_WALK_BLOCK 256
 #endif
@@ -133,7 +137,7 @@ __global__ void __launch_bounds__(kWalkBlock) __maxnreg__(REGS == 80 ? MHW_REG80
     constexpr int AR = ARV == 4 ? 0 : (ARV == 5 ? 1 : ARV);
     const DevGraph& g = P.g;
 #if MHW_ROWBUF_SMEM
-    __shared__ uint32_t rowbuf[8][kWalkBlock];
+    __shared__ uint32_t rowbuf[kRowG][kWalkBlock];
 #endif
     constexpr bool TYPED = AR && needs_utype<KIND>();
     constexpr bool CC = AR && second_order(KIND);
@@ -219,7 +223,7 @@ __global__ void __launch_bounds__(kWalkBlock) __maxnreg__(REGS == 80 ? MHW_REG80
         // (~27 us) apart were evicted separately from the busy L2 (ncu: 4.76 GB
         // of DRAM writes for 2.2 GB of rows). ph: the row's first id sits at
         // slot ph (0 or 4) of its 32-byte group (rows are 16-byte aligned).
-        const uint32_t ph = (uint32_t)((row * P.stride) & 7u);
+        const uint32_t ph = (uint32_t)((row * P.stride) & (kRowG - 1u));
         uint32_t* const orow_al = orow - ph;
         rowbuf[ph][threadIdx.x] = v0;
 #else
@@ -570,17 +574,25 @@ __global__ void __launch_bounds__(kWalkBlock) __maxnreg__(REGS == 80 ? MHW_REG80
 #if MHW_ROWBUF_SMEM
             {
                 const uint32_t ab = ph + len;  // index from the aligned group base of the row
-                rowbuf[ab & 7u][threadIdx.x] = next;
-                if ((ab & 7u) == 7u) {
-                    if (ab >= 8u || ph == 0u) {
-                        stg256(orow_al + (ab & ~7u),
-                               make_uint4(rowbuf[0][threadIdx.x], rowbuf[1][threadIdx.x], rowbuf[2][threadIdx.x],
-                                          rowbuf[3][threadIdx.x]),
-                               make_uint4(rowbuf[4][threadIdx.x], rowbuf[5][threadIdx.x], rowbuf[6][threadIdx.x],
-                                          rowbuf[7][threadIdx.x]));
-                    } else {  // first group of a row starting mid-sector: its upper half only
-                        *reinterpret_cast<uint4*>(orow) = make_uint4(rowbuf[4][threadIdx.x], rowbuf[5][threadIdx.x],
-                                                                     rowbuf[6][threadIdx.x], rowbuf[7][threadIdx.x]);
+                rowbuf[ab & (kRowG - 1u)][threadIdx.x] = next;
+                if ((ab & (kRowG - 1u)) == kRowG - 1u) {
+                    // the whole group leaves together, sector by sector; the
+                    // first group of a row starts at slot ph (a multiple of 4)
+                    uint32_t* const gp = orow_al + (ab & ~(kRowG - 1u));
+                    const uint32_t lo = ab < kRowG ? ph : 0u;
+#pragma unroll
+                    for (uint32_t k = 0; k < kRowG; k += 8) {
+                        if (lo <= k) {
+                            stg256(gp + k,
+                                   make_uint4(rowbuf[k][threadIdx.x], rowbuf[k + 1][threadIdx.x], rowbuf[k + 2][threadIdx.x],
+                                              rowbuf[k + 3][threadIdx.x]),
+                                   make_uint4(rowbuf[k + 4][threadIdx.x], rowbuf[k + 5][threadIdx.x],
+                                              rowbuf[k + 6][threadIdx.x], rowbuf[k + 7][threadIdx.x]));
+                        } else if (lo == k + 4) {  // the row starts mid-sector: upper half only
+                            *reinterpret_cast<uint4*>(gp + k + 4) =
+                                make_uint4(rowbuf[k + 4][threadIdx.x], rowbuf[k + 5][threadIdx.x], rowbuf[k + 6][threadIdx.x],
+                                           rowbuf[k + 7][threadIdx.x]);
+                        }
                     }
                 }
             }
@@ -634,8 +646,9 @@ __global__ void __launch_bounds__(kWalkBlock) __maxnreg__(REGS == 80 ? MHW_REG80
 #if MHW_ROWBUF_SMEM
         {
             const uint32_t ab = ph + len;              // next free index from the aligned base
-            const uint32_t gb = ab & ~7u;              // base of the pending group
-            for (uint32_t sl = gb < ph ? ph : 0u; sl < (ab & 7u); ++sl) orow_al[gb + sl] = rowbuf[sl][threadIdx.x];
+            const uint32_t gb = ab & ~(kRowG - 1u);    // base of the pending group
+            for (uint32_t sl = gb < ph ? ph : 0u; sl < (ab & (kRowG - 1u)); ++sl)
+                orow_al[gb + sl] = rowbuf[sl][threadIdx.x];
         }
 #else
         const uint32_t base4 = len & ~3u;
