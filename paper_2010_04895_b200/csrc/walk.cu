@@ -1564,6 +1564,8 @@ size_t g_l2_saved[64] = {};
 
 void l2_limit_acquire(int dev, size_t bytes) {
     std::lock_guard<std::mutex> lk(g_l2_mu);
+    // MHW_L2_PERSIST_MB: set-aside size override (experiment: slack above the window size)
+    if (const char* e = std::getenv("MHW_L2_PERSIST_MB")) bytes = (size_t)std::atoll(e) << 20;
     size_t cur = 0;
     MHW_CK(cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize));
     if (g_l2_users[dev & 63]++ == 0) g_l2_saved[dev & 63] = cur;
