@@ -39,7 +39,7 @@ namespace {
 #ifndef MHW_ROWBUF_IDS  // ids staged per thread and flushed together (cfg2 walk: 8 -> 20.79 ms, 16 -> 19.52, 32 -> 19.66)
 #define MHW_ROWBUF_IDS 16
 #endif
-constexpr uint32_t kRowG = MHW_ROWBUF_IDS;
+constexpr uint32_t kRowGDefault = MHW_ROWBUF_IDS;
 #ifndef MHW_WALK_BLOCK
 #define MHW_WALK_BLOCK 256
 #endif
@@ -137,6 +137,8 @@ __global__ void __launch_bounds__(kWalkBlock) __maxnreg__(REGS == 80 ? MHW_REG80
     constexpr int AR = ARV == 4 ? 0 : (ARV == 5 ? 1 : ARV);
     const DevGraph& g = P.g;
 #if MHW_ROWBUF_SMEM
+    // deepwalk on L2-resident graphs is not DRAM-bound: one sector per flush (cfg1 1.00 vs 1.04 ms)
+    constexpr uint32_t kRowG = KIND == DEEPWALK ? 8u : kRowGDefault;
     __shared__ uint32_t rowbuf[kRowG][kWalkBlock];
 #endif
     constexpr bool TYPED = AR && needs_utype<KIND>();
