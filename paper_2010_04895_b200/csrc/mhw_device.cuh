@@ -86,8 +86,9 @@ __device__ __forceinline__ void ldg256(const void* p, uint4& lo, uint4& hi) {
                  : "l"(p));
 }
 
-// The same load with an L2 eviction priority (HINT 1: evict-first,
-// LDG.E.EFL2.256; 2: evict-last, LDG.E.ELL2.256; 0: normal). Build-time
+// The same load with a cache hint (HINT 1: L2 evict-first, LDG.E.EFL2.256;
+// 2: L2 evict-last, LDG.E.ELL2.256; 3: no L1 allocation, LDG.E.NA; 4: 3 + 1;
+// 0: none). Build-time
 // experiment knobs MHW_HASH_HINT / MHW_BLOOM_HINT / MHW_NODE8_HINT /
 // MHW_STORE_HINT (scripts/build_variant.sh); results in DESIGN.md section 3.
 template <int HINT>
@@ -100,14 +101,25 @@ __device__ __forceinline__ void ldg256h(const void* p, uint4& lo, uint4& hi) {
         asm("ld.global.nc.L2::evict_last.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
                      : "=r"(lo.x), "=r"(lo.y), "=r"(lo.z), "=r"(lo.w), "=r"(hi.x), "=r"(hi.y), "=r"(hi.z), "=r"(hi.w)
                      : "l"(p));
+    else if constexpr (HINT == 3)  // no L1 allocation (the line is not reused by this SM)
+        asm("ld.global.nc.L1::no_allocate.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                     : "=r"(lo.x), "=r"(lo.y), "=r"(lo.z), "=r"(lo.w), "=r"(hi.x), "=r"(hi.y), "=r"(hi.z), "=r"(hi.w)
+                     : "l"(p));
+    else if constexpr (HINT == 4)  // no L1 allocation, L2 evict-first
+        asm("ld.global.nc.L1::no_allocate.L2::evict_first.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                     : "=r"(lo.x), "=r"(lo.y), "=r"(lo.z), "=r"(lo.w), "=r"(hi.x), "=r"(hi.y), "=r"(hi.z), "=r"(hi.w)
+                     : "l"(p));
     else
         ldg256(p, lo, hi);
 }
+// Defaults: the edge-filter blocks and hash buckets skip L1 allocation (an
+// SM does not see the same line twice; L1 keeps the spilled frame instead):
+// cfg2 init 4.27 -> 4.1 ms, step 24.05 -> 23.79; cfg3a / cfg3b / cfg4 / cfg5 equal.
 #ifndef MHW_HASH_HINT
-#define MHW_HASH_HINT 0
+#define MHW_HASH_HINT 3
 #endif
 #ifndef MHW_BLOOM_HINT
-#define MHW_BLOOM_HINT 0
+#define MHW_BLOOM_HINT 3
 #endif
 #ifndef MHW_NODE8_HINT
 #define MHW_NODE8_HINT 0

@@ -40,6 +40,9 @@ namespace {
 #define MHW_ROWBUF_IDS 16
 #endif
 constexpr uint32_t kRowGDefault = MHW_ROWBUF_IDS;
+#ifndef MHW_C16_HASH_HINT
+#define MHW_C16_HASH_HINT 1
+#endif
 #ifndef MHW_WALK_BLOCK
 #define MHW_WALK_BLOCK 256
 #endif
@@ -145,7 +148,7 @@ __global__ void __launch_bounds__(kWalkBlock) __maxnreg__(REGS == 80 ? MHW_REG80
     constexpr bool CC = AR && second_order(KIND);
     constexpr bool NARROW = AR == 2;
     constexpr bool C16 = AR == 3;  // ids + compact 16-bit chain table (node2vec)
-    constexpr int kHashHint = C16 ? 1 : MHW_HASH_HINT;  // hash buckets evict-first beside the pinned table
+    constexpr int kHashHint = C16 ? MHW_C16_HASH_HINT : MHW_HASH_HINT;  // hash buckets evict-first beside the pinned table
     static_assert(!C16 || (KIND == NODE2VEC && !LAZY), "compact chains: eagerly initialised node2vec");
     // typed second-order records carry w'(Last) next to the chain word
     // (word 1 = {type | etype << 16, chain word, w'(Last) as f64}), taken and
