@@ -43,6 +43,9 @@ constexpr uint32_t kRowGDefault = MHW_ROWBUF_IDS;
 #ifndef MHW_C16_HASH_HINT
 #define MHW_C16_HASH_HINT 1
 #endif
+#ifndef MHW_IDS_ALL_HINT  // compact chains: the Last's id loads (the candidate's: MHW_IDS_HINT)
+#define MHW_IDS_ALL_HINT 3
+#endif
 #ifndef MHW_WALK_BLOCK
 #define MHW_WALK_BLOCK 256
 #endif
@@ -159,7 +162,7 @@ __global__ void __launch_bounds__(kWalkBlock) __maxnreg__(REGS == 80 ? MHW_REG80
     const uint4* const arcs = (AR && KIND != DEEPWALK) ? P.ac : g.arc;
     auto load_rec = [&](uint64_t arc, uint4& b) {
         if constexpr (C16) {
-            const uint32_t u = __ldg(g.ids + arc);
+            const uint32_t u = ldg32h<MHW_IDS_ALL_HINT>(g.ids + arc);
             const uint2 r = __ldg(P.nodes8 + u);
             return make_uint4(u, r.y, r.x, 0u);
         }
@@ -170,10 +173,11 @@ __global__ void __launch_bounds__(kWalkBlock) __maxnreg__(REGS == 80 ? MHW_REG80
         }
         if constexpr (TYPED) {
             uint4 a;
-            ldg256(arcs + RS * arc, a, b);  // the whole 32-byte record in one request
+            // metapath2vec: no L1 allocation (cfg3a 43.33 -> 42.77 ms; cfg5's wide records 876 -> 969, cfg1 1.00 -> 1.34)
+            ldg256h<(KIND == METAPATH2VEC ? 3 : MHW_REC_HINT)>(arcs + RS * arc, a, b);  // the whole 32-byte record in one request
             return a;
         }
-        return __ldg(arcs + RS * arc);
+        return ldg128h<MHW_REC_HINT>(arcs + RS * arc);
     };
     auto rec_node = [&](const uint4& a, const uint4& b) {
         NodeRec r = arc_node(a);
@@ -376,7 +380,7 @@ __global__ void __launch_bounds__(kWalkBlock) __maxnreg__(REGS == 80 ? MHW_REG80
                     // id and slice are in registers, nothing to fetch)
                     if (e < kLocked && (C16 ? ((e >> 30) == 3u || ((e >> 30) == P.m.spec_cls && (e >> 30) != 0u))
                                             : (e >> 30) == P.m.spec_cls)) {
-                        xl = C16 ? make_uint2(__ldg(g.ids + c.off + (e & kIdxMask)), 0u)
+                        xl = C16 ? make_uint2(ldg32h<MHW_IDS_ALL_HINT>(g.ids + c.off + (e & kIdxMask)), 0u)
                                  : __ldg(reinterpret_cast<const uint2*>(P.ac) + c.off + (e & kIdxMask));
                         spec_l = true;
                     }
@@ -475,7 +479,7 @@ __global__ void __launch_bounds__(kWalkBlock) __maxnreg__(REGS == 80 ? MHW_REG80
                     // hub state: the word holds no class; alpha(s, Last) from
                     // the Last's id (a pure function of (state, Last), as cached)
                     if (!spec_l) {
-                        xl = make_uint2(__ldg(g.ids + c.off + last), 0u);
+                        xl = make_uint2(ldg32h<MHW_IDS_ALL_HINT>(g.ids + c.off + last), 0u);
                         spec_l = true;
                     }
                     cls_l = alpha_class<kHashHint>(g, P.m, c, xl.x, nullptr);
