@@ -1464,6 +1464,11 @@ void with_variant(int regs, bool lazy, int ar, F&& f) {
 template <int KIND, int REGS, bool LAZY, int AR>
 int walk_grid() {
     int per_sm = 0;
+    // MHW_CARVEOUT: preferred shared-memory carve-out in percent (experiment; the
+    // kernel's own need, 9-17 KB per block for the row staging, is honoured)
+    if (const char* cv = std::getenv("MHW_CARVEOUT"))
+        MHW_CK(cudaFuncSetAttribute(k_walk<KIND, REGS, LAZY, AR>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                    std::atoi(cv)));
     MHW_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_walk<KIND, REGS, LAZY, AR>, kWalkBlock, 0));
     return std::max(1, per_sm) * sms();
 }
