@@ -160,6 +160,10 @@ __device__ __forceinline__ uint32_t ldg32h(const uint32_t* p) {
         asm("ld.global.nc.L1::no_allocate.u32 %0, [%1];" : "=r"(r) : "l"(p));
         return r;
     }
+    if constexpr (HINT == 4) {  // no L1 allocation, L2 evict-first
+        asm("ld.global.nc.L1::no_allocate.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(r) : "l"(p), "l"(l2_policy<1>()));
+        return r;
+    }
     asm("ld.global.nc.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(r) : "l"(p), "l"(l2_policy<HINT>()));
     return r;
 }
