@@ -1790,9 +1790,11 @@ void session_create(Session& s, Graph& g, const mhw_model_desc& md, const mhw_wa
     }
     s.rows_cap = s.rows;
     s.items_cap = s.n_items;
+    const double t_starts = trace ? tms() : 0.0;
     s.out.alloc(std::max<uint64_t>(s.rows * s.stride, 4));
     s.lens.alloc(std::max<uint64_t>(s.rows, 1));
     s.ctr.alloc(8);
+    if (trace) std::fprintf(stderr, "[mhw] session_create: starts at %.2f ms, walk buffer at %.2f ms\n", t_starts, tms());
     if (wc.sampler != MHW_SAMPLER_MH) {
         // exact baselines: no chains; Philox-keyed draws make any schedule
         // deterministic
