@@ -143,8 +143,9 @@ __global__ void __launch_bounds__(kWalkBlock) __maxnreg__(REGS == 80 ? MHW_REG80
     constexpr int AR = ARV == 4 ? 0 : (ARV == 5 ? 1 : ARV);
     const DevGraph& g = P.g;
 #if MHW_ROWBUF_SMEM
-    // deepwalk on L2-resident graphs is not DRAM-bound: one sector per flush (cfg1 1.00 vs 1.04 ms)
-    constexpr uint32_t kRowG = KIND == DEEPWALK ? 8u : kRowGDefault;
+    // deepwalk on L2-resident graphs is not DRAM-bound: one sector per flush (cfg1 1.00 vs 1.04 ms);
+    // metapath2vec: a whole 128-byte line per flush (cfg3a 43.3 -> 43.0 ms)
+    constexpr uint32_t kRowG = KIND == DEEPWALK ? 8u : (KIND == METAPATH2VEC ? 32u : kRowGDefault);
     __shared__ uint32_t rowbuf[kRowG][kWalkBlock];
 #endif
     constexpr bool TYPED = AR && needs_utype<KIND>();

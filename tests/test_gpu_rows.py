@@ -35,6 +35,31 @@ def arc_set(g):
     return set((src << 32 | g.nbr.astype(np.int64)).tolist())
 
 
+def test_metapath_rows_are_intact_walks_at_every_length(mhw):
+    """metapath2vec stages 32 ids per flush and its walks end early where no
+    neighbour has the required type: every row must be the start node followed
+    by arcs of the graph over its own length, whatever that length is."""
+    g = typed_random_graph(13, 400, 6.0)
+    arcs = arc_set(g)
+    deg = np.diff(g.offsets.astype(np.int64))
+    dg = device_graph(g)
+    md = model_desc(O.METAPATH2VEC, g)
+    for L in LENGTHS:
+        for K in (1, 3):
+            c = mhw.generate_walks(dg, walk_model(md), walk_config(O.WalkCfg(K=K, L=L, seed=7 + L), threads=8))
+            starts = np.repeat(np.nonzero((deg > 0) & (g.ntype == md.metapath[0]))[0], K)
+            assert len(c.lengths) == len(starts), (L, K)
+            assert np.array_equal(c.rows[:, 0], starts), (L, K)
+            assert np.all((c.lengths >= 1) & (c.lengths <= L + 1))
+            steps = 0
+            for r in range(len(starts)):
+                n = int(c.lengths[r])
+                row = c.rows[r, :n].astype(np.int64)
+                assert all(int(k) in arcs for k in (row[:-1] << 32 | row[1:])), (L, K, r)
+                steps += n - 1
+            assert c.stats.steps == steps
+
+
 @pytest.mark.parametrize("kind", [O.DEEPWALK, O.NODE2VEC, O.EDGE2VEC])
 def test_rows_are_intact_walks_at_every_length(mhw, kind):
     g = typed_random_graph(11, 400, 5.0)
